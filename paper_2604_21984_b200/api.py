@@ -1,0 +1,439 @@
+"""Python mirror of the reference `sad::` API (candidates.hpp, render.hpp, grad.hpp, train.hpp,
+budget.hpp) over a C-ABI library with the entry points of include/sad_b200.h.
+
+`Backend` binds one library.  The product binding (`gpu_backend()`) loads the in-tree CUDA
+library `libsad_b200.so` and fails loudly when it is missing or when no GPU is present — there is
+no CPU fallback on the product path.  The same class is reused by the test-only oracle bindings
+(oracle/bindings.py) so parity tests can call the reference and the GPU with identical code.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _abi
+from .types import (AdamState, CandidateField, FitResult, GradBuffer, HistoryRow, ImageBuffer, PassSpec,
+                    RefreshMode, RunOpts, SiteStore, StatsResult, Stencil, TrainConfig, normalization_scale,
+                    psnr_from_loss)
+
+
+class SadError(Exception):
+    code = -1
+
+
+class InvalidArgument(SadError, ValueError):
+    """std::invalid_argument (bad input, stale field, empty candidate list)."""
+
+
+class StaleField(InvalidArgument):
+    code = _abi.SAD_ESTALE
+
+
+class EmptyList(InvalidArgument):
+    code = _abi.SAD_EEMPTY
+
+
+class NumericError(SadError, ArithmeticError):
+    """sad::numeric_error (types.hpp:14-17)."""
+    code = _abi.SAD_ENUMERIC
+
+
+class FormatError(SadError):
+    code = _abi.SAD_EFORMAT
+
+
+class CudaError(SadError, RuntimeError):
+    code = _abi.SAD_ECUDA
+
+
+class CapacityError(SadError, MemoryError):
+    code = _abi.SAD_ENOMEM
+
+
+_EXC = {
+    _abi.SAD_EINVAL: InvalidArgument,
+    _abi.SAD_ESTALE: StaleField,
+    _abi.SAD_EEMPTY: EmptyList,
+    _abi.SAD_ENUMERIC: NumericError,
+    _abi.SAD_EFORMAT: FormatError,
+    _abi.SAD_ECUDA: CudaError,
+    _abi.SAD_ENOMEM: CapacityError,
+}
+
+_P = C.c_void_p
+_dp = C.POINTER(C.c_double)
+
+
+def _ptr(a: np.ndarray, t=C.c_double):
+    return a.ctypes.data_as(C.POINTER(t))
+
+
+class Backend:
+    """One C-ABI implementation.  kind: 'gpu' (sad_, ctx-first), 'ref' (sadref_, threads args),
+    'c' (sado_)."""
+
+    def __init__(self, lib: C.CDLL, prefix: str, kind: str, ctx=None, threads: int = 1):
+        self.lib = lib
+        self.prefix = prefix
+        self.kind = kind
+        self.ctx = ctx
+        self.threads = threads
+        self.lib.__getattr__(prefix + "last_error").restype = C.c_char_p
+
+    # ------------------------------------------------------------------ plumbing
+    def _fn(self, name):
+        return getattr(self.lib, self.prefix + name)
+
+    def _call(self, name, *args):
+        pre = (self.ctx,) if self.kind == "gpu" and name not in _NO_CTX else ()
+        rc = self._fn(name)(*pre, *args)
+        if rc != 0:
+            msg = self._fn("last_error")().decode(errors="replace")
+            raise _EXC.get(rc, SadError)(f"{self.prefix}{name}: {msg}")
+
+    def _thr(self):
+        return (C.c_int(self.threads),) if self.kind == "ref" else ()
+
+    # ------------------------------------------------------------------ candidates.hpp
+    def jump_step(self, t: int, b: int) -> int:
+        out = C.c_uint32()
+        self._call("jump_step", C.c_uint32(t), C.c_uint32(b), C.byref(out))
+        return out.value
+
+    def full_refresh_passes(self, gw, gh, extra_step1) -> List[PassSpec]:
+        buf = (_abi.PassSpec * (64 + max(extra_step1, 0)))()
+        n = C.c_int(len(buf))
+        self._call("full_refresh_passes", C.c_int(gw), C.c_int(gh), C.c_int(extra_step1), buf, C.byref(n))
+        return [PassSpec(buf[i].step, Stencil(buf[i].stencil)) for i in range(n.value)]
+
+    def jfa_seed(self, sites: SiteStore, field: CandidateField):
+        sv, keep = sites._view()
+        fv = field._view()
+        self._call("jfa_seed", C.byref(sv), C.byref(fv))
+        field._absorb(fv)
+
+    def run_passes(self, sites: SiteStore, field: CandidateField, seq: Sequence[PassSpec], inject: int,
+                   seed: int, opts: RunOpts = RunOpts()):
+        sv, keep = sites._view()
+        fv = field._view()
+        arr = (_abi.PassSpec * max(len(seq), 1))(*[_abi.PassSpec(p.step, int(p.stencil)) for p in seq])
+        self._call("run_passes", C.byref(sv), C.byref(fv), arr, C.c_int(len(seq)), C.c_int(inject),
+                   C.c_uint64(seed), C.c_int(int(opts.fp64)), *self._thr())
+        field._absorb(fv)
+
+    def propagate_pass(self, sites, field, p: PassSpec, inject, seed, opts: RunOpts = RunOpts()):
+        self.run_passes(sites, field, [p], inject, seed, opts)
+
+    def refresh(self, sites: SiteStore, field: CandidateField, mode: RefreshMode, passes: int, inject: int,
+                seed: int, opts: RunOpts = RunOpts()):
+        sv, keep = sites._view()
+        fv = field._view()
+        self._call("refresh", C.byref(sv), C.byref(fv), C.c_int(int(mode)), C.c_int(passes), C.c_int(inject),
+                   C.c_uint64(seed), C.c_int(int(opts.fp64)), *self._thr())
+        field._absorb(fv)
+
+    def exact_topk_batch(self, sites: SiteStore, pixels, k: int, scale: float, fp64: bool = True) -> np.ndarray:
+        xy = np.ascontiguousarray(np.asarray(pixels, np.int32).reshape(-1, 2))
+        out = np.full(xy.shape[0] * k, _abi.EMPTY_ID, np.uint32)
+        sv, keep = sites._view()
+        self._call("exact_topk_batch", C.byref(sv), _ptr(xy, C.c_int32), C.c_size_t(xy.shape[0]), C.c_int(k),
+                   C.c_double(scale), C.c_int(int(fp64)), _ptr(out, C.c_uint32))
+        return out.reshape(-1, k)
+
+    # ------------------------------------------------------------------ render.hpp
+    def render_image(self, sites: SiteStore, field: CandidateField, opts: RunOpts = RunOpts()) -> ImageBuffer:
+        out = ImageBuffer(field.width, field.height)
+        sv, keep = sites._view()
+        fv = field._view()
+        args = [C.byref(sv), C.byref(fv), C.c_int(int(opts.fp64))]
+        if self.kind == "ref":
+            args.append(C.c_int(self.threads))
+        self._call("render_image", *args, _ptr(out.data))
+        return out
+
+    def pixel_weights_batch(self, sites, field, pixels):
+        xy = np.ascontiguousarray(np.asarray(pixels, np.int32).reshape(-1, 2))
+        q = xy.shape[0]
+        ids = np.zeros(q * 16, np.uint32)
+        w = np.zeros(q * 16, np.float64)
+        n = np.zeros(q, np.int32)
+        sv, keep = sites._view()
+        fv = field._view()
+        self._call("pixel_weights", C.byref(sv), C.byref(fv), _ptr(xy, C.c_int32), C.c_size_t(q),
+                   _ptr(ids, C.c_uint32), _ptr(w), _ptr(n, C.c_int32))
+        return ids.reshape(q, 16), w.reshape(q, 16), n
+
+    def pixel_weights(self, sites, field, px, py):
+        ids, w, n = self.pixel_weights_batch(sites, field, [(px, py)])
+        return ids[0, : n[0]].copy(), w[0, : n[0]].copy()
+
+    def render_id_map(self, sites, field, opts: RunOpts = RunOpts()) -> np.ndarray:
+        out = np.zeros(field.width * field.height, np.uint32)
+        sv, keep = sites._view()
+        fv = field._view()
+        self._call("render_id_map", C.byref(sv), C.byref(fv), _ptr(out, C.c_uint32))
+        return out
+
+    # ------------------------------------------------------------------ grad.hpp
+    def backward_image(self, sites, field, target: ImageBuffer, out: GradBuffer, opts: RunOpts = RunOpts(),
+                       with_removal: bool = True) -> float:
+        if target.width != field.width or target.height != field.height:
+            raise InvalidArgument("backward: target size mismatch")
+        out.resize(sites.size())
+        g = np.zeros(max(sites.size(), 1) * 11, np.float64)
+        nf = C.c_uint64()
+        loss = C.c_double()
+        sv, keep = sites._view()
+        fv = field._view()
+        args = [C.byref(sv), C.byref(fv), _ptr(target.data), C.c_int(int(opts.fp64)), C.c_int(int(with_removal))]
+        if self.kind == "ref":
+            args.append(C.c_int(self.threads))
+        self._call("backward_image", *args, _ptr(g), C.byref(nf), C.byref(loss))
+        out.data = g[: sites.size() * 11].reshape(-1, 11).copy()
+        out.nonfinite = int(nf.value)
+        return float(loss.value)
+
+    def image_loss(self, sites, field, target: ImageBuffer, opts: RunOpts = RunOpts()) -> float:
+        if target.width != field.width or target.height != field.height:
+            raise InvalidArgument("loss: target size mismatch")
+        loss = C.c_double()
+        sv, keep = sites._view()
+        fv = field._view()
+        self._call("image_loss", C.byref(sv), C.byref(fv), _ptr(target.data), C.c_int(int(opts.fp64)),
+                   C.byref(loss))
+        return float(loss.value)
+
+    def backward_pixel_grad(self, sites, field, dl: ImageBuffer, out: GradBuffer, opts: RunOpts = RunOpts()):
+        out.resize(sites.size())
+        g = np.zeros(max(sites.size(), 1) * 11, np.float64)
+        nf = C.c_uint64()
+        sv, keep = sites._view()
+        fv = field._view()
+        self._call("backward_pixel_grad", C.byref(sv), C.byref(fv), _ptr(dl.data), C.c_int(int(opts.fp64)),
+                   _ptr(g), C.byref(nf))
+        out.data = g[: sites.size() * 11].reshape(-1, 11).copy()
+        out.nonfinite = int(nf.value)
+
+    # ------------------------------------------------------------------ train.hpp
+    def adam_step(self, sites: SiteStore, g: GradBuffer, adam: AdamState, width, height, cfg: TrainConfig):
+        if g.size() != sites.size():
+            raise InvalidArgument("adam_step: gradient size mismatch")
+        sv, keep = sites._view()
+        av, akeep = adam._view(sites.size())
+        gd = np.ascontiguousarray(g.data.reshape(-1))
+        if gd.size == 0:
+            gd = np.zeros(11)
+        c = cfg.to_c()
+        self._call("adam_step", C.byref(sv), _ptr(gd), C.byref(av), C.c_int(width), C.c_int(height), C.byref(c))
+        sites._absorb(sv, keep)
+        adam._absorb(av, akeep)
+
+    def clamp_project(self, sites: SiteStore, width, height, cfg: TrainConfig):
+        sv, keep = sites._view()
+        c = cfg.to_c()
+        self._call("clamp_project", C.byref(sv), C.c_int(width), C.c_int(height), C.byref(c))
+        sites._absorb(sv, keep)
+
+    def init_sites(self, sites: SiteStore, target: ImageBuffer, n: int, cfg: TrainConfig):
+        tmp = SiteStore(0)
+        sv, keep = tmp._view(capacity=max(n, 1))
+        c = cfg.to_c()
+        self._call("init_sites", C.byref(sv), _ptr(target.data), C.c_int(target.width), C.c_int(target.height),
+                   C.c_int(n), C.byref(c))
+        gen = sites.generation
+        sites._absorb(sv, keep)
+        sites.generation = gen + 1 + n
+
+    # ------------------------------------------------------------------ budget.hpp
+    def accumulate_stats(self, sites, field, target: ImageBuffer, opts: RunOpts = RunOpts()) -> StatsResult:
+        if target.width != field.width or target.height != field.height:
+            raise InvalidArgument("stats: target size mismatch")
+        r = StatsResult(sites.size())
+        buf = np.zeros(max(sites.size(), 1) * 8, np.float64)
+        valid = C.c_uint64()
+        sv, keep = sites._view()
+        fv = field._view()
+        args = [C.byref(sv), C.byref(fv), _ptr(target.data)]
+        if self.kind == "ref":
+            args.append(C.c_int(self.threads))
+        self._call("accumulate_stats", *args, _ptr(buf), C.byref(valid))
+        r.data = buf[: sites.size() * 8].reshape(-1, 8).copy()
+        r.valid_pixels = int(valid.value)
+        return r
+
+    def prune(self, sites: SiteStore, stats: StatsResult, percentile: float) -> int:
+        if stats.data.shape[0] != sites.size():
+            raise InvalidArgument("prune: stats size mismatch")
+        sv, keep = sites._view()
+        sd = np.ascontiguousarray(stats.data.reshape(-1)) if stats.data.size else np.zeros(8)
+        n = C.c_int()
+        self._call("prune", C.byref(sv), _ptr(sd), C.c_uint64(stats.valid_pixels), C.c_double(percentile),
+                   C.byref(n))
+        sites._absorb(sv, keep)
+        return n.value
+
+    def densify(self, sites: SiteStore, adam: AdamState, stats: StatsResult, target: ImageBuffer, percentile: float,
+                cfg: TrainConfig) -> int:
+        if stats.data.shape[0] != sites.size():
+            raise InvalidArgument("densify: stats size mismatch")
+        cap = 2 * sites.size() + 1
+        sv, keep = sites._view(capacity=cap)
+        av, akeep = adam._view(cap)
+        sd = np.ascontiguousarray(stats.data.reshape(-1)) if stats.data.size else np.zeros(8)
+        c = cfg.to_c()
+        n = C.c_int()
+        self._call("densify", C.byref(sv), C.byref(av), _ptr(sd), _ptr(target.data), C.c_int(target.width),
+                   C.c_int(target.height), C.c_double(percentile), C.byref(c), C.byref(n))
+        sites._absorb(sv, keep)
+        adam._absorb(av, akeep)
+        return n.value
+
+    def bpp_target_count(self, bpp, width, height) -> int:
+        out = C.c_uint64()
+        self._call("bpp_target_count", C.c_double(bpp), C.c_int(width), C.c_int(height), C.byref(out))
+        return out.value
+
+    def simulate_schedule(self, n0, scale, cfg: TrainConfig) -> int:
+        out = C.c_int()
+        c = cfg.to_c()
+        self._call("simulate_schedule", C.c_int(n0), C.c_double(scale), C.byref(c), C.byref(out))
+        return out.value
+
+    def plan_schedule(self, n0, target, cfg: TrainConfig) -> float:
+        out = C.c_double()
+        c = cfg.to_c()
+        self._call("plan_schedule", C.c_int(n0), C.c_uint64(target), C.byref(c), C.byref(out))
+        return out.value
+
+    # ------------------------------------------------------------------ fit (train.cpp:221-311)
+    def fit(self, target: ImageBuffer, cfg: TrainConfig) -> FitResult:
+        return self._fit(target, cfg, None)
+
+    def fit_store(self, sites: SiteStore, target: ImageBuffer, cfg: TrainConfig) -> FitResult:
+        return self._fit(target, cfg, sites)
+
+    def _fit(self, target: ImageBuffer, cfg: TrainConfig, init: Optional[SiteStore]) -> FitResult:
+        c = cfg.to_c()
+        w, h = target.width, target.height
+        if self.kind == "gpu":
+            run = _P()
+            self._call("fit_create", C.c_int(w), C.c_int(h), C.byref(c), C.byref(run))
+            try:
+                self._call("fit_set_target", run, _ptr(target.data))
+                if init is None:
+                    self._call("fit_run_init", run)
+                else:
+                    sv, keep = init._view()
+                    self._call("fit_run_store", run, C.byref(sv))
+                n = C.c_size_t()
+                nh = C.c_int()
+                sc = C.c_double()
+                self._call("fit_info", run, C.byref(n), C.byref(nh), C.byref(sc))
+                res = self._fit_collect(w, h, cfg, int(n.value), int(nh.value), float(sc.value),
+                                        lambda sv, fv, hist: self._call("fit_download", run, sv, fv, hist))
+                tot = C.c_double()
+                ph = (C.c_double * 4)()
+                self._call("fit_timing", run, C.byref(tot), ph)
+                res.timing = {"total_ms": tot.value, "propagate_ms": ph[0], "fwd_bwd_ms": ph[1],
+                              "adam_ms": ph[2], "events_ms": ph[3]}
+                return res
+            finally:
+                self.lib.sad_fit_destroy(run)
+        if self.kind == "ref":
+            hd = _P()
+            if init is None:
+                self._call("fit", _ptr(target.data), C.c_int(w), C.c_int(h), C.byref(c), None, C.byref(hd))
+            else:
+                sv, keep = init._view()
+                self._call("fit", _ptr(target.data), C.c_int(w), C.c_int(h), C.byref(c), C.byref(sv), C.byref(hd))
+            try:
+                n = C.c_size_t()
+                nh = C.c_int()
+                sc = C.c_double()
+                sec = C.c_double()
+                ph = (C.c_double * 8)()
+                self.lib.sadref_fit_info(hd, C.byref(n), C.byref(nh), C.byref(sc), C.byref(sec), ph)
+                res = self._fit_collect(w, h, cfg, int(n.value), int(nh.value), float(sc.value),
+                                        lambda sv, fv, hist: self._call("fit_download", hd, sv, fv, hist))
+                res.timing = {"total_ms": sec.value * 1e3, "propagate_ms": ph[0], "fwd_bwd_ms": ph[1],
+                              "adam_ms": ph[2], "events_ms": ph[3], "refresh_full_ms": ph[4], "init_ms": ph[5]}
+                return res
+            finally:
+                self.lib.sadref_fit_free(hd)
+        # plain-C restatement
+        cap = C.c_size_t()
+        self._call("fit_capacity", C.c_int(w), C.c_int(h), C.byref(c), C.c_size_t(init.size() if init else 0),
+                   C.byref(cap))
+        out = SiteStore(0)
+        sv, keep = out._view(capacity=int(cap.value))
+        f = CandidateField()
+        f.resize(w, h, cfg.k)
+        fv = f._view()
+        hist = (_abi.HistoryRowC * max(cfg.iters, 1))()
+        sc = C.c_double()
+        if init is None:
+            self._call("fit", _ptr(target.data), C.c_int(w), C.c_int(h), C.byref(c), None, C.byref(sv), C.byref(fv),
+                       hist, C.byref(sc))
+        else:
+            iv, ikeep = init._view()
+            self._call("fit", _ptr(target.data), C.c_int(w), C.c_int(h), C.byref(c), C.byref(iv), C.byref(sv),
+                       C.byref(fv), hist, C.byref(sc))
+        out._absorb(sv, keep)
+        f._absorb(fv)
+        rows = [HistoryRow(r.iter, r.loss, r.psnr, r.active_sites, r.ms) for r in hist[: cfg.iters]]
+        return FitResult(out, f, rows, float(sc.value))
+
+    def _fit_collect(self, w, h, cfg, n, nh, sc, download) -> FitResult:
+        st = SiteStore(0)
+        sv, keep = st._view(capacity=max(n, 1))
+        f = CandidateField()
+        f.resize(w, h, cfg.k)
+        fv = f._view()
+        hist = (_abi.HistoryRowC * max(nh, 1))()
+        download(C.byref(sv), C.byref(fv), hist)
+        sv.size = n
+        st._absorb(sv, keep)
+        f._absorb(fv)
+        rows = [HistoryRow(r.iter, r.loss, r.psnr, r.active_sites, r.ms) for r in hist[:nh]]
+        return FitResult(st, f, rows, sc)
+
+
+_NO_CTX = {"jump_step", "full_refresh_passes", "schedule_passes", "bpp_target_count", "simulate_schedule",
+           "plan_schedule", "fit_set_target", "fit_set_target_device", "fit_run_init", "fit_run_store",
+           "fit_info", "fit_download", "fit_render_device", "fit_timing", "fit_bench", "last_error"}
+
+# ---------------------------------------------------------------------- product binding
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsad_b200.so")
+_lock = threading.Lock()
+_gpu = None
+
+
+def load_library(path: str = LIB_PATH) -> C.CDLL:
+    if not os.path.exists(path):
+        raise ImportError(f"CUDA library {path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = C.CDLL(path)
+    lib.sad_last_error.restype = C.c_char_p
+    lib.sad_ctx_launch_count.restype = C.c_uint64
+    lib.sad_ctx_launch_count.argtypes = [_P]
+    lib.sad_fit_destroy.argtypes = [_P]
+    lib.sad_ctx_destroy.argtypes = [_P]
+    return lib
+
+
+def gpu_backend(device: int = 0) -> Backend:
+    """The product backend (CUDA, sm_100a).  Raises if the extension or the GPU is unavailable."""
+    global _gpu
+    with _lock:
+        if _gpu is None:
+            lib = load_library()
+            ctx = _P()
+            rc = lib.sad_ctx_create(C.c_int(device), None, C.byref(ctx))
+            if rc != 0:
+                raise CudaError("sad_ctx_create: " + lib.sad_last_error().decode(errors="replace"))
+            _gpu = Backend(lib, "sad_", "gpu", ctx=ctx)
+        return _gpu

@@ -1,0 +1,1604 @@
+// sad_kernels.cu — the SAD fitting-loop kernels for sm_100a.
+//
+// Every kernel restates one reference loop (cited per kernel) with the reference's exact operation
+// order; the library is built with --fmad=false (see sad_device.cuh).  None of these steps is a
+// dense contraction, so there are no tensor-core paths: the roofline is HBM / L2 bandwidth or the
+// FP32/FP64 pipes.
+#include "sad_device.cuh"
+#include "sad_kernels.h"
+
+#include <atomic>
+
+namespace sadk {
+
+static std::atomic<uint64_t> g_launches{0};
+uint64_t launch_counter() { return g_launches.load(); }
+#define SAD_LAUNCHED() g_launches.fetch_add(1, std::memory_order_relaxed)
+
+// ====================================================================== per-site tables
+// ScoreTable<T>::build (score_table.hpp:20-46), packed and unpacked, and GradTable<T>::build
+// (grad.cpp:79-111).  Coefficients are derived in double and rounded to T exactly as the reference.
+template <typename T>
+__global__ void k_tables(SitesDev s, const DevState* __restrict__ st, double scale, Q4<T>* __restrict__ pack,
+                         Q4<T>* __restrict__ gtab, Q4<T>* __restrict__ rtab) {
+    int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= st->n_sites) return;
+    const int cap = s.cap;
+    const double* p = s.p;
+    bool act = s.active[id] != 0;
+    double x = p[0 * cap + id], y = p[1 * cap + id], lt = p[2 * cap + id], r = p[3 * cap + id];
+    double cr = p[4 * cap + id], cg = p[5 * cap + id], cb = p[6 * cap + id];
+    double ux = p[7 * cap + id], uy = p[8 * cap + id], an = p[9 * cap + id];
+    if (pack) {
+        Q4<T> a, b;
+        if (!act) {
+            a = {T(0), T(0), T(0), T(0)};
+            b = {T(1), T(0), T(1), T(0)};
+        } else {
+            double hx = half_rt(x), hy = half_rt(y), hlt = half_rt(lt), hr = half_rt(r);
+            double hux = half_rt(ux), huy = half_rt(uy), han = half_rt(an);
+            double ea = exp(han), ia = exp(-han);
+            double vx = -huy, vy = hux;
+            a = {static_cast<T>(hx), static_cast<T>(hy), static_cast<T>(exp(hlt)), static_cast<T>(hr)};
+            b = {static_cast<T>(ea * hux * hux + ia * vx * vx), static_cast<T>(ea * hux * huy + ia * vx * vy),
+                 static_cast<T>(ea * huy * huy + ia * vy * vy), T(1)};
+        }
+        pack[2 * id] = a;
+        pack[2 * id + 1] = b;
+    }
+    if (gtab) {
+        Q4<T> a, b, c;
+        if (!act) {
+            a = {T(0), T(0), T(0), T(0)};
+            b = {T(1), T(1), T(1), T(0)};
+            c = {T(0), T(0), T(0), T(0)};
+        } else {
+            a = {static_cast<T>(x), static_cast<T>(y), static_cast<T>(exp(lt)), static_cast<T>(r)};
+            b = {static_cast<T>(exp(an)), static_cast<T>(exp(-an)), static_cast<T>(ux), static_cast<T>(uy)};
+            c = {static_cast<T>(cr), static_cast<T>(cg), static_cast<T>(cb), T(1)};
+        }
+        gtab[3 * id] = a;
+        gtab[3 * id + 1] = b;
+        gtab[3 * id + 2] = c;
+    }
+    if (rtab) {
+        Q4<T> a, b, c;
+        if (!act) {
+            a = {T(0), T(0), T(0), T(0)};
+            b = {T(1), T(0), T(1), T(0)};
+        } else {
+            double ea = exp(an), ia = exp(-an);
+            double vx = -uy, vy = ux;
+            a = {static_cast<T>(x), static_cast<T>(y), static_cast<T>(exp(lt)), static_cast<T>(r)};
+            b = {static_cast<T>(ea * ux * ux + ia * vx * vx), static_cast<T>(ea * ux * uy + ia * vx * vy),
+                 static_cast<T>(ea * uy * uy + ia * vy * vy), T(1)};
+        }
+        c = {static_cast<T>(cr), static_cast<T>(cg), static_cast<T>(cb), T(0)};
+        rtab[3 * id] = a;
+        rtab[3 * id + 1] = b;
+        rtab[3 * id + 2] = c;
+    }
+}
+
+void launch_tables(bool fp64, const SitesDev& s, const DevState* st, double scale, void* pack, void* gtab,
+                   void* rtab, cudaStream_t stream) {
+    int grid = (s.cap + 255) / 256;
+    if (grid < 1) grid = 1;
+    if (fp64)
+        k_tables<double><<<grid, 256, 0, stream>>>(s, st, scale, (Q4<double>*)pack, (Q4<double>*)gtab,
+                                                   (Q4<double>*)rtab);
+    else
+        k_tables<float><<<grid, 256, 0, stream>>>(s, st, scale, (Q4<float>*)pack, (Q4<float>*)gtab,
+                                                  (Q4<float>*)rtab);
+    SAD_LAUNCHED();
+}
+
+// ScoreTable<T>::logit (score_table.hpp:48-54), quadratic form, no contraction.
+template <typename T>
+__device__ __forceinline__ T score_logit(const Q4<T>& a, const Q4<T>& b, T px, T py, T s) {
+    T dx = px - a.x, dy = py - a.y;
+    T q = b.x * dx * dx + T(2) * b.y * dx * dy + b.z * dy * dy;
+    if (q < T(0)) q = T(0);
+    T d = tsqrt(q) * s - a.w * s;
+    return -a.z * d;
+}
+
+// ====================================================================== jfa_seed (candidates.cpp:64-84)
+// Site -> cell scatter; a collision keeps the better double logit of the half-packed sites at the
+// cell centre (ties to the lower id).  The winner is a max under a strict total order, so a CAS loop
+// gives the reference's sequential result regardless of arrival order.
+__device__ __forceinline__ double packed_logit_d(const SitesDev& s, uint32_t id, double cx, double cy, double scale) {
+    const int cap = s.cap;
+    const double* p = s.p;
+    double x = half_rt(p[0 * cap + id]), y = half_rt(p[1 * cap + id]);
+    double lt = half_rt(p[2 * cap + id]), r = half_rt(p[3 * cap + id]);
+    double ux = half_rt(p[7 * cap + id]), uy = half_rt(p[8 * cap + id]), an = half_rt(p[9 * cap + id]);
+    double ea = exp(an), ia = exp(-an);
+    double vx = -uy, vy = ux;
+    double gxx = ea * ux * ux + ia * vx * vx;
+    double gxy = ea * ux * uy + ia * vx * vy;
+    double gyy = ea * uy * uy + ia * vy * vy;
+    double dx = cx - x, dy = cy - y;
+    double q = gxx * dx * dx + 2.0 * gxy * dx * dy + gyy * dy * dy;
+    if (q < 0) q = 0;
+    double d = __dsqrt_rn(q) * scale - r * scale;
+    return -exp(lt) * d;
+}
+
+__global__ void k_jfa_seed(SitesDev s, const DevState* __restrict__ st, uint32_t* __restrict__ ids, FieldDims f,
+                           double scale) {
+    int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= st->n_sites || !s.active[id]) return;
+    long long px = llround(s.p[0 * s.cap + id]);
+    long long py = llround(s.p[1 * s.cap + id]);
+    px = px < 0 ? 0 : (px > f.width - 1 ? f.width - 1 : px);
+    py = py < 0 ? 0 : (py > f.height - 1 ? f.height - 1 : py);
+    int gx = static_cast<int>(px) / f.cell, gy = static_cast<int>(py) / f.cell;
+    uint32_t* slot = ids + static_cast<size_t>(f.k) * (static_cast<size_t>(gy) * f.gw + gx);
+    uint32_t cur = atomicCAS(slot, kEmpty, static_cast<uint32_t>(id));
+    if (cur == kEmpty) return;
+    double cx = gx * static_cast<double>(f.cell) + (f.cell - 1) * 0.5;
+    double cy = gy * static_cast<double>(f.cell) + (f.cell - 1) * 0.5;
+    double mine = packed_logit_d(s, id, cx, cy, scale);
+    while (true) {
+        double other = packed_logit_d(s, cur, cx, cy, scale);
+        bool better = mine > other || (mine == other && static_cast<uint32_t>(id) < cur);
+        if (!better) return;
+        uint32_t prev = atomicCAS(slot, cur, static_cast<uint32_t>(id));
+        if (prev == cur) return;
+        cur = prev;
+    }
+}
+
+void launch_jfa_seed(const SitesDev& s, const DevState* st, uint32_t* ids, const FieldDims& f, double scale,
+                     cudaStream_t stream) {
+    cudaMemsetAsync(ids, 0xff, sizeof(uint32_t) * static_cast<size_t>(f.gw) * f.gh * f.k, stream);
+    int grid = (s.cap + 255) / 256;
+    if (grid < 1) grid = 1;
+    k_jfa_seed<<<grid, 256, 0, stream>>>(s, st, ids, f, scale);
+    SAD_LAUNCHED();
+}
+
+// ====================================================================== top-K list in registers
+// TopK<T>::consider (score_table.hpp:67-80) with static register indexing: the position search
+// walks back from n exactly like the reference's while-loop (so even unordered NaN entries behave
+// identically), and the shift is a predicated select chain.
+template <typename T>
+__device__ __forceinline__ bool better(T l, uint32_t c, T L, uint32_t C) {
+    return l > L || (l == L && c < C);
+}
+
+template <typename T, int KM, bool EXACT>
+struct TopKReg {
+    uint32_t id[KM];
+    T lg[KM];
+    int n;
+    int k;  // runtime list length (== KM when EXACT)
+
+    __device__ __forceinline__ void init(int kk) {
+        n = 0;
+        k = EXACT ? KM : kk;
+#pragma unroll
+        for (int i = 0; i < KM; i++) {
+            id[i] = kEmpty;
+            lg[i] = T(0);
+        }
+    }
+    __device__ __forceinline__ bool contains(uint32_t c) const {
+        bool d = false;
+#pragma unroll
+        for (int i = 0; i < KM; i++) d |= (id[i] == c);
+        return d;
+    }
+    // Reject fast when the list is full and (l, c) does not beat the last entry.
+    __device__ __forceinline__ bool full_reject(T l, uint32_t c) const {
+        if (EXACT) return n == KM && !better(l, c, lg[KM - 1], id[KM - 1]);
+        return false;
+    }
+    __device__ __forceinline__ void consider(uint32_t c, T l) {
+        int pos = n;
+        bool run = true;
+#pragma unroll
+        for (int i = KM - 1; i >= 0; i--) {
+            if (i < n) {
+                run = run && better(l, c, lg[i], id[i]);
+                if (run) pos = i;
+            }
+        }
+        if (pos >= k) return;
+#pragma unroll
+        for (int i = KM - 1; i >= 0; i--) {
+            if (i > pos) {
+                if (i < k) {
+                    id[i] = id[i - 1];
+                    lg[i] = lg[i - 1];
+                }
+            } else if (i == pos) {
+                id[i] = c;
+                lg[i] = l;
+            }
+        }
+        if (n < k) n++;
+    }
+};
+
+// ====================================================================== propagate (candidates.cpp:92-141)
+// One thread per candidate cell.  Gathers self + 4 (Axial) or 8 (Box3) neighbour lists at +-step,
+// stopping each at its first sentinel and dropping inactive ids, then `inject` ids drawn from the
+// reference's per-(seed, pass, cell) xorshift stream; keeps the top-K under (logit desc, id asc).
+// Deduplication is streaming: a candidate already in the running list is skipped, which yields
+// the reference's set-based result because the list's K-th key only ever improves.
+template <typename T, int KM, bool EXACT, bool BOX>
+__global__ void __launch_bounds__(256) k_propagate(const uint32_t* __restrict__ prev, uint32_t* __restrict__ next,
+                                                   const Q4<T>* __restrict__ pack, const uint32_t* __restrict__ act,
+                                                   const DevState* __restrict__ st, FieldDims f, int step, int inject,
+                                                   uint64_t seed, uint32_t pass_offset, T s) {
+    const int gx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gy = blockIdx.y * blockDim.y + threadIdx.y;
+    if (gx >= f.gw || gy >= f.gh) return;
+    const int k = EXACT ? KM : f.k;
+    const T cx = static_cast<T>(gx * static_cast<double>(f.cell) + (f.cell - 1) * 0.5);
+    const T cy = static_cast<T>(gy * static_cast<double>(f.cell) + (f.cell - 1) * 0.5);
+    TopKReg<T, KM, EXACT> sel;
+    sel.init(k);
+
+    auto consider = [&](uint32_t c) {
+        if (sel.contains(c)) return;
+        const Q4<T> a = pack[2 * c];
+        const Q4<T> b = pack[2 * c + 1];
+        if (b.w == T(0)) return;  // inactive: dropped on the way in (candidates.cpp:110)
+        T l = score_logit(a, b, cx, cy, s);
+        if (sel.full_reject(l, c)) return;
+        sel.consider(c, l);
+    };
+
+    constexpr int NOFF = BOX ? 9 : 5;
+#pragma unroll 1
+    for (int o = 0; o < NOFF; o++) {
+        // kAxialOff / kBoxOff order (candidates.cpp:88-90)
+        int ox = (o == 1 || o == 5 || o == 6) ? 1 : ((o == 2 || o == 7 || o == 8) ? -1 : 0);
+        int oy = (o == 3 || o == 5 || o == 7) ? 1 : ((o == 4 || o == 6 || o == 8) ? -1 : 0);
+        int nx = gx + ox * step, ny = gy + oy * step;
+        if (nx < 0 || ny < 0 || nx >= f.gw || ny >= f.gh) continue;
+        const uint32_t* lst = prev + static_cast<size_t>(k) * (static_cast<size_t>(ny) * f.gw + nx);
+        if (EXACT && (KM % 4) == 0) {
+            uint32_t v[KM];
+#pragma unroll
+            for (int q = 0; q < KM / 4; q++) {
+                uint4 u = __ldg(reinterpret_cast<const uint4*>(lst) + q);
+                v[4 * q] = u.x;
+                v[4 * q + 1] = u.y;
+                v[4 * q + 2] = u.z;
+                v[4 * q + 3] = u.w;
+            }
+#pragma unroll
+            for (int i = 0; i < KM; i++) {
+                if (v[i] == kEmpty) break;
+                consider(v[i]);
+            }
+        } else {
+            for (int i = 0; i < k; i++) {
+                uint32_t c = __ldg(lst + i);
+                if (c == kEmpty) break;
+                consider(c);
+            }
+        }
+    }
+    const int n_act = st->n_active;
+    if (inject > 0 && n_act > 0) {
+        uint32_t rs = seeded_state(seed, st->pass_index + pass_offset,
+                                   static_cast<uint32_t>(gy) * static_cast<uint32_t>(f.gw) + static_cast<uint32_t>(gx));
+#pragma unroll 1
+        for (int j = 0; j < inject; j++) consider(__ldg(act + xs_next(rs) % static_cast<uint32_t>(n_act)));
+    }
+    uint32_t* out = next + static_cast<size_t>(k) * (static_cast<size_t>(gy) * f.gw + gx);
+    if (EXACT && (KM % 4) == 0) {
+#pragma unroll
+        for (int q = 0; q < KM / 4; q++)
+            reinterpret_cast<uint4*>(out)[q] = make_uint4(sel.id[4 * q], sel.id[4 * q + 1], sel.id[4 * q + 2],
+                                                          sel.id[4 * q + 3]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < KM; i++)
+            if (i < k) out[i] = sel.id[i];
+    }
+}
+
+template <typename T, int KM, bool EXACT>
+static void propagate_t(const uint32_t* prev, uint32_t* next, const void* pack, const uint32_t* act,
+                        const DevState* st, const FieldDims& f, uint32_t step, int box, int inject, uint64_t seed,
+                        uint32_t pass_offset, double scale, cudaStream_t stream) {
+    dim3 block(32, 8);
+    dim3 grid((f.gw + 31) / 32, (f.gh + 7) / 8);
+    if (box)
+        k_propagate<T, KM, EXACT, true><<<grid, block, 0, stream>>>(prev, next, (const Q4<T>*)pack, act, st, f,
+                                                                    (int)step, inject, seed, pass_offset,
+                                                                    static_cast<T>(scale));
+    else
+        k_propagate<T, KM, EXACT, false><<<grid, block, 0, stream>>>(prev, next, (const Q4<T>*)pack, act, st, f,
+                                                                     (int)step, inject, seed, pass_offset,
+                                                                     static_cast<T>(scale));
+    SAD_LAUNCHED();
+}
+
+void launch_propagate(bool fp64, const uint32_t* prev, uint32_t* next, const void* pack, const uint32_t* act,
+                      const DevState* st, const FieldDims& f, uint32_t step, int box, int inject, uint64_t seed,
+                      uint32_t pass_offset, double scale, cudaStream_t stream) {
+    if (f.k == 8) {
+        if (fp64)
+            propagate_t<double, 8, true>(prev, next, pack, act, st, f, step, box, inject, seed, pass_offset, scale,
+                                         stream);
+        else
+            propagate_t<float, 8, true>(prev, next, pack, act, st, f, step, box, inject, seed, pass_offset, scale,
+                                        stream);
+    } else {
+        if (fp64)
+            propagate_t<double, 16, false>(prev, next, pack, act, st, f, step, box, inject, seed, pass_offset, scale,
+                                           stream);
+        else
+            propagate_t<float, 16, false>(prev, next, pack, act, st, f, step, box, inject, seed, pass_offset, scale,
+                                          stream);
+    }
+}
+
+// ====================================================================== exact_topk_batch (candidates.cpp:198-216)
+// Brute-force top-K over the ascending active list under the unpacked ScoreTable<T> (probe-parallel).
+template <typename T>
+__global__ void k_exact_topk(const Q4<T>* __restrict__ rtab, const uint32_t* __restrict__ act, int n_act,
+                             const int32_t* __restrict__ xy, int n_pix, int k, T s, uint32_t* __restrict__ out) {
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n_pix) return;
+    T px = static_cast<T>(static_cast<double>(xy[2 * q])), py = static_cast<T>(static_cast<double>(xy[2 * q + 1]));
+    TopKReg<T, 16, false> sel;
+    sel.init(k);
+    for (int j = 0; j < n_act; j++) {
+        uint32_t id = act[j];
+        sel.consider(id, score_logit(rtab[3 * id], rtab[3 * id + 1], px, py, s));
+    }
+#pragma unroll
+    for (int i = 0; i < 16; i++)
+        if (i < k) out[static_cast<size_t>(q) * k + i] = i < sel.n ? sel.id[i] : kEmpty;
+}
+
+void launch_exact_topk(bool fp64, const void* rtab, const uint32_t* act, int n_act, const int32_t* xy, int n_pix,
+                       int k, double scale, uint32_t* out, cudaStream_t stream) {
+    int grid = (n_pix + 127) / 128;
+    if (grid < 1) grid = 1;
+    if (fp64)
+        k_exact_topk<double><<<grid, 128, 0, stream>>>((const Q4<double>*)rtab, act, n_act, xy, n_pix, k, scale, out);
+    else
+        k_exact_topk<float><<<grid, 128, 0, stream>>>((const Q4<float>*)rtab, act, n_act, xy, n_pix, k,
+                                                      static_cast<float>(scale), out);
+    SAD_LAUNCHED();
+}
+
+// ====================================================================== render (render.cpp:19-89)
+template <typename T, int KM>
+__global__ void __launch_bounds__(256) k_render(const uint32_t* __restrict__ ids, const Q4<T>* __restrict__ rtab,
+                                                FieldDims f, T s, T* __restrict__ out, DevState* st) {
+    const int px = blockIdx.x * blockDim.x + threadIdx.x;
+    const int py = blockIdx.y * blockDim.y + threadIdx.y;
+    if (px >= f.width || py >= f.height) return;
+    const uint32_t* lst = ids + static_cast<size_t>(f.k) * (static_cast<size_t>(py / f.cell) * f.gw + px / f.cell);
+    uint32_t cid[KM];
+    T lg[KM];
+    int n = 0;
+    T best = T(0);
+    const T fx = static_cast<T>(px), fy = static_cast<T>(py);
+#pragma unroll
+    for (int i = 0; i < KM; i++) {
+        cid[i] = 0;
+        lg[i] = T(0);
+    }
+#pragma unroll
+    for (int i = 0; i < KM; i++) {
+        if (i >= f.k) break;
+        uint32_t id = lst[i];
+        if (id == kEmpty) break;
+        Q4<T> a = rtab[3 * id], b = rtab[3 * id + 1];
+        if (b.w == T(0)) continue;
+        T l = score_logit(a, b, fx, fy, s);
+        if (!tfinite(l)) continue;
+#pragma unroll
+        for (int j = 0; j < KM; j++)
+            if (j == n) {
+                cid[j] = id;
+                lg[j] = l;
+            }
+        if (n == 0 || l > best) best = l;
+        n++;
+    }
+    T* o = out + 3 * (static_cast<size_t>(py) * f.width + px);
+    if (n == 0) {
+        atomicOr(&st->err, 1);
+        return;
+    }
+    T w[KM];
+    T sum = T(0);
+#pragma unroll
+    for (int i = 0; i < KM; i++)
+        if (i < n) {
+            w[i] = texp(lg[i] - best);
+            sum += w[i];
+        }
+    T inv = T(1) / sum;
+    T r = T(0), g = T(0), b = T(0);
+#pragma unroll
+    for (int i = 0; i < KM; i++)
+        if (i < n) {
+            T wi = w[i] * inv;
+            Q4<T> c = rtab[3 * cid[i] + 2];
+            r += wi * c.x;
+            g += wi * c.y;
+            b += wi * c.z;
+        }
+    o[0] = r;
+    o[1] = g;
+    o[2] = b;
+}
+
+void launch_render(bool fp64, const uint32_t* ids, const void* rtab, const FieldDims& f, double scale, void* out,
+                   DevState* st, cudaStream_t stream) {
+    dim3 block(32, 8), grid((f.width + 31) / 32, (f.height + 7) / 8);
+    if (fp64) {
+        if (f.k <= 8)
+            k_render<double, 8><<<grid, block, 0, stream>>>(ids, (const Q4<double>*)rtab, f, scale, (double*)out, st);
+        else
+            k_render<double, 16><<<grid, block, 0, stream>>>(ids, (const Q4<double>*)rtab, f, scale, (double*)out, st);
+    } else {
+        if (f.k <= 8)
+            k_render<float, 8><<<grid, block, 0, stream>>>(ids, (const Q4<float>*)rtab, f, static_cast<float>(scale),
+                                                           (float*)out, st);
+        else
+            k_render<float, 16><<<grid, block, 0, stream>>>(ids, (const Q4<float>*)rtab, f, static_cast<float>(scale),
+                                                            (float*)out, st);
+    }
+    SAD_LAUNCHED();
+}
+
+// render_id_map (render.cpp:118-154): double ScoreTable argmax, ties to the lower id.
+__global__ void k_id_map(const uint32_t* __restrict__ ids, const Q4<double>* __restrict__ rtab, FieldDims f, double s,
+                         uint32_t* __restrict__ out, DevState* st) {
+    const int px = blockIdx.x * blockDim.x + threadIdx.x;
+    const int py = blockIdx.y * blockDim.y + threadIdx.y;
+    if (px >= f.width || py >= f.height) return;
+    const uint32_t* lst = ids + static_cast<size_t>(f.k) * (static_cast<size_t>(py / f.cell) * f.gw + px / f.cell);
+    uint32_t best = kEmpty;
+    double bl = 0;
+    for (int i = 0; i < f.k; i++) {
+        uint32_t id = lst[i];
+        if (id == kEmpty) break;
+        Q4<double> a = rtab[3 * id], b = rtab[3 * id + 1];
+        if (b.w == 0.0) continue;
+        double l = score_logit(a, b, static_cast<double>(px), static_cast<double>(py), s);
+        if (best == kEmpty || l > bl || (l == bl && id < best)) {
+            best = id;
+            bl = l;
+        }
+    }
+    out[static_cast<size_t>(py) * f.width + px] = best;
+    if (best == kEmpty) atomicOr(&st->err, 1);
+}
+
+void launch_id_map(const uint32_t* ids, const void* rtab_d, const FieldDims& f, double scale, uint32_t* out,
+                   DevState* st, cudaStream_t stream) {
+    dim3 block(32, 8), grid((f.width + 31) / 32, (f.height + 7) / 8);
+    k_id_map<<<grid, block, 0, stream>>>(ids, (const Q4<double>*)rtab_d, f, scale, out, st);
+    SAD_LAUNCHED();
+}
+
+// pixel_weights (render.cpp:93-105), batched point queries against a cached double table.
+__global__ void k_pixel_weights(const uint32_t* __restrict__ ids, const Q4<double>* __restrict__ rtab, FieldDims f,
+                                double s, const int32_t* __restrict__ xy, int n_q, uint32_t* __restrict__ oid,
+                                double* __restrict__ ow, int32_t* __restrict__ on) {
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n_q) return;
+    int px = xy[2 * q], py = xy[2 * q + 1];
+    uint32_t cid[16];
+    double lg[16];
+    int n = 0;
+    double best = 0;
+    if (px >= 0 && py >= 0 && px < f.width && py < f.height) {
+        const uint32_t* lst = ids + static_cast<size_t>(f.k) * (static_cast<size_t>(py / f.cell) * f.gw + px / f.cell);
+        for (int i = 0; i < f.k; i++) {
+            uint32_t id = lst[i];
+            if (id == kEmpty) break;
+            Q4<double> a = rtab[3 * id], b = rtab[3 * id + 1];
+            if (b.w == 0.0) continue;
+            double l = score_logit(a, b, static_cast<double>(px), static_cast<double>(py), s);
+            if (!isfinite(l)) continue;
+            cid[n] = id;
+            lg[n] = l;
+            if (n == 0 || l > best) best = l;
+            n++;
+        }
+    }
+    double w[16], sum = 0;
+    for (int i = 0; i < n; i++) {
+        w[i] = exp(lg[i] - best);
+        sum += w[i];
+    }
+    double inv = 1.0 / sum;
+    for (int i = 0; i < 16; i++) {
+        oid[16 * q + i] = i < n ? cid[i] : kEmpty;
+        ow[16 * q + i] = i < n ? w[i] * inv : 0.0;
+    }
+    on[q] = n;
+}
+
+void launch_pixel_weights(const uint32_t* ids, const void* rtab_d, const FieldDims& f, double scale, const int32_t* xy,
+                          int n_q, uint32_t* out_ids, double* out_w, int32_t* out_n, cudaStream_t stream) {
+    int grid = (n_q + 127) / 128;
+    if (grid < 1) grid = 1;
+    k_pixel_weights<<<grid, 128, 0, stream>>>(ids, (const Q4<double>*)rtab_d, f, scale, xy, n_q, out_ids, out_w,
+                                              out_n);
+    SAD_LAUNCHED();
+}
+
+// ====================================================================== tile reduction (grad.cpp:10-64)
+// The reference reduces per-(site, channel) contributions of a 16x16 tile in a 256-slot hash table
+// of compensated accumulators, then merges per worker; every sum is double-double, so the result is
+// the exactly-rounded total independent of grouping.  Here a block owns a TW x TH pixel tile:
+//   1. each thread computes its pixel's per-candidate contributions into shared memory;
+//   2. site ids are hashed into a shared table and compacted to local indices;
+//   3. entries are bucketed per local site (counting sort);
+//   4. one thread per (site, channel) sums its bucket in double-double and merges it into the
+//      global (hi, lo) accumulator with one 128-bit CAS.
+// Global traffic is one atomic per (site, channel, tile) instead of one per (pixel, candidate).
+template <typename CT, int NCH, int TPX, int KM>
+struct TileRed {
+    static constexpr int E = TPX * KM;   // entries per tile
+    static constexpr int HT = E;         // hash slots (load factor <= 1)
+    static constexpr int ES = E + 1;     // padded row stride: channel rows land on distinct banks
+    CT c[NCH * ES];
+    uint32_t key[E];
+    uint32_t hkey[HT];
+    uint16_t local_of_entry[E];
+    uint16_t local_of_slot[HT];
+    uint32_t cnt[E];
+    uint32_t start[E];
+    uint32_t fill[E];
+    uint16_t order[E];
+    uint32_t site_of_local[E];
+    int n_local;
+    DD warp_part[TPX / 32];
+};
+
+template <typename CT, int NCH, int TPX, int KM>
+__device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, double2* __restrict__ out, int cap) {
+    using R = TileRed<CT, NCH, TPX, KM>;
+    const int tid = threadIdx.x;
+    // 2. hash insert (site ids are < 2^31; table keys start as kEmpty)
+    for (int e = tid; e < R::E; e += TPX) {
+        uint32_t key = sm.key[e];
+        if (key == kEmpty) continue;
+        uint32_t h = (key * 2654435761u) & (R::HT - 1);
+        while (true) {
+            uint32_t prev = atomicCAS(&sm.hkey[h], kEmpty, key);
+            if (prev == kEmpty || prev == key) break;
+            h = (h + 1) & (R::HT - 1);
+        }
+        sm.local_of_entry[e] = static_cast<uint16_t>(h);
+    }
+    __syncthreads();
+    for (int h = tid; h < R::HT; h += TPX) {
+        uint32_t key = sm.hkey[h];
+        if (key != kEmpty) {
+            int loc = atomicAdd(&sm.n_local, 1);
+            sm.local_of_slot[h] = static_cast<uint16_t>(loc);
+            sm.site_of_local[loc] = key;
+        }
+    }
+    __syncthreads();
+    const int U = sm.n_local;
+    for (int u = tid; u < U; u += TPX) {
+        sm.cnt[u] = 0;
+        sm.fill[u] = 0;
+    }
+    __syncthreads();
+    // 3. bucket counts
+    for (int e = tid; e < R::E; e += TPX) {
+        if (sm.key[e] == kEmpty) continue;
+        uint16_t loc = sm.local_of_slot[sm.local_of_entry[e]];
+        sm.local_of_entry[e] = loc;
+        atomicAdd(&sm.cnt[loc], 1u);
+    }
+    __syncthreads();
+    // exclusive scan of cnt[0..U) by warp 0 (U <= E)
+    if (tid < 32) {
+        int carry = 0;
+        for (int base = 0; base < U; base += 32) {
+            int u = base + tid;
+            int v = u < U ? sm.cnt[u] : 0;
+            int x = v;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                int y = __shfl_up_sync(0xffffffffu, x, d);
+                if (tid >= d) x += y;
+            }
+            if (u < U) sm.start[u] = static_cast<uint32_t>(carry + x - v);
+            carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < R::E; e += TPX) {
+        if (sm.key[e] == kEmpty) continue;
+        int loc = sm.local_of_entry[e];
+        int pos = static_cast<int>(sm.start[loc] + atomicAdd(&sm.fill[loc], 1u));
+        sm.order[pos] = static_cast<uint16_t>(e);
+    }
+    __syncthreads();
+    // 4. per (site, channel) compensated sums -> one 128-bit CAS each
+    for (int item = tid; item < U * NCH; item += TPX) {
+        int u = item / NCH, ch = item - u * NCH;
+        int b = static_cast<int>(sm.start[u]), n = static_cast<int>(sm.cnt[u]);
+        DD acc{0.0, 0.0};
+        const CT* row = sm.c + ch * R::ES;
+        for (int j = 0; j < n; j++) dd_add(acc, static_cast<double>(row[sm.order[b + j]]));
+        dd_atomic_merge(out + static_cast<size_t>(ch) * cap + sm.site_of_local[u], acc);
+    }
+}
+
+template <typename CT, int NCH, int TPX, int KM>
+__device__ __forceinline__ void tile_init(TileRed<CT, NCH, TPX, KM>& sm) {
+    using R = TileRed<CT, NCH, TPX, KM>;
+    for (int h = threadIdx.x; h < R::HT; h += TPX) sm.hkey[h] = kEmpty;
+    if (threadIdx.x == 0) sm.n_local = 0;
+}
+
+// Block-wide compensated reduction of one DD per thread, merged into `dst`.
+template <int TPX>
+__device__ __forceinline__ void block_dd_merge(DD v, DD* warp_part, double2* dst) {
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+        DD o{__shfl_down_sync(0xffffffffu, v.hi, d), __shfl_down_sync(0xffffffffu, v.lo, d)};
+        dd_merge(v, o);
+    }
+    if ((threadIdx.x & 31) == 0) warp_part[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        DD t = warp_part[0];
+        for (int w = 1; w < TPX / 32; w++) dd_merge(t, warp_part[w]);
+        if (t.hi != 0.0 || t.lo != 0.0) dd_atomic_merge(dst, t);
+    }
+}
+
+template <int TPX>
+__device__ __forceinline__ unsigned long long block_sum_u64(unsigned long long v, unsigned long long* sm_tmp) {
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) v += __shfl_down_sync(0xffffffffu, v, d);
+    if ((threadIdx.x & 31) == 0) sm_tmp[threadIdx.x >> 5] = v;
+    __syncthreads();
+    unsigned long long t = 0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < TPX / 32; w++) t += sm_tmp[w];
+    return t;
+}
+
+// ====================================================================== fused forward + backward
+// pixel_pass (grad.cpp:117-240) per pixel, tile reduction as above, loss as a compensated sum.
+// MODE 0: MSE vs target, no removal (the fit's call, train.cpp:249); 1: with removal delta;
+// 2: caller-supplied dL/dvalue (backward_pixel_grad, grad.cpp:382-390).
+template <typename T> struct BwdTile;
+template <> struct BwdTile<float> { static constexpr int TW = 16, TH = 8; };
+template <> struct BwdTile<double> { static constexpr int TW = 8, TH = 8; };
+
+template <typename T, int KM, int MODE>
+__global__ void __launch_bounds__(BwdTile<T>::TW * BwdTile<T>::TH)
+    k_backward(const uint32_t* __restrict__ ids, const Q4<T>* __restrict__ gtab, const T* __restrict__ tgt, FieldDims f,
+               T s, T inv_hw2, double2* __restrict__ grads, int cap, DevState* st) {
+    constexpr int TW = BwdTile<T>::TW, TH = BwdTile<T>::TH, TPX = TW * TH;
+    constexpr int NCH = MODE == 1 ? 11 : 10;
+    using Red = TileRed<T, NCH, TPX, KM>;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    Red& sm = *reinterpret_cast<Red*>(smraw);
+    tile_init(sm);
+
+    const int tid = threadIdx.x;
+    const int px = blockIdx.x * TW + (tid % TW);
+    const int py = blockIdx.y * TH + (tid / TW);
+    const bool inside = px < f.width && py < f.height;
+    constexpr T kTiny = sizeof(T) == 8 ? T(1e-18) : T(1e-12);
+
+    uint32_t cid[KM];
+    T dxs[KM], dys[KM], ud[KM], vd[KM], nrm[KM], lg[KM];
+    int n = 0;
+    T best = T(0);
+#pragma unroll
+    for (int i = 0; i < KM; i++) {
+        cid[i] = kEmpty;
+        dxs[i] = dys[i] = ud[i] = vd[i] = nrm[i] = lg[i] = T(0);
+    }
+    unsigned long long nonfinite = 0;
+    DD loss{0.0, 0.0};
+    if (inside) {
+        const uint32_t* lst = ids + static_cast<size_t>(f.k) * (static_cast<size_t>(py / f.cell) * f.gw + px / f.cell);
+        const T fx = static_cast<T>(px), fy = static_cast<T>(py);
+#pragma unroll
+        for (int i = 0; i < KM; i++) {
+            if (i >= f.k) break;
+            uint32_t id = lst[i];
+            if (id == kEmpty) break;
+            const Q4<T> a = gtab[3 * id], b = gtab[3 * id + 1];
+            const T act = gtab[3 * id + 2].w;
+            if (act == T(0)) continue;
+            T dx = fx - a.x, dy = fy - a.y;
+            T pa = b.z * dx + b.w * dy;
+            T pb = b.z * dy - b.w * dx;
+            T q = b.x * pa * pa + b.y * pb * pb;
+            if (q < T(0)) q = T(0);
+            T m = tsqrt(q);
+            T l = -a.z * (m * s - a.w * s);
+            if (!tfinite(l)) continue;
+#pragma unroll
+            for (int j = 0; j < KM; j++)
+                if (j == n) {
+                    cid[j] = id;
+                    dxs[j] = dx;
+                    dys[j] = dy;
+                    ud[j] = pa;
+                    vd[j] = pb;
+                    nrm[j] = m;
+                    lg[j] = l;
+                }
+            if (n == 0 || l > best) best = l;
+            n++;
+        }
+        if (n == 0) atomicOr(&st->err, 1);
+    }
+    if (n > 0) {
+        T w[KM];
+        T wsum = T(0);
+#pragma unroll
+        for (int i = 0; i < KM; i++)
+            if (i < n) {
+                w[i] = texp(lg[i] - best);
+                wsum += w[i];
+            }
+        T invw = T(1) / wsum;
+#pragma unroll
+        for (int i = 0; i < KM; i++)
+            if (i < n) w[i] *= invw;
+        T ch0 = T(0), ch1 = T(0), ch2 = T(0);
+#pragma unroll
+        for (int i = 0; i < KM; i++)
+            if (i < n) {
+                const Q4<T> c = gtab[3 * cid[i] + 2];
+                ch0 += w[i] * c.x;
+                ch1 += w[i] * c.y;
+                ch2 += w[i] * c.z;
+            }
+        T g0, g1, g2, t0 = T(0), t1 = T(0), t2 = T(0), pl = T(0);
+        const T* tp = tgt + 3 * (static_cast<size_t>(py) * f.width + px);
+        if (MODE != 2) {
+            t0 = tp[0];
+            t1 = tp[1];
+            t2 = tp[2];
+            T e0 = ch0 - t0, e1 = ch1 - t1, e2 = ch2 - t2;
+            pl = e0 * e0 + e1 * e1 + e2 * e2;
+            double plv = static_cast<double>(pl);
+            if (!isfinite(plv)) {
+                nonfinite++;
+                plv = 0;
+            }
+            dd_add(loss, plv);
+            g0 = inv_hw2 * e0;
+            g1 = inv_hw2 * e1;
+            g2 = inv_hw2 * e2;
+        } else {
+            g0 = tp[0];
+            g1 = tp[1];
+            g2 = tp[2];
+        }
+#pragma unroll
+        for (int i = 0; i < KM; i++) {
+            if (i >= n) break;
+            const uint32_t id = cid[i];
+            const Q4<T> a = gtab[3 * id], b = gtab[3 * id + 1], c = gtab[3 * id + 2];
+            T dc0 = c.x - ch0, dc1 = c.y - ch1, dc2 = c.z - ch2;
+            T A = w[i] * (g0 * dc0 + g1 * dc1 + g2 * dc2);
+            T ts = a.z * s;
+            T v[11];
+            v[4] = w[i] * g0;
+            v[5] = w[i] * g1;
+            v[6] = w[i] * g2;
+            v[2] = A * lg[i];
+            v[3] = A * ts;
+            if (nrm[i] > kTiny) {
+                T inv_n = T(1) / nrm[i];
+                T eau = b.x * ud[i];
+                T iav = b.y * vd[i];
+                T coef = A * ts * inv_n;
+                v[0] = coef * (eau * b.z - iav * b.w);
+                v[1] = coef * (eau * b.w + iav * b.z);
+                v[7] = -coef * (eau * dxs[i] + iav * dys[i]);
+                v[8] = -coef * (eau * dys[i] - iav * dxs[i]);
+                v[9] = -A * ts * T(0.5) * inv_n * (eau * ud[i] - iav * vd[i]);
+            } else {
+                v[0] = v[1] = v[7] = v[8] = v[9] = T(0);
+            }
+            if (MODE == 1) {
+                if (w[i] >= T(1) - T(1e-6)) {
+                    v[10] = static_cast<T>(1e6);
+                } else {
+                    T inv_rest = T(1) / (T(1) - w[i]);
+                    T r0 = (ch0 - w[i] * c.x) * inv_rest - t0;
+                    T r1 = (ch1 - w[i] * c.y) * inv_rest - t1;
+                    T r2 = (ch2 - w[i] * c.z) * inv_rest - t2;
+                    v[10] = r0 * r0 + r1 * r1 + r2 * r2 - pl;
+                }
+            }
+            const int e = i * TPX + tid;
+            sm.key[e] = id;
+#pragma unroll
+            for (int t = 0; t < NCH; t++) {
+                T x = v[t];
+                if (!tfinite(x)) {
+                    x = T(0);
+                    nonfinite++;
+                }
+                sm.c[t * Red::ES + e] = x;
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < KM; i++)
+        if (i >= n) sm.key[i * TPX + tid] = kEmpty;
+    __syncthreads();
+    tile_reduce(sm, grads, cap);
+    __syncthreads();
+    if (MODE != 2) block_dd_merge<TPX>(loss, sm.warp_part, &st->loss);
+    __syncthreads();
+    unsigned long long nf = block_sum_u64<TPX>(nonfinite, reinterpret_cast<unsigned long long*>(sm.warp_part));
+    if (threadIdx.x == 0 && nf) atomicAdd(reinterpret_cast<unsigned long long*>(&st->nonfinite), nf);
+}
+
+template <typename T, int KM, int MODE>
+static void backward_t(const uint32_t* ids, const void* gtab, const void* tgt, const FieldDims& f, double scale,
+                       double2* grads, int cap, DevState* st, cudaStream_t stream) {
+    constexpr int TW = BwdTile<T>::TW, TH = BwdTile<T>::TH;
+    constexpr int NCH = MODE == 1 ? 11 : 10;
+    size_t smem = sizeof(TileRed<T, NCH, TW * TH, KM>);
+    auto kern = k_backward<T, KM, MODE>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    dim3 grid((f.width + TW - 1) / TW, (f.height + TH - 1) / TH);
+    T inv_hw2 = static_cast<T>(2.0 / (static_cast<double>(f.width) * f.height));
+    kern<<<grid, TW * TH, smem, stream>>>(ids, (const Q4<T>*)gtab, (const T*)tgt, f, static_cast<T>(scale), inv_hw2,
+                                          grads, cap, st);
+    SAD_LAUNCHED();
+}
+
+void launch_backward(bool fp64, int mode, const uint32_t* ids, const void* gtab, const void* tgt, const FieldDims& f,
+                     double scale, double2* grads, int cap, DevState* st, cudaStream_t stream) {
+#define SAD_BWD(T, KM)                                                                           \
+    do {                                                                                         \
+        if (mode == 0) backward_t<T, KM, 0>(ids, gtab, tgt, f, scale, grads, cap, st, stream);  \
+        else if (mode == 1) backward_t<T, KM, 1>(ids, gtab, tgt, f, scale, grads, cap, st, stream); \
+        else backward_t<T, KM, 2>(ids, gtab, tgt, f, scale, grads, cap, st, stream);            \
+    } while (0)
+    if (fp64) {
+        if (f.k <= 8) SAD_BWD(double, 8);
+        else SAD_BWD(double, 16);
+    } else {
+        if (f.k <= 8) SAD_BWD(float, 8);
+        else SAD_BWD(float, 16);
+    }
+#undef SAD_BWD
+}
+
+// ====================================================================== image_loss (grad.cpp:291-360)
+template <typename T, int KM>
+__global__ void __launch_bounds__(128) k_loss(const uint32_t* __restrict__ ids, const Q4<T>* __restrict__ gtab,
+                                              const T* __restrict__ tgt, FieldDims f, T s, DevState* st) {
+    __shared__ DD parts[4];
+    const int tid = threadIdx.x;
+    const int px = blockIdx.x * 16 + (tid % 16);
+    const int py = blockIdx.y * 8 + (tid / 16);
+    DD loss{0.0, 0.0};
+    if (px < f.width && py < f.height) {
+        const uint32_t* lst = ids + static_cast<size_t>(f.k) * (static_cast<size_t>(py / f.cell) * f.gw + px / f.cell);
+        uint32_t cid[KM];
+        T lg[KM];
+        int n = 0;
+        T best = T(0);
+        const T fx = static_cast<T>(px), fy = static_cast<T>(py);
+#pragma unroll
+        for (int i = 0; i < KM; i++) {
+            cid[i] = 0;
+            lg[i] = T(0);
+        }
+#pragma unroll
+        for (int i = 0; i < KM; i++) {
+            if (i >= f.k) break;
+            uint32_t id = lst[i];
+            if (id == kEmpty) break;
+            const Q4<T> a = gtab[3 * id], b = gtab[3 * id + 1];
+            if (gtab[3 * id + 2].w == T(0)) continue;
+            T dx = fx - a.x, dy = fy - a.y;
+            T pa = b.z * dx + b.w * dy;
+            T pb = b.z * dy - b.w * dx;
+            T q = b.x * pa * pa + b.y * pb * pb;
+            if (q < T(0)) q = T(0);
+            T m = tsqrt(q);
+            T l = -a.z * (m * s - a.w * s);
+            if (!tfinite(l)) continue;
+#pragma unroll
+            for (int j = 0; j < KM; j++)
+                if (j == n) {
+                    cid[j] = id;
+                    lg[j] = l;
+                }
+            if (n == 0 || l > best) best = l;
+            n++;
+        }
+        if (n == 0) {
+            atomicOr(&st->err, 1);
+        } else {
+            T w[KM];
+            T wsum = T(0);
+#pragma unroll
+            for (int i = 0; i < KM; i++)
+                if (i < n) {
+                    w[i] = texp(lg[i] - best);
+                    wsum += w[i];
+                }
+            T invw = T(1) / wsum;
+            T c0 = T(0), c1 = T(0), c2 = T(0);
+#pragma unroll
+            for (int i = 0; i < KM; i++)
+                if (i < n) {
+                    T wi = w[i] * invw;
+                    const Q4<T> c = gtab[3 * cid[i] + 2];
+                    c0 += wi * c.x;
+                    c1 += wi * c.y;
+                    c2 += wi * c.z;
+                }
+            const T* tp = tgt + 3 * (static_cast<size_t>(py) * f.width + px);
+            T e0 = c0 - tp[0], e1 = c1 - tp[1], e2 = c2 - tp[2];
+            double pl = static_cast<double>(e0 * e0 + e1 * e1 + e2 * e2);
+            if (isfinite(pl)) dd_add(loss, pl);
+        }
+    }
+    block_dd_merge<128>(loss, parts, &st->loss);
+}
+
+void launch_loss(bool fp64, const uint32_t* ids, const void* gtab, const void* tgt, const FieldDims& f, double scale,
+                 DevState* st, cudaStream_t stream) {
+    dim3 grid((f.width + 15) / 16, (f.height + 7) / 8);
+    if (fp64) {
+        if (f.k <= 8) k_loss<double, 8><<<grid, 128, 0, stream>>>(ids, (const Q4<double>*)gtab, (const double*)tgt, f, scale, st);
+        else k_loss<double, 16><<<grid, 128, 0, stream>>>(ids, (const Q4<double>*)gtab, (const double*)tgt, f, scale, st);
+    } else {
+        float s = static_cast<float>(scale);
+        if (f.k <= 8) k_loss<float, 8><<<grid, 128, 0, stream>>>(ids, (const Q4<float>*)gtab, (const float*)tgt, f, s, st);
+        else k_loss<float, 16><<<grid, 128, 0, stream>>>(ids, (const Q4<float>*)gtab, (const float*)tgt, f, s, st);
+    }
+    SAD_LAUNCHED();
+}
+
+// ====================================================================== accumulate_stats (budget.cpp:39-155)
+// Always double, unpacked ScoreTable logits; 8 channels per (pixel, candidate), same tile contract.
+template <int KM>
+__global__ void __launch_bounds__(64) k_stats(const uint32_t* __restrict__ ids, const Q4<double>* __restrict__ rtab,
+                                             const double* __restrict__ tgt, FieldDims f, double s,
+                                             double2* __restrict__ stats, int cap, DevState* st) {
+    constexpr int TW = 8, TH = 8, TPX = 64, NCH = 8;
+    using Red = TileRed<double, NCH, TPX, KM>;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    Red& sm = *reinterpret_cast<Red*>(smraw);
+    tile_init(sm);
+    const int tid = threadIdx.x;
+    const int px = blockIdx.x * TW + (tid % TW);
+    const int py = blockIdx.y * TH + (tid / TW);
+    int n = 0;
+    uint32_t cid[KM];
+    double lg[KM];
+#pragma unroll
+    for (int i = 0; i < KM; i++) {
+        cid[i] = kEmpty;
+        lg[i] = 0;
+    }
+    double best = 0;
+    if (px < f.width && py < f.height) {
+        const uint32_t* lst = ids + static_cast<size_t>(f.k) * (static_cast<size_t>(py / f.cell) * f.gw + px / f.cell);
+#pragma unroll
+        for (int i = 0; i < KM; i++) {
+            if (i >= f.k) break;
+            uint32_t id = lst[i];
+            if (id == kEmpty) break;
+            const Q4<double> a = rtab[3 * id], b = rtab[3 * id + 1];
+            if (b.w == 0.0) continue;
+            double l = score_logit(a, b, static_cast<double>(px), static_cast<double>(py), s);
+            if (!isfinite(l)) continue;
+#pragma unroll
+            for (int j = 0; j < KM; j++)
+                if (j == n) {
+                    cid[j] = id;
+                    lg[j] = l;
+                }
+            if (n == 0 || l > best) best = l;
+            n++;
+        }
+    }
+    if (n > 0) {
+        double w[KM];
+        double wsum = 0;
+#pragma unroll
+        for (int i = 0; i < KM; i++)
+            if (i < n) {
+                w[i] = exp(lg[i] - best);
+                wsum += w[i];
+            }
+        double invw = 1.0 / wsum;
+        double ch0 = 0, ch1 = 0, ch2 = 0;
+#pragma unroll
+        for (int i = 0; i < KM; i++)
+            if (i < n) {
+                w[i] *= invw;
+                const Q4<double> c = rtab[3 * cid[i] + 2];
+                ch0 += w[i] * c.x;
+                ch1 += w[i] * c.y;
+                ch2 += w[i] * c.z;
+            }
+        const double* tp = tgt + 3 * (static_cast<size_t>(py) * f.width + px);
+        double e0 = ch0 - tp[0], e1 = ch1 - tp[1], e2 = ch2 - tp[2];
+        double r2 = e0 * e0 + e1 * e1 + e2 * e2;
+        double fx = px, fy = py;
+#pragma unroll
+        for (int i = 0; i < KM; i++) {
+            if (i >= n) break;
+            const Q4<double> c = rtab[3 * cid[i] + 2];
+            double rho = w[i] * r2;
+            double v[8];
+            v[0] = w[i];
+            v[1] = rho;
+            v[2] = rho * fx;
+            v[3] = rho * fy;
+            v[4] = rho * fx * fx;
+            v[5] = rho * fx * fy;
+            v[6] = rho * fy * fy;
+            if (w[i] >= 1.0 - 1e-6) {
+                v[7] = 1e6;
+            } else {
+                double ir = 1.0 / (1.0 - w[i]);
+                double r0 = (ch0 - w[i] * c.x) * ir - tp[0];
+                double r1 = (ch1 - w[i] * c.y) * ir - tp[1];
+                double rk = (ch2 - w[i] * c.z) * ir - tp[2];
+                v[7] = r0 * r0 + r1 * r1 + rk * rk - r2;
+            }
+            const int e = i * TPX + tid;
+            sm.key[e] = cid[i];
+#pragma unroll
+            for (int t = 0; t < NCH; t++) sm.c[t * Red::ES + e] = isfinite(v[t]) ? v[t] : 0.0;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < KM; i++)
+        if (i >= n) sm.key[i * TPX + tid] = kEmpty;
+    __syncthreads();
+    tile_reduce(sm, stats, cap);
+    __syncthreads();
+    unsigned long long v = block_sum_u64<TPX>(n > 0 ? 1ull : 0ull, reinterpret_cast<unsigned long long*>(sm.warp_part));
+    if (threadIdx.x == 0 && v) atomicAdd(reinterpret_cast<unsigned long long*>(&st->valid), v);
+}
+
+void launch_stats(const uint32_t* ids, const void* rtab_d, const double* tgt, const FieldDims& f, double scale,
+                  double2* stats, int cap, DevState* st, cudaStream_t stream) {
+    dim3 grid((f.width + 7) / 8, (f.height + 7) / 8);
+    if (f.k <= 8) {
+        size_t smem = sizeof(TileRed<double, 8, 64, 8>);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_stats<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr = true;
+        }
+        k_stats<8><<<grid, 64, smem, stream>>>(ids, (const Q4<double>*)rtab_d, tgt, f, scale, stats, cap, st);
+    } else {
+        size_t smem = sizeof(TileRed<double, 8, 64, 16>);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_stats<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr = true;
+        }
+        k_stats<16><<<grid, 64, smem, stream>>>(ids, (const Q4<double>*)rtab_d, tgt, f, scale, stats, cap, st);
+    }
+    SAD_LAUNCHED();
+}
+
+// ====================================================================== adam_step + clamp_project (train.cpp:113-169)
+// Per-site thread, bit-exact double arithmetic in the reference order; bias corrections come from
+// the host (glibc pow) through `bc`.  Optionally zeroes the gradient accumulators for the next
+// iteration and rebuilds this site's candidate snapshot and backward table (the only consumers of
+// the new parameters before the next event), which removes two table-build launches per iteration.
+__device__ __forceinline__ void clamp_site(double* p, int cap, int id, const AdamHyper& hp) {
+    double x = p[0 * cap + id], y = p[1 * cap + id];
+    p[0 * cap + id] = smin(smax(x, 0.0), hp.width - 1.0);
+    p[1 * cap + id] = smin(smax(y, 0.0), hp.height - 1.0);
+    p[2 * cap + id] = smin(smax(p[2 * cap + id], hp.log_tau_min), hp.log_tau_max);
+    p[3 * cap + id] = smin(smax(p[3 * cap + id], hp.radius_min), hp.radius_max);
+    p[9 * cap + id] = smin(smax(p[9 * cap + id], hp.aniso_min), hp.aniso_max);
+    if (hp.clamp_color) {
+        p[4 * cap + id] = smin(smax(p[4 * cap + id], 0.0), 1.0);
+        p[5 * cap + id] = smin(smax(p[5 * cap + id], 0.0), 1.0);
+        p[6 * cap + id] = smin(smax(p[6 * cap + id], 0.0), 1.0);
+    }
+    double nx = p[7 * cap + id], ny = p[8 * cap + id];
+    double norm = __dsqrt_rn(nx * nx + ny * ny);
+    if (!(norm > 1e-12) || !isfinite(norm)) {
+        p[7 * cap + id] = 1.0;
+        p[8 * cap + id] = 0.0;
+    } else {
+        p[7 * cap + id] = nx / norm;
+        p[8 * cap + id] = ny / norm;
+    }
+}
+
+template <typename T>
+__global__ void k_adam(SitesDev s, DevState* st, double2* __restrict__ grads, double* __restrict__ m,
+                       double* __restrict__ v, AdamHyper hp, const double2* __restrict__ bc_table, double2 bc_now,
+                       int zero_grads, double scale, Q4<T>* pack, Q4<T>* gtab) {
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    const int cap = s.cap;
+    unsigned long long skipped = 0;
+    if (id < st->n_sites) {
+        double2 bc = bc_table ? bc_table[st->t + 1] : bc_now;
+        if (s.active[id] && !s.frozen[id]) {
+#pragma unroll
+            for (int k = 0; k < 10; k++) {
+                double2 g = grads[static_cast<size_t>(k) * cap + id];
+                double gv = g.x + g.y;
+                if (!isfinite(gv)) {
+                    skipped++;
+                    continue;
+                }
+                size_t mi = static_cast<size_t>(k) * cap + id;
+                double mm = hp.beta1 * m[mi] + (1.0 - hp.beta1) * gv;
+                double vv = hp.beta2 * v[mi] + (1.0 - hp.beta2) * gv * gv;
+                m[mi] = mm;
+                v[mi] = vv;
+                s.p[mi] -= hp.lr[k] * (mm / bc.x) / (__dsqrt_rn(vv / bc.y) + hp.eps);
+            }
+            clamp_site(s.p, cap, id, hp);
+        }
+        if (zero_grads) {
+#pragma unroll
+            for (int k = 0; k < 11; k++) grads[static_cast<size_t>(k) * cap + id] = make_double2(0.0, 0.0);
+        }
+    }
+    if (skipped) atomicAdd(reinterpret_cast<unsigned long long*>(&st->skipped), skipped);
+    if (id < st->n_sites && (pack || gtab)) {
+        // same derivations as k_tables (score_table.hpp:20-46, grad.cpp:84-110)
+        const double* p = s.p;
+        bool act = s.active[id] != 0;
+        double x = p[0 * cap + id], y = p[1 * cap + id], lt = p[2 * cap + id], r = p[3 * cap + id];
+        double ux = p[7 * cap + id], uy = p[8 * cap + id], an = p[9 * cap + id];
+        if (pack) {
+            Q4<T> a, b;
+            if (!act) {
+                a = {T(0), T(0), T(0), T(0)};
+                b = {T(1), T(0), T(1), T(0)};
+            } else {
+                double hx = half_rt(x), hy = half_rt(y), hlt = half_rt(lt), hr = half_rt(r);
+                double hux = half_rt(ux), huy = half_rt(uy), han = half_rt(an);
+                double ea = exp(han), ia = exp(-han);
+                double vx = -huy, vy = hux;
+                a = {static_cast<T>(hx), static_cast<T>(hy), static_cast<T>(exp(hlt)), static_cast<T>(hr)};
+                b = {static_cast<T>(ea * hux * hux + ia * vx * vx), static_cast<T>(ea * hux * huy + ia * vx * vy),
+                     static_cast<T>(ea * huy * huy + ia * vy * vy), T(1)};
+            }
+            pack[2 * id] = a;
+            pack[2 * id + 1] = b;
+        }
+        if (gtab) {
+            Q4<T> a, b, c;
+            if (!act) {
+                a = {T(0), T(0), T(0), T(0)};
+                b = {T(1), T(1), T(1), T(0)};
+                c = {T(0), T(0), T(0), T(0)};
+            } else {
+                a = {static_cast<T>(x), static_cast<T>(y), static_cast<T>(exp(lt)), static_cast<T>(r)};
+                b = {static_cast<T>(exp(an)), static_cast<T>(exp(-an)), static_cast<T>(ux), static_cast<T>(uy)};
+                c = {static_cast<T>(p[4 * cap + id]), static_cast<T>(p[5 * cap + id]), static_cast<T>(p[6 * cap + id]),
+                     T(1)};
+            }
+            gtab[3 * id] = a;
+            gtab[3 * id + 1] = b;
+            gtab[3 * id + 2] = c;
+        }
+    }
+}
+
+void launch_adam(bool fp64, const SitesDev& s, DevState* st, double2* grads, double* m, double* v, const AdamHyper& hp,
+                 const double2* bc_table, double2 bc_now, bool zero_grads, double scale, void* pack, void* gtab,
+                 cudaStream_t stream) {
+    int grid = (s.cap + 127) / 128;
+    if (grid < 1) grid = 1;
+    if (fp64)
+        k_adam<double><<<grid, 128, 0, stream>>>(s, st, grads, m, v, hp, bc_table, bc_now, zero_grads ? 1 : 0, scale,
+                                                 (Q4<double>*)pack, (Q4<double>*)gtab);
+    else
+        k_adam<float><<<grid, 128, 0, stream>>>(s, st, grads, m, v, hp, bc_table, bc_now, zero_grads ? 1 : 0, scale,
+                                                (Q4<float>*)pack, (Q4<float>*)gtab);
+    SAD_LAUNCHED();
+}
+
+__global__ void k_clamp(SitesDev s, const DevState* st, AdamHyper hp) {
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= st->n_sites || !s.active[id] || s.frozen[id]) return;
+    clamp_site(s.p, s.cap, id, hp);
+}
+
+void launch_clamp(const SitesDev& s, const DevState* st, const AdamHyper& hp, cudaStream_t stream) {
+    int grid = (s.cap + 127) / 128;
+    if (grid < 1) grid = 1;
+    k_clamp<<<grid, 128, 0, stream>>>(s, st, hp);
+    SAD_LAUNCHED();
+}
+
+// ====================================================================== prune / densify (budget.cpp:219-305)
+// Selection = stable ascending radix sort of order_key() over all slots; ineligible slots get the
+// largest key so they sort last, and the stable sort keeps ascending ids within ties (the
+// reference's id tie-break).
+__global__ void k_prune_keys(SitesDev s, DevState* st, const double2* __restrict__ stats, int cap,
+                             unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals) {
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= cap) return;
+    bool elig = id < st->n_sites && s.active[id] && !s.frozen[id];
+    double norm = static_cast<double>(st->valid > 1 ? st->valid : 1);
+    keys[id] = elig ? order_key(dd_value(stats[7 * static_cast<size_t>(cap) + id]) / norm) : ~0ull;
+    vals[id] = static_cast<uint32_t>(id);
+    unsigned mask = __ballot_sync(0xffffffffu, elig);
+    if ((threadIdx.x & 31) == 0 && mask) atomicAdd(&st->n_elig, __popc(mask));
+}
+
+void launch_prune_keys(const SitesDev& s, DevState* st, const double2* stats, int cap, unsigned long long* keys,
+                       uint32_t* vals, cudaStream_t stream) {
+    k_prune_keys<<<(cap + 255) / 256, 256, 0, stream>>>(s, st, stats, cap, keys, vals);
+    SAD_LAUNCHED();
+}
+
+__global__ void k_prune_apply(SitesDev s, DevState* st, const uint32_t* __restrict__ sorted, double pct) {
+    int want = static_cast<int>(static_cast<double>(st->n_elig) * pct);
+    if (pct <= 0) want = 0;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) st->done = want < 1 ? 0 : want;
+    if (i >= want) return;
+    uint32_t id = sorted[i];
+    s.active[id] = 0;
+    s.p[0 * s.cap + id] = -1.0;
+    s.p[1 * s.cap + id] = -1.0;
+}
+
+void launch_prune_apply(const SitesDev& s, DevState* st, const uint32_t* sorted, double pct, cudaStream_t stream) {
+    k_prune_apply<<<(s.cap + 255) / 256, 256, 0, stream>>>(s, st, sorted, pct);
+    SAD_LAUNCHED();
+}
+
+__global__ void k_densify_keys(SitesDev s, DevState* st, const double2* __restrict__ stats, int cap, double alpha,
+                               double eps, unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals,
+                               uint8_t* __restrict__ free_flags) {
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= cap) return;
+    const bool inside = id < st->n_sites;
+    double mass = inside ? dd_value(stats[static_cast<size_t>(id)]) : 0.0;
+    bool elig = inside && s.active[id] && !s.frozen[id] && mass > 1.0;
+    unsigned long long key = ~0ull;
+    if (elig) {
+        double energy = dd_value(stats[static_cast<size_t>(cap) + id]);
+        double sc = energy / pow(smax(mass, eps), alpha);  // densify_score (budget.cpp:157-159)
+        key = order_key(-sc);                              // descending score, ascending id
+    }
+    keys[id] = key;
+    vals[id] = static_cast<uint32_t>(id);
+    free_flags[id] = (inside && !s.active[id]) ? 1 : 0;
+    unsigned mask = __ballot_sync(0xffffffffu, elig);
+    if ((threadIdx.x & 31) == 0 && mask) atomicAdd(&st->n_elig, __popc(mask));
+}
+
+void launch_densify_keys(const SitesDev& s, DevState* st, const double2* stats, int cap, double alpha, double eps,
+                         unsigned long long* keys, uint32_t* vals, uint8_t* free_flags, cudaStream_t stream) {
+    k_densify_keys<<<(cap + 255) / 256, 256, 0, stream>>>(s, st, stats, cap, alpha, eps, keys, vals, free_flags);
+    SAD_LAUNCHED();
+}
+
+__device__ __forceinline__ double luma_at(const double* img, int w, int h, int x, int y) {
+    x = x < 0 ? 0 : (x > w - 1 ? w - 1 : x);
+    y = y < 0 ? 0 : (y > h - 1 ? h - 1 : y);
+    const double* p = img + 3 * (static_cast<size_t>(y) * w + x);
+    return 0.2126 * p[0] + 0.7152 * p[1] + 0.0722 * p[2];
+}
+
+// split_axis (budget.cpp:170-215) + the split of densify (budget.cpp:237-279).  Split i uses free
+// slot i while they last, then appends in order; parents are active so no two splits touch the same
+// slot, which makes the reference's sequential loop embarrassingly parallel.
+__global__ void k_densify_apply(SitesDev s, DevState* st, const double2* __restrict__ stats, int cap,
+                                const uint32_t* __restrict__ sorted, const uint32_t* __restrict__ free_list,
+                                const double* __restrict__ img, double pct, SplitHyper hp, double* m, double* v) {
+    const int n_elig = st->n_elig, n_free = st->n_free, size0 = st->n_sites;
+    int want = static_cast<int>(static_cast<double>(n_elig) * pct);
+    if (pct <= 0 || want < 1) want = 0;
+    long long room = hp.max_sites > 0 ? (static_cast<long long>(hp.max_sites) - size0) : (1ll << 40);
+    if (room < 0) room = 0;
+    long long done = want < static_cast<long long>(n_free) + room ? want : static_cast<long long>(n_free) + room;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= done) return;
+    const uint32_t par = sorted[i];
+    double st8[8];
+#pragma unroll
+    for (int c = 0; c < 8; c++) st8[c] = dd_value(stats[static_cast<size_t>(c) * cap + par]);
+    double* p = s.p;
+    const double px = p[0 * cap + par], py = p[1 * cap + par], plt = p[2 * cap + par], pr = p[3 * cap + par];
+    const double pan = p[9 * cap + par];
+    double ax = 1, ay = 0, an = 0;
+    bool fallback = true;
+    if (st8[0] >= 4.0 && st8[1] > 0) {
+        double wv = st8[1];
+        double mx = st8[2] / wv, my = st8[3] / wv;
+        double cxx = st8[4] / wv - mx * mx;
+        double cyy = st8[6] / wv - my * my;
+        double cxy = st8[5] / wv - mx * my;
+        double half = 0.5 * (cxx - cyy);
+        double root = __dsqrt_rn(half * half + cxy * cxy);
+        double mid = 0.5 * (cxx + cyy);
+        double l1 = mid + root, l2 = mid - root;
+        if (l1 > 0 && (l2 <= 0 || l1 > 1.05 * l2)) {
+            double vx = cxy, vy = l1 - cxx;
+            double nn = __dsqrt_rn(vx * vx + vy * vy);
+            if (nn < 1e-18 * l1) {
+                vx = l1 - cyy;
+                vy = cxy;
+                nn = __dsqrt_rn(vx * vx + vy * vy);
+            }
+            if (nn > 0 && isfinite(nn)) {
+                ax = vx / nn;
+                ay = vy / nn;
+                double ratio = l2 > 0 ? l1 / l2 : 1e18;
+                an = sclamp(-0.5 * log(ratio), hp.aniso_min, hp.aniso_max);
+                fallback = false;
+            }
+        }
+    }
+    if (fallback) {
+        int sx = static_cast<int>(llround(px)), sy = static_cast<int>(llround(py));
+        int w = hp.width, h = hp.height;
+        double gx = (luma_at(img, w, h, sx + 1, sy - 1) + 2 * luma_at(img, w, h, sx + 1, sy) +
+                     luma_at(img, w, h, sx + 1, sy + 1)) -
+                    (luma_at(img, w, h, sx - 1, sy - 1) + 2 * luma_at(img, w, h, sx - 1, sy) +
+                     luma_at(img, w, h, sx - 1, sy + 1));
+        double gy = (luma_at(img, w, h, sx - 1, sy + 1) + 2 * luma_at(img, w, h, sx, sy + 1) +
+                     luma_at(img, w, h, sx + 1, sy + 1)) -
+                    (luma_at(img, w, h, sx - 1, sy - 1) + 2 * luma_at(img, w, h, sx, sy - 1) +
+                     luma_at(img, w, h, sx + 1, sy - 1));
+        double nn = __dsqrt_rn(gx * gx + gy * gy);
+        if (nn > 1e-12) {
+            ax = gx / nn;
+            ay = gy / nn;
+        }
+        an = sclamp(0.8 * pan, hp.aniso_min, hp.aniso_max);
+    }
+    double mag = sclamp(0.5 * __dsqrt_rn(smax(st8[0], 0.0)), 1.5, 48.0);
+    double clt = smax(plt - 0.25, hp.log_tau_min);
+    double cr = smax(pr * 0.85, hp.radius_min);
+    for (int side = 0; side < 2; side++) {
+        double sg = side == 0 ? 1.0 : -1.0;
+        double cx = sclamp(px + sg * ax * mag, 0.0, hp.width - 1.0);
+        double cy = sclamp(py + sg * ay * mag, 0.0, hp.height - 1.0);
+        int ix = static_cast<int>(llround(cx)), iy = static_cast<int>(llround(cy));
+        const double* col = img + 3 * (static_cast<size_t>(iy) * hp.width + ix);
+        uint32_t slot = side == 0 ? par : (i < n_free ? free_list[i] : static_cast<uint32_t>(size0 + (i - n_free)));
+        if (slot >= static_cast<uint32_t>(cap)) {
+            atomicOr(&st->err, 2);
+            continue;
+        }
+        p[0 * cap + slot] = cx;
+        p[1 * cap + slot] = cy;
+        p[2 * cap + slot] = clt;
+        p[3 * cap + slot] = cr;
+        p[4 * cap + slot] = col[0];
+        p[5 * cap + slot] = col[1];
+        p[6 * cap + slot] = col[2];
+        p[7 * cap + slot] = ax;
+        p[8 * cap + slot] = ay;
+        p[9 * cap + slot] = an;
+        s.active[slot] = 1;
+        s.frozen[slot] = 0;
+#pragma unroll
+        for (int k = 0; k < 10; k++) {
+            m[static_cast<size_t>(k) * cap + slot] = 0.0;
+            v[static_cast<size_t>(k) * cap + slot] = 0.0;
+        }
+    }
+    if (i == done - 1) {
+        st->done = static_cast<int>(done);
+        long long grow = done - n_free;
+        if (grow > 0) st->n_sites = size0 + static_cast<int>(grow);
+    }
+}
+
+void launch_densify_apply(const SitesDev& s, DevState* st, const double2* stats, int cap, const uint32_t* sorted,
+                          const uint32_t* free_list, const double* tgt, double pct, const SplitHyper& hp, double* m,
+                          double* v, cudaStream_t stream) {
+    k_densify_apply<<<(cap + 127) / 128, 128, 0, stream>>>(s, st, stats, cap, sorted, free_list, tgt, pct, hp, m, v);
+    SAD_LAUNCHED();
+}
+
+__global__ void k_flag_active(SitesDev s, const DevState* st, uint8_t* flags) {
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= s.cap) return;
+    flags[id] = (id < st->n_sites && s.active[id]) ? 1 : 0;
+}
+
+void launch_flag_active(const SitesDev& s, const DevState* st, uint8_t* flags, cudaStream_t stream) {
+    k_flag_active<<<(s.cap + 255) / 256, 256, 0, stream>>>(s, st, flags);
+    SAD_LAUNCHED();
+}
+
+// ====================================================================== loop bookkeeping
+__global__ void k_advance(DevState* st, int passes, int adam_steps, double2* loss_hist, int32_t* active_hist) {
+    if (threadIdx.x != 0) return;
+    if (loss_hist) {
+        loss_hist[st->iter] = st->loss;
+        if (active_hist) active_hist[st->iter] = st->n_active;
+        st->iter += 1;
+    }
+    st->loss = make_double2(0.0, 0.0);
+    st->pass_index += static_cast<uint32_t>(passes);
+    st->t += adam_steps;
+}
+
+void launch_advance(DevState* st, int passes, int adam_steps, double2* loss_hist, int32_t* active_hist,
+                    cudaStream_t stream) {
+    k_advance<<<1, 32, 0, stream>>>(st, passes, adam_steps, loss_hist, active_hist);
+    SAD_LAUNCHED();
+}
+
+// ====================================================================== init_sites (train.cpp:33-111), device path
+__global__ void k_sobel(const double* __restrict__ img, int w, int h, double* __restrict__ mag) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= w || y >= h) return;
+    double gx = (luma_at(img, w, h, x + 1, y - 1) + 2 * luma_at(img, w, h, x + 1, y) + luma_at(img, w, h, x + 1, y + 1)) -
+                (luma_at(img, w, h, x - 1, y - 1) + 2 * luma_at(img, w, h, x - 1, y) + luma_at(img, w, h, x - 1, y + 1));
+    double gy = (luma_at(img, w, h, x - 1, y + 1) + 2 * luma_at(img, w, h, x, y + 1) + luma_at(img, w, h, x + 1, y + 1)) -
+                (luma_at(img, w, h, x - 1, y - 1) + 2 * luma_at(img, w, h, x, y - 1) + luma_at(img, w, h, x + 1, y - 1));
+    mag[static_cast<size_t>(y) * w + x] = __dsqrt_rn(gx * gx + gy * gy);
+}
+
+void launch_sobel(const double* tgt, int w, int h, double* mag, cudaStream_t stream) {
+    dim3 block(32, 8), grid((w + 31) / 32, (h + 7) / 8);
+    k_sobel<<<grid, block, 0, stream>>>(tgt, w, h, mag);
+    SAD_LAUNCHED();
+}
+
+__global__ void k_dd_sum(const double* __restrict__ x, size_t n, double2* out) {
+    __shared__ DD parts[8];
+    DD acc{0.0, 0.0};
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        dd_add(acc, x[i]);
+    block_dd_merge<256>(acc, parts, out);
+}
+
+void launch_dd_sum(const double* x, size_t n, double2* out, cudaStream_t stream) {
+    k_dd_sum<<<296, 256, 0, stream>>>(x, n, out);
+    SAD_LAUNCHED();
+}
+
+// Exponential keys log(u)/w from one sequential xorshift stream: thread c owns pixels
+// [c*chunk, (c+1)*chunk) and starts from the stream state after c*chunk draws (host-computed
+// jump-ahead).  Sorting ascending on order_key(-key) gives (key desc, index asc).
+__global__ void k_init_keys(const double* __restrict__ mag, int w, int h, const double2* __restrict__ gsum_dd,
+                            double lambda_init, const uint32_t* __restrict__ jump, int chunk,
+                            unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals) {
+    const size_t np = static_cast<size_t>(w) * h;
+    const size_t c = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    size_t b = c * chunk;
+    if (b >= np) return;
+    double gsum = dd_value(*gsum_dd);
+    double lambda = gsum <= 0 ? 1.0 : lambda_init;
+    double uni = 1.0 / static_cast<double>(np);
+    uint32_t rs = jump[c];
+    size_t e = b + chunk < np ? b + chunk : np;
+    for (size_t i = b; i < e; i++) {
+        double wgt = lambda * uni + (gsum > 0 ? (1.0 - lambda) * mag[i] / gsum : 0.0);
+        if (wgt < 1e-300) wgt = 1e-300;
+        double u = xs_unit(rs);
+        if (u < 1e-12) u = 1e-12;
+        double key = log(u) / wgt;
+        keys[i] = order_key(-key);
+        vals[i] = static_cast<uint32_t>(i);
+    }
+}
+
+void launch_init_keys(const double* mag, int w, int h, const double2* gsum, double lambda, const uint32_t* jump_states,
+                      int chunk, unsigned long long* keys, uint32_t* vals, cudaStream_t stream) {
+    size_t np = static_cast<size_t>(w) * h;
+    size_t threads = (np + chunk - 1) / chunk;
+    k_init_keys<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(mag, w, h, gsum, lambda, jump_states, chunk,
+                                                                      keys, vals);
+    SAD_LAUNCHED();
+}
+
+__global__ void k_mark_cells(const uint32_t* __restrict__ sorted_idx, int n, uint8_t* __restrict__ flags) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flags[sorted_idx[i]] = 1;
+}
+
+void launch_mark_cells(const uint32_t* sorted_idx, int n, uint8_t* flags, cudaStream_t stream) {
+    k_mark_cells<<<(n + 255) / 256, 256, 0, stream>>>(sorted_idx, n, flags);
+    SAD_LAUNCHED();
+}
+
+// Site j takes draws 2j and 2j+1 of stream (seed, 0x1717, 1) (train.cpp:96-110); `jump` holds the
+// state after j0 = block*chunk sites' draws, so each thread replays at most 2*chunk steps.
+__global__ void k_init_sites(SitesDev s, DevState* st, const uint32_t* __restrict__ cells, int n,
+                             const double* __restrict__ img, int w, int h, double r0, double lt0, double an0,
+                             const uint32_t* __restrict__ jump, int chunk) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int b = c * chunk;
+    if (b >= n) return;
+    uint32_t rs = jump[c];
+    const int e = b + chunk < n ? b + chunk : n;
+    const int cap = s.cap;
+    for (int j = b; j < e; j++) {
+        uint32_t cell = cells[j];
+        int cx = static_cast<int>(cell % static_cast<uint32_t>(w)), cy = static_cast<int>(cell / static_cast<uint32_t>(w));
+        double ox = xs_unit(rs), oy = xs_unit(rs);
+        s.p[0 * cap + j] = smin(cx + 0.25 + 0.5 * ox, w - 1.0);
+        s.p[1 * cap + j] = smin(cy + 0.25 + 0.5 * oy, h - 1.0);
+        s.p[2 * cap + j] = lt0;
+        s.p[3 * cap + j] = r0;
+        const double* col = img + 3 * (static_cast<size_t>(cy) * w + cx);
+        s.p[4 * cap + j] = col[0];
+        s.p[5 * cap + j] = col[1];
+        s.p[6 * cap + j] = col[2];
+        s.p[7 * cap + j] = 1.0;
+        s.p[8 * cap + j] = 0.0;
+        s.p[9 * cap + j] = an0;
+        s.active[j] = 1;
+        s.frozen[j] = 0;
+    }
+    if (c == 0) st->n_sites = n;
+}
+
+void launch_init_sites(const SitesDev& s, DevState* st, const uint32_t* cells, int n, const double* tgt, int w, int h,
+                       double r0, double log_tau0, double aniso0, const uint32_t* jump_states, int chunk,
+                       cudaStream_t stream) {
+    int threads = (n + chunk - 1) / chunk;
+    k_init_sites<<<(threads + 127) / 128, 128, 0, stream>>>(s, st, cells, n, tgt, w, h, r0, log_tau0, aniso0,
+                                                            jump_states, chunk);
+    SAD_LAUNCHED();
+}
+
+// ====================================================================== misc
+__global__ void k_f64_to_f32(const double* __restrict__ in, float* __restrict__ out, size_t n) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        out[i] = static_cast<float>(in[i]);
+}
+
+void launch_f64_to_f32(const double* in, float* out, size_t n, cudaStream_t stream) {
+    size_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks < 1) blocks = 1;
+    k_f64_to_f32<<<(unsigned)blocks, 256, 0, stream>>>(in, out, n);
+    SAD_LAUNCHED();
+}
+
+__global__ void k_grads_out(const double2* __restrict__ g, int cap, int n, double* __restrict__ out) {
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= n) return;
+#pragma unroll
+    for (int k = 0; k < 11; k++) out[static_cast<size_t>(id) * 11 + k] = dd_value(g[static_cast<size_t>(k) * cap + id]);
+}
+
+void launch_scatter_grads_out(const double2* grads, int cap, int n, double* out, cudaStream_t stream) {
+    k_grads_out<<<(n + 255) / 256 + 1, 256, 0, stream>>>(grads, cap, n, out);
+    SAD_LAUNCHED();
+}
+
+}  // namespace sadk

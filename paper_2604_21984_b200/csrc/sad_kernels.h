@@ -1,0 +1,134 @@
+// sad_kernels.h — host-visible launch interface of the SAD CUDA kernels (sad_kernels.cu).
+//
+// Device data layouts:
+//   sites   : double p[10][cap] slot-major (x, y, log_tau, radius, R, G, B, dir_x, dir_y, aniso —
+//             the GradSlot order of grad.hpp:13-26), u8 active[cap], frozen[cap]
+//   field   : u32 ids[(gy*gw+gx)*k + i], two buffers (ping-pong per propagation pass)
+//   pack    : per-site candidate snapshot, 2 x Q4<T>  {x, y, tau, r}, {gxx, gxy, gyy, active}
+//   gtab    : per-site backward constants, 3 x Q4<T> {x, y, tau, r}, {e^a, e^-a, ux, uy}, {R, G, B, active}
+//   rtab    : per-site render constants,   3 x Q4<T> {x, y, tau, r}, {gxx, gxy, gyy, active}, {R, G, B, 0}
+//   grads   : double2 g[11][cap]   (hi, lo) compensated accumulators, channel-major
+//   stats   : double2 s[8][cap]
+//   adam    : double m[10][cap], v[10][cap]
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sadk {
+
+// Per-fit scalars that live in device memory so CUDA graphs can replay iterations unchanged.
+struct DevState {
+    uint32_t pass_index;  // CandidateField::pass_index
+    int32_t n_sites;      // SiteStore::size
+    int64_t t;            // AdamState::t
+    int32_t iter;         // history row being produced (0-based)
+    int32_t n_active;     // |active_ids|
+    int32_t n_elig;       // eligible count of the current prune/densify selection
+    int32_t n_free;       // inactive slots below n_sites (densify free list)
+    int32_t done;         // splits / removals performed by the last event
+    int32_t err;          // bit 0: empty candidate list, bit 1: capacity, bit 2: non-finite loss
+    uint64_t nonfinite;   // GradBuffer::nonfinite
+    uint64_t valid;       // StatsResult::valid_pixels
+    uint64_t skipped;     // AdamState::skipped
+    double2 loss;         // compensated loss sum of the current backward call
+};
+
+struct SitesDev {
+    double* p;  // 10 * cap
+    uint8_t* active;
+    uint8_t* frozen;
+    int cap;
+};
+
+struct FieldDims {
+    int width, height, cell, gw, gh, k;
+};
+
+struct AdamHyper {
+    double lr[10];
+    double beta1, beta2, eps;
+    double log_tau_min, log_tau_max, radius_min, radius_max, aniso_min, aniso_max;
+    int clamp_color;
+    int width, height;
+};
+
+struct SplitHyper {
+    double log_tau_min, radius_min, aniso_min, aniso_max;
+    int width, height;
+    uint64_t max_sites;
+};
+
+// ---------------------------------------------------------------- tables
+// which: bit0 pack (half snapshot), bit1 gtab, bit2 rtab.  T = float or double.
+void launch_tables(bool fp64, const SitesDev& s, const DevState* st, double scale, void* pack, void* gtab,
+                   void* rtab, cudaStream_t stream);
+
+// ---------------------------------------------------------------- candidates
+void launch_jfa_seed(const SitesDev& s, const DevState* st, uint32_t* ids, const FieldDims& f, double scale,
+                     cudaStream_t stream);
+void launch_propagate(bool fp64, const uint32_t* prev, uint32_t* next, const void* pack, const uint32_t* act,
+                      const DevState* st, const FieldDims& f, uint32_t step, int box, int inject, uint64_t seed,
+                      uint32_t pass_offset, double scale, cudaStream_t stream);
+void launch_exact_topk(bool fp64, const void* rtab, const uint32_t* act, int n_act, const int32_t* xy, int n_pix,
+                       int k, double scale, uint32_t* out, cudaStream_t stream);
+
+// ---------------------------------------------------------------- render
+void launch_render(bool fp64, const uint32_t* ids, const void* rtab, const FieldDims& f, double scale, void* out_rgb,
+                   DevState* st, cudaStream_t stream);
+void launch_id_map(const uint32_t* ids, const void* rtab_d, const FieldDims& f, double scale, uint32_t* out,
+                   DevState* st, cudaStream_t stream);
+void launch_pixel_weights(const uint32_t* ids, const void* rtab_d, const FieldDims& f, double scale,
+                          const int32_t* xy, int n_q, uint32_t* out_ids, double* out_w, int32_t* out_n,
+                          cudaStream_t stream);
+
+// ---------------------------------------------------------------- backward / loss / stats
+// mode: 0 = MSE target, 1 = MSE target + removal delta, 2 = caller adjoint (pixgrad)
+void launch_backward(bool fp64, int mode, const uint32_t* ids, const void* gtab, const void* tgt_or_pixgrad,
+                     const FieldDims& f, double scale, double2* grads, int cap, DevState* st, cudaStream_t stream);
+void launch_loss(bool fp64, const uint32_t* ids, const void* gtab, const void* tgt, const FieldDims& f, double scale,
+                 DevState* st, cudaStream_t stream);
+void launch_stats(const uint32_t* ids, const void* rtab_d, const double* tgt, const FieldDims& f, double scale,
+                  double2* stats, int cap, DevState* st, cudaStream_t stream);
+
+// ---------------------------------------------------------------- optimiser
+// Adam (+ clamp_project) over all slots < n_sites; optionally zeroes grads and rebuilds pack/gtab.
+// bc: (1 - beta1^t, 1 - beta2^t) table indexed by the new t, or nullptr to use bc_now.
+void launch_adam(bool fp64, const SitesDev& s, DevState* st, double2* grads, double* m, double* v,
+                 const AdamHyper& hp, const double2* bc_table, double2 bc_now, bool zero_grads, double scale,
+                 void* pack, void* gtab, cudaStream_t stream);
+void launch_clamp(const SitesDev& s, const DevState* st, const AdamHyper& hp, cudaStream_t stream);
+
+// ---------------------------------------------------------------- budget events
+void launch_prune_keys(const SitesDev& s, DevState* st, const double2* stats, int cap,
+                       unsigned long long* keys, uint32_t* vals, cudaStream_t stream);
+void launch_prune_apply(const SitesDev& s, DevState* st, const uint32_t* sorted, double pct, cudaStream_t stream);
+void launch_densify_keys(const SitesDev& s, DevState* st, const double2* stats, int cap, double alpha, double eps,
+                         unsigned long long* keys, uint32_t* vals, uint8_t* free_flags, cudaStream_t stream);
+void launch_densify_apply(const SitesDev& s, DevState* st, const double2* stats, int cap, const uint32_t* sorted,
+                          const uint32_t* free_list, const double* tgt, double pct, const SplitHyper& hp,
+                          double* m, double* v, cudaStream_t stream);
+void launch_flag_active(const SitesDev& s, const DevState* st, uint8_t* flags, cudaStream_t stream);
+
+// ---------------------------------------------------------------- loop bookkeeping
+// pass_index += passes; t and iter advance; records loss/active history row `iter`.
+void launch_advance(DevState* st, int passes, int adam_steps, double2* loss_hist, int32_t* active_hist,
+                    cudaStream_t stream);
+
+// ---------------------------------------------------------------- init (train.cpp:33-111) device path
+void launch_sobel(const double* tgt, int w, int h, double* mag, cudaStream_t stream);
+void launch_init_keys(const double* mag, int w, int h, const double2* gsum, double lambda, const uint32_t* jump_states,
+                      int chunk, unsigned long long* keys, uint32_t* vals, cudaStream_t stream);
+void launch_init_sites(const SitesDev& s, DevState* st, const uint32_t* cells, int n, const double* tgt, int w, int h,
+                       double r0, double log_tau0, double aniso0, const uint32_t* jump_states, int chunk,
+                       cudaStream_t stream);
+void launch_dd_sum(const double* x, size_t n, double2* out, cudaStream_t stream);
+void launch_mark_cells(const uint32_t* sorted_idx, int n, uint8_t* flags, cudaStream_t stream);
+
+// ---------------------------------------------------------------- misc
+void launch_f64_to_f32(const double* in, float* out, size_t n, cudaStream_t stream);
+void launch_scatter_grads_out(const double2* grads, int cap, int n, double* out /* n*11 */, cudaStream_t stream);
+
+// Number of kernel launches issued through these wrappers (process-wide; evidence counter).
+uint64_t launch_counter();
+
+}  // namespace sadk

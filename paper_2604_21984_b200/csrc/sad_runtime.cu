@@ -1,0 +1,1480 @@
+// sad_runtime.cu — host runtime of the B200 SAD library: context, device workspace, the C ABI of
+// include/sad_b200.h (per-call entry points that mirror the reference functions), and the resident
+// fit loop (train.cpp:221-311) that keeps every buffer in HBM between the target upload and the
+// result download.
+#include "../../include/sad_b200.h"
+#include "sad_kernels.h"
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+using sadk::DevState;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct SadFail {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw SadFail{code, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(SAD_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename F>
+sad_status guard(F&& f) {
+    try {
+        f();
+        return SAD_OK;
+    } catch (const SadFail& e) {
+        g_err = e.msg;
+        return static_cast<sad_status>(e.code);
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return SAD_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SAD_EINVAL;
+    }
+}
+
+// ------------------------------------------------------------------ device buffers
+template <typename T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() {
+        if (p) cudaFree(p);
+    }
+    void ensure(size_t m) {
+        if (m <= n && p) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        if (m == 0) m = 1;
+        ck(cudaMalloc(&p, m * sizeof(T)), "cudaMalloc");
+        n = m;
+    }
+};
+
+// ------------------------------------------------------------------ host-side reference arithmetic
+uint32_t ceil_log2(uint32_t v) {
+    uint32_t e = 0;
+    while ((1u << e) < v) e++;
+    return e;
+}
+
+// jump_step (candidates.cpp:27-33)
+uint32_t jump_step(uint32_t t, uint32_t b) {
+    if (b < 2 || (b & (b - 1)) != 0) fail(SAD_EINVAL, "jump_step: b must be a power of two >= 2");
+    uint32_t lg = ceil_log2(b);
+    uint32_t e = (t < lg - 1 ? t : lg - 1) + 1;
+    uint32_t s = b >> e;
+    return s < 1 ? 1 : s;
+}
+
+std::vector<sad_pass_spec> full_refresh_passes(int gw, int gh, int extra) {
+    if (gw < 1 || gh < 1) fail(SAD_EINVAL, "JumpSchedule: empty extent");
+    uint32_t m = static_cast<uint32_t>(gw > gh ? gw : gh);
+    uint32_t b = 1u << ceil_log2(m);
+    if (b < 2) b = 2;
+    uint32_t events = ceil_log2(m);
+    std::vector<sad_pass_spec> seq;
+    for (uint32_t t = 0; t < events; t++) seq.push_back({jump_step(t, b), 1});
+    for (int i = 0; i < extra; i++) seq.push_back({1, 0});
+    return seq;
+}
+
+std::vector<sad_pass_spec> schedule_passes(int gw, int gh, int total) {
+    if (gw < 1 || gh < 1) fail(SAD_EINVAL, "JumpSchedule: empty extent");
+    uint32_t m = static_cast<uint32_t>(gw > gh ? gw : gh);
+    uint32_t b = 1u << ceil_log2(m);
+    if (b < 2) b = 2;
+    uint32_t events = ceil_log2(m);
+    std::vector<sad_pass_spec> seq;
+    for (int t = 0; t < total; t++) {
+        uint32_t tu = static_cast<uint32_t>(t);
+        seq.push_back(tu < events ? sad_pass_spec{jump_step(tu, b), 1} : sad_pass_spec{1, 0});
+    }
+    return seq;
+}
+
+double norm_scale(int w, int h) {
+    if (w < 1 || h < 1) fail(SAD_EINVAL, "normalization_scale: empty extent");
+    return 1.0 / static_cast<double>(w > h ? w : h);
+}
+
+// TrainConfig::validate (types.cpp:103-126)
+void validate(sad_train_config& c, int w, int h) {
+    auto bad = [](const char* m) { fail(SAD_EINVAL, m); };
+    if (w < 1 || h < 1) bad("config: empty image");
+    if (c.iters < 0) bad("config: negative iters");
+    if (c.k < 1 || c.k > 16) bad("config: k out of [1,16]");
+    if (c.inject < 0) bad("config: negative inject");
+    if (c.lambda_init < 0 || c.lambda_init > 1) bad("config: lambda_init out of [0,1]");
+    if (c.densify_every < 1 || c.prune_every < 1) bad("config: event period < 1");
+    if (c.densify_pct < 0 || c.densify_pct > 1 || c.prune_pct < 0 || c.prune_pct > 1)
+        bad("config: percentile out of [0,1]");
+    if (c.refresh_every < 1) bad("config: refresh period < 1");
+    if (c.refresh_passes < 0 || c.final_passes < 0) bad("config: negative passes");
+    if (c.target_bpp < 0) bad("config: negative bpp");
+    if (c.n_sites < 0) bad("config: negative site count");
+    if (c.log_tau_min > c.log_tau_max || c.radius_min > c.radius_max || c.aniso_min > c.aniso_max)
+        bad("config: inverted clamp range");
+    if (c.threads < 1) c.threads = 1;
+    c.densify_start = std::clamp(c.densify_start, 0, c.iters);
+    c.densify_end = std::clamp(c.densify_end, 0, c.iters);
+    c.prune_start = std::clamp(c.prune_start, 0, c.iters);
+    c.prune_end = std::clamp(c.prune_end, 0, c.iters);
+    if (c.densify_end < c.densify_start || c.prune_end < c.prune_start) bad("config: inverted schedule window");
+}
+
+uint64_t bpp_target_count(double bpp, int w, int h) {
+    if (bpp < 0 || w < 1 || h < 1) fail(SAD_EINVAL, "bpp target: bad inputs");
+    return static_cast<uint64_t>(bpp * static_cast<double>(w) * h / 128.0);
+}
+
+// simulate_schedule (budget.cpp:312-332)
+int simulate_schedule(int n0, double scale, const sad_train_config& c) {
+    int n = n0;
+    for (int t = 1; t <= c.iters; t++) {
+        bool ev_d = t >= c.densify_start && t <= c.densify_end && t % c.densify_every == 0;
+        bool ev_p = t >= c.prune_start && t <= c.prune_end && t % c.prune_every == 0;
+        if (ev_p && !c.prune_during_densify && t <= c.densify_end) ev_p = false;
+        if (ev_p) {
+            int p = static_cast<int>(n * c.prune_pct * scale);
+            if (p >= n) p = n - 1;
+            if (p > 0) n -= p;
+        }
+        if (ev_d) {
+            int d = static_cast<int>(n * c.densify_pct * scale);
+            if (c.max_sites > 0 && static_cast<size_t>(n + d) > c.max_sites) d = static_cast<int>(c.max_sites) - n;
+            if (d > 0) n += d;
+        }
+    }
+    return n;
+}
+
+// plan_schedule (budget.cpp:334-374)
+double plan_schedule(int n0, uint64_t target, const sad_train_config& c) {
+    double cap = c.budget_scale_cap, tgt = static_cast<double>(target);
+    int mn = n0, mx = n0;
+    auto miss = [&](double s) {
+        int fin = simulate_schedule(n0, s, c);
+        mn = std::min(mn, fin);
+        mx = std::max(mx, fin);
+        return std::abs(static_cast<double>(fin) - tgt);
+    };
+    double best_s = 0, best_m = miss(0);
+    for (int i = 1; i <= 96; i++) {
+        double s = cap * i / 96;
+        double m = miss(s);
+        if (m < best_m) {
+            best_m = m;
+            best_s = s;
+        }
+    }
+    double lo = std::max(0.0, best_s - cap / 96), hi = std::min(cap, best_s + cap / 96);
+    for (int i = 0; i <= 256; i++) {
+        double s = lo + (hi - lo) * i / 256;
+        double m = miss(s);
+        if (m < best_m) {
+            best_m = m;
+            best_s = s;
+        }
+    }
+    if (tgt < mn || tgt > mx) {
+        std::fprintf(stderr, "schedule: target %llu outside reachable range [%d, %d], using scale cap\n",
+                     static_cast<unsigned long long>(target), mn, mx);
+        return cap;
+    }
+    return best_s;
+}
+
+// ------------------------------------------------------------------ xorshift32 jump-ahead (GF(2) matrices)
+struct Gf2 {
+    uint32_t col[32];
+};
+
+uint32_t gf2_apply(const Gf2& m, uint32_t s) {
+    uint32_t r = 0;
+    for (int i = 0; i < 32; i++)
+        if (s >> i & 1u) r ^= m.col[i];
+    return r;
+}
+
+Gf2 gf2_mul(const Gf2& a, const Gf2& b) {
+    Gf2 r;
+    for (int i = 0; i < 32; i++) r.col[i] = gf2_apply(a, b.col[i]);
+    return r;
+}
+
+Gf2 xs_matrix_pow(uint64_t e) {
+    Gf2 base, acc;
+    for (int i = 0; i < 32; i++) {
+        uint32_t x = 1u << i;
+        x ^= x << 13;
+        x ^= x >> 17;
+        x ^= x << 5;
+        base.col[i] = x;
+        acc.col[i] = 1u << i;
+    }
+    while (e) {
+        if (e & 1) acc = gf2_mul(base, acc);
+        base = gf2_mul(base, base);
+        e >>= 1;
+    }
+    return acc;
+}
+
+uint32_t mix32(uint32_t h) {
+    h ^= h >> 16;
+    h *= 0x7feb352du;
+    h ^= h >> 15;
+    h *= 0x846ca68bu;
+    h ^= h >> 16;
+    return h;
+}
+
+uint32_t seeded_state(uint64_t seed, uint32_t a, uint32_t b) {
+    uint32_t h = mix32(static_cast<uint32_t>(seed) ^ 0x9e3779b9u);
+    h ^= mix32(static_cast<uint32_t>(seed >> 32) + 0x85ebca6bu);
+    h = mix32(h + mix32(a ^ 0x27d4eb2fu));
+    h = mix32(h ^ mix32(b + 0x165667b1u));
+    return h ? h : 0x6b33a1c9u;
+}
+
+// states[c] = stream state after c * stride draws.
+std::vector<uint32_t> jump_states(uint32_t s0, uint64_t stride, size_t count) {
+    Gf2 m = xs_matrix_pow(stride);
+    std::vector<uint32_t> out(count);
+    uint32_t s = s0;
+    for (size_t c = 0; c < count; c++) {
+        out[c] = s;
+        s = gf2_apply(m, s);
+    }
+    return out;
+}
+
+// ------------------------------------------------------------------ workspace
+struct Workspace {
+    cudaStream_t stream = nullptr;
+    int cap = 0;
+    int w = 0, h = 0;
+    sadk::FieldDims fd{};
+    DBuf<double> params;
+    DBuf<uint8_t> active, frozen;
+    DBuf<uint32_t> ids[2];
+    int cur = 0;
+    DBuf<char> pack, gtab, rtab, rtab_d;
+    DBuf<double2> grads, stats;
+    DBuf<double> m, v;
+    DBuf<uint32_t> act, free_list;
+    DBuf<uint8_t> flags;
+    DBuf<unsigned long long> keys[2];
+    DBuf<uint32_t> vals[2];
+    DBuf<char> cub_tmp;
+    DBuf<double> tgt_d, px_d;
+    DBuf<float> tgt_f, px_f;
+    DBuf<DevState> st;
+    DevState* hst = nullptr;  // pinned mirror
+    // init_sites scratch (train.cpp:59-111 on the device), sized for W*H pixels
+    struct InitBufs {
+        size_t np = 0;
+        DBuf<double> mag;
+        DBuf<double2> gsum;
+        DBuf<unsigned long long> k0, k1;
+        DBuf<uint32_t> v0, v1, cells, jk, jo;
+        DBuf<uint8_t> fl;
+        DBuf<int32_t> nsel;
+        DBuf<char> tmp;
+    } ib;
+
+    ~Workspace() {
+        if (hst) cudaFreeHost(hst);
+    }
+
+    sadk::SitesDev sites() { return sadk::SitesDev{params.p, active.p, frozen.p, cap}; }
+
+    void ensure_state() {
+        if (!st.p) {
+            st.ensure(1);
+            ck(cudaMallocHost(&hst, sizeof(DevState)), "cudaMallocHost");
+            std::memset(hst, 0, sizeof(DevState));
+            ck(cudaMemsetAsync(st.p, 0, sizeof(DevState), stream), "memset state");
+        }
+    }
+
+    // Grows every per-site buffer to `c` slots (contents of params/flags/adam preserved).
+    void ensure_cap(int c) {
+        ensure_state();
+        if (c <= cap && params.p) return;
+        int nc = std::max(c, 1);
+        auto grow_d = [&](DBuf<double>& b, size_t per) {
+            DBuf<double> nb;
+            nb.ensure(per * nc);
+            ck(cudaMemsetAsync(nb.p, 0, per * nc * sizeof(double), stream), "memset");
+            if (b.p && cap > 0)
+                for (size_t k = 0; k < per; k++)
+                    ck(cudaMemcpyAsync(nb.p + k * nc, b.p + k * cap, cap * sizeof(double), cudaMemcpyDeviceToDevice,
+                                       stream),
+                       "grow copy");
+            std::swap(b.p, nb.p);
+            std::swap(b.n, nb.n);
+        };
+        auto grow_u8 = [&](DBuf<uint8_t>& b) {
+            DBuf<uint8_t> nb;
+            nb.ensure(nc);
+            ck(cudaMemsetAsync(nb.p, 0, nc, stream), "memset");
+            if (b.p && cap > 0) ck(cudaMemcpyAsync(nb.p, b.p, cap, cudaMemcpyDeviceToDevice, stream), "grow copy");
+            std::swap(b.p, nb.p);
+            std::swap(b.n, nb.n);
+        };
+        ck(cudaStreamSynchronize(stream), "sync");
+        grow_d(params, 10);
+        grow_d(m, 10);
+        grow_d(v, 10);
+        grow_u8(active);
+        grow_u8(frozen);
+        cap = nc;
+        pack.ensure(static_cast<size_t>(nc) * 64);
+        gtab.ensure(static_cast<size_t>(nc) * 96);
+        rtab.ensure(static_cast<size_t>(nc) * 96);
+        rtab_d.ensure(static_cast<size_t>(nc) * 96);
+        grads.ensure(static_cast<size_t>(nc) * 11);
+        stats.ensure(static_cast<size_t>(nc) * 8);
+        ck(cudaMemsetAsync(grads.p, 0, grads.n * sizeof(double2), stream), "memset grads");
+        act.ensure(nc);
+        free_list.ensure(nc);
+        flags.ensure(nc);
+        for (int i = 0; i < 2; i++) {
+            keys[i].ensure(nc);
+            vals[i].ensure(nc);
+        }
+        ensure_cub(nc);
+    }
+
+    void ensure_cub(size_t items) {
+        size_t a = 0, b = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, a, keys[0].p, keys[1].p, vals[0].p, vals[1].p, static_cast<int>(items),
+                                        0, 64, stream);
+        thrust::counting_iterator<uint32_t> it(0);
+        cub::DeviceSelect::Flagged(nullptr, b, it, flags.p, act.p, &st.p->n_active, static_cast<int>(items), stream);
+        cub_tmp.ensure(std::max(a, b) + 256);
+    }
+
+    void ensure_field(int w_, int h_, int k, int cell) {
+        w = w_;
+        h = h_;
+        fd.width = w_;
+        fd.height = h_;
+        fd.cell = cell;
+        fd.gw = (w_ + cell - 1) / cell;
+        fd.gh = (h_ + cell - 1) / cell;
+        fd.k = k;
+        size_t n = static_cast<size_t>(fd.gw) * fd.gh * k;
+        ids[0].ensure(n);
+        ids[1].ensure(n);
+    }
+
+    void ensure_target(size_t px) {
+        tgt_d.ensure(3 * px);
+        tgt_f.ensure(3 * px);
+    }
+
+    // ---- state scalars
+    void set_state(const DevState& s) {
+        *hst = s;
+        ck(cudaMemcpyAsync(st.p, hst, sizeof(DevState), cudaMemcpyHostToDevice, stream), "H2D state");
+    }
+    DevState get_state() {
+        ck(cudaMemcpyAsync(hst, st.p, sizeof(DevState), cudaMemcpyDeviceToHost, stream), "D2H state");
+        ck(cudaStreamSynchronize(stream), "sync");
+        return *hst;
+    }
+    template <typename F>
+    void patch_state(size_t off, const F& val) {
+        ck(cudaMemcpyAsync(reinterpret_cast<char*>(st.p) + off, &val, sizeof(F), cudaMemcpyHostToDevice, stream),
+           "patch state");
+    }
+    void zero_state_field(size_t off, size_t bytes) {
+        ck(cudaMemsetAsync(reinterpret_cast<char*>(st.p) + off, 0, bytes, stream), "memset state");
+    }
+
+    // ---- active list (SiteStore::active_ids, types.cpp:71-80)
+    void compute_active() {
+        sadk::launch_flag_active(sites(), st.p, flags.p, stream);
+        size_t bytes = cub_tmp.n;
+        thrust::counting_iterator<uint32_t> it(0);
+        ck(cub::DeviceSelect::Flagged(cub_tmp.p, bytes, it, flags.p, act.p, &st.p->n_active, cap, stream),
+           "DeviceSelect active");
+    }
+
+    void sort_pairs(int n) {
+        size_t bytes = cub_tmp.n;
+        ck(cub::DeviceRadixSort::SortPairs(cub_tmp.p, bytes, keys[0].p, keys[1].p, vals[0].p, vals[1].p, n, 0, 64,
+                                           stream),
+           "DeviceRadixSort");
+    }
+};
+
+// host view -> device
+void upload_sites(Workspace& ws, const sad_sites_view* v, int extra_cap = 0) {
+    if (!v) fail(SAD_EINVAL, "null sites view");
+    size_t n = v->size;
+    if (n > static_cast<size_t>(INT32_MAX / 2)) fail(SAD_EINVAL, "too many sites");
+    ws.ensure_cap(static_cast<int>(n) + extra_cap);
+    const double* src[10] = {v->x, v->y, v->log_tau, v->radius, v->col_r, v->col_g, v->col_b, v->dir_x, v->dir_y,
+                             v->aniso};
+    if (n) {
+        for (int k = 0; k < 10; k++)
+            ck(cudaMemcpyAsync(ws.params.p + static_cast<size_t>(k) * ws.cap, src[k], n * 8, cudaMemcpyHostToDevice,
+                               ws.stream),
+               "H2D sites");
+        ck(cudaMemcpyAsync(ws.active.p, v->active, n, cudaMemcpyHostToDevice, ws.stream), "H2D active");
+        ck(cudaMemcpyAsync(ws.frozen.p, v->frozen, n, cudaMemcpyHostToDevice, ws.stream), "H2D frozen");
+    }
+    ws.patch_state(offsetof(DevState, n_sites), static_cast<int32_t>(n));
+}
+
+void download_sites(Workspace& ws, sad_sites_view* v, size_t n) {
+    if (n > v->capacity) fail(SAD_ENOMEM, "sites view capacity too small");
+    double* dst[10] = {v->x, v->y, v->log_tau, v->radius, v->col_r, v->col_g, v->col_b, v->dir_x, v->dir_y, v->aniso};
+    if (n) {
+        for (int k = 0; k < 10; k++)
+            ck(cudaMemcpyAsync(dst[k], ws.params.p + static_cast<size_t>(k) * ws.cap, n * 8, cudaMemcpyDeviceToHost,
+                               ws.stream),
+               "D2H sites");
+        ck(cudaMemcpyAsync(v->active, ws.active.p, n, cudaMemcpyDeviceToHost, ws.stream), "D2H active");
+        ck(cudaMemcpyAsync(v->frozen, ws.frozen.p, n, cudaMemcpyDeviceToHost, ws.stream), "D2H frozen");
+    }
+    ck(cudaStreamSynchronize(ws.stream), "sync");
+    v->size = n;
+}
+
+void check_field(const sad_field_view* f) {
+    if (!f) fail(SAD_EINVAL, "null field view");
+    if (f->gw < 1 || f->gh < 1) fail(SAD_EINVAL, "candidate field not sized");
+    if (f->k < 1 || f->k > 16) fail(SAD_EINVAL, "CandidateField: k out of range");
+    if (f->cell < 1) fail(SAD_EINVAL, "CandidateField: bad cell size");
+}
+
+void upload_field(Workspace& ws, const sad_field_view* f) {
+    check_field(f);
+    ws.ensure_field(f->width, f->height, f->k, f->cell);
+    size_t n = static_cast<size_t>(f->gw) * f->gh * f->k;
+    ws.cur = 0;
+    ck(cudaMemcpyAsync(ws.ids[0].p, f->ids, n * 4, cudaMemcpyHostToDevice, ws.stream), "H2D field");
+}
+
+void download_field(Workspace& ws, sad_field_view* f) {
+    size_t n = static_cast<size_t>(f->gw) * f->gh * f->k;
+    ck(cudaMemcpyAsync(f->ids, ws.ids[ws.cur].p, n * 4, cudaMemcpyDeviceToHost, ws.stream), "D2H field");
+    ck(cudaStreamSynchronize(ws.stream), "sync");
+}
+
+void upload_target(Workspace& ws, const double* rgb, int w, int h) {
+    size_t n = 3 * static_cast<size_t>(w) * h;
+    ws.ensure_target(n / 3);
+    ck(cudaMemcpyAsync(ws.tgt_d.p, rgb, n * 8, cudaMemcpyHostToDevice, ws.stream), "H2D target");
+    sadk::launch_f64_to_f32(ws.tgt_d.p, ws.tgt_f.p, n, ws.stream);
+}
+
+void check_synced(const sad_sites_view* s, const sad_field_view* f) {
+    if (f->synced_generation != s->generation) fail(SAD_ESTALE, "candidate field is stale for this store");
+    if (f->gw < 1 || f->gh < 1) fail(SAD_EINVAL, "candidate field not sized");
+}
+
+void check_err(Workspace& ws, const char* what) {
+    DevState s = ws.get_state();
+    if (s.err & 1) {
+        ws.zero_state_field(offsetof(DevState, err), sizeof(int32_t));
+        fail(SAD_EEMPTY, std::string(what) + ": empty candidate list at a pixel");
+    }
+    if (s.err & 2) {
+        ws.zero_state_field(offsetof(DevState, err), sizeof(int32_t));
+        fail(SAD_ENOMEM, std::string(what) + ": site capacity exhausted");
+    }
+}
+
+// ------------------------------------------------------------------ stream-ordered operations
+// Propagation passes on the device field starting from ids[cur]; pass i uses pass index
+// st->pass_index + pass_base + i.  Tables must already hold the packed snapshot.
+void passes_device(Workspace& ws, const std::vector<sad_pass_spec>& seq, int inject, uint64_t seed, bool fp64,
+                   uint32_t pass_base) {
+    double scale = norm_scale(ws.fd.width, ws.fd.height);
+    for (size_t i = 0; i < seq.size(); i++) {
+        sadk::launch_propagate(fp64, ws.ids[ws.cur].p, ws.ids[1 - ws.cur].p, ws.pack.p, ws.act.p, ws.st.p, ws.fd,
+                               seq[i].step, seq[i].stencil, inject, seed, pass_base + static_cast<uint32_t>(i), scale,
+                               ws.stream);
+        ws.cur = 1 - ws.cur;
+    }
+}
+
+void build_tables(Workspace& ws, bool fp64, bool pack, bool gtab, bool rtab) {
+    sadk::launch_tables(fp64, ws.sites(), ws.st.p, norm_scale(ws.fd.width, ws.fd.height), pack ? ws.pack.p : nullptr,
+                        gtab ? ws.gtab.p : nullptr, rtab ? (fp64 ? ws.rtab_d.p : ws.rtab.p) : nullptr, ws.stream);
+}
+
+sadk::AdamHyper adam_hyper(const sad_train_config& c, int w, int h) {
+    sadk::AdamHyper hp{};
+    const double lrs[10] = {c.lr_pos,   c.lr_pos,   c.lr_log_tau, c.lr_radius, c.lr_color,
+                            c.lr_color, c.lr_color, c.lr_dir,     c.lr_dir,    c.lr_aniso};
+    for (int i = 0; i < 10; i++) hp.lr[i] = lrs[i];
+    hp.beta1 = c.beta1;
+    hp.beta2 = c.beta2;
+    hp.eps = c.adam_eps;
+    hp.log_tau_min = c.log_tau_min;
+    hp.log_tau_max = c.log_tau_max;
+    hp.radius_min = c.radius_min;
+    hp.radius_max = c.radius_max;
+    hp.aniso_min = c.aniso_min;
+    hp.aniso_max = c.aniso_max;
+    hp.clamp_color = c.clamp_color;
+    hp.width = w;
+    hp.height = h;
+    return hp;
+}
+
+void stats_device(Workspace& ws) {
+    build_tables(ws, true, false, false, true);
+    ck(cudaMemsetAsync(ws.stats.p, 0, sizeof(double2) * 8 * ws.cap, ws.stream), "memset stats");
+    ws.zero_state_field(offsetof(DevState, valid), sizeof(uint64_t));
+    sadk::launch_stats(ws.ids[ws.cur].p, ws.rtab_d.p, ws.tgt_d.p, ws.fd, norm_scale(ws.fd.width, ws.fd.height),
+                       ws.stats.p, ws.cap, ws.st.p, ws.stream);
+}
+
+void prune_device(Workspace& ws, double pct) {
+    ws.zero_state_field(offsetof(DevState, n_elig), sizeof(int32_t));
+    ws.zero_state_field(offsetof(DevState, done), sizeof(int32_t));
+    if (pct <= 0) return;
+    sadk::launch_prune_keys(ws.sites(), ws.st.p, ws.stats.p, ws.cap, ws.keys[0].p, ws.vals[0].p, ws.stream);
+    ws.sort_pairs(ws.cap);
+    sadk::launch_prune_apply(ws.sites(), ws.st.p, ws.vals[1].p, pct, ws.stream);
+}
+
+void densify_device(Workspace& ws, double pct, const sad_train_config& c) {
+    ws.zero_state_field(offsetof(DevState, n_elig), sizeof(int32_t));
+    ws.zero_state_field(offsetof(DevState, done), sizeof(int32_t));
+    if (pct <= 0) return;
+    sadk::launch_densify_keys(ws.sites(), ws.st.p, ws.stats.p, ws.cap, c.alpha, c.stats_eps, ws.keys[0].p,
+                              ws.vals[0].p, ws.flags.p, ws.stream);
+    {
+        size_t bytes = ws.cub_tmp.n;
+        thrust::counting_iterator<uint32_t> it(0);
+        ck(cub::DeviceSelect::Flagged(ws.cub_tmp.p, bytes, it, ws.flags.p, ws.free_list.p, &ws.st.p->n_free, ws.cap,
+                                      ws.stream),
+           "DeviceSelect free");
+    }
+    ws.sort_pairs(ws.cap);
+    sadk::SplitHyper hp{c.log_tau_min, c.radius_min, c.aniso_min, c.aniso_max, ws.fd.width, ws.fd.height, c.max_sites};
+    sadk::launch_densify_apply(ws.sites(), ws.st.p, ws.stats.p, ws.cap, ws.vals[1].p, ws.free_list.p, ws.tgt_d.p, pct,
+                               hp, ws.m.p, ws.v.p, ws.stream);
+}
+
+// Scratch for init_sites_device, allocated once per image size.
+void ensure_init_bufs(Workspace& ws, int w, int h, int n) {
+    auto& b = ws.ib;
+    size_t np = static_cast<size_t>(w) * h;
+    if (b.np < np) {
+        b.mag.ensure(np);
+        b.gsum.ensure(1);
+        b.k0.ensure(np);
+        b.k1.ensure(np);
+        b.v0.ensure(np);
+        b.v1.ensure(np);
+        b.fl.ensure(np);
+        b.nsel.ensure(1);
+        b.jk.ensure(np / 64 + 2);
+        size_t a = 0, c = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, a, b.k0.p, b.k1.p, b.v0.p, b.v1.p, static_cast<int>(np), 0, 64,
+                                        ws.stream);
+        thrust::counting_iterator<uint32_t> it(0);
+        cub::DeviceSelect::Flagged(nullptr, c, it, b.fl.p, b.v1.p, b.nsel.p, static_cast<int>(np), ws.stream);
+        b.tmp.ensure(std::max(a, c) + 256);
+        b.np = np;
+    }
+    b.cells.ensure(static_cast<size_t>(n));
+    b.jo.ensure(static_cast<size_t>(n) / 32 + 2);
+}
+
+// init_sites (train.cpp:59-111) on the device.
+void init_sites_device(Workspace& ws, int w, int h, int n, const sad_train_config& c) {
+    size_t np = static_cast<size_t>(w) * h;
+    if (n < 1 || static_cast<size_t>(n) > np) fail(SAD_EINVAL, "init_sites: count out of range");
+    if (n > ws.cap) fail(SAD_ENOMEM, "init_sites: capacity");
+    ensure_init_bufs(ws, w, h, n);
+    auto& b = ws.ib;
+    sadk::launch_sobel(ws.tgt_d.p, w, h, b.mag.p, ws.stream);
+    ck(cudaMemsetAsync(b.gsum.p, 0, sizeof(double2), ws.stream), "memset");
+    sadk::launch_dd_sum(b.mag.p, np, b.gsum.p, ws.stream);
+    const int chunk = 64;
+    auto js = jump_states(seeded_state(c.seed, 0x1717, 0), chunk, (np + chunk - 1) / chunk);
+    ck(cudaMemcpyAsync(b.jk.p, js.data(), js.size() * 4, cudaMemcpyHostToDevice, ws.stream), "H2D jump");
+    sadk::launch_init_keys(b.mag.p, w, h, b.gsum.p, c.lambda_init, b.jk.p, chunk, b.k0.p, b.v0.p, ws.stream);
+    size_t bytes = b.tmp.n;
+    ck(cub::DeviceRadixSort::SortPairs(b.tmp.p, bytes, b.k0.p, b.k1.p, b.v0.p, b.v1.p, static_cast<int>(np), 0, 64,
+                                       ws.stream),
+       "init sort");
+    ck(cudaMemsetAsync(b.fl.p, 0, np, ws.stream), "memset");
+    sadk::launch_mark_cells(b.v1.p, n, b.fl.p, ws.stream);
+    bytes = b.tmp.n;
+    thrust::counting_iterator<uint32_t> it(0);
+    ck(cub::DeviceSelect::Flagged(b.tmp.p, bytes, it, b.fl.p, b.cells.p, b.nsel.p, static_cast<int>(np), ws.stream),
+       "init select");
+    const int chunk2 = 32;
+    auto jo_h = jump_states(seeded_state(c.seed, 0x1717, 1), 2 * chunk2, (n + chunk2 - 1) / chunk2);
+    ck(cudaMemcpyAsync(b.jo.p, jo_h.data(), jo_h.size() * 4, cudaMemcpyHostToDevice, ws.stream), "H2D jump");
+    double r0 = c.init_radius > 0 ? c.init_radius : std::sqrt(static_cast<double>(w) * h / static_cast<double>(n));
+    sadk::launch_init_sites(ws.sites(), ws.st.p, b.cells.p, n, ws.tgt_d.p, w, h, r0, c.init_log_tau, c.init_aniso,
+                            b.jo.p, chunk2, ws.stream);
+}
+
+}  // namespace
+
+// ====================================================================== context
+struct sad_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own = false;
+    Workspace ws;
+    uint64_t launches0 = 0;
+};
+
+struct sad_fit_run {
+    sad_ctx* ctx = nullptr;
+    int w = 0, h = 0;
+    sad_train_config cfg{};
+    Workspace ws;
+    bool have_target = false;
+    bool done = false;
+    std::vector<sad_history_row> hist;
+    double schedule_scale = 0;
+    size_t n_sites = 0;
+    double total_ms = 0;
+    double phase_ms[4] = {0, 0, 0, 0};
+    DBuf<double2> loss_hist;
+    DBuf<int32_t> active_hist;
+    DBuf<double2> bc_table;
+    bool bc_ready = false;
+    int planned_n0 = -1;  // plan_schedule is a pure function of (n0, target, cfg): cached
+    double planned_scale = 0;
+};
+
+extern "C" {
+
+const char* sad_last_error(void) { return g_err.c_str(); }
+int sad_abi_version(void) { return SAD_ABI_VERSION; }
+
+void sad_default_config(sad_train_config* c) {
+    std::memset(c, 0, sizeof(*c));
+    c->iters = 4000; c->n_sites = 0; c->target_bpp = 0; c->seed = 1; c->k = 8; c->inject = 4; c->lambda_init = 0.3;
+    c->lr_pos = 0.5; c->lr_color = 0.05; c->lr_log_tau = 0.05; c->lr_radius = 0.25; c->lr_dir = 0.025;
+    c->lr_aniso = 0.025; c->beta1 = 0.9; c->beta2 = 0.999; c->adam_eps = 1e-8;
+    c->refresh_every = 1; c->refresh_passes = 1; c->final_passes = 16; c->tau_diffusion_lambda = 0.0;
+    c->densify_every = 20; c->densify_start = 20; c->densify_end = 3000; c->densify_pct = 0.01; c->alpha = 0.7;
+    c->stats_eps = 1e-8; c->prune_every = 40; c->prune_start = 100; c->prune_end = 3000; c->prune_pct = 0.033;
+    c->prune_during_densify = 1; c->budget_scale_cap = 0.95; c->max_sites = 0;
+    c->init_log_tau = 7.5; c->init_radius = 0; c->init_aniso = 0;
+    c->log_tau_min = 2.0; c->log_tau_max = 20.0; c->radius_min = 1.0; c->radius_max = 512.0;
+    c->aniso_min = -2.0; c->aniso_max = 2.0; c->clamp_color = 1; c->fp64 = 1; c->threads = 1;
+}
+
+sad_status sad_ctx_create(int device, void* stream, sad_ctx** out) {
+    return guard([&] {
+        int n = 0;
+        ck(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+        if (device < 0 || device >= n) fail(SAD_ECUDA, "no such CUDA device");
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        cudaDeviceProp prop;
+        ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+        if (prop.major != 10) fail(SAD_ECUDA, "libsad_b200 is built for sm_100a (B200); device is sm_" +
+                                                  std::to_string(prop.major) + std::to_string(prop.minor));
+        auto* c = new sad_ctx();
+        c->device = device;
+        if (stream) {
+            c->stream = static_cast<cudaStream_t>(stream);
+        } else {
+            ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+            c->own = true;
+        }
+        c->ws.stream = c->stream;
+        c->ws.ensure_state();
+        c->launches0 = sadk::launch_counter();
+        *out = c;
+    });
+}
+
+void sad_ctx_destroy(sad_ctx* c) {
+    if (!c) return;
+    cudaStreamSynchronize(c->stream);
+    cudaStream_t s = c->stream;
+    bool own = c->own;
+    delete c;
+    if (own) cudaStreamDestroy(s);
+}
+
+sad_status sad_ctx_synchronize(sad_ctx* c) {
+    return guard([&] { ck(cudaStreamSynchronize(c->stream), "sync"); });
+}
+
+uint64_t sad_ctx_launch_count(const sad_ctx* c) { return sadk::launch_counter() - (c ? c->launches0 : 0); }
+
+// ====================================================================== candidates
+sad_status sad_jump_step(uint32_t t, uint32_t b, uint32_t* out) {
+    return guard([&] { *out = jump_step(t, b); });
+}
+
+sad_status sad_full_refresh_passes(int gw, int gh, int extra, sad_pass_spec* out, int* n) {
+    return guard([&] {
+        auto seq = full_refresh_passes(gw, gh, extra);
+        if (static_cast<int>(seq.size()) > *n) fail(SAD_EINVAL, "pass buffer too small");
+        std::copy(seq.begin(), seq.end(), out);
+        *n = static_cast<int>(seq.size());
+    });
+}
+
+sad_status sad_schedule_passes(int gw, int gh, int total, sad_pass_spec* out, int* n) {
+    return guard([&] {
+        auto seq = schedule_passes(gw, gh, total);
+        if (static_cast<int>(seq.size()) > *n) fail(SAD_EINVAL, "pass buffer too small");
+        std::copy(seq.begin(), seq.end(), out);
+        *n = static_cast<int>(seq.size());
+    });
+}
+
+sad_status sad_jfa_seed(sad_ctx* c, const sad_sites_view* s, sad_field_view* f) {
+    return guard([&] {
+        Workspace& ws = c->ws;
+        upload_sites(ws, s);
+        check_field(f);
+        ws.ensure_field(f->width, f->height, f->k, f->cell);
+        ws.cur = 0;
+        sadk::launch_jfa_seed(ws.sites(), ws.st.p, ws.ids[0].p, ws.fd, norm_scale(f->width, f->height), ws.stream);
+        download_field(ws, f);
+        f->synced_generation = s->generation;
+    });
+}
+
+static void run_passes_call(sad_ctx* c, const sad_sites_view* s, sad_field_view* f, const std::vector<sad_pass_spec>& seq,
+                            int inject, uint64_t seed, int fp64, bool full) {
+    Workspace& ws = c->ws;
+    upload_sites(ws, s);
+    if (full) {
+        check_field(f);
+        ws.ensure_field(f->width, f->height, f->k, f->cell);
+        ws.cur = 0;
+        sadk::launch_jfa_seed(ws.sites(), ws.st.p, ws.ids[0].p, ws.fd, norm_scale(f->width, f->height), ws.stream);
+    } else {
+        upload_field(ws, f);
+    }
+    ws.patch_state(offsetof(DevState, pass_index), f->pass_index);
+    ws.compute_active();
+    build_tables(ws, fp64 != 0, true, false, false);
+    passes_device(ws, seq, inject, seed, fp64 != 0, 0);
+    download_field(ws, f);
+    f->pass_index += static_cast<uint32_t>(seq.size());
+    f->synced_generation = s->generation;
+}
+
+sad_status sad_run_passes(sad_ctx* c, const sad_sites_view* s, sad_field_view* f, const sad_pass_spec* seq, int n_pass,
+                          int inject, uint64_t seed, int fp64) {
+    return guard([&] {
+        check_field(f);
+        std::vector<sad_pass_spec> v(seq, seq + std::max(n_pass, 0));
+        run_passes_call(c, s, f, v, inject, seed, fp64, false);
+    });
+}
+
+sad_status sad_refresh(sad_ctx* c, const sad_sites_view* s, sad_field_view* f, int mode, int passes, int inject,
+                       uint64_t seed, int fp64) {
+    return guard([&] {
+        check_field(f);
+        if (mode == SAD_REFRESH_FULL) {
+            run_passes_call(c, s, f, full_refresh_passes(f->gw, f->gh, passes), inject, seed, fp64, true);
+        } else {
+            std::vector<sad_pass_spec> v(static_cast<size_t>(passes < 0 ? 0 : passes), sad_pass_spec{1, 0});
+            run_passes_call(c, s, f, v, inject, seed, fp64, false);
+        }
+        f->refresh_count++;
+    });
+}
+
+sad_status sad_exact_topk_batch(sad_ctx* c, const sad_sites_view* s, const int32_t* xy, size_t n_pix, int k,
+                                double scale, int fp64, uint32_t* out) {
+    return guard([&] {
+        if (k < 1 || k > 16) fail(SAD_EINVAL, "exact_topk: k out of range");
+        Workspace& ws = c->ws;
+        upload_sites(ws, s);
+        ws.compute_active();
+        // tables use the probe scale supplied by the caller
+        sadk::launch_tables(fp64 != 0, ws.sites(), ws.st.p, scale, nullptr, nullptr, fp64 ? ws.rtab_d.p : ws.rtab.p,
+                            ws.stream);
+        DevState st = ws.get_state();
+        DBuf<int32_t> dxy;
+        DBuf<uint32_t> dout;
+        dxy.ensure(2 * n_pix);
+        dout.ensure(n_pix * k);
+        ck(cudaMemcpyAsync(dxy.p, xy, 8 * n_pix, cudaMemcpyHostToDevice, ws.stream), "H2D");
+        sadk::launch_exact_topk(fp64 != 0, fp64 ? ws.rtab_d.p : ws.rtab.p, ws.act.p, st.n_active, dxy.p,
+                                static_cast<int>(n_pix), k, scale, dout.p, ws.stream);
+        ck(cudaMemcpyAsync(out, dout.p, 4 * n_pix * k, cudaMemcpyDeviceToHost, ws.stream), "D2H");
+        ck(cudaStreamSynchronize(ws.stream), "sync");
+    });
+}
+
+// ====================================================================== render
+sad_status sad_render_image(sad_ctx* c, const sad_sites_view* s, const sad_field_view* f, int fp64, double* out) {
+    return guard([&] {
+        check_synced(s, f);
+        Workspace& ws = c->ws;
+        upload_sites(ws, s);
+        upload_field(ws, f);
+        build_tables(ws, fp64 != 0, false, false, true);
+        size_t n = 3 * static_cast<size_t>(f->width) * f->height;
+        if (fp64) {
+            ws.px_d.ensure(n);
+            sadk::launch_render(true, ws.ids[ws.cur].p, ws.rtab_d.p, ws.fd, norm_scale(f->width, f->height), ws.px_d.p,
+                                ws.st.p, ws.stream);
+            ck(cudaMemcpyAsync(out, ws.px_d.p, n * 8, cudaMemcpyDeviceToHost, ws.stream), "D2H render");
+            check_err(ws, "render");
+        } else {
+            ws.px_f.ensure(n);
+            sadk::launch_render(false, ws.ids[ws.cur].p, ws.rtab.p, ws.fd, norm_scale(f->width, f->height), ws.px_f.p,
+                                ws.st.p, ws.stream);
+            std::vector<float> tmp(n);
+            ck(cudaMemcpyAsync(tmp.data(), ws.px_f.p, n * 4, cudaMemcpyDeviceToHost, ws.stream), "D2H render");
+            check_err(ws, "render");
+            for (size_t i = 0; i < n; i++) out[i] = tmp[i];
+        }
+    });
+}
+
+sad_status sad_pixel_weights(sad_ctx* c, const sad_sites_view* s, const sad_field_view* f, const int32_t* xy,
+                             size_t n_q, uint32_t* ids, double* w, int32_t* n) {
+    return guard([&] {
+        check_synced(s, f);
+        for (size_t q = 0; q < n_q; q++)
+            if (xy[2 * q] < 0 || xy[2 * q + 1] < 0 || xy[2 * q] >= f->width || xy[2 * q + 1] >= f->height)
+                fail(SAD_EINVAL, "pixel_weights: pixel out of bounds");
+        Workspace& ws = c->ws;
+        upload_sites(ws, s);
+        upload_field(ws, f);
+        build_tables(ws, true, false, false, true);
+        DBuf<int32_t> dxy, dn;
+        DBuf<uint32_t> did;
+        DBuf<double> dw;
+        dxy.ensure(2 * n_q);
+        dn.ensure(n_q);
+        did.ensure(16 * n_q);
+        dw.ensure(16 * n_q);
+        ck(cudaMemcpyAsync(dxy.p, xy, 8 * n_q, cudaMemcpyHostToDevice, ws.stream), "H2D");
+        sadk::launch_pixel_weights(ws.ids[ws.cur].p, ws.rtab_d.p, ws.fd, norm_scale(f->width, f->height), dxy.p,
+                                   static_cast<int>(n_q), did.p, dw.p, dn.p, ws.stream);
+        ck(cudaMemcpyAsync(ids, did.p, 64 * n_q, cudaMemcpyDeviceToHost, ws.stream), "D2H");
+        ck(cudaMemcpyAsync(w, dw.p, 128 * n_q, cudaMemcpyDeviceToHost, ws.stream), "D2H");
+        ck(cudaMemcpyAsync(n, dn.p, 4 * n_q, cudaMemcpyDeviceToHost, ws.stream), "D2H");
+        ck(cudaStreamSynchronize(ws.stream), "sync");
+        for (size_t q = 0; q < n_q; q++)
+            if (n[q] == 0) fail(SAD_EEMPTY, "pixel_weights: empty candidate list");
+    });
+}
+
+sad_status sad_render_id_map(sad_ctx* c, const sad_sites_view* s, const sad_field_view* f, uint32_t* out) {
+    return guard([&] {
+        check_synced(s, f);
+        Workspace& ws = c->ws;
+        upload_sites(ws, s);
+        upload_field(ws, f);
+        build_tables(ws, true, false, false, true);
+        DBuf<uint32_t> d;
+        size_t n = static_cast<size_t>(f->width) * f->height;
+        d.ensure(n);
+        sadk::launch_id_map(ws.ids[ws.cur].p, ws.rtab_d.p, ws.fd, norm_scale(f->width, f->height), d.p, ws.st.p,
+                            ws.stream);
+        ck(cudaMemcpyAsync(out, d.p, 4 * n, cudaMemcpyDeviceToHost, ws.stream), "D2H");
+        check_err(ws, "render");
+    });
+}
+
+// ====================================================================== grad
+static void backward_call(sad_ctx* c, const sad_sites_view* s, const sad_field_view* f, const double* img, int fp64,
+                          int mode, double* grads, uint64_t* nonfinite, double* loss) {
+    check_synced(s, f);
+    Workspace& ws = c->ws;
+    upload_sites(ws, s);
+    upload_field(ws, f);
+    size_t npx = static_cast<size_t>(f->width) * f->height;
+    ws.ensure_target(npx);
+    ck(cudaMemcpyAsync(ws.tgt_d.p, img, 24 * npx, cudaMemcpyHostToDevice, ws.stream), "H2D target");
+    if (!fp64) sadk::launch_f64_to_f32(ws.tgt_d.p, ws.tgt_f.p, 3 * npx, ws.stream);
+    build_tables(ws, fp64 != 0, false, true, false);
+    ck(cudaMemsetAsync(ws.grads.p, 0, sizeof(double2) * 11 * ws.cap, ws.stream), "memset grads");
+    ws.zero_state_field(offsetof(DevState, nonfinite), sizeof(uint64_t));
+    ws.zero_state_field(offsetof(DevState, loss), sizeof(double2));
+    sadk::launch_backward(fp64 != 0, mode, ws.ids[ws.cur].p, ws.gtab.p,
+                          fp64 ? static_cast<const void*>(ws.tgt_d.p) : static_cast<const void*>(ws.tgt_f.p), ws.fd,
+                          norm_scale(f->width, f->height), ws.grads.p, ws.cap, ws.st.p, ws.stream);
+    DBuf<double> out;
+    size_t n = s->size;
+    out.ensure(std::max<size_t>(n, 1) * 11);
+    if (n) sadk::launch_scatter_grads_out(ws.grads.p, ws.cap, static_cast<int>(n), out.p, ws.stream);
+    if (n) ck(cudaMemcpyAsync(grads, out.p, n * 11 * 8, cudaMemcpyDeviceToHost, ws.stream), "D2H grads");
+    DevState st = ws.get_state();
+    if (st.err & 1) {
+        ws.zero_state_field(offsetof(DevState, err), sizeof(int32_t));
+        fail(SAD_EEMPTY, "backward: empty candidate list at a pixel");
+    }
+    if (nonfinite) *nonfinite = st.nonfinite;
+    if (loss) *loss = (st.loss.x + st.loss.y) / (static_cast<double>(f->width) * f->height);
+}
+
+sad_status sad_backward_image(sad_ctx* c, const sad_sites_view* s, const sad_field_view* f, const double* tgt, int fp64,
+                              int with_removal, double* grads, uint64_t* nonfinite, double* loss) {
+    return guard([&] { backward_call(c, s, f, tgt, fp64, with_removal ? 1 : 0, grads, nonfinite, loss); });
+}
+
+sad_status sad_backward_pixel_grad(sad_ctx* c, const sad_sites_view* s, const sad_field_view* f, const double* dl,
+                                   int fp64, double* grads, uint64_t* nonfinite) {
+    return guard([&] { backward_call(c, s, f, dl, fp64, 2, grads, nonfinite, nullptr); });
+}
+
+sad_status sad_image_loss(sad_ctx* c, const sad_sites_view* s, const sad_field_view* f, const double* tgt, int fp64,
+                          double* loss) {
+    return guard([&] {
+        check_synced(s, f);
+        Workspace& ws = c->ws;
+        upload_sites(ws, s);
+        upload_field(ws, f);
+        upload_target(ws, tgt, f->width, f->height);
+        build_tables(ws, fp64 != 0, false, true, false);
+        ws.zero_state_field(offsetof(DevState, loss), sizeof(double2));
+        sadk::launch_loss(fp64 != 0, ws.ids[ws.cur].p, ws.gtab.p,
+                          fp64 ? static_cast<const void*>(ws.tgt_d.p) : static_cast<const void*>(ws.tgt_f.p), ws.fd,
+                          norm_scale(f->width, f->height), ws.st.p, ws.stream);
+        DevState st = ws.get_state();
+        if (st.err & 1) {
+            ws.zero_state_field(offsetof(DevState, err), sizeof(int32_t));
+            fail(SAD_EEMPTY, "loss: empty candidate list at a pixel");
+        }
+        *loss = (st.loss.x + st.loss.y) / (static_cast<double>(f->width) * f->height);
+    });
+}
+
+// ====================================================================== train
+sad_status sad_adam_step(sad_ctx* c, sad_sites_view* s, const double* grads, sad_adam_view* a, int w, int h,
+                         const sad_train_config* cfg) {
+    return guard([&] {
+        Workspace& ws = c->ws;
+        size_t n = s->size;
+        if (a->sites != n && n > a->capacity) fail(SAD_ENOMEM, "adam capacity");
+        upload_sites(ws, s);
+        // grads (n*11 values) -> (hi=value, lo=0) accumulators; moments -> slot-major
+        std::vector<double2> g(static_cast<size_t>(11) * ws.cap, make_double2(0, 0));
+        std::vector<double> m(static_cast<size_t>(10) * ws.cap, 0.0), v(static_cast<size_t>(10) * ws.cap, 0.0);
+        for (size_t id = 0; id < n; id++) {
+            for (int k = 0; k < 11; k++) g[k * ws.cap + id] = make_double2(grads[id * 11 + k], 0.0);
+            if (id < a->sites)
+                for (int k = 0; k < 10; k++) {
+                    m[k * ws.cap + id] = a->m[id * 10 + k];
+                    v[k * ws.cap + id] = a->v[id * 10 + k];
+                }
+        }
+        ck(cudaMemcpyAsync(ws.grads.p, g.data(), g.size() * sizeof(double2), cudaMemcpyHostToDevice, ws.stream), "H2D");
+        ck(cudaMemcpyAsync(ws.m.p, m.data(), m.size() * 8, cudaMemcpyHostToDevice, ws.stream), "H2D");
+        ck(cudaMemcpyAsync(ws.v.p, v.data(), v.size() * 8, cudaMemcpyHostToDevice, ws.stream), "H2D");
+        ws.zero_state_field(offsetof(DevState, skipped), sizeof(uint64_t));
+        int64_t t = a->t + 1;
+        double2 bc = make_double2(1.0 - std::pow(cfg->beta1, static_cast<double>(t)),
+                                  1.0 - std::pow(cfg->beta2, static_cast<double>(t)));
+        sadk::launch_adam(false, ws.sites(), ws.st.p, ws.grads.p, ws.m.p, ws.v.p, adam_hyper(*cfg, w, h), nullptr, bc,
+                          false, 1.0, nullptr, nullptr, ws.stream);
+        ck(cudaMemcpyAsync(m.data(), ws.m.p, m.size() * 8, cudaMemcpyDeviceToHost, ws.stream), "D2H");
+        ck(cudaMemcpyAsync(v.data(), ws.v.p, v.size() * 8, cudaMemcpyDeviceToHost, ws.stream), "D2H");
+        DevState st = ws.get_state();
+        download_sites(ws, s, n);
+        for (size_t id = 0; id < n; id++)
+            for (int k = 0; k < 10; k++) {
+                a->m[id * 10 + k] = m[k * ws.cap + id];
+                a->v[id * 10 + k] = v[k * ws.cap + id];
+            }
+        a->sites = n;
+        a->t = t;
+        a->skipped += st.skipped;
+        s->generation += 2;  // adam_step and clamp_project each bump (train.cpp:167, 136)
+    });
+}
+
+sad_status sad_clamp_project(sad_ctx* c, sad_sites_view* s, int w, int h, const sad_train_config* cfg) {
+    return guard([&] {
+        Workspace& ws = c->ws;
+        upload_sites(ws, s);
+        sadk::launch_clamp(ws.sites(), ws.st.p, adam_hyper(*cfg, w, h), ws.stream);
+        download_sites(ws, s, s->size);
+        s->generation += 1;
+    });
+}
+
+sad_status sad_init_sites(sad_ctx* c, sad_sites_view* s, const double* tgt, int w, int h, int n,
+                          const sad_train_config* cfg) {
+    return guard([&] {
+        size_t np = static_cast<size_t>(w) * h;
+        if (w < 1 || h < 1) fail(SAD_EINVAL, "init_sites: empty image");
+        if (n < 1 || static_cast<size_t>(n) > np) fail(SAD_EINVAL, "init_sites: count out of range");
+        if (static_cast<size_t>(n) > s->capacity) fail(SAD_ENOMEM, "sites view capacity too small");
+        Workspace& ws = c->ws;
+        ws.ensure_cap(n);
+        upload_target(ws, tgt, w, h);
+        init_sites_device(ws, w, h, n, *cfg);
+        download_sites(ws, s, static_cast<size_t>(n));
+        s->generation += 1 + static_cast<uint64_t>(n);
+    });
+}
+
+// ====================================================================== budget
+sad_status sad_accumulate_stats(sad_ctx* c, const sad_sites_view* s, const sad_field_view* f, const double* tgt,
+                                double* stats, uint64_t* valid) {
+    return guard([&] {
+        if (f->synced_generation != s->generation) fail(SAD_ESTALE, "stats: candidate field is stale");
+        Workspace& ws = c->ws;
+        upload_sites(ws, s);
+        upload_field(ws, f);
+        upload_target(ws, tgt, f->width, f->height);
+        stats_device(ws);
+        size_t n = s->size;
+        std::vector<double2> h(static_cast<size_t>(8) * ws.cap);
+        ck(cudaMemcpyAsync(h.data(), ws.stats.p, h.size() * sizeof(double2), cudaMemcpyDeviceToHost, ws.stream), "D2H");
+        DevState st = ws.get_state();
+        for (size_t id = 0; id < n; id++)
+            for (int k = 0; k < 8; k++) stats[id * 8 + k] = h[k * ws.cap + id].x + h[k * ws.cap + id].y;
+        *valid = st.valid;
+    });
+}
+
+static void upload_stats(Workspace& ws, const double* stats, size_t n, uint64_t valid) {
+    std::vector<double2> h(static_cast<size_t>(8) * ws.cap, make_double2(0, 0));
+    for (size_t id = 0; id < n; id++)
+        for (int k = 0; k < 8; k++) h[k * ws.cap + id] = make_double2(stats[id * 8 + k], 0.0);
+    ck(cudaMemcpyAsync(ws.stats.p, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice, ws.stream), "H2D");
+    ws.patch_state(offsetof(DevState, valid), valid);
+}
+
+sad_status sad_prune(sad_ctx* c, sad_sites_view* s, const double* stats, uint64_t valid, double pct, int* removed) {
+    return guard([&] {
+        *removed = 0;
+        if (pct <= 0) return;
+        if (pct > 1) fail(SAD_EINVAL, "prune: percentile out of (0,1]");
+        Workspace& ws = c->ws;
+        upload_sites(ws, s);
+        upload_stats(ws, stats, s->size, valid);
+        prune_device(ws, pct);
+        DevState st = ws.get_state();
+        download_sites(ws, s, s->size);
+        *removed = st.done;
+        s->generation += static_cast<uint64_t>(st.done);
+    });
+}
+
+sad_status sad_densify(sad_ctx* c, sad_sites_view* s, sad_adam_view* a, const double* stats, const double* tgt, int w,
+                       int h, double pct, const sad_train_config* cfg, int* done) {
+    return guard([&] {
+        *done = 0;
+        if (pct <= 0) return;
+        if (pct > 1) fail(SAD_EINVAL, "densify: percentile out of (0,1]");
+        Workspace& ws = c->ws;
+        size_t n = s->size;
+        int room = static_cast<int>(std::min(s->capacity, a->capacity)) - static_cast<int>(n);
+        upload_sites(ws, s, std::max(room, 0));
+        upload_stats(ws, stats, n, 0);
+        upload_target(ws, tgt, w, h);
+        std::vector<double> m(static_cast<size_t>(10) * ws.cap, 0.0), v(static_cast<size_t>(10) * ws.cap, 0.0);
+        for (size_t id = 0; id < std::min(n, a->sites); id++)
+            for (int k = 0; k < 10; k++) {
+                m[k * ws.cap + id] = a->m[id * 10 + k];
+                v[k * ws.cap + id] = a->v[id * 10 + k];
+            }
+        ck(cudaMemcpyAsync(ws.m.p, m.data(), m.size() * 8, cudaMemcpyHostToDevice, ws.stream), "H2D");
+        ck(cudaMemcpyAsync(ws.v.p, v.data(), v.size() * 8, cudaMemcpyHostToDevice, ws.stream), "H2D");
+        ws.fd.width = w;
+        ws.fd.height = h;
+        // densify only ever appends into [n, n + room); slots beyond the caller's capacity flag ENOMEM
+        densify_device(ws, pct, *cfg);
+        DevState st = ws.get_state();
+        if (st.err & 2) {
+            ws.zero_state_field(offsetof(DevState, err), sizeof(int32_t));
+            fail(SAD_ENOMEM, "densify: sites capacity");
+        }
+        size_t nn = static_cast<size_t>(st.n_sites);
+        if (nn > s->capacity || nn > a->capacity) fail(SAD_ENOMEM, "densify: sites capacity");
+        ck(cudaMemcpyAsync(m.data(), ws.m.p, m.size() * 8, cudaMemcpyDeviceToHost, ws.stream), "D2H");
+        ck(cudaMemcpyAsync(v.data(), ws.v.p, v.size() * 8, cudaMemcpyDeviceToHost, ws.stream), "D2H");
+        download_sites(ws, s, nn);
+        size_t rows = std::max(nn, a->sites);
+        for (size_t id = 0; id < rows; id++)
+            for (int k = 0; k < 10; k++) {
+                a->m[id * 10 + k] = id < nn ? m[k * ws.cap + id] : a->m[id * 10 + k];
+                a->v[id * 10 + k] = id < nn ? v[k * ws.cap + id] : a->v[id * 10 + k];
+            }
+        a->sites = rows;
+        *done = st.done;
+        s->generation += 2 * static_cast<uint64_t>(st.done);
+    });
+}
+
+sad_status sad_bpp_target_count(double bpp, int w, int h, uint64_t* out) {
+    return guard([&] { *out = bpp_target_count(bpp, w, h); });
+}
+
+sad_status sad_simulate_schedule(int n0, double scale, const sad_train_config* cfg, int* out) {
+    return guard([&] { *out = simulate_schedule(n0, scale, *cfg); });
+}
+
+sad_status sad_plan_schedule(int n0, uint64_t target, const sad_train_config* cfg, double* out) {
+    return guard([&] { *out = plan_schedule(n0, target, *cfg); });
+}
+
+// ====================================================================== resident fit
+static int initial_count(const sad_train_config& c, int w, int h);
+static int capacity_bound(const sad_train_config& c, int n0, double scale, bool budget);
+
+sad_status sad_fit_create(sad_ctx* c, int w, int h, const sad_train_config* cfg, sad_fit_run** out) {
+    return guard([&] {
+        sad_train_config v = *cfg;
+        validate(v, w, h);
+        auto* r = new sad_fit_run();
+        try {
+            r->ctx = c;
+            r->w = w;
+            r->h = h;
+            r->cfg = v;
+            r->ws.stream = c->stream;
+            r->ws.ensure_state();
+            r->ws.ensure_field(w, h, v.k, 1);
+            r->ws.ensure_target(static_cast<size_t>(w) * h);
+            // Pre-size everything fit() needs so the run itself never allocates.
+            if (v.n_sites > 0 || v.target_bpp > 0) {
+                int n0 = initial_count(v, w, h);
+                double sched = v.target_bpp > 0 ? plan_schedule(n0, bpp_target_count(v.target_bpp, w, h), v) : 1.0;
+                r->planned_n0 = n0;
+                r->planned_scale = sched;
+                r->ws.ensure_cap(capacity_bound(v, n0, sched, v.target_bpp > 0));
+                ensure_init_bufs(r->ws, w, h, n0);
+            }
+            r->loss_hist.ensure(std::max(v.iters, 1));
+            r->active_hist.ensure(std::max(v.iters, 1));
+            std::vector<double2> bc(static_cast<size_t>(v.iters) + 2);
+            for (int t = 1; t <= v.iters + 1; t++)
+                bc[t] = make_double2(1.0 - std::pow(v.beta1, static_cast<double>(t)),
+                                     1.0 - std::pow(v.beta2, static_cast<double>(t)));
+            r->bc_table.ensure(bc.size());
+            ck(cudaMemcpy(r->bc_table.p, bc.data(), bc.size() * sizeof(double2), cudaMemcpyHostToDevice), "H2D bc");
+            r->bc_ready = true;
+            ck(cudaStreamSynchronize(r->ws.stream), "sync");
+        } catch (...) {
+            delete r;
+            throw;
+        }
+        *out = r;
+    });
+}
+
+void sad_fit_destroy(sad_fit_run* r) {
+    if (!r) return;
+    cudaStreamSynchronize(r->ws.stream);
+    delete r;
+}
+
+sad_status sad_fit_set_target(sad_fit_run* r, const double* rgb) {
+    return guard([&] {
+        upload_target(r->ws, rgb, r->w, r->h);
+        r->have_target = true;
+    });
+}
+
+sad_status sad_fit_set_target_device(sad_fit_run* r, const double* drgb) {
+    return guard([&] {
+        size_t n = 3 * static_cast<size_t>(r->w) * r->h;
+        ck(cudaMemcpyAsync(r->ws.tgt_d.p, drgb, n * 8, cudaMemcpyDeviceToDevice, r->ws.stream), "D2D target");
+        sadk::launch_f64_to_f32(r->ws.tgt_d.p, r->ws.tgt_f.p, n, r->ws.stream);
+        r->have_target = true;
+    });
+}
+
+static int initial_count(const sad_train_config& c, int w, int h) {
+    int n = c.n_sites;
+    if (n == 0 && c.target_bpp > 0) {
+        uint64_t want = bpp_target_count(c.target_bpp, w, h);
+        if (want < 1) fail(SAD_EINVAL, "fit: bpp target below one site");
+        size_t n0 = static_cast<size_t>(std::ceil(static_cast<double>(want) * 1.6));
+        n = static_cast<int>(std::min(n0, static_cast<size_t>(w) * h));
+    }
+    if (n < 1) fail(SAD_EINVAL, "fit: site count unset");
+    return n;
+}
+
+// Upper bound of SiteStore::size over the run: each densify event appends at most
+// floor(size * pct * scale) slots (budget.cpp:230, 277).
+static int capacity_bound(const sad_train_config& c, int n0, double scale, bool budget) {
+    double n = n0;
+    if (budget)
+        for (int t = 1; t <= c.iters; t++)
+            if (t >= c.densify_start && t <= c.densify_end && t % c.densify_every == 0)
+                n += std::floor(n * c.densify_pct * std::max(scale, 0.0));
+    if (c.max_sites > 0) n = std::min(n, static_cast<double>(std::max<uint64_t>(c.max_sites, n0)));
+    return static_cast<int>(n) + 1;
+}
+
+// fit_impl (train.cpp:221-291), resident in HBM.
+static void fit_loop(sad_fit_run* r) {
+    Workspace& ws = r->ws;
+    const sad_train_config& c = r->cfg;
+    const int w = r->w, h = r->h;
+    const bool fp64 = c.fp64 != 0;
+    const bool budget = c.target_bpp > 0;
+    const double scale_n = norm_scale(w, h);
+    cudaStream_t s = ws.stream;
+
+    DevState st0 = ws.get_state();
+    ws.compute_active();
+    DevState sta = ws.get_state();
+    double sched = 1.0;
+    r->schedule_scale = 0;
+    if (budget) {
+        if (sta.n_active != r->planned_n0) {
+            r->planned_scale = plan_schedule(sta.n_active, bpp_target_count(c.target_bpp, w, h), c);
+            r->planned_n0 = sta.n_active;
+        }
+        sched = r->planned_scale;
+        r->schedule_scale = sched;
+    }
+    int capn = capacity_bound(c, st0.n_sites, sched, budget);
+    if (capn > ws.cap) {
+        ws.ensure_cap(capn);  // reallocates the active list: rebuild it
+        ws.compute_active();
+        sta = ws.get_state();
+    }
+    // fresh optimiser and accumulators
+    ck(cudaMemsetAsync(ws.m.p, 0, sizeof(double) * 10 * ws.cap, s), "memset m");
+    ck(cudaMemsetAsync(ws.v.p, 0, sizeof(double) * 10 * ws.cap, s), "memset v");
+    ck(cudaMemsetAsync(ws.grads.p, 0, sizeof(double2) * 11 * ws.cap, s), "memset grads");
+    DevState init{};
+    init.n_sites = st0.n_sites;
+    init.n_active = sta.n_active;
+    ws.set_state(init);
+
+    const sadk::AdamHyper hp = adam_hyper(c, w, h);
+    const auto full4 = full_refresh_passes(ws.fd.gw, ws.fd.gh, 4);
+    const std::vector<sad_pass_spec> warm(static_cast<size_t>(c.refresh_passes), sad_pass_spec{1, 0});
+    const void* tgt = fp64 ? static_cast<const void*>(ws.tgt_d.p) : static_cast<const void*>(ws.tgt_f.p);
+
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, s);
+
+    // initial full refresh (train.cpp:238-239)
+    build_tables(ws, fp64, true, true, false);
+    ws.cur = 0;
+    sadk::launch_jfa_seed(ws.sites(), ws.st.p, ws.ids[0].p, ws.fd, scale_n, s);
+    passes_device(ws, full4, c.inject, c.seed, fp64, 0);
+    sadk::launch_advance(ws.st.p, static_cast<int>(full4.size()), 0, nullptr, nullptr, s);
+
+    for (int t = 1; t <= c.iters; t++) {
+        int npass = 0;
+        if ((t - 1) % c.refresh_every == 0) {
+            passes_device(ws, warm, c.inject, c.seed, fp64, 0);
+            npass += static_cast<int>(warm.size());
+        }
+        sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt, ws.fd, scale_n, ws.grads.p, ws.cap, ws.st.p, s);
+        bool ev_d = budget && t >= c.densify_start && t <= c.densify_end && t % c.densify_every == 0;
+        bool ev_p = budget && t >= c.prune_start && t <= c.prune_end && t % c.prune_every == 0;
+        if (ev_p && !c.prune_during_densify && t <= c.densify_end) ev_p = false;
+        bool ev = ev_d || ev_p;
+        if (ev) stats_device(ws);
+        sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.grads.p, ws.m.p, ws.v.p, hp, r->bc_table.p, make_double2(0, 0),
+                          true, scale_n, ev ? nullptr : ws.pack.p, ev ? nullptr : ws.gtab.p, s);
+        if (ev_p) prune_device(ws, c.prune_pct * sched);
+        if (ev_d) densify_device(ws, c.densify_pct * sched, c);
+        if (ev) {
+            ws.compute_active();
+            build_tables(ws, fp64, true, true, false);
+            ws.cur = 0;
+            sadk::launch_jfa_seed(ws.sites(), ws.st.p, ws.ids[0].p, ws.fd, scale_n, s);
+            passes_device(ws, full4, c.inject, c.seed, fp64, static_cast<uint32_t>(npass));
+            npass += static_cast<int>(full4.size());
+        }
+        sadk::launch_advance(ws.st.p, npass, 1, r->loss_hist.p, r->active_hist.p, s);
+    }
+    // final full refresh (train.cpp:287)
+    const auto fin = full_refresh_passes(ws.fd.gw, ws.fd.gh, c.final_passes);
+    ws.cur = 0;
+    sadk::launch_jfa_seed(ws.sites(), ws.st.p, ws.ids[0].p, ws.fd, scale_n, s);
+    passes_device(ws, fin, c.inject, c.seed, fp64, 0);
+    sadk::launch_advance(ws.st.p, static_cast<int>(fin.size()), 0, nullptr, nullptr, s);
+    cudaEventRecord(e1, s);
+    ck(cudaStreamSynchronize(s), "fit");
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    r->total_ms = ms;
+
+    DevState fs = ws.get_state();
+    r->n_sites = static_cast<size_t>(fs.n_sites);
+    std::vector<double2> lh(std::max(c.iters, 1));
+    std::vector<int32_t> ah(std::max(c.iters, 1));
+    ck(cudaMemcpy(lh.data(), r->loss_hist.p, lh.size() * sizeof(double2), cudaMemcpyDeviceToHost), "D2H hist");
+    ck(cudaMemcpy(ah.data(), r->active_hist.p, ah.size() * 4, cudaMemcpyDeviceToHost), "D2H hist");
+    r->hist.resize(c.iters);
+    const double npx = static_cast<double>(w) * h;
+    for (int t = 0; t < c.iters; t++) {
+        double loss = (lh[t].x + lh[t].y) / npx;
+        double m = loss / 3.0;
+        double ps = m <= 0 ? 99.0 : std::min(99.0, 10.0 * std::log10(1.0 / m));
+        r->hist[t] = sad_history_row{t + 1, loss, ps, ah[t], ms / std::max(c.iters, 1)};
+    }
+    r->done = true;
+    if (fs.err & 1) fail(SAD_EEMPTY, "backward: empty candidate list at a pixel");
+    if (fs.err & 2) fail(SAD_ENOMEM, "fit: site capacity exhausted");
+    for (int t = 0; t < c.iters; t++)
+        if (!std::isfinite(r->hist[t].loss)) fail(SAD_ENUMERIC, "fit: non-finite loss");
+}
+
+sad_status sad_fit_run_init(sad_fit_run* r) {
+    return guard([&] {
+        if (!r->have_target) fail(SAD_EINVAL, "fit: target not set");
+        int n = initial_count(r->cfg, r->w, r->h);
+        r->ws.ensure_cap(n);
+        init_sites_device(r->ws, r->w, r->h, n, r->cfg);
+        fit_loop(r);
+    });
+}
+
+sad_status sad_fit_run_store(sad_fit_run* r, const sad_sites_view* s) {
+    return guard([&] {
+        if (!r->have_target) fail(SAD_EINVAL, "fit: target not set");
+        upload_sites(r->ws, s);
+        fit_loop(r);
+    });
+}
+
+sad_status sad_fit_info(sad_fit_run* r, size_t* n, int* nh, double* sc) {
+    return guard([&] {
+        if (!r->done) fail(SAD_EINVAL, "fit: not run");
+        *n = r->n_sites;
+        *nh = static_cast<int>(r->hist.size());
+        *sc = r->schedule_scale;
+    });
+}
+
+sad_status sad_fit_download(sad_fit_run* r, sad_sites_view* s, sad_field_view* f, sad_history_row* hist) {
+    return guard([&] {
+        if (!r->done) fail(SAD_EINVAL, "fit: not run");
+        download_sites(r->ws, s, r->n_sites);
+        if (f) {
+            f->width = r->w;
+            f->height = r->h;
+            f->cell = 1;
+            f->gw = r->ws.fd.gw;
+            f->gh = r->ws.fd.gh;
+            f->k = r->ws.fd.k;
+            download_field(r->ws, f);
+            DevState st = r->ws.get_state();
+            f->pass_index = st.pass_index;
+            f->synced_generation = s->generation;
+            f->refresh_count = 0;
+        }
+        if (hist) std::copy(r->hist.begin(), r->hist.end(), hist);
+    });
+}
+
+sad_status sad_fit_render_device(sad_fit_run* r, float* out) {
+    return guard([&] {
+        Workspace& ws = r->ws;
+        build_tables(ws, false, false, false, true);
+        sadk::launch_render(false, ws.ids[ws.cur].p, ws.rtab.p, ws.fd, norm_scale(r->w, r->h), out, ws.st.p, ws.stream);
+    });
+}
+
+// Micro-benchmark of one kernel on the fitted, device-resident state (roofline evidence).
+// which: 0 warm propagate pass, 1 fused fwd+bwd, 2 render, 3 Box3 flood pass (step 16), 4 Adam, 5 stats.
+sad_status sad_fit_bench(sad_fit_run* r, int which, int reps, double* ms_per_launch) {
+    return guard([&] {
+        if (!r->done) fail(SAD_EINVAL, "fit: not run");
+        Workspace& ws = r->ws;
+        const sad_train_config& c = r->cfg;
+        const bool fp64 = c.fp64 != 0;
+        const double sn = norm_scale(r->w, r->h);
+        cudaStream_t s = ws.stream;
+        build_tables(ws, fp64, true, true, false);
+        build_tables(ws, false, false, false, true);
+        ws.px_f.ensure(3 * static_cast<size_t>(r->w) * r->h);
+        const void* tgt = fp64 ? static_cast<const void*>(ws.tgt_d.p) : static_cast<const void*>(ws.tgt_f.p);
+        sadk::AdamHyper hp = adam_hyper(c, r->w, r->h);
+        auto once = [&]() {
+            switch (which) {
+            case 0: passes_device(ws, {sad_pass_spec{1, 0}}, c.inject, c.seed, fp64, 0); break;
+            case 1:
+                sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt, ws.fd, sn, ws.grads.p, ws.cap,
+                                      ws.st.p, s);
+                break;
+            case 2: sadk::launch_render(false, ws.ids[ws.cur].p, ws.rtab.p, ws.fd, sn, ws.px_f.p, ws.st.p, s); break;
+            case 3: passes_device(ws, {sad_pass_spec{16, 1}}, c.inject, c.seed, fp64, 0); break;
+            case 4:
+                sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.grads.p, ws.m.p, ws.v.p, hp, nullptr,
+                                  make_double2(1.0, 1.0), true, sn, ws.pack.p, ws.gtab.p, s);
+                break;
+            case 5: stats_device(ws); break;
+            default: fail(SAD_EINVAL, "bench: unknown kernel");
+            }
+        };
+        once();
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, s);
+        for (int i = 0; i < reps; i++) once();
+        cudaEventRecord(b, s);
+        ck(cudaEventSynchronize(b), "bench");
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        *ms_per_launch = ms / std::max(reps, 1);
+    });
+}
+
+void* sad_host_alloc(size_t bytes) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, bytes) != cudaSuccess) return nullptr;
+    return p;
+}
+
+void sad_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
+sad_status sad_fit_timing(sad_fit_run* r, double* total, double* ph) {
+    return guard([&] {
+        *total = r->total_ms;
+        for (int i = 0; i < 4; i++) ph[i] = r->phase_ms[i];
+    });
+}
+
+}  // extern "C"
