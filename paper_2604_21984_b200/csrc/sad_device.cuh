@@ -51,7 +51,7 @@ __device__ __forceinline__ double half_rt(double v) {
 
 // ------------------------------------------------------------------ glibc expf, bit-exact port
 // exp(x) = 2^(k/32) * 2^(r/32) with a cubic in r; table entries are bits(2^(i/32)) - (i << 47).
-__constant__ unsigned long long kExp2fTab[32] = {
+__device__ const unsigned long long kExp2fTab[32] = {
     0x3ff0000000000000ull, 0x3fefd9b0d3158574ull, 0x3fefb5586cf9890full, 0x3fef9301d0125b51ull,
     0x3fef72b83c7d517bull, 0x3fef54873168b9aaull, 0x3fef387a6e756238ull, 0x3fef1e9df51fdee1ull,
     0x3fef06fe0a31b715ull, 0x3feef1a7373aa9cbull, 0x3feedea64c123422ull, 0x3feece086061892dull,
@@ -81,7 +81,7 @@ __device__ __forceinline__ float sad_expf(float x) {
     uint64_t ki = static_cast<uint64_t>(__double_as_longlong(kd));
     kd -= kShift;
     double r = __fma_rn(kInvLn2N, xd, -kd);
-    uint64_t t = kExp2fTab[ki & 31u];
+    uint64_t t = __ldg(&kExp2fTab[ki & 31u]);  // L1-cached: lanes index freely without serialising
     t += ki << 47;
     double s = __longlong_as_double(static_cast<long long>(t));
     double zz = __fma_rn(kC0, r, kC1);

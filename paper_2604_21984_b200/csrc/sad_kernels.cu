@@ -565,7 +565,7 @@ struct TileRed {
 };
 
 template <typename CT, int NCH, int TPX, int KM>
-__device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, double2* __restrict__ out, int cap) {
+__device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, const RedTarget& red) {
     using R = TileRed<CT, NCH, TPX, KM>;
     const int tid = threadIdx.x;
     // 2. hash insert (site ids are < 2^31; table keys start as kEmpty)
@@ -591,10 +591,7 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, doubl
     }
     __syncthreads();
     const int U = sm.n_local;
-    for (int u = tid; u < U; u += TPX) {
-        sm.cnt[u] = 0;
-        sm.fill[u] = 0;
-    }
+    for (int u = tid; u < U; u += TPX) sm.cnt[u] = 0;
     __syncthreads();
     // 3. bucket counts
     for (int e = tid; e < R::E; e += TPX) {
@@ -609,7 +606,7 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, doubl
         int carry = 0;
         for (int base = 0; base < U; base += 32) {
             int u = base + tid;
-            int v = u < U ? sm.cnt[u] : 0;
+            int v = u < U ? static_cast<int>(sm.cnt[u]) : 0;
             int x = v;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
@@ -624,18 +621,33 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, doubl
     for (int e = tid; e < R::E; e += TPX) {
         if (sm.key[e] == kEmpty) continue;
         int loc = sm.local_of_entry[e];
-        int pos = static_cast<int>(sm.start[loc] + atomicAdd(&sm.fill[loc], 1u));
+        int pos = static_cast<int>(atomicAdd(&sm.start[loc], 1u));
         sm.order[pos] = static_cast<uint16_t>(e);
     }
     __syncthreads();
-    // 4. per (site, channel) compensated sums -> one 128-bit CAS each
+    for (int u = tid; u < U; u += TPX) sm.start[u] -= sm.cnt[u];  // cursor back to the bucket start
+    __syncthreads();
+    // 4. claim one record slot per (site, tile), then per (site, channel) compensated sums
+    for (int u = tid; u < U; u += TPX) sm.fill[u] = static_cast<uint32_t>(atomicAdd(red.cnt + sm.site_of_local[u], 1));
+    __syncthreads();
     for (int item = tid; item < U * NCH; item += TPX) {
         int u = item / NCH, ch = item - u * NCH;
         int b = static_cast<int>(sm.start[u]), n = static_cast<int>(sm.cnt[u]);
-        DD acc{0.0, 0.0};
+        DD a0{0.0, 0.0}, a1{0.0, 0.0};
         const CT* row = sm.c + ch * R::ES;
-        for (int j = 0; j < n; j++) dd_add(acc, static_cast<double>(row[sm.order[b + j]]));
-        dd_atomic_merge(out + static_cast<size_t>(ch) * cap + sm.site_of_local[u], acc);
+        int j = 0;
+        for (; j + 2 <= n; j += 2) {  // two independent chains for ILP; merged below (order independent)
+            dd_add(a0, static_cast<double>(row[sm.order[b + j]]));
+            dd_add(a1, static_cast<double>(row[sm.order[b + j + 1]]));
+        }
+        if (j < n) dd_add(a0, static_cast<double>(row[sm.order[b + j]]));
+        dd_merge(a0, a1);
+        const uint32_t site = sm.site_of_local[u];
+        const uint32_t slot = sm.fill[u];
+        if (slot < static_cast<uint32_t>(red.maxt))
+            red.part[(static_cast<size_t>(site) * red.maxt + slot) * red.stride + ch] = make_double2(a0.hi, a0.lo);
+        else
+            dd_atomic_merge(red.over + static_cast<size_t>(ch) * red.cap + site, a0);
     }
 }
 
@@ -663,6 +675,23 @@ __device__ __forceinline__ void block_dd_merge(DD v, DD* warp_part, double2* dst
     }
 }
 
+// Block-wide compensated reduction stored (no atomics) to dst (one partial per block).
+template <int TPX>
+__device__ __forceinline__ void block_dd_store(DD v, DD* warp_part, double2* dst) {
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+        DD o{__shfl_down_sync(0xffffffffu, v.hi, d), __shfl_down_sync(0xffffffffu, v.lo, d)};
+        dd_merge(v, o);
+    }
+    if ((threadIdx.x & 31) == 0) warp_part[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        DD t = warp_part[0];
+        for (int w = 1; w < TPX / 32; w++) dd_merge(t, warp_part[w]);
+        *dst = make_double2(t.hi, t.lo);
+    }
+}
+
 template <int TPX>
 __device__ __forceinline__ unsigned long long block_sum_u64(unsigned long long v, unsigned long long* sm_tmp) {
 #pragma unroll
@@ -686,7 +715,7 @@ template <> struct BwdTile<double> { static constexpr int TW = 8, TH = 8; };
 template <typename T, int KM, int MODE>
 __global__ void __launch_bounds__(BwdTile<T>::TW * BwdTile<T>::TH)
     k_backward(const uint32_t* __restrict__ ids, const Q4<T>* __restrict__ gtab, const T* __restrict__ tgt, FieldDims f,
-               T s, T inv_hw2, double2* __restrict__ grads, int cap, DevState* st) {
+               T s, T inv_hw2, RedTarget red, double2* __restrict__ loss_part, DevState* st) {
     constexpr int TW = BwdTile<T>::TW, TH = BwdTile<T>::TH, TPX = TW * TH;
     constexpr int NCH = MODE == 1 ? 11 : 10;
     using Red = TileRed<T, NCH, TPX, KM>;
@@ -845,17 +874,22 @@ __global__ void __launch_bounds__(BwdTile<T>::TW * BwdTile<T>::TH)
     for (int i = 0; i < KM; i++)
         if (i >= n) sm.key[i * TPX + tid] = kEmpty;
     __syncthreads();
-    tile_reduce(sm, grads, cap);
+    tile_reduce(sm, red);
     __syncthreads();
-    if (MODE != 2) block_dd_merge<TPX>(loss, sm.warp_part, &st->loss);
+    if (MODE != 2) block_dd_store<TPX>(loss, sm.warp_part, loss_part + blockIdx.y * gridDim.x + blockIdx.x);
     __syncthreads();
     unsigned long long nf = block_sum_u64<TPX>(nonfinite, reinterpret_cast<unsigned long long*>(sm.warp_part));
     if (threadIdx.x == 0 && nf) atomicAdd(reinterpret_cast<unsigned long long*>(&st->nonfinite), nf);
 }
 
+int backward_blocks(bool fp64, const FieldDims& f) {
+    int tw = fp64 ? BwdTile<double>::TW : BwdTile<float>::TW, th = fp64 ? BwdTile<double>::TH : BwdTile<float>::TH;
+    return ((f.width + tw - 1) / tw) * ((f.height + th - 1) / th);
+}
+
 template <typename T, int KM, int MODE>
 static void backward_t(const uint32_t* ids, const void* gtab, const void* tgt, const FieldDims& f, double scale,
-                       double2* grads, int cap, DevState* st, cudaStream_t stream) {
+                       const RedTarget& red, double2* loss_part, DevState* st, cudaStream_t stream) {
     constexpr int TW = BwdTile<T>::TW, TH = BwdTile<T>::TH;
     constexpr int NCH = MODE == 1 ? 11 : 10;
     size_t smem = sizeof(TileRed<T, NCH, TW * TH, KM>);
@@ -868,17 +902,17 @@ static void backward_t(const uint32_t* ids, const void* gtab, const void* tgt, c
     dim3 grid((f.width + TW - 1) / TW, (f.height + TH - 1) / TH);
     T inv_hw2 = static_cast<T>(2.0 / (static_cast<double>(f.width) * f.height));
     kern<<<grid, TW * TH, smem, stream>>>(ids, (const Q4<T>*)gtab, (const T*)tgt, f, static_cast<T>(scale), inv_hw2,
-                                          grads, cap, st);
+                                          red, loss_part, st);
     SAD_LAUNCHED();
 }
 
 void launch_backward(bool fp64, int mode, const uint32_t* ids, const void* gtab, const void* tgt, const FieldDims& f,
-                     double scale, double2* grads, int cap, DevState* st, cudaStream_t stream) {
-#define SAD_BWD(T, KM)                                                                           \
-    do {                                                                                         \
-        if (mode == 0) backward_t<T, KM, 0>(ids, gtab, tgt, f, scale, grads, cap, st, stream);  \
-        else if (mode == 1) backward_t<T, KM, 1>(ids, gtab, tgt, f, scale, grads, cap, st, stream); \
-        else backward_t<T, KM, 2>(ids, gtab, tgt, f, scale, grads, cap, st, stream);            \
+                     double scale, const RedTarget& red, double2* loss_part, DevState* st, cudaStream_t stream) {
+#define SAD_BWD(T, KM)                                                                                 \
+    do {                                                                                               \
+        if (mode == 0) backward_t<T, KM, 0>(ids, gtab, tgt, f, scale, red, loss_part, st, stream);      \
+        else if (mode == 1) backward_t<T, KM, 1>(ids, gtab, tgt, f, scale, red, loss_part, st, stream); \
+        else backward_t<T, KM, 2>(ids, gtab, tgt, f, scale, red, loss_part, st, stream);                \
     } while (0)
     if (fp64) {
         if (f.k <= 8) SAD_BWD(double, 8);
@@ -893,7 +927,8 @@ void launch_backward(bool fp64, int mode, const uint32_t* ids, const void* gtab,
 // ====================================================================== image_loss (grad.cpp:291-360)
 template <typename T, int KM>
 __global__ void __launch_bounds__(128) k_loss(const uint32_t* __restrict__ ids, const Q4<T>* __restrict__ gtab,
-                                              const T* __restrict__ tgt, FieldDims f, T s, DevState* st) {
+                                              const T* __restrict__ tgt, FieldDims f, T s, double2* __restrict__ loss_part,
+                                              DevState* st) {
     __shared__ DD parts[4];
     const int tid = threadIdx.x;
     const int px = blockIdx.x * 16 + (tid % 16);
@@ -963,20 +998,69 @@ __global__ void __launch_bounds__(128) k_loss(const uint32_t* __restrict__ ids, 
             if (isfinite(pl)) dd_add(loss, pl);
         }
     }
-    block_dd_merge<128>(loss, parts, &st->loss);
+    block_dd_store<128>(loss, parts, loss_part + blockIdx.y * gridDim.x + blockIdx.x);
 }
 
+int loss_blocks(const FieldDims& f) { return ((f.width + 15) / 16) * ((f.height + 7) / 8); }
+
 void launch_loss(bool fp64, const uint32_t* ids, const void* gtab, const void* tgt, const FieldDims& f, double scale,
-                 DevState* st, cudaStream_t stream) {
+                 double2* lp, DevState* st, cudaStream_t stream) {
     dim3 grid((f.width + 15) / 16, (f.height + 7) / 8);
     if (fp64) {
-        if (f.k <= 8) k_loss<double, 8><<<grid, 128, 0, stream>>>(ids, (const Q4<double>*)gtab, (const double*)tgt, f, scale, st);
-        else k_loss<double, 16><<<grid, 128, 0, stream>>>(ids, (const Q4<double>*)gtab, (const double*)tgt, f, scale, st);
+        if (f.k <= 8) k_loss<double, 8><<<grid, 128, 0, stream>>>(ids, (const Q4<double>*)gtab, (const double*)tgt, f, scale, lp, st);
+        else k_loss<double, 16><<<grid, 128, 0, stream>>>(ids, (const Q4<double>*)gtab, (const double*)tgt, f, scale, lp, st);
     } else {
         float s = static_cast<float>(scale);
-        if (f.k <= 8) k_loss<float, 8><<<grid, 128, 0, stream>>>(ids, (const Q4<float>*)gtab, (const float*)tgt, f, s, st);
-        else k_loss<float, 16><<<grid, 128, 0, stream>>>(ids, (const Q4<float>*)gtab, (const float*)tgt, f, s, st);
+        if (f.k <= 8) k_loss<float, 8><<<grid, 128, 0, stream>>>(ids, (const Q4<float>*)gtab, (const float*)tgt, f, s, lp, st);
+        else k_loss<float, 16><<<grid, 128, 0, stream>>>(ids, (const Q4<float>*)gtab, (const float*)tgt, f, s, lp, st);
     }
+    SAD_LAUNCHED();
+}
+
+// Compensated sum of per-block loss partials into dst (one block; order independent).
+__global__ void k_loss_reduce(const double2* __restrict__ part, int n, double2* dst) {
+    __shared__ DD parts[8];
+    DD acc{0.0, 0.0};
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dd_merge(acc, DD{part[i].x, part[i].y});
+    block_dd_store<256>(acc, parts, dst);
+}
+
+void launch_loss_reduce(const double2* loss_part, int n, double2* dst, cudaStream_t stream) {
+    k_loss_reduce<<<1, 256, 0, stream>>>(loss_part, n, dst);
+    SAD_LAUNCHED();
+}
+
+// Merge of per-(site, tile) records into the totals (consumer side of RedTarget).
+__device__ __forceinline__ DD red_total(const RedTarget& red, int id, int ch, int n) {
+    double2 o = red.over[static_cast<size_t>(ch) * red.cap + id];
+    DD acc{o.x, o.y};
+    const double2* rec = red.part + static_cast<size_t>(id) * red.maxt * red.stride + ch;
+    for (int s = 0; s < n; s++) {
+        double2 r = rec[static_cast<size_t>(s) * red.stride];
+        dd_merge(acc, DD{r.x, r.y});
+    }
+    return acc;
+}
+
+template <int NCH>
+__global__ void k_finalize(RedTarget red, const DevState* __restrict__ st) {
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= st->n_sites) return;
+    int n = red.cnt[id];
+    if (n > red.maxt) n = red.maxt;
+#pragma unroll 1
+    for (int ch = 0; ch < NCH; ch++) {
+        DD t = red_total(red, id, ch, n);
+        red.over[static_cast<size_t>(ch) * red.cap + id] = make_double2(t.hi, t.lo);
+    }
+    red.cnt[id] = 0;
+}
+
+void launch_finalize(const RedTarget& red, int n_ch, const DevState* st, cudaStream_t stream) {
+    int grid = (red.cap + 127) / 128;
+    if (n_ch == 8) k_finalize<8><<<grid, 128, 0, stream>>>(red, st);
+    else if (n_ch == 10) k_finalize<10><<<grid, 128, 0, stream>>>(red, st);
+    else k_finalize<11><<<grid, 128, 0, stream>>>(red, st);
     SAD_LAUNCHED();
 }
 
@@ -984,8 +1068,8 @@ void launch_loss(bool fp64, const uint32_t* ids, const void* gtab, const void* t
 // Always double, unpacked ScoreTable logits; 8 channels per (pixel, candidate), same tile contract.
 template <int KM>
 __global__ void __launch_bounds__(64) k_stats(const uint32_t* __restrict__ ids, const Q4<double>* __restrict__ rtab,
-                                             const double* __restrict__ tgt, FieldDims f, double s,
-                                             double2* __restrict__ stats, int cap, DevState* st) {
+                                             const double* __restrict__ tgt, FieldDims f, double s, RedTarget red,
+                                             DevState* st) {
     constexpr int TW = 8, TH = 8, TPX = 64, NCH = 8;
     using Red = TileRed<double, NCH, TPX, KM>;
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -1080,14 +1164,14 @@ __global__ void __launch_bounds__(64) k_stats(const uint32_t* __restrict__ ids, 
     for (int i = 0; i < KM; i++)
         if (i >= n) sm.key[i * TPX + tid] = kEmpty;
     __syncthreads();
-    tile_reduce(sm, stats, cap);
+    tile_reduce(sm, red);
     __syncthreads();
     unsigned long long v = block_sum_u64<TPX>(n > 0 ? 1ull : 0ull, reinterpret_cast<unsigned long long*>(sm.warp_part));
     if (threadIdx.x == 0 && v) atomicAdd(reinterpret_cast<unsigned long long*>(&st->valid), v);
 }
 
 void launch_stats(const uint32_t* ids, const void* rtab_d, const double* tgt, const FieldDims& f, double scale,
-                  double2* stats, int cap, DevState* st, cudaStream_t stream) {
+                  const RedTarget& red, DevState* st, cudaStream_t stream) {
     dim3 grid((f.width + 7) / 8, (f.height + 7) / 8);
     if (f.k <= 8) {
         size_t smem = sizeof(TileRed<double, 8, 64, 8>);
@@ -1096,7 +1180,7 @@ void launch_stats(const uint32_t* ids, const void* rtab_d, const double* tgt, co
             cudaFuncSetAttribute(k_stats<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             attr = true;
         }
-        k_stats<8><<<grid, 64, smem, stream>>>(ids, (const Q4<double>*)rtab_d, tgt, f, scale, stats, cap, st);
+        k_stats<8><<<grid, 64, smem, stream>>>(ids, (const Q4<double>*)rtab_d, tgt, f, scale, red, st);
     } else {
         size_t smem = sizeof(TileRed<double, 8, 64, 16>);
         static bool attr = false;
@@ -1104,7 +1188,7 @@ void launch_stats(const uint32_t* ids, const void* rtab_d, const double* tgt, co
             cudaFuncSetAttribute(k_stats<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             attr = true;
         }
-        k_stats<16><<<grid, 64, smem, stream>>>(ids, (const Q4<double>*)rtab_d, tgt, f, scale, stats, cap, st);
+        k_stats<16><<<grid, 64, smem, stream>>>(ids, (const Q4<double>*)rtab_d, tgt, f, scale, red, st);
     }
     SAD_LAUNCHED();
 }
@@ -1138,7 +1222,7 @@ __device__ __forceinline__ void clamp_site(double* p, int cap, int id, const Ada
 }
 
 template <typename T>
-__global__ void k_adam(SitesDev s, DevState* st, double2* __restrict__ grads, double* __restrict__ m,
+__global__ void k_adam(SitesDev s, DevState* st, RedTarget grads, double* __restrict__ m,
                        double* __restrict__ v, AdamHyper hp, const double2* __restrict__ bc_table, double2 bc_now,
                        int zero_grads, double scale, Q4<T>* pack, Q4<T>* gtab) {
     const int id = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1146,11 +1230,13 @@ __global__ void k_adam(SitesDev s, DevState* st, double2* __restrict__ grads, do
     unsigned long long skipped = 0;
     if (id < st->n_sites) {
         double2 bc = bc_table ? bc_table[st->t + 1] : bc_now;
+        int nrec = grads.cnt[id];
+        if (nrec > grads.maxt) nrec = grads.maxt;
         if (s.active[id] && !s.frozen[id]) {
-#pragma unroll
+#pragma unroll 1
             for (int k = 0; k < 10; k++) {
-                double2 g = grads[static_cast<size_t>(k) * cap + id];
-                double gv = g.x + g.y;
+                DD g = red_total(grads, id, k, nrec);
+                double gv = g.hi + g.lo;
                 if (!isfinite(gv)) {
                     skipped++;
                     continue;
@@ -1166,7 +1252,8 @@ __global__ void k_adam(SitesDev s, DevState* st, double2* __restrict__ grads, do
         }
         if (zero_grads) {
 #pragma unroll
-            for (int k = 0; k < 11; k++) grads[static_cast<size_t>(k) * cap + id] = make_double2(0.0, 0.0);
+            for (int k = 0; k < 11; k++) grads.over[static_cast<size_t>(k) * cap + id] = make_double2(0.0, 0.0);
+            grads.cnt[id] = 0;
         }
     }
     if (skipped) atomicAdd(reinterpret_cast<unsigned long long*>(&st->skipped), skipped);
@@ -1212,7 +1299,7 @@ __global__ void k_adam(SitesDev s, DevState* st, double2* __restrict__ grads, do
     }
 }
 
-void launch_adam(bool fp64, const SitesDev& s, DevState* st, double2* grads, double* m, double* v, const AdamHyper& hp,
+void launch_adam(bool fp64, const SitesDev& s, DevState* st, const RedTarget& grads, double* m, double* v, const AdamHyper& hp,
                  const double2* bc_table, double2 bc_now, bool zero_grads, double scale, void* pack, void* gtab,
                  cudaStream_t stream) {
     int grid = (s.cap + 127) / 128;
@@ -1438,21 +1525,33 @@ void launch_flag_active(const SitesDev& s, const DevState* st, uint8_t* flags, c
 }
 
 // ====================================================================== loop bookkeeping
-__global__ void k_advance(DevState* st, int passes, int adam_steps, double2* loss_hist, int32_t* active_hist) {
+__global__ void k_advance(DevState* st, int passes, int adam_steps, double2* loss_hist, int32_t* active_hist,
+                          const double2* __restrict__ loss_part, int n_part) {
+    __shared__ DD parts[8];
+    DD acc{0.0, 0.0};
+    if (loss_hist)
+        for (int i = threadIdx.x; i < n_part; i += blockDim.x) dd_merge(acc, DD{loss_part[i].x, loss_part[i].y});
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+        DD o{__shfl_down_sync(0xffffffffu, acc.hi, d), __shfl_down_sync(0xffffffffu, acc.lo, d)};
+        dd_merge(acc, o);
+    }
+    if ((threadIdx.x & 31) == 0) parts[threadIdx.x >> 5] = acc;
+    __syncthreads();
     if (threadIdx.x != 0) return;
+    for (int w = 1; w < 8; w++) dd_merge(acc, parts[w]);
     if (loss_hist) {
-        loss_hist[st->iter] = st->loss;
+        loss_hist[st->iter] = make_double2(acc.hi, acc.lo);
         if (active_hist) active_hist[st->iter] = st->n_active;
         st->iter += 1;
     }
-    st->loss = make_double2(0.0, 0.0);
     st->pass_index += static_cast<uint32_t>(passes);
     st->t += adam_steps;
 }
 
 void launch_advance(DevState* st, int passes, int adam_steps, double2* loss_hist, int32_t* active_hist,
-                    cudaStream_t stream) {
-    k_advance<<<1, 32, 0, stream>>>(st, passes, adam_steps, loss_hist, active_hist);
+                    const double2* loss_part, int n_part, cudaStream_t stream) {
+    k_advance<<<1, 256, 0, stream>>>(st, passes, adam_steps, loss_hist, active_hist, loss_part, n_part);
     SAD_LAUNCHED();
 }
 

@@ -40,6 +40,20 @@ struct SitesDev {
     int cap;
 };
 
+// Destination of a tile reduction (grad.cpp:37-64 semantics): each tile that touches a site claims
+// one record slot for it with a single atomicAdd and stores its compensated per-channel partials
+// there; the consumer merges the records in any order (double-double is order independent).  A
+// site that collects more than `maxt` tiles in one pass falls back to a 128-bit CAS merge into
+// `over`.  Consumers also merge `over`.
+struct RedTarget {
+    double2* over;  // [nch][cap]   (hi, lo) accumulators, CAS fallback and finalized totals
+    double2* part;  // [cap][maxt][stride] records
+    int32_t* cnt;   // [cap] records claimed per site
+    int cap;
+    int maxt;
+    int stride;     // channels per record (11 for gradients, 8 for stats)
+};
+
 struct FieldDims {
     int width, height, cell, gw, gh, k;
 };
@@ -83,17 +97,24 @@ void launch_pixel_weights(const uint32_t* ids, const void* rtab_d, const FieldDi
 
 // ---------------------------------------------------------------- backward / loss / stats
 // mode: 0 = MSE target, 1 = MSE target + removal delta, 2 = caller adjoint (pixgrad)
+// Per-block loss partials go to loss_part[block]; launch_loss_reduce / launch_advance reduce them.
+int backward_blocks(bool fp64, const FieldDims& f);
 void launch_backward(bool fp64, int mode, const uint32_t* ids, const void* gtab, const void* tgt_or_pixgrad,
-                     const FieldDims& f, double scale, double2* grads, int cap, DevState* st, cudaStream_t stream);
+                     const FieldDims& f, double scale, const RedTarget& red, double2* loss_part, DevState* st,
+                     cudaStream_t stream);
+int loss_blocks(const FieldDims& f);
 void launch_loss(bool fp64, const uint32_t* ids, const void* gtab, const void* tgt, const FieldDims& f, double scale,
-                 DevState* st, cudaStream_t stream);
+                 double2* loss_part, DevState* st, cudaStream_t stream);
+void launch_loss_reduce(const double2* loss_part, int n, double2* dst, cudaStream_t stream);
 void launch_stats(const uint32_t* ids, const void* rtab_d, const double* tgt, const FieldDims& f, double scale,
-                  double2* stats, int cap, DevState* st, cudaStream_t stream);
+                  const RedTarget& red, DevState* st, cudaStream_t stream);
+// Merges records into red.over (n_ch channels) for sites < n_sites and resets the record counters.
+void launch_finalize(const RedTarget& red, int n_ch, const DevState* st, cudaStream_t stream);
 
 // ---------------------------------------------------------------- optimiser
 // Adam (+ clamp_project) over all slots < n_sites; optionally zeroes grads and rebuilds pack/gtab.
 // bc: (1 - beta1^t, 1 - beta2^t) table indexed by the new t, or nullptr to use bc_now.
-void launch_adam(bool fp64, const SitesDev& s, DevState* st, double2* grads, double* m, double* v,
+void launch_adam(bool fp64, const SitesDev& s, DevState* st, const RedTarget& grads, double* m, double* v,
                  const AdamHyper& hp, const double2* bc_table, double2 bc_now, bool zero_grads, double scale,
                  void* pack, void* gtab, cudaStream_t stream);
 void launch_clamp(const SitesDev& s, const DevState* st, const AdamHyper& hp, cudaStream_t stream);
@@ -111,8 +132,9 @@ void launch_flag_active(const SitesDev& s, const DevState* st, uint8_t* flags, c
 
 // ---------------------------------------------------------------- loop bookkeeping
 // pass_index += passes; t and iter advance; records loss/active history row `iter`.
+// With loss_hist: reduces loss_part[0..n_part) into history row `iter` and advances iter.
 void launch_advance(DevState* st, int passes, int adam_steps, double2* loss_hist, int32_t* active_hist,
-                    cudaStream_t stream);
+                    const double2* loss_part, int n_part, cudaStream_t stream);
 
 // ---------------------------------------------------------------- init (train.cpp:33-111) device path
 void launch_sobel(const double* tgt, int w, int h, double* mag, cudaStream_t stream);

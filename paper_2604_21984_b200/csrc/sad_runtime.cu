@@ -283,7 +283,11 @@ struct Workspace {
     DBuf<uint32_t> ids[2];
     int cur = 0;
     DBuf<char> pack, gtab, rtab, rtab_d;
-    DBuf<double2> grads, stats;
+    DBuf<double2> grads, stats;       // RedTarget.over: [11][cap] / [8][cap]
+    DBuf<double2> gpart, spart;       // RedTarget.part records
+    DBuf<int32_t> gcnt, scnt;         // RedTarget.cnt
+    DBuf<double2> loss_part;          // per-block loss partials
+    int maxt = 16;                    // record slots per site and pass
     DBuf<double> m, v;
     DBuf<uint32_t> act, free_list;
     DBuf<uint8_t> flags;
@@ -311,6 +315,17 @@ struct Workspace {
     }
 
     sadk::SitesDev sites() { return sadk::SitesDev{params.p, active.p, frozen.p, cap}; }
+    sadk::RedTarget gred() { return sadk::RedTarget{grads.p, gpart.p, gcnt.p, cap, maxt, 11}; }
+    sadk::RedTarget sred() { return sadk::RedTarget{stats.p, spart.p, scnt.p, cap, maxt, 8}; }
+    void zero_red(bool g) {
+        if (g) {
+            ck(cudaMemsetAsync(grads.p, 0, sizeof(double2) * 11 * cap, stream), "memset grads");
+            ck(cudaMemsetAsync(gcnt.p, 0, sizeof(int32_t) * cap, stream), "memset gcnt");
+        } else {
+            ck(cudaMemsetAsync(stats.p, 0, sizeof(double2) * 8 * cap, stream), "memset stats");
+            ck(cudaMemsetAsync(scnt.p, 0, sizeof(int32_t) * cap, stream), "memset scnt");
+        }
+    }
 
     void ensure_state() {
         if (!st.p) {
@@ -359,7 +374,13 @@ struct Workspace {
         rtab_d.ensure(static_cast<size_t>(nc) * 96);
         grads.ensure(static_cast<size_t>(nc) * 11);
         stats.ensure(static_cast<size_t>(nc) * 8);
+        gpart.ensure(static_cast<size_t>(nc) * maxt * 11);
+        spart.ensure(static_cast<size_t>(nc) * maxt * 8);
+        gcnt.ensure(nc);
+        scnt.ensure(nc);
         ck(cudaMemsetAsync(grads.p, 0, grads.n * sizeof(double2), stream), "memset grads");
+        ck(cudaMemsetAsync(gcnt.p, 0, gcnt.n * sizeof(int32_t), stream), "memset gcnt");
+        ck(cudaMemsetAsync(scnt.p, 0, scnt.n * sizeof(int32_t), stream), "memset scnt");
         act.ensure(nc);
         free_list.ensure(nc);
         flags.ensure(nc);
@@ -391,6 +412,8 @@ struct Workspace {
         size_t n = static_cast<size_t>(fd.gw) * fd.gh * k;
         ids[0].ensure(n);
         ids[1].ensure(n);
+        loss_part.ensure(static_cast<size_t>(std::max({sadk::backward_blocks(false, fd), sadk::backward_blocks(true, fd),
+                                                       sadk::loss_blocks(fd)})));
     }
 
     void ensure_target(size_t px) {
@@ -554,10 +577,11 @@ sadk::AdamHyper adam_hyper(const sad_train_config& c, int w, int h) {
 
 void stats_device(Workspace& ws) {
     build_tables(ws, true, false, false, true);
-    ck(cudaMemsetAsync(ws.stats.p, 0, sizeof(double2) * 8 * ws.cap, ws.stream), "memset stats");
+    ws.zero_red(false);
     ws.zero_state_field(offsetof(DevState, valid), sizeof(uint64_t));
     sadk::launch_stats(ws.ids[ws.cur].p, ws.rtab_d.p, ws.tgt_d.p, ws.fd, norm_scale(ws.fd.width, ws.fd.height),
-                       ws.stats.p, ws.cap, ws.st.p, ws.stream);
+                       ws.sred(), ws.st.p, ws.stream);
+    sadk::launch_finalize(ws.sred(), 8, ws.st.p, ws.stream);
 }
 
 void prune_device(Workspace& ws, double pct) {
@@ -925,12 +949,15 @@ static void backward_call(sad_ctx* c, const sad_sites_view* s, const sad_field_v
     ck(cudaMemcpyAsync(ws.tgt_d.p, img, 24 * npx, cudaMemcpyHostToDevice, ws.stream), "H2D target");
     if (!fp64) sadk::launch_f64_to_f32(ws.tgt_d.p, ws.tgt_f.p, 3 * npx, ws.stream);
     build_tables(ws, fp64 != 0, false, true, false);
-    ck(cudaMemsetAsync(ws.grads.p, 0, sizeof(double2) * 11 * ws.cap, ws.stream), "memset grads");
+    ws.zero_red(true);
     ws.zero_state_field(offsetof(DevState, nonfinite), sizeof(uint64_t));
     ws.zero_state_field(offsetof(DevState, loss), sizeof(double2));
     sadk::launch_backward(fp64 != 0, mode, ws.ids[ws.cur].p, ws.gtab.p,
                           fp64 ? static_cast<const void*>(ws.tgt_d.p) : static_cast<const void*>(ws.tgt_f.p), ws.fd,
-                          norm_scale(f->width, f->height), ws.grads.p, ws.cap, ws.st.p, ws.stream);
+                          norm_scale(f->width, f->height), ws.gred(), ws.loss_part.p, ws.st.p, ws.stream);
+    sadk::launch_finalize(ws.gred(), 11, ws.st.p, ws.stream);
+    if (mode != 2)
+        sadk::launch_loss_reduce(ws.loss_part.p, sadk::backward_blocks(fp64 != 0, ws.fd), &ws.st.p->loss, ws.stream);
     DBuf<double> out;
     size_t n = s->size;
     out.ensure(std::max<size_t>(n, 1) * 11);
@@ -967,7 +994,8 @@ sad_status sad_image_loss(sad_ctx* c, const sad_sites_view* s, const sad_field_v
         ws.zero_state_field(offsetof(DevState, loss), sizeof(double2));
         sadk::launch_loss(fp64 != 0, ws.ids[ws.cur].p, ws.gtab.p,
                           fp64 ? static_cast<const void*>(ws.tgt_d.p) : static_cast<const void*>(ws.tgt_f.p), ws.fd,
-                          norm_scale(f->width, f->height), ws.st.p, ws.stream);
+                          norm_scale(f->width, f->height), ws.loss_part.p, ws.st.p, ws.stream);
+        sadk::launch_loss_reduce(ws.loss_part.p, sadk::loss_blocks(ws.fd), &ws.st.p->loss, ws.stream);
         DevState st = ws.get_state();
         if (st.err & 1) {
             ws.zero_state_field(offsetof(DevState, err), sizeof(int32_t));
@@ -997,13 +1025,14 @@ sad_status sad_adam_step(sad_ctx* c, sad_sites_view* s, const double* grads, sad
                 }
         }
         ck(cudaMemcpyAsync(ws.grads.p, g.data(), g.size() * sizeof(double2), cudaMemcpyHostToDevice, ws.stream), "H2D");
+        ck(cudaMemsetAsync(ws.gcnt.p, 0, sizeof(int32_t) * ws.cap, ws.stream), "memset gcnt");
         ck(cudaMemcpyAsync(ws.m.p, m.data(), m.size() * 8, cudaMemcpyHostToDevice, ws.stream), "H2D");
         ck(cudaMemcpyAsync(ws.v.p, v.data(), v.size() * 8, cudaMemcpyHostToDevice, ws.stream), "H2D");
         ws.zero_state_field(offsetof(DevState, skipped), sizeof(uint64_t));
         int64_t t = a->t + 1;
         double2 bc = make_double2(1.0 - std::pow(cfg->beta1, static_cast<double>(t)),
                                   1.0 - std::pow(cfg->beta2, static_cast<double>(t)));
-        sadk::launch_adam(false, ws.sites(), ws.st.p, ws.grads.p, ws.m.p, ws.v.p, adam_hyper(*cfg, w, h), nullptr, bc,
+        sadk::launch_adam(false, ws.sites(), ws.st.p, ws.gred(), ws.m.p, ws.v.p, adam_hyper(*cfg, w, h), nullptr, bc,
                           false, 1.0, nullptr, nullptr, ws.stream);
         ck(cudaMemcpyAsync(m.data(), ws.m.p, m.size() * 8, cudaMemcpyDeviceToHost, ws.stream), "D2H");
         ck(cudaMemcpyAsync(v.data(), ws.v.p, v.size() * 8, cudaMemcpyDeviceToHost, ws.stream), "D2H");
@@ -1072,6 +1101,7 @@ static void upload_stats(Workspace& ws, const double* stats, size_t n, uint64_t 
     for (size_t id = 0; id < n; id++)
         for (int k = 0; k < 8; k++) h[k * ws.cap + id] = make_double2(stats[id * 8 + k], 0.0);
     ck(cudaMemcpyAsync(ws.stats.p, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice, ws.stream), "H2D");
+    ck(cudaMemsetAsync(ws.scnt.p, 0, sizeof(int32_t) * ws.cap, ws.stream), "memset scnt");
     ws.patch_state(offsetof(DevState, valid), valid);
 }
 
@@ -1272,7 +1302,7 @@ static void fit_loop(sad_fit_run* r) {
     // fresh optimiser and accumulators
     ck(cudaMemsetAsync(ws.m.p, 0, sizeof(double) * 10 * ws.cap, s), "memset m");
     ck(cudaMemsetAsync(ws.v.p, 0, sizeof(double) * 10 * ws.cap, s), "memset v");
-    ck(cudaMemsetAsync(ws.grads.p, 0, sizeof(double2) * 11 * ws.cap, s), "memset grads");
+    ws.zero_red(true);
     DevState init{};
     init.n_sites = st0.n_sites;
     init.n_active = sta.n_active;
@@ -1293,7 +1323,8 @@ static void fit_loop(sad_fit_run* r) {
     ws.cur = 0;
     sadk::launch_jfa_seed(ws.sites(), ws.st.p, ws.ids[0].p, ws.fd, scale_n, s);
     passes_device(ws, full4, c.inject, c.seed, fp64, 0);
-    sadk::launch_advance(ws.st.p, static_cast<int>(full4.size()), 0, nullptr, nullptr, s);
+    const int nbw = sadk::backward_blocks(fp64, ws.fd);
+    sadk::launch_advance(ws.st.p, static_cast<int>(full4.size()), 0, nullptr, nullptr, nullptr, 0, s);
 
     for (int t = 1; t <= c.iters; t++) {
         int npass = 0;
@@ -1301,13 +1332,14 @@ static void fit_loop(sad_fit_run* r) {
             passes_device(ws, warm, c.inject, c.seed, fp64, 0);
             npass += static_cast<int>(warm.size());
         }
-        sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt, ws.fd, scale_n, ws.grads.p, ws.cap, ws.st.p, s);
+        sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt, ws.fd, scale_n, ws.gred(), ws.loss_part.p,
+                              ws.st.p, s);
         bool ev_d = budget && t >= c.densify_start && t <= c.densify_end && t % c.densify_every == 0;
         bool ev_p = budget && t >= c.prune_start && t <= c.prune_end && t % c.prune_every == 0;
         if (ev_p && !c.prune_during_densify && t <= c.densify_end) ev_p = false;
         bool ev = ev_d || ev_p;
         if (ev) stats_device(ws);
-        sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.grads.p, ws.m.p, ws.v.p, hp, r->bc_table.p, make_double2(0, 0),
+        sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.gred(), ws.m.p, ws.v.p, hp, r->bc_table.p, make_double2(0, 0),
                           true, scale_n, ev ? nullptr : ws.pack.p, ev ? nullptr : ws.gtab.p, s);
         if (ev_p) prune_device(ws, c.prune_pct * sched);
         if (ev_d) densify_device(ws, c.densify_pct * sched, c);
@@ -1319,14 +1351,14 @@ static void fit_loop(sad_fit_run* r) {
             passes_device(ws, full4, c.inject, c.seed, fp64, static_cast<uint32_t>(npass));
             npass += static_cast<int>(full4.size());
         }
-        sadk::launch_advance(ws.st.p, npass, 1, r->loss_hist.p, r->active_hist.p, s);
+        sadk::launch_advance(ws.st.p, npass, 1, r->loss_hist.p, r->active_hist.p, ws.loss_part.p, nbw, s);
     }
     // final full refresh (train.cpp:287)
     const auto fin = full_refresh_passes(ws.fd.gw, ws.fd.gh, c.final_passes);
     ws.cur = 0;
     sadk::launch_jfa_seed(ws.sites(), ws.st.p, ws.ids[0].p, ws.fd, scale_n, s);
     passes_device(ws, fin, c.inject, c.seed, fp64, 0);
-    sadk::launch_advance(ws.st.p, static_cast<int>(fin.size()), 0, nullptr, nullptr, s);
+    sadk::launch_advance(ws.st.p, static_cast<int>(fin.size()), 0, nullptr, nullptr, nullptr, 0, s);
     cudaEventRecord(e1, s);
     ck(cudaStreamSynchronize(s), "fit");
     float ms = 0;
@@ -1430,14 +1462,16 @@ sad_status sad_fit_bench(sad_fit_run* r, int which, int reps, double* ms_per_lau
         auto once = [&]() {
             switch (which) {
             case 0: passes_device(ws, {sad_pass_spec{1, 0}}, c.inject, c.seed, fp64, 0); break;
-            case 1:
-                sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt, ws.fd, sn, ws.grads.p, ws.cap,
-                                      ws.st.p, s);
+            case 1:  // record counters reset each launch as Adam does in the fit (memset timed separately)
+                ck(cudaMemsetAsync(ws.gcnt.p, 0, sizeof(int32_t) * ws.cap, s), "memset");
+                sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt, ws.fd, sn, ws.gred(),
+                                      ws.loss_part.p, ws.st.p, s);
                 break;
+            case 6: ck(cudaMemsetAsync(ws.gcnt.p, 0, sizeof(int32_t) * ws.cap, s), "memset"); break;
             case 2: sadk::launch_render(false, ws.ids[ws.cur].p, ws.rtab.p, ws.fd, sn, ws.px_f.p, ws.st.p, s); break;
             case 3: passes_device(ws, {sad_pass_spec{16, 1}}, c.inject, c.seed, fp64, 0); break;
             case 4:
-                sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.grads.p, ws.m.p, ws.v.p, hp, nullptr,
+                sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.gred(), ws.m.p, ws.v.p, hp, nullptr,
                                   make_double2(1.0, 1.0), true, sn, ws.pack.p, ws.gtab.p, s);
                 break;
             case 5: stats_device(ws); break;
@@ -1457,6 +1491,11 @@ sad_status sad_fit_bench(sad_fit_run* r, int which, int reps, double* ms_per_lau
         cudaEventDestroy(a);
         cudaEventDestroy(b);
         *ms_per_launch = ms / std::max(reps, 1);
+        if (which == 1) {  // subtract the counter reset
+            double base = 0;
+            sad_status rc = sad_fit_bench(r, 6, reps, &base);
+            if (rc == SAD_OK) *ms_per_launch = std::max(0.0, *ms_per_launch - base);
+        }
     });
 }
 
