@@ -539,30 +539,67 @@ void launch_pixel_weights(const uint32_t* ids, const void* rtab_d, const FieldDi
 // The reference reduces per-(site, channel) contributions of a 16x16 tile in a 256-slot hash table
 // of compensated accumulators, then merges per worker; every sum is double-double, so the result is
 // the exactly-rounded total independent of grouping.  Here a block owns a TW x TH pixel tile:
-//   1. each thread computes its pixel's per-candidate contributions into shared memory;
-//   2. site ids are hashed into a shared table and compacted to local indices;
-//   3. entries are bucketed per local site (counting sort);
-//   4. one thread per (site, channel) sums its bucket in double-double and merges it into the
-//      global (hi, lo) accumulator with one 128-bit CAS.
-// Global traffic is one atomic per (site, channel, tile) instead of one per (pixel, candidate).
+//   1. each thread computes its pixel's per-candidate contributions into shared memory
+//      (entry e = slot * TPX + pixel, channel-major rows);
+//   2. site ids are hashed into a shared table and compacted to local bucket ids;
+//   3. entries are bucketed per site (counting sort) into `order`, bucket of each sorted position in
+//      `posloc`;
+//   4. every thread sums PT = KM consecutive sorted positions for all channels at once (10
+//      independent double-double chains — balanced work, high ILP); a bucket split across threads
+//      is finished by its first thread, which merges the carries of the following threads;
+//   5. each (site, tile) total is one record, claimed with one atomicAdd per site (RedTarget).
 template <typename CT, int NCH, int TPX, int KM>
 struct TileRed {
-    static constexpr int E = TPX * KM;   // entries per tile
-    static constexpr int HT = E;         // hash slots (load factor <= 1)
-    static constexpr int ES = E + 1;     // padded row stride: channel rows land on distinct banks
-    CT c[NCH * ES];
-    uint32_t key[E];
-    uint32_t hkey[HT];
+    static constexpr int E = TPX * KM;  // entries per tile
+    static constexpr int HT = E;        // hash slots (load factor <= 1)
+    static constexpr int ES = E + 1;    // padded row stride: channel rows land on distinct banks
+    static constexpr int PT = KM;       // sorted positions per thread in step 4
+    union {
+        CT c[NCH * ES];
+        DD carry[2 * TPX * NCH];  // step 4 chunk partials, written after every read of c[]
+    };
+    union {
+        uint32_t key[E];  // site id per entry (steps 1-2)
+        struct {
+            uint16_t order[E];   // entry of each sorted position (steps 3-4)
+            uint16_t posloc[E];  // bucket of each sorted position
+        } srt;
+    };
+    union {
+        uint32_t hkey[HT];  // hash keys (step 2)
+        uint32_t cnt[E];    // bucket sizes (step 3)
+    };
     uint16_t local_of_entry[E];
     uint16_t local_of_slot[HT];
-    uint32_t cnt[E];
     uint32_t start[E];
-    uint32_t fill[E];
-    uint16_t order[E];
     uint32_t site_of_local[E];
+    uint32_t slot_of_local[E];
     int n_local;
     DD warp_part[TPX / 32];
 };
+
+template <typename CT>
+__device__ __forceinline__ bool c_finite(CT x);
+template <>
+__device__ __forceinline__ bool c_finite<float>(float x) {
+    return (__float_as_uint(x) & 0x7f800000u) != 0x7f800000u;
+}
+template <>
+__device__ __forceinline__ bool c_finite<double>(double x) {
+    return isfinite(x);
+}
+
+template <int NCH>
+__device__ __forceinline__ void write_record(const RedTarget& red, uint32_t site, uint32_t slot, const DD* acc) {
+    if (slot < static_cast<uint32_t>(red.maxt)) {
+        double2* rec = red.part + (static_cast<size_t>(site) * red.maxt + slot) * red.stride;
+#pragma unroll
+        for (int ch = 0; ch < NCH; ch++) rec[ch] = make_double2(acc[ch].hi, acc[ch].lo);
+    } else {
+#pragma unroll
+        for (int ch = 0; ch < NCH; ch++) dd_atomic_merge(red.over + static_cast<size_t>(ch) * red.cap + site, acc[ch]);
+    }
+}
 
 template <typename CT, int NCH, int TPX, int KM>
 __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, const RedTarget& red) {
@@ -591,17 +628,23 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, const
     }
     __syncthreads();
     const int U = sm.n_local;
-    for (int u = tid; u < U; u += TPX) sm.cnt[u] = 0;
-    __syncthreads();
-    // 3. bucket counts
-    for (int e = tid; e < R::E; e += TPX) {
-        if (sm.key[e] == kEmpty) continue;
-        uint16_t loc = sm.local_of_slot[sm.local_of_entry[e]];
-        sm.local_of_entry[e] = loc;
-        atomicAdd(&sm.cnt[loc], 1u);
+    for (int u = tid; u < U; u += TPX) {
+        sm.cnt[u] = 0;  // aliases hkey: safe after the barrier
+        sm.slot_of_local[u] = static_cast<uint32_t>(atomicAdd(red.cnt + sm.site_of_local[u], 1));
     }
     __syncthreads();
-    // exclusive scan of cnt[0..U) by warp 0 (U <= E)
+    // 3. bucket counts (entries with key == kEmpty get bucket 0xffff)
+    for (int e = tid; e < R::E; e += TPX) {
+        uint16_t loc = 0xffffu;
+        if (sm.key[e] != kEmpty) {
+            loc = sm.local_of_slot[sm.local_of_entry[e]];
+            atomicAdd(&sm.cnt[loc], 1u);
+        }
+        sm.local_of_entry[e] = loc;
+    }
+    __syncthreads();
+    // exclusive scan of cnt[0..U) by warp 0 (U <= E); n_valid = total
+    __shared__ int n_valid;
     if (tid < 32) {
         int carry = 0;
         for (int base = 0; base < U; base += 32) {
@@ -616,38 +659,97 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, const
             if (u < U) sm.start[u] = static_cast<uint32_t>(carry + x - v);
             carry += __shfl_sync(0xffffffffu, x, 31);
         }
+        if (tid == 0) n_valid = carry;
     }
-    __syncthreads();
+    __syncthreads();  // key[] is dead from here: its storage becomes order/posloc
     for (int e = tid; e < R::E; e += TPX) {
-        if (sm.key[e] == kEmpty) continue;
         int loc = sm.local_of_entry[e];
+        if (loc == 0xffff) continue;
         int pos = static_cast<int>(atomicAdd(&sm.start[loc], 1u));
-        sm.order[pos] = static_cast<uint16_t>(e);
+        sm.srt.order[pos] = static_cast<uint16_t>(e);
     }
     __syncthreads();
     for (int u = tid; u < U; u += TPX) sm.start[u] -= sm.cnt[u];  // cursor back to the bucket start
-    __syncthreads();
-    // 4. claim one record slot per (site, tile), then per (site, channel) compensated sums
-    for (int u = tid; u < U; u += TPX) sm.fill[u] = static_cast<uint32_t>(atomicAdd(red.cnt + sm.site_of_local[u], 1));
-    __syncthreads();
-    for (int item = tid; item < U * NCH; item += TPX) {
-        int u = item / NCH, ch = item - u * NCH;
-        int b = static_cast<int>(sm.start[u]), n = static_cast<int>(sm.cnt[u]);
-        DD a0{0.0, 0.0}, a1{0.0, 0.0};
-        const CT* row = sm.c + ch * R::ES;
-        int j = 0;
-        for (; j + 2 <= n; j += 2) {  // two independent chains for ILP; merged below (order independent)
-            dd_add(a0, static_cast<double>(row[sm.order[b + j]]));
-            dd_add(a1, static_cast<double>(row[sm.order[b + j + 1]]));
+    // 4. buckets split into chunks of PT sorted entries; thread t sums chunks t and t + TPX for all
+    //    channels (convergent fixed-trip loops, NCH independent double-double chains)
+    const int U2 = U;
+    uint16_t* chunk_base = sm.local_of_slot;  // dead after counting: chunk index of each bucket's first chunk
+    uint16_t* chunk_bucket = sm.local_of_entry;  // dead after the scatter: bucket of each chunk
+    __shared__ int n_chunks;
+    if (tid < 32) {
+        int carry = 0;
+        for (int base = 0; base < U2; base += 32) {
+            int u = base + tid;
+            int v = u < U2 ? static_cast<int>((sm.cnt[u] + R::PT - 1) / R::PT) : 0;
+            int x = v;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                int y = __shfl_up_sync(0xffffffffu, x, d);
+                if (tid >= d) x += y;
+            }
+            if (u < U2) chunk_base[u] = static_cast<uint16_t>(carry + x - v);
+            carry += __shfl_sync(0xffffffffu, x, 31);
         }
-        if (j < n) dd_add(a0, static_cast<double>(row[sm.order[b + j]]));
-        dd_merge(a0, a1);
+        if (tid == 0) n_chunks = carry;
+    }
+    __syncthreads();
+    for (int u = tid; u < U2; u += TPX) {
+        int c0 = chunk_base[u], nc = static_cast<int>((sm.cnt[u] + R::PT - 1) / R::PT);
+        for (int c = c0; c < c0 + nc; c++) chunk_bucket[c] = static_cast<uint16_t>(u);
+    }
+    __syncthreads();
+    const int NC = n_chunks;
+    DD acc0[NCH], acc1[NCH];
+    auto sum_chunk = [&](int c, DD* acc) {
+#pragma unroll
+        for (int ch = 0; ch < NCH; ch++) acc[ch] = DD{0.0, 0.0};
+        const int u = chunk_bucket[c];
+        const int off = (c - chunk_base[u]) * R::PT;
+        const int n = static_cast<int>(sm.cnt[u]) - off;
+        const int b = static_cast<int>(sm.start[u]) + off;
+#pragma unroll
+        for (int j = 0; j < R::PT; j++) {
+            if (j < n) {
+                const int e = sm.srt.order[b + j];
+#pragma unroll
+                for (int ch = 0; ch < NCH; ch++) dd_add(acc[ch], static_cast<double>(sm.c[ch * R::ES + e]));
+            }
+        }
+    };
+    if (tid < NC) sum_chunk(tid, acc0);
+    if (tid + TPX < NC) sum_chunk(tid + TPX, acc1);
+    // chunks beyond 2*TPX (more than ~TPX distinct sites in one tile): merged straight into `over`
+    for (int c = tid + 2 * TPX; c < NC; c += TPX) {
+        DD tmp[NCH];
+        sum_chunk(c, tmp);
+        const uint32_t site = sm.site_of_local[chunk_bucket[c]];
+#pragma unroll
+        for (int ch = 0; ch < NCH; ch++) dd_atomic_merge(red.over + static_cast<size_t>(ch) * red.cap + site, tmp[ch]);
+    }
+    __syncthreads();  // every read of c[] is done: its storage becomes the chunk partials
+    if (tid < NC) {
+#pragma unroll
+        for (int ch = 0; ch < NCH; ch++) sm.carry[tid * NCH + ch] = acc0[ch];
+    }
+    if (tid + TPX < NC) {
+#pragma unroll
+        for (int ch = 0; ch < NCH; ch++) sm.carry[(tid + TPX) * NCH + ch] = acc1[ch];
+    }
+    __syncthreads();
+    // 5. per (site, channel): merge the site's chunks and store the record (or CAS on slot overflow)
+    const int NCK = NC < 2 * TPX ? NC : 2 * TPX;
+    for (int item = tid; item < U2 * NCH; item += TPX) {
+        const int u = item / NCH, ch = item - u * NCH;
+        const int c0 = chunk_base[u];
+        const int c1 = c0 + static_cast<int>((sm.cnt[u] + R::PT - 1) / R::PT);
+        DD t{0.0, 0.0};
+        for (int c = c0; c < c1 && c < NCK; c++) dd_merge(t, sm.carry[c * NCH + ch]);
         const uint32_t site = sm.site_of_local[u];
-        const uint32_t slot = sm.fill[u];
+        const uint32_t slot = sm.slot_of_local[u];
         if (slot < static_cast<uint32_t>(red.maxt))
-            red.part[(static_cast<size_t>(site) * red.maxt + slot) * red.stride + ch] = make_double2(a0.hi, a0.lo);
+            red.part[(static_cast<size_t>(site) * red.maxt + slot) * red.stride + ch] = make_double2(t.hi, t.lo);
         else
-            dd_atomic_merge(red.over + static_cast<size_t>(ch) * red.cap + site, a0);
+            dd_atomic_merge(red.over + static_cast<size_t>(ch) * red.cap + site, t);
     }
 }
 
@@ -729,69 +831,68 @@ __global__ void __launch_bounds__(BwdTile<T>::TW * BwdTile<T>::TH)
     const bool inside = px < f.width && py < f.height;
     constexpr T kTiny = sizeof(T) == 8 ? T(1e-18) : T(1e-12);
 
+    // Candidates stay in their list slots; `ok` marks the ones the reference keeps (active, finite
+    // logit, before the first sentinel).  Iterating slots in order with `ok` predication visits the
+    // kept candidates in the reference's order, so every sum below rounds identically.
     uint32_t cid[KM];
     T dxs[KM], dys[KM], ud[KM], vd[KM], nrm[KM], lg[KM];
-    int n = 0;
+    bool ok[KM];
+    bool any = false;
     T best = T(0);
-#pragma unroll
-    for (int i = 0; i < KM; i++) {
-        cid[i] = kEmpty;
-        dxs[i] = dys[i] = ud[i] = vd[i] = nrm[i] = lg[i] = T(0);
-    }
     unsigned long long nonfinite = 0;
     DD loss{0.0, 0.0};
-    if (inside) {
+    {
         const uint32_t* lst = ids + static_cast<size_t>(f.k) * (static_cast<size_t>(py / f.cell) * f.gw + px / f.cell);
         const T fx = static_cast<T>(px), fy = static_cast<T>(py);
+        bool stop = !inside;
 #pragma unroll
         for (int i = 0; i < KM; i++) {
-            if (i >= f.k) break;
-            uint32_t id = lst[i];
-            if (id == kEmpty) break;
-            const Q4<T> a = gtab[3 * id], b = gtab[3 * id + 1];
-            const T act = gtab[3 * id + 2].w;
-            if (act == T(0)) continue;
-            T dx = fx - a.x, dy = fy - a.y;
-            T pa = b.z * dx + b.w * dy;
-            T pb = b.z * dy - b.w * dx;
-            T q = b.x * pa * pa + b.y * pb * pb;
-            if (q < T(0)) q = T(0);
-            T m = tsqrt(q);
-            T l = -a.z * (m * s - a.w * s);
-            if (!tfinite(l)) continue;
-#pragma unroll
-            for (int j = 0; j < KM; j++)
-                if (j == n) {
-                    cid[j] = id;
-                    dxs[j] = dx;
-                    dys[j] = dy;
-                    ud[j] = pa;
-                    vd[j] = pb;
-                    nrm[j] = m;
-                    lg[j] = l;
-                }
-            if (n == 0 || l > best) best = l;
-            n++;
+            uint32_t id = kEmpty;
+            if (!stop && i < f.k) id = lst[i];
+            stop = stop || id == kEmpty;
+            cid[i] = id;
+            ok[i] = false;
+            dxs[i] = dys[i] = ud[i] = vd[i] = nrm[i] = lg[i] = T(0);
+            if (!stop) {
+                const Q4<T> a = gtab[3 * id], b = gtab[3 * id + 1];
+                const T act = gtab[3 * id + 2].w;
+                T dx = fx - a.x, dy = fy - a.y;
+                T pa = b.z * dx + b.w * dy;
+                T pb = b.z * dy - b.w * dx;
+                T q = b.x * pa * pa + b.y * pb * pb;
+                if (q < T(0)) q = T(0);
+                T m = tsqrt(q);
+                T l = -a.z * (m * s - a.w * s);
+                ok[i] = act != T(0) && c_finite(l);
+                dxs[i] = dx;
+                dys[i] = dy;
+                ud[i] = pa;
+                vd[i] = pb;
+                nrm[i] = m;
+                lg[i] = l;
+                if (ok[i] && (!any || l > best)) best = l;
+                any = any || ok[i];
+            }
         }
-        if (n == 0) atomicOr(&st->err, 1);
+        if (inside && !any) atomicOr(&st->err, 1);
     }
-    if (n > 0) {
+    if (any) {
         T w[KM];
         T wsum = T(0);
 #pragma unroll
-        for (int i = 0; i < KM; i++)
-            if (i < n) {
+        for (int i = 0; i < KM; i++) {
+            w[i] = T(0);
+            if (ok[i]) {
                 w[i] = texp(lg[i] - best);
                 wsum += w[i];
             }
+        }
         T invw = T(1) / wsum;
-#pragma unroll
-        for (int i = 0; i < KM; i++)
-            if (i < n) w[i] *= invw;
         T ch0 = T(0), ch1 = T(0), ch2 = T(0);
 #pragma unroll
         for (int i = 0; i < KM; i++)
-            if (i < n) {
+            if (ok[i]) {
+                w[i] *= invw;
                 const Q4<T> c = gtab[3 * cid[i] + 2];
                 ch0 += w[i] * c.x;
                 ch1 += w[i] * c.y;
@@ -806,7 +907,7 @@ __global__ void __launch_bounds__(BwdTile<T>::TW * BwdTile<T>::TH)
             T e0 = ch0 - t0, e1 = ch1 - t1, e2 = ch2 - t2;
             pl = e0 * e0 + e1 * e1 + e2 * e2;
             double plv = static_cast<double>(pl);
-            if (!isfinite(plv)) {
+            if (!c_finite(pl)) {
                 nonfinite++;
                 plv = 0;
             }
@@ -821,7 +922,11 @@ __global__ void __launch_bounds__(BwdTile<T>::TW * BwdTile<T>::TH)
         }
 #pragma unroll
         for (int i = 0; i < KM; i++) {
-            if (i >= n) break;
+            const int e = i * TPX + tid;
+            if (!ok[i]) {
+                sm.key[e] = kEmpty;
+                continue;
+            }
             const uint32_t id = cid[i];
             const Q4<T> a = gtab[3 * id], b = gtab[3 * id + 1], c = gtab[3 * id + 2];
             T dc0 = c.x - ch0, dc1 = c.y - ch1, dc2 = c.z - ch2;
@@ -857,22 +962,21 @@ __global__ void __launch_bounds__(BwdTile<T>::TW * BwdTile<T>::TH)
                     v[10] = r0 * r0 + r1 * r1 + r2 * r2 - pl;
                 }
             }
-            const int e = i * TPX + tid;
             sm.key[e] = id;
 #pragma unroll
             for (int t = 0; t < NCH; t++) {
                 T x = v[t];
-                if (!tfinite(x)) {
+                if (!c_finite(x)) {
                     x = T(0);
                     nonfinite++;
                 }
                 sm.c[t * Red::ES + e] = x;
             }
         }
-    }
+    } else {
 #pragma unroll
-    for (int i = 0; i < KM; i++)
-        if (i >= n) sm.key[i * TPX + tid] = kEmpty;
+        for (int i = 0; i < KM; i++) sm.key[i * TPX + tid] = kEmpty;
+    }
     __syncthreads();
     tile_reduce(sm, red);
     __syncthreads();
