@@ -102,6 +102,11 @@ template <> __device__ __forceinline__ double tsqrt<double>(double x) { return _
 
 template <typename T> __device__ __forceinline__ bool tfinite(T x) { return isfinite(static_cast<double>(x)); }
 
+// IEEE round-to-nearest reciprocal: the same value as T(1) / x, with a shorter instruction sequence.
+template <typename T> __device__ __forceinline__ T trcp(T x);
+template <> __device__ __forceinline__ float trcp<float>(float x) { return __frcp_rn(x); }
+template <> __device__ __forceinline__ double trcp<double>(double x) { return __drcp_rn(x); }
+
 // std::max / std::min semantics (NaN-propagating exactly as libstdc++ does)
 __device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
 __device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }

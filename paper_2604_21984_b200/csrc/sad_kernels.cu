@@ -304,6 +304,139 @@ __global__ void __launch_bounds__(256) k_propagate(const uint32_t* __restrict__ 
     }
 }
 
+// Axial (step-s, 5-list) pass specialised for K = 8.  Same result as k_propagate, fewer divergent
+// slots: the cell's own list is scored and ordered with an 8-input sorting network (the insertion
+// sort of TopK::consider yields the same order for distinct, finite keys), the neighbour entries
+// that are not in it and the injected ids are compacted into a per-thread shared-memory queue, and
+// only the queue is scored and inserted.  The TopK result over a set of distinct candidates is
+// independent of feed order (strict total order), and a repeated candidate is either already in the
+// list (skipped) or worse than the current K-th (rejected), so the map is identical.  Own lists with
+// a repeated id or a non-finite logit (never produced by the fit) take the generic streaming path.
+constexpr int kAxQ = 36;  // 4 neighbour lists x 8 + 4 injected (larger inject: generic kernel)
+
+template <typename T>
+__device__ __forceinline__ void cex(T& la, uint32_t& ia, T& lb, uint32_t& ib) {
+    // after the exchange (la, ia) is the better of the two under (logit desc, id asc)
+    bool sw = better(lb, ib, la, ia);
+    T tl = sw ? lb : la;
+    uint32_t ti = sw ? ib : ia;
+    lb = sw ? la : lb;
+    ib = sw ? ia : ib;
+    la = tl;
+    ia = ti;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_propagate_ax8(const uint32_t* __restrict__ prev, uint32_t* __restrict__ next,
+                                                       const Q4<T>* __restrict__ pack, const uint32_t* __restrict__ act,
+                                                       const DevState* __restrict__ st, FieldDims f, int step,
+                                                       int inject, uint64_t seed, uint32_t pass_offset, T s) {
+    __shared__ uint32_t q[kAxQ * 256];
+    const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+    const int gx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gy = blockIdx.y * blockDim.y + threadIdx.y;
+    if (gx >= f.gw || gy >= f.gh) return;
+    const T cx = static_cast<T>(gx * static_cast<double>(f.cell) + (f.cell - 1) * 0.5);
+    const T cy = static_cast<T>(gy * static_cast<double>(f.cell) + (f.cell - 1) * 0.5);
+    TopKReg<T, 8, true> sel;
+    sel.init(8);
+
+    // ---- own list: score, then sort with a network
+    const uint32_t* own = prev + 8 * (static_cast<size_t>(gy) * f.gw + gx);
+    uint4 o0 = __ldg(reinterpret_cast<const uint4*>(own)), o1 = __ldg(reinterpret_cast<const uint4*>(own) + 1);
+    uint32_t oid[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+    T ol[8];
+    bool stop = false, fallback = false;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        stop = stop || oid[i] == kEmpty;
+        ol[i] = -INFINITY;
+        if (!stop) {
+            const Q4<T> a = pack[2 * oid[i]], b = pack[2 * oid[i] + 1];
+            if (b.w != T(0)) {
+                ol[i] = score_logit(a, b, cx, cy, s);
+                fallback |= !isfinite(static_cast<double>(ol[i]));
+            } else {
+                oid[i] = kEmpty;  // inactive: dropped
+            }
+        } else {
+            oid[i] = kEmpty;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i++)
+#pragma unroll
+        for (int j = i + 1; j < 8; j++) fallback |= (oid[i] != kEmpty && oid[i] == oid[j]);
+    if (!fallback) {
+        // Batcher odd-even merge sort, 19 comparators; kEmpty entries carry -inf and sort last
+        cex(ol[0], oid[0], ol[1], oid[1]); cex(ol[2], oid[2], ol[3], oid[3]);
+        cex(ol[4], oid[4], ol[5], oid[5]); cex(ol[6], oid[6], ol[7], oid[7]);
+        cex(ol[0], oid[0], ol[2], oid[2]); cex(ol[1], oid[1], ol[3], oid[3]);
+        cex(ol[4], oid[4], ol[6], oid[6]); cex(ol[5], oid[5], ol[7], oid[7]);
+        cex(ol[1], oid[1], ol[2], oid[2]); cex(ol[5], oid[5], ol[6], oid[6]);
+        cex(ol[0], oid[0], ol[4], oid[4]); cex(ol[1], oid[1], ol[5], oid[5]);
+        cex(ol[2], oid[2], ol[6], oid[6]); cex(ol[3], oid[3], ol[7], oid[7]);
+        cex(ol[2], oid[2], ol[4], oid[4]); cex(ol[3], oid[3], ol[5], oid[5]);
+        cex(ol[1], oid[1], ol[2], oid[2]); cex(ol[3], oid[3], ol[4], oid[4]);
+        cex(ol[5], oid[5], ol[6], oid[6]);
+        int n = 0;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            sel.id[i] = oid[i];
+            sel.lg[i] = oid[i] == kEmpty ? T(0) : ol[i];
+            n += oid[i] != kEmpty;
+        }
+        sel.n = n;
+    } else {
+        // generic streaming insertion in list order (reference semantics incl. NaN)
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            uint32_t c = oid[i];
+            if (c == kEmpty || sel.contains(c)) continue;
+            sel.consider(c, ol[i]);
+        }
+    }
+
+    // ---- neighbour entries not already in the list, then injected ids, into the queue
+    int nq = 0;
+#pragma unroll 1
+    for (int o = 1; o < 5; o++) {
+        int nx = gx + (o == 1 ? step : (o == 2 ? -step : 0));
+        int ny = gy + (o == 3 ? step : (o == 4 ? -step : 0));
+        if (nx < 0 || ny < 0 || nx >= f.gw || ny >= f.gh) continue;
+        const uint4* lst = reinterpret_cast<const uint4*>(prev + 8 * (static_cast<size_t>(ny) * f.gw + nx));
+        uint4 u0 = __ldg(lst), u1 = __ldg(lst + 1);
+        uint32_t v[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+        bool end = false;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            end = end || v[i] == kEmpty;
+            if (!end && !sel.contains(v[i])) q[nq++ * 256 + tid] = v[i];
+        }
+    }
+    const int n_act = st->n_active;
+    if (inject > 0 && n_act > 0) {
+        uint32_t rs = seeded_state(seed, st->pass_index + pass_offset,
+                                   static_cast<uint32_t>(gy) * static_cast<uint32_t>(f.gw) + static_cast<uint32_t>(gx));
+        for (int j = 0; j < inject; j++) q[nq++ * 256 + tid] = __ldg(act + xs_next(rs) % static_cast<uint32_t>(n_act));
+    }
+    // ---- score and insert the queue
+#pragma unroll 1
+    for (int j = 0; j < nq; j++) {
+        const uint32_t c = q[j * 256 + tid];
+        if (sel.contains(c)) continue;
+        const Q4<T> b = pack[2 * c + 1];
+        if (b.w == T(0)) continue;
+        const Q4<T> a = pack[2 * c];
+        T l = score_logit(a, b, cx, cy, s);
+        if (sel.full_reject(l, c)) continue;
+        sel.consider(c, l);
+    }
+    uint4* out = reinterpret_cast<uint4*>(next + 8 * (static_cast<size_t>(gy) * f.gw + gx));
+    out[0] = make_uint4(sel.id[0], sel.id[1], sel.id[2], sel.id[3]);
+    out[1] = make_uint4(sel.id[4], sel.id[5], sel.id[6], sel.id[7]);
+}
+
 template <typename T, int KM, bool EXACT>
 static void propagate_t(const uint32_t* prev, uint32_t* next, const void* pack, const uint32_t* act,
                         const DevState* st, const FieldDims& f, uint32_t step, int box, int inject, uint64_t seed,
@@ -324,6 +457,19 @@ static void propagate_t(const uint32_t* prev, uint32_t* next, const void* pack, 
 void launch_propagate(bool fp64, const uint32_t* prev, uint32_t* next, const void* pack, const uint32_t* act,
                       const DevState* st, const FieldDims& f, uint32_t step, int box, int inject, uint64_t seed,
                       uint32_t pass_offset, double scale, cudaStream_t stream) {
+    if (f.k == 8 && !box && inject <= 4) {
+        dim3 block(32, 8);
+        dim3 grid((f.gw + 31) / 32, (f.gh + 7) / 8);
+        if (fp64)
+            k_propagate_ax8<double><<<grid, block, 0, stream>>>(prev, next, (const Q4<double>*)pack, act, st, f,
+                                                                (int)step, inject, seed, pass_offset, scale);
+        else
+            k_propagate_ax8<float><<<grid, block, 0, stream>>>(prev, next, (const Q4<float>*)pack, act, st, f,
+                                                               (int)step, inject, seed, pass_offset,
+                                                               static_cast<float>(scale));
+        SAD_LAUNCHED();
+        return;
+    }
     if (f.k == 8) {
         if (fp64)
             propagate_t<double, 8, true>(prev, next, pack, act, st, f, step, box, inject, seed, pass_offset, scale,
@@ -421,7 +567,7 @@ __global__ void __launch_bounds__(256) k_render(const uint32_t* __restrict__ ids
             w[i] = texp(lg[i] - best);
             sum += w[i];
         }
-    T inv = T(1) / sum;
+    T inv = trcp(sum);
     T r = T(0), g = T(0), b = T(0);
 #pragma unroll
     for (int i = 0; i < KM; i++)
@@ -887,7 +1033,7 @@ __global__ void __launch_bounds__(BwdTile<T>::TW * BwdTile<T>::TH)
                 wsum += w[i];
             }
         }
-        T invw = T(1) / wsum;
+        T invw = trcp(wsum);
         T ch0 = T(0), ch1 = T(0), ch2 = T(0);
 #pragma unroll
         for (int i = 0; i < KM; i++)
@@ -939,7 +1085,7 @@ __global__ void __launch_bounds__(BwdTile<T>::TW * BwdTile<T>::TH)
             v[2] = A * lg[i];
             v[3] = A * ts;
             if (nrm[i] > kTiny) {
-                T inv_n = T(1) / nrm[i];
+                T inv_n = trcp(nrm[i]);
                 T eau = b.x * ud[i];
                 T iav = b.y * vd[i];
                 T coef = A * ts * inv_n;
@@ -955,7 +1101,7 @@ __global__ void __launch_bounds__(BwdTile<T>::TW * BwdTile<T>::TH)
                 if (w[i] >= T(1) - T(1e-6)) {
                     v[10] = static_cast<T>(1e6);
                 } else {
-                    T inv_rest = T(1) / (T(1) - w[i]);
+                    T inv_rest = trcp(T(1) - w[i]);
                     T r0 = (ch0 - w[i] * c.x) * inv_rest - t0;
                     T r1 = (ch1 - w[i] * c.y) * inv_rest - t1;
                     T r2 = (ch2 - w[i] * c.z) * inv_rest - t2;
@@ -963,15 +1109,20 @@ __global__ void __launch_bounds__(BwdTile<T>::TW * BwdTile<T>::TH)
                 }
             }
             sm.key[e] = id;
+            // non-finite components are zeroed and counted (grad.cpp:232-237); one combined test first
+            bool bad = false;
 #pragma unroll
-            for (int t = 0; t < NCH; t++) {
-                T x = v[t];
-                if (!c_finite(x)) {
-                    x = T(0);
-                    nonfinite++;
-                }
-                sm.c[t * Red::ES + e] = x;
+            for (int t = 0; t < NCH; t++) bad |= !c_finite(v[t]);
+            if (bad) {
+#pragma unroll
+                for (int t = 0; t < NCH; t++)
+                    if (!c_finite(v[t])) {
+                        v[t] = T(0);
+                        nonfinite++;
+                    }
             }
+#pragma unroll
+            for (int t = 0; t < NCH; t++) sm.c[t * Red::ES + e] = v[t];
         }
     } else {
 #pragma unroll
@@ -1085,7 +1236,7 @@ __global__ void __launch_bounds__(128) k_loss(const uint32_t* __restrict__ ids, 
                     w[i] = texp(lg[i] - best);
                     wsum += w[i];
                 }
-            T invw = T(1) / wsum;
+            T invw = trcp(wsum);
             T c0 = T(0), c1 = T(0), c2 = T(0);
 #pragma unroll
             for (int i = 0; i < KM; i++)
@@ -1325,48 +1476,80 @@ __device__ __forceinline__ void clamp_site(double* p, int cap, int id, const Ada
     }
 }
 
+// One 16-lane group per site: lane k < 10 merges the gradient records of slot k, applies the Adam
+// update of that parameter and its clamp; dir is renormalised from both lanes' values exchanged by
+// shuffle; lane 0 then rebuilds the site's candidate snapshot and backward table.
 template <typename T>
-__global__ void k_adam(SitesDev s, DevState* st, RedTarget grads, double* __restrict__ m,
-                       double* __restrict__ v, AdamHyper hp, const double2* __restrict__ bc_table, double2 bc_now,
-                       int zero_grads, double scale, Q4<T>* pack, Q4<T>* gtab) {
-    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarget grads, double* __restrict__ m,
+                                              double* __restrict__ v, AdamHyper hp,
+                                              const double2* __restrict__ bc_table, double2 bc_now, int zero_grads,
+                                              double scale, Q4<T>* pack, Q4<T>* gtab) {
+    const int lane16 = threadIdx.x & 15;
+    const int id = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
+    const unsigned gmask = 0xffffu << (threadIdx.x & 16);
     const int cap = s.cap;
+    const bool live = id < st->n_sites;
+    const int k = lane16;
     unsigned long long skipped = 0;
-    if (id < st->n_sites) {
-        double2 bc = bc_table ? bc_table[st->t + 1] : bc_now;
-        int nrec = grads.cnt[id];
-        if (nrec > grads.maxt) nrec = grads.maxt;
-        if (s.active[id] && !s.frozen[id]) {
-#pragma unroll 1
-            for (int k = 0; k < 10; k++) {
-                DD g = red_total(grads, id, k, nrec);
-                double gv = g.hi + g.lo;
-                if (!isfinite(gv)) {
-                    skipped++;
-                    continue;
-                }
-                size_t mi = static_cast<size_t>(k) * cap + id;
+    if (live) {
+        const bool upd = s.active[id] && !s.frozen[id];
+        double p = 0.0;
+        if (k < 10) p = s.p[static_cast<size_t>(k) * cap + id];
+        if (upd && k < 10) {
+            const double2 bc = bc_table ? bc_table[st->t + 1] : bc_now;
+            int nrec = grads.cnt[id];
+            if (nrec > grads.maxt) nrec = grads.maxt;
+            DD g = red_total(grads, id, k, nrec);
+            double gv = g.hi + g.lo;
+            if (!isfinite(gv)) {
+                skipped++;
+            } else {
+                const size_t mi = static_cast<size_t>(k) * cap + id;
                 double mm = hp.beta1 * m[mi] + (1.0 - hp.beta1) * gv;
                 double vv = hp.beta2 * v[mi] + (1.0 - hp.beta2) * gv * gv;
                 m[mi] = mm;
                 v[mi] = vv;
-                s.p[mi] -= hp.lr[k] * (mm / bc.x) / (__dsqrt_rn(vv / bc.y) + hp.eps);
+                p -= hp.lr[k] * (mm / bc.x) / (__dsqrt_rn(vv / bc.y) + hp.eps);
             }
-            clamp_site(s.p, cap, id, hp);
+            // clamp_project (train.cpp:113-137)
+            switch (k) {
+            case 0: p = smin(smax(p, 0.0), hp.width - 1.0); break;
+            case 1: p = smin(smax(p, 0.0), hp.height - 1.0); break;
+            case 2: p = smin(smax(p, hp.log_tau_min), hp.log_tau_max); break;
+            case 3: p = smin(smax(p, hp.radius_min), hp.radius_max); break;
+            case 4:
+            case 5:
+            case 6:
+                if (hp.clamp_color) p = smin(smax(p, 0.0), 1.0);
+                break;
+            case 9: p = smin(smax(p, hp.aniso_min), hp.aniso_max); break;
+            default: break;
+            }
         }
+        const double nx = __shfl_sync(gmask, p, (threadIdx.x & 16) + 7);
+        const double ny = __shfl_sync(gmask, p, (threadIdx.x & 16) + 8);
+        if (upd && (k == 7 || k == 8)) {
+            double norm = __dsqrt_rn(nx * nx + ny * ny);
+            if (!(norm > 1e-12) || !isfinite(norm)) p = k == 7 ? 1.0 : 0.0;
+            else p = (k == 7 ? nx : ny) / norm;
+        }
+        if (upd && k < 10) s.p[static_cast<size_t>(k) * cap + id] = p;
         if (zero_grads) {
-#pragma unroll
-            for (int k = 0; k < 11; k++) grads.over[static_cast<size_t>(k) * cap + id] = make_double2(0.0, 0.0);
-            grads.cnt[id] = 0;
+            if (k < 11) grads.over[static_cast<size_t>(k) * cap + id] = make_double2(0.0, 0.0);
+            if (k == 0) grads.cnt[id] = 0;
         }
+    } else {
+        __shfl_sync(gmask, 0.0, (threadIdx.x & 16) + 7);
+        __shfl_sync(gmask, 0.0, (threadIdx.x & 16) + 8);
     }
     if (skipped) atomicAdd(reinterpret_cast<unsigned long long*>(&st->skipped), skipped);
-    if (id < st->n_sites && (pack || gtab)) {
+    __syncwarp();
+    if (live && lane16 == 0 && (pack || gtab)) {
         // same derivations as k_tables (score_table.hpp:20-46, grad.cpp:84-110)
-        const double* p = s.p;
+        const double* pp = s.p;
         bool act = s.active[id] != 0;
-        double x = p[0 * cap + id], y = p[1 * cap + id], lt = p[2 * cap + id], r = p[3 * cap + id];
-        double ux = p[7 * cap + id], uy = p[8 * cap + id], an = p[9 * cap + id];
+        double x = pp[0 * cap + id], y = pp[1 * cap + id], lt = pp[2 * cap + id], r = pp[3 * cap + id];
+        double ux = pp[7 * cap + id], uy = pp[8 * cap + id], an = pp[9 * cap + id];
         if (pack) {
             Q4<T> a, b;
             if (!act) {
@@ -1393,8 +1576,8 @@ __global__ void k_adam(SitesDev s, DevState* st, RedTarget grads, double* __rest
             } else {
                 a = {static_cast<T>(x), static_cast<T>(y), static_cast<T>(exp(lt)), static_cast<T>(r)};
                 b = {static_cast<T>(exp(an)), static_cast<T>(exp(-an)), static_cast<T>(ux), static_cast<T>(uy)};
-                c = {static_cast<T>(p[4 * cap + id]), static_cast<T>(p[5 * cap + id]), static_cast<T>(p[6 * cap + id]),
-                     T(1)};
+                c = {static_cast<T>(pp[4 * cap + id]), static_cast<T>(pp[5 * cap + id]),
+                     static_cast<T>(pp[6 * cap + id]), T(1)};
             }
             gtab[3 * id] = a;
             gtab[3 * id + 1] = b;
@@ -1406,7 +1589,7 @@ __global__ void k_adam(SitesDev s, DevState* st, RedTarget grads, double* __rest
 void launch_adam(bool fp64, const SitesDev& s, DevState* st, const RedTarget& grads, double* m, double* v, const AdamHyper& hp,
                  const double2* bc_table, double2 bc_now, bool zero_grads, double scale, void* pack, void* gtab,
                  cudaStream_t stream) {
-    int grid = (s.cap + 127) / 128;
+    int grid = (s.cap + 7) / 8;  // 8 sites (16 lanes each) per 128-thread block
     if (grid < 1) grid = 1;
     if (fp64)
         k_adam<double><<<grid, 128, 0, stream>>>(s, st, grads, m, v, hp, bc_table, bc_now, zero_grads ? 1 : 0, scale,
