@@ -413,7 +413,8 @@ _lock = threading.Lock()
 _gpu = None
 
 
-def load_library(path: str = LIB_PATH) -> C.CDLL:
+def load_library(path: Optional[str] = None) -> C.CDLL:
+    path = path or LIB_PATH
     if not os.path.exists(path):
         raise ImportError(f"CUDA library {path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
     lib = C.CDLL(path)

@@ -7,6 +7,20 @@
 #include "sad_device.cuh"
 #include "sad_kernels.h"
 
+#ifndef SAD_EXPERIMENT
+#define SAD_EXPERIMENT 0
+#endif
+#if SAD_EXPERIMENT == 3
+__device__ unsigned long long g_phase_clk[16];
+#define PH(i) do { __syncthreads(); if (threadIdx.x == 0) { long long _c = clock64(); atomicAdd(&g_phase_clk[i], (unsigned long long)(_c - _t0)); _t0 = _c; } } while (0)
+extern "C" void sad_exp_phase(unsigned long long* out, int reset) {
+    if (reset) { unsigned long long z[16] = {0}; cudaMemcpyToSymbol(g_phase_clk, z, sizeof z); }
+    else cudaMemcpyFromSymbol(out, g_phase_clk, 16 * sizeof(unsigned long long));
+}
+#else
+#define PH(i) do { } while (0)
+#endif
+
 #include <atomic>
 
 namespace sadk {
@@ -751,6 +765,9 @@ template <typename CT, int NCH, int TPX, int KM>
 __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, const RedTarget& red) {
     using R = TileRed<CT, NCH, TPX, KM>;
     const int tid = threadIdx.x;
+#if SAD_EXPERIMENT == 3
+    long long _t0 = clock64();
+#endif
     // 2. hash insert (site ids are < 2^31; table keys start as kEmpty)
     for (int e = tid; e < R::E; e += TPX) {
         uint32_t key = sm.key[e];
@@ -764,6 +781,7 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, const
         sm.local_of_entry[e] = static_cast<uint16_t>(h);
     }
     __syncthreads();
+    PH(1);
     for (int h = tid; h < R::HT; h += TPX) {
         uint32_t key = sm.hkey[h];
         if (key != kEmpty) {
@@ -776,9 +794,17 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, const
     const int U = sm.n_local;
     for (int u = tid; u < U; u += TPX) {
         sm.cnt[u] = 0;  // aliases hkey: safe after the barrier
-        sm.slot_of_local[u] = static_cast<uint32_t>(atomicAdd(red.cnt + sm.site_of_local[u], 1));
+        const uint32_t site = sm.site_of_local[u];
+        uint32_t slot = static_cast<uint32_t>(atomicAdd(red.cnt + site, 1));
+        if (slot >= static_cast<uint32_t>(red.maxt)) {  // overflow record from the pool, linked per site
+            int r = atomicAdd(red.otop, 1);
+            if (r < red.ocap) red.onext[r] = atomicExch(red.head + site, r);
+            slot = r < red.ocap ? static_cast<uint32_t>(red.maxt + r) : 0xffffffffu;
+        }
+        sm.slot_of_local[u] = slot;
     }
     __syncthreads();
+    PH(2);
     // 3. bucket counts (entries with key == kEmpty get bucket 0xffff)
     for (int e = tid; e < R::E; e += TPX) {
         uint16_t loc = 0xffffu;
@@ -808,6 +834,7 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, const
         if (tid == 0) n_valid = carry;
     }
     __syncthreads();  // key[] is dead from here: its storage becomes order/posloc
+    PH(3);
     for (int e = tid; e < R::E; e += TPX) {
         int loc = sm.local_of_entry[e];
         if (loc == 0xffff) continue;
@@ -816,6 +843,7 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, const
     }
     __syncthreads();
     for (int u = tid; u < U; u += TPX) sm.start[u] -= sm.cnt[u];  // cursor back to the bucket start
+    PH(4);
     // 4. buckets split into chunks of PT sorted entries; thread t sums chunks t and t + TPX for all
     //    channels (convergent fixed-trip loops, NCH independent double-double chains)
     const int U2 = U;
@@ -845,6 +873,7 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, const
     }
     __syncthreads();
     const int NC = n_chunks;
+    PH(5);
     DD acc0[NCH], acc1[NCH];
     auto sum_chunk = [&](int c, DD* acc) {
 #pragma unroll
@@ -873,6 +902,7 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, const
         for (int ch = 0; ch < NCH; ch++) dd_atomic_merge(red.over + static_cast<size_t>(ch) * red.cap + site, tmp[ch]);
     }
     __syncthreads();  // every read of c[] is done: its storage becomes the chunk partials
+    PH(6);
     if (tid < NC) {
 #pragma unroll
         for (int ch = 0; ch < NCH; ch++) sm.carry[tid * NCH + ch] = acc0[ch];
@@ -882,6 +912,7 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, const
         for (int ch = 0; ch < NCH; ch++) sm.carry[(tid + TPX) * NCH + ch] = acc1[ch];
     }
     __syncthreads();
+    PH(7);
     // 5. per (site, channel): merge the site's chunks and store the record (or CAS on slot overflow)
     const int NCK = NC < 2 * TPX ? NC : 2 * TPX;
     for (int item = tid; item < U2 * NCH; item += TPX) {
@@ -892,11 +923,18 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, const
         for (int c = c0; c < c1 && c < NCK; c++) dd_merge(t, sm.carry[c * NCH + ch]);
         const uint32_t site = sm.site_of_local[u];
         const uint32_t slot = sm.slot_of_local[u];
-        if (slot < static_cast<uint32_t>(red.maxt))
+        if (slot < static_cast<uint32_t>(red.maxt)) {
             red.part[(static_cast<size_t>(site) * red.maxt + slot) * red.stride + ch] = make_double2(t.hi, t.lo);
-        else
+        } else if (slot != 0xffffffffu) {
+            red.opart[static_cast<size_t>(slot - red.maxt) * red.stride + ch] = make_double2(t.hi, t.lo);
+        } else {  // pool exhausted
+#if SAD_EXPERIMENT == 3
+            if (ch == 0) atomicAdd(&g_phase_clk[15], 1ull);
+#endif
             dd_atomic_merge(red.over + static_cast<size_t>(ch) * red.cap + site, t);
+        }
     }
+    PH(8);
 }
 
 template <typename CT, int NCH, int TPX, int KM>
@@ -969,6 +1007,9 @@ __global__ void __launch_bounds__(BwdTile<T>::TW * BwdTile<T>::TH)
     using Red = TileRed<T, NCH, TPX, KM>;
     extern __shared__ __align__(16) unsigned char smraw[];
     Red& sm = *reinterpret_cast<Red*>(smraw);
+#if SAD_EXPERIMENT == 3
+    long long _t0 = clock64();
+#endif
     tile_init(sm);
 
     const int tid = threadIdx.x;
@@ -1129,6 +1170,7 @@ __global__ void __launch_bounds__(BwdTile<T>::TW * BwdTile<T>::TH)
         for (int i = 0; i < KM; i++) sm.key[i * TPX + tid] = kEmpty;
     }
     __syncthreads();
+    PH(0);
     tile_reduce(sm, red);
     __syncthreads();
     if (MODE != 2) block_dd_store<TPX>(loss, sm.warp_part, loss_part + blockIdx.y * gridDim.x + blockIdx.x);
@@ -1294,6 +1336,10 @@ __device__ __forceinline__ DD red_total(const RedTarget& red, int id, int ch, in
         double2 r = rec[static_cast<size_t>(s) * red.stride];
         dd_merge(acc, DD{r.x, r.y});
     }
+    for (int r = red.head[id]; r >= 0; r = red.onext[r]) {
+        double2 o2 = red.opart[static_cast<size_t>(r) * red.stride + ch];
+        dd_merge(acc, DD{o2.x, o2.y});
+    }
     return acc;
 }
 
@@ -1309,6 +1355,7 @@ __global__ void k_finalize(RedTarget red, const DevState* __restrict__ st) {
         red.over[static_cast<size_t>(ch) * red.cap + id] = make_double2(t.hi, t.lo);
     }
     red.cnt[id] = 0;
+    red.head[id] = -1;
 }
 
 void launch_finalize(const RedTarget& red, int n_ch, const DevState* st, cudaStream_t stream) {
@@ -1537,6 +1584,7 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
         if (zero_grads) {
             if (k < 11) grads.over[static_cast<size_t>(k) * cap + id] = make_double2(0.0, 0.0);
             if (k == 0) grads.cnt[id] = 0;
+            if (k == 1) grads.head[id] = -1;
         }
     } else {
         __shfl_sync(gmask, 0.0, (threadIdx.x & 16) + 7);
@@ -1813,7 +1861,8 @@ void launch_flag_active(const SitesDev& s, const DevState* st, uint8_t* flags, c
 
 // ====================================================================== loop bookkeeping
 __global__ void k_advance(DevState* st, int passes, int adam_steps, double2* loss_hist, int32_t* active_hist,
-                          const double2* __restrict__ loss_part, int n_part) {
+                          const double2* __restrict__ loss_part, int n_part, int32_t* otop) {
+    if (otop && threadIdx.x == 0) *otop = 0;
     __shared__ DD parts[8];
     DD acc{0.0, 0.0};
     if (loss_hist)
@@ -1837,8 +1886,8 @@ __global__ void k_advance(DevState* st, int passes, int adam_steps, double2* los
 }
 
 void launch_advance(DevState* st, int passes, int adam_steps, double2* loss_hist, int32_t* active_hist,
-                    const double2* loss_part, int n_part, cudaStream_t stream) {
-    k_advance<<<1, 256, 0, stream>>>(st, passes, adam_steps, loss_hist, active_hist, loss_part, n_part);
+                    const double2* loss_part, int n_part, int32_t* otop, cudaStream_t stream) {
+    k_advance<<<1, 256, 0, stream>>>(st, passes, adam_steps, loss_hist, active_hist, loss_part, n_part, otop);
     SAD_LAUNCHED();
 }
 

@@ -52,6 +52,12 @@ struct RedTarget {
     int cap;
     int maxt;
     int stride;     // channels per record (11 for gradients, 8 for stats)
+    // overflow pool: records beyond maxt per site go to opart[r], linked per site from head[site]
+    int32_t* head;  // [cap] first overflow record of the site, -1 = none
+    int32_t* onext; // [ocap] next record of the same site
+    double2* opart; // [ocap][stride]
+    int32_t* otop;  // pool allocation counter (reset per pass)
+    int ocap;
 };
 
 struct FieldDims {
@@ -134,7 +140,7 @@ void launch_flag_active(const SitesDev& s, const DevState* st, uint8_t* flags, c
 // pass_index += passes; t and iter advance; records loss/active history row `iter`.
 // With loss_hist: reduces loss_part[0..n_part) into history row `iter` and advances iter.
 void launch_advance(DevState* st, int passes, int adam_steps, double2* loss_hist, int32_t* active_hist,
-                    const double2* loss_part, int n_part, cudaStream_t stream);
+                    const double2* loss_part, int n_part, int32_t* otop, cudaStream_t stream);
 
 // ---------------------------------------------------------------- init (train.cpp:33-111) device path
 void launch_sobel(const double* tgt, int w, int h, double* mag, cudaStream_t stream);

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -287,7 +288,7 @@ struct Workspace {
     DBuf<double2> gpart, spart;       // RedTarget.part records
     DBuf<int32_t> gcnt, scnt;         // RedTarget.cnt
     DBuf<double2> loss_part;          // per-block loss partials
-    int maxt = 16;                    // record slots per site and pass
+    int maxt = getenv("SAD_MAXT") ? atoi(getenv("SAD_MAXT")) : 16;  // record slots per site and pass
     DBuf<double> m, v;
     DBuf<uint32_t> act, free_list;
     DBuf<uint8_t> flags;
@@ -315,15 +316,38 @@ struct Workspace {
     }
 
     sadk::SitesDev sites() { return sadk::SitesDev{params.p, active.p, frozen.p, cap}; }
-    sadk::RedTarget gred() { return sadk::RedTarget{grads.p, gpart.p, gcnt.p, cap, maxt, 11}; }
-    sadk::RedTarget sred() { return sadk::RedTarget{stats.p, spart.p, scnt.p, cap, maxt, 8}; }
+    DBuf<int32_t> ghead, shead, gnext, snext, otops;  // overflow lists (otops: [0] grads, [1] stats)
+    DBuf<double2> gopart, sopart;
+    int ocap = 0;
+    sadk::RedTarget gred() {
+        return sadk::RedTarget{grads.p, gpart.p, gcnt.p, cap, maxt, 11, ghead.p, gnext.p, gopart.p, otops.p, ocap};
+    }
+    sadk::RedTarget sred() {
+        return sadk::RedTarget{stats.p, spart.p, scnt.p, cap, maxt, 8, shead.p, snext.p, sopart.p, otops.p + 1, ocap};
+    }
+    // overflow pool sized from the number of reduction tiles (each tile adds at most its bucket count)
+    void ensure_pool(size_t tiles) {
+        size_t want = std::max<size_t>(tiles * 16, 4096);
+        if (static_cast<size_t>(ocap) >= want && otops.p) return;
+        gnext.ensure(want);
+        snext.ensure(want);
+        gopart.ensure(want * 11);
+        sopart.ensure(want * 8);
+        otops.ensure(2);
+        ck(cudaMemsetAsync(otops.p, 0, 2 * sizeof(int32_t), stream), "memset otop");
+        ocap = static_cast<int>(want);
+    }
     void zero_red(bool g) {
         if (g) {
             ck(cudaMemsetAsync(grads.p, 0, sizeof(double2) * 11 * cap, stream), "memset grads");
             ck(cudaMemsetAsync(gcnt.p, 0, sizeof(int32_t) * cap, stream), "memset gcnt");
+            ck(cudaMemsetAsync(ghead.p, 0xff, sizeof(int32_t) * cap, stream), "memset ghead");
+            ck(cudaMemsetAsync(otops.p, 0, sizeof(int32_t), stream), "memset otop");
         } else {
             ck(cudaMemsetAsync(stats.p, 0, sizeof(double2) * 8 * cap, stream), "memset stats");
             ck(cudaMemsetAsync(scnt.p, 0, sizeof(int32_t) * cap, stream), "memset scnt");
+            ck(cudaMemsetAsync(shead.p, 0xff, sizeof(int32_t) * cap, stream), "memset shead");
+            ck(cudaMemsetAsync(otops.p + 1, 0, sizeof(int32_t), stream), "memset otop");
         }
     }
 
@@ -378,6 +402,10 @@ struct Workspace {
         spart.ensure(static_cast<size_t>(nc) * maxt * 8);
         gcnt.ensure(nc);
         scnt.ensure(nc);
+        ghead.ensure(nc);
+        shead.ensure(nc);
+        ck(cudaMemsetAsync(ghead.p, 0xff, ghead.n * sizeof(int32_t), stream), "memset ghead");
+        ck(cudaMemsetAsync(shead.p, 0xff, shead.n * sizeof(int32_t), stream), "memset shead");
         ck(cudaMemsetAsync(grads.p, 0, grads.n * sizeof(double2), stream), "memset grads");
         ck(cudaMemsetAsync(gcnt.p, 0, gcnt.n * sizeof(int32_t), stream), "memset gcnt");
         ck(cudaMemsetAsync(scnt.p, 0, scnt.n * sizeof(int32_t), stream), "memset scnt");
@@ -414,6 +442,8 @@ struct Workspace {
         ids[1].ensure(n);
         loss_part.ensure(static_cast<size_t>(std::max({sadk::backward_blocks(false, fd), sadk::backward_blocks(true, fd),
                                                        sadk::loss_blocks(fd)})));
+        ensure_pool(static_cast<size_t>(std::max(sadk::backward_blocks(false, fd),
+                                                 ((w_ + 7) / 8) * ((h_ + 7) / 8))));
     }
 
     void ensure_target(size_t px) {
@@ -955,7 +985,7 @@ static void backward_call(sad_ctx* c, const sad_sites_view* s, const sad_field_v
     sadk::launch_backward(fp64 != 0, mode, ws.ids[ws.cur].p, ws.gtab.p,
                           fp64 ? static_cast<const void*>(ws.tgt_d.p) : static_cast<const void*>(ws.tgt_f.p), ws.fd,
                           norm_scale(f->width, f->height), ws.gred(), ws.loss_part.p, ws.st.p, ws.stream);
-    sadk::launch_finalize(ws.gred(), 11, ws.st.p, ws.stream);
+    sadk::launch_finalize(ws.gred(), mode == 1 ? 11 : 10, ws.st.p, ws.stream);  // channel 10 only with removal
     if (mode != 2)
         sadk::launch_loss_reduce(ws.loss_part.p, sadk::backward_blocks(fp64 != 0, ws.fd), &ws.st.p->loss, ws.stream);
     DBuf<double> out;
@@ -1324,7 +1354,7 @@ static void fit_loop(sad_fit_run* r) {
     sadk::launch_jfa_seed(ws.sites(), ws.st.p, ws.ids[0].p, ws.fd, scale_n, s);
     passes_device(ws, full4, c.inject, c.seed, fp64, 0);
     const int nbw = sadk::backward_blocks(fp64, ws.fd);
-    sadk::launch_advance(ws.st.p, static_cast<int>(full4.size()), 0, nullptr, nullptr, nullptr, 0, s);
+    sadk::launch_advance(ws.st.p, static_cast<int>(full4.size()), 0, nullptr, nullptr, nullptr, 0, ws.otops.p, s);
 
     for (int t = 1; t <= c.iters; t++) {
         int npass = 0;
@@ -1351,14 +1381,14 @@ static void fit_loop(sad_fit_run* r) {
             passes_device(ws, full4, c.inject, c.seed, fp64, static_cast<uint32_t>(npass));
             npass += static_cast<int>(full4.size());
         }
-        sadk::launch_advance(ws.st.p, npass, 1, r->loss_hist.p, r->active_hist.p, ws.loss_part.p, nbw, s);
+        sadk::launch_advance(ws.st.p, npass, 1, r->loss_hist.p, r->active_hist.p, ws.loss_part.p, nbw, ws.otops.p, s);
     }
     // final full refresh (train.cpp:287)
     const auto fin = full_refresh_passes(ws.fd.gw, ws.fd.gh, c.final_passes);
     ws.cur = 0;
     sadk::launch_jfa_seed(ws.sites(), ws.st.p, ws.ids[0].p, ws.fd, scale_n, s);
     passes_device(ws, fin, c.inject, c.seed, fp64, 0);
-    sadk::launch_advance(ws.st.p, static_cast<int>(fin.size()), 0, nullptr, nullptr, nullptr, 0, s);
+    sadk::launch_advance(ws.st.p, static_cast<int>(fin.size()), 0, nullptr, nullptr, nullptr, 0, ws.otops.p, s);
     cudaEventRecord(e1, s);
     ck(cudaStreamSynchronize(s), "fit");
     float ms = 0;
@@ -1462,12 +1492,18 @@ sad_status sad_fit_bench(sad_fit_run* r, int which, int reps, double* ms_per_lau
         auto once = [&]() {
             switch (which) {
             case 0: passes_device(ws, {sad_pass_spec{1, 0}}, c.inject, c.seed, fp64, 0); break;
-            case 1:  // record counters reset each launch as Adam does in the fit (memset timed separately)
+            case 1:  // record counters reset each launch as Adam does in the fit (memsets timed separately)
                 ck(cudaMemsetAsync(ws.gcnt.p, 0, sizeof(int32_t) * ws.cap, s), "memset");
+                ck(cudaMemsetAsync(ws.ghead.p, 0xff, sizeof(int32_t) * ws.cap, s), "memset");
+                ck(cudaMemsetAsync(ws.otops.p, 0, sizeof(int32_t), s), "memset");
                 sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt, ws.fd, sn, ws.gred(),
                                       ws.loss_part.p, ws.st.p, s);
                 break;
-            case 6: ck(cudaMemsetAsync(ws.gcnt.p, 0, sizeof(int32_t) * ws.cap, s), "memset"); break;
+            case 6:
+                ck(cudaMemsetAsync(ws.gcnt.p, 0, sizeof(int32_t) * ws.cap, s), "memset");
+                ck(cudaMemsetAsync(ws.ghead.p, 0xff, sizeof(int32_t) * ws.cap, s), "memset");
+                ck(cudaMemsetAsync(ws.otops.p, 0, sizeof(int32_t), s), "memset");
+                break;
             case 2: sadk::launch_render(false, ws.ids[ws.cur].p, ws.rtab.p, ws.fd, sn, ws.px_f.p, ws.st.p, s); break;
             case 3: passes_device(ws, {sad_pass_spec{16, 1}}, c.inject, c.seed, fp64, 0); break;
             case 4:

@@ -107,7 +107,10 @@ def test_golden_budget(kind):
     tgt = sad.ImageBuffer(48, 48, d["target"])
     s = B.accumulate_stats(st, f, tgt)
     assert s.valid_pixels == d["valid"][0]
-    assert np.allclose(s.data, d["stats"], rtol=1e-12, atol=1e-300)
+    # double exp on the device may differ from glibc by an ulp; removal sums can cancel, so the bound
+    # is relative to each channel's scale
+    scale = np.max(np.abs(d["stats"]), axis=0, keepdims=True)
+    assert np.all(np.abs(s.data - d["stats"]) <= 1e-12 * np.abs(d["stats"]) + 1e-13 * scale)
     ref = sad.StatsResult(st.size())
     ref.data, ref.valid_pixels = d["stats"], int(d["valid"][0])
     a = st.copy()

@@ -24,8 +24,11 @@ p.add_argument("--height", type=int, default=512)
 p.add_argument("--iters", type=int, default=200)
 p.add_argument("--bpp", type=float, default=2.0)
 p.add_argument("--n-sites", type=int, default=0)
+p.add_argument("--lib", default=None, help="alternative libsad_b200.so (ablation builds)")
 a = p.parse_args()
 
+if a.lib:
+    api.LIB_PATH = a.lib
 G = sad.gpu_backend(0)
 cfg = sad.TrainConfig(iters=a.iters, target_bpp=a.bpp if not a.n_sites else 0.0, n_sites=a.n_sites, fp64=False)
 run = C.c_void_p()
