@@ -235,6 +235,9 @@ sad_status sad_fit_download(sad_fit_run* run, sad_sites_view* sites, sad_field_v
 sad_status sad_fit_render_device(sad_fit_run* run, float* device_rgb);
 /* Total kernel time of the last run in ms and per-phase split (propagate, fwd_bwd, adam, events). */
 sad_status sad_fit_timing(sad_fit_run* run, double* total_ms, double* phase_ms4);
+/* Enables per-phase CUDA-event timing for the next runs (propagate, fwd+bwd, Adam+bookkeeping,
+ * events); costs a few microseconds per iteration and disables graph replay while on. */
+sad_status sad_fit_set_profiling(sad_fit_run* run, int on);
 /* Times `reps` launches of one kernel on the fitted, device-resident state with CUDA events on the
  * run's stream.  which: 0 warm propagate pass, 1 fused fwd+bwd, 2 render, 3 Box3 flood pass
  * (step 16), 4 Adam, 5 stats.  Evidence for the roofline numbers; not part of the reference API. */

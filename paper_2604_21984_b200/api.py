@@ -404,7 +404,8 @@ class Backend:
 
 _NO_CTX = {"jump_step", "full_refresh_passes", "schedule_passes", "bpp_target_count", "simulate_schedule",
            "plan_schedule", "fit_set_target", "fit_set_target_device", "fit_run_init", "fit_run_store",
-           "fit_info", "fit_download", "fit_render_device", "fit_timing", "fit_bench", "last_error"}
+           "fit_info", "fit_download", "fit_render_device", "fit_timing", "fit_bench", "fit_set_profiling",
+           "last_error"}
 
 # ---------------------------------------------------------------------- product binding
 _HERE = os.path.dirname(os.path.abspath(__file__))

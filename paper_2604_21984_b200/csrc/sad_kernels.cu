@@ -27,6 +27,7 @@ namespace sadk {
 
 static std::atomic<uint64_t> g_launches{0};
 uint64_t launch_counter() { return g_launches.load(); }
+void add_launches(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 #define SAD_LAUNCHED() g_launches.fetch_add(1, std::memory_order_relaxed)
 
 // ====================================================================== per-site tables
@@ -1185,17 +1186,20 @@ int backward_blocks(bool fp64, const FieldDims& f) {
 }
 
 template <typename T, int KM, int MODE>
+static void backward_attr() {
+    constexpr int TW = BwdTile<T>::TW, TH = BwdTile<T>::TH;
+    constexpr int NCH = MODE == 1 ? 11 : 10;
+    cudaFuncSetAttribute(k_backward<T, KM, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(TileRed<T, NCH, TW * TH, KM>));
+}
+
+template <typename T, int KM, int MODE>
 static void backward_t(const uint32_t* ids, const void* gtab, const void* tgt, const FieldDims& f, double scale,
                        const RedTarget& red, double2* loss_part, DevState* st, cudaStream_t stream) {
     constexpr int TW = BwdTile<T>::TW, TH = BwdTile<T>::TH;
     constexpr int NCH = MODE == 1 ? 11 : 10;
     size_t smem = sizeof(TileRed<T, NCH, TW * TH, KM>);
     auto kern = k_backward<T, KM, MODE>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
     dim3 grid((f.width + TW - 1) / TW, (f.height + TH - 1) / TH);
     T inv_hw2 = static_cast<T>(2.0 / (static_cast<double>(f.width) * f.height));
     kern<<<grid, TW * TH, smem, stream>>>(ids, (const Q4<T>*)gtab, (const T*)tgt, f, static_cast<T>(scale), inv_hw2,
@@ -1472,24 +1476,35 @@ __global__ void __launch_bounds__(64) k_stats(const uint32_t* __restrict__ ids, 
     if (threadIdx.x == 0 && v) atomicAdd(reinterpret_cast<unsigned long long*>(&st->valid), v);
 }
 
+// Opt-in shared-memory sizes of the tile-reduction kernels; called once per context, before any
+// launch can be captured into a CUDA graph.
+void prepare_kernels() {
+    backward_attr<float, 8, 0>();
+    backward_attr<float, 8, 1>();
+    backward_attr<float, 8, 2>();
+    backward_attr<float, 16, 0>();
+    backward_attr<float, 16, 1>();
+    backward_attr<float, 16, 2>();
+    backward_attr<double, 8, 0>();
+    backward_attr<double, 8, 1>();
+    backward_attr<double, 8, 2>();
+    backward_attr<double, 16, 0>();
+    backward_attr<double, 16, 1>();
+    backward_attr<double, 16, 2>();
+    cudaFuncSetAttribute(k_stats<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(TileRed<double, 8, 64, 8>));
+    cudaFuncSetAttribute(k_stats<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(TileRed<double, 8, 64, 16>));
+}
+
 void launch_stats(const uint32_t* ids, const void* rtab_d, const double* tgt, const FieldDims& f, double scale,
                   const RedTarget& red, DevState* st, cudaStream_t stream) {
     dim3 grid((f.width + 7) / 8, (f.height + 7) / 8);
     if (f.k <= 8) {
         size_t smem = sizeof(TileRed<double, 8, 64, 8>);
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_stats<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = true;
-        }
         k_stats<8><<<grid, 64, smem, stream>>>(ids, (const Q4<double>*)rtab_d, tgt, f, scale, red, st);
     } else {
         size_t smem = sizeof(TileRed<double, 8, 64, 16>);
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_stats<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = true;
-        }
         k_stats<16><<<grid, 64, smem, stream>>>(ids, (const Q4<double>*)rtab_d, tgt, f, scale, red, st);
     }
     SAD_LAUNCHED();

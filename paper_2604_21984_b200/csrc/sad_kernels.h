@@ -158,5 +158,9 @@ void launch_scatter_grads_out(const double2* grads, int cap, int n, double* out 
 
 // Number of kernel launches issued through these wrappers (process-wide; evidence counter).
 uint64_t launch_counter();
+// Graph replays re-run captured launches without passing through the wrappers: account for them.
+void add_launches(uint64_t n);
+// Sets per-kernel attributes (opt-in shared memory); call once per device before launching.
+void prepare_kernels();
 
 }  // namespace sadk

@@ -722,13 +722,23 @@ struct sad_fit_run {
     double schedule_scale = 0;
     size_t n_sites = 0;
     double total_ms = 0;
-    double phase_ms[4] = {0, 0, 0, 0};
+    double phase_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     DBuf<double2> loss_hist;
     DBuf<int32_t> active_hist;
     DBuf<double2> bc_table;
     bool bc_ready = false;
     int planned_n0 = -1;  // plan_schedule is a pure function of (n0, target, cfg): cached
     double planned_scale = 0;
+    // CUDA graphs of the plain iteration, per (field buffer parity, warm refresh this iteration)
+    cudaGraphExec_t plain[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    bool profile = false;  // per-phase CUDA-event timing (disables graphs)
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
+    uint64_t plain_launches[2][2] = {{0, 0}, {0, 0}};
+    ~sad_fit_run() {
+        for (auto& a : plain)
+            for (auto& g : a)
+                if (g) cudaGraphExecDestroy(g);
+    }
 };
 
 extern "C" {
@@ -769,6 +779,7 @@ sad_status sad_ctx_create(int device, void* stream, sad_ctx** out) {
             c->own = true;
         }
         c->ws.stream = c->stream;
+        sadk::prepare_kernels();
         c->ws.ensure_state();
         c->launches0 = sadk::launch_counter();
         *out = c;
@@ -1347,6 +1358,27 @@ static void fit_loop(sad_fit_run* r) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0, s);
+    // phase timing: 0 propagate (warm + event refresh passes), 1 fwd+bwd, 2 Adam + bookkeeping,
+    // 3 events (stats, selection, compaction, seeding), 4 init refresh + final refresh
+    for (auto& m : r->marks) {
+        cudaEventDestroy(m.second.first);
+        cudaEventDestroy(m.second.second);
+    }
+    r->marks.clear();
+    const bool prof = r->profile;
+    auto mark = [&](int ph, auto&& fn) {
+        if (!prof) {
+            fn();
+            return;
+        }
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, s);
+        fn();
+        cudaEventRecord(b, s);
+        r->marks.push_back({ph, {a, b}});
+    };
 
     // initial full refresh (train.cpp:238-239)
     build_tables(ws, fp64, true, true, false);
@@ -1356,32 +1388,84 @@ static void fit_loop(sad_fit_run* r) {
     const int nbw = sadk::backward_blocks(fp64, ws.fd);
     sadk::launch_advance(ws.st.p, static_cast<int>(full4.size()), 0, nullptr, nullptr, nullptr, 0, ws.otops.p, s);
 
-    for (int t = 1; t <= c.iters; t++) {
-        int npass = 0;
-        if ((t - 1) % c.refresh_every == 0) {
-            passes_device(ws, warm, c.inject, c.seed, fp64, 0);
-            npass += static_cast<int>(warm.size());
+    const bool use_graphs = getenv("SAD_NO_GRAPHS") == nullptr && !prof;
+    // One plain iteration: warm pass(es) -> fused fwd+bwd -> Adam (+ tables for the next pass) ->
+    // bookkeeping.  All per-iteration scalars live in DevState, so the sequence is replayable.
+    auto plain_iteration = [&](bool rf) {
+        int np = 0;
+        if (rf) {
+            mark(0, [&] { passes_device(ws, warm, c.inject, c.seed, fp64, 0); });
+            np = static_cast<int>(warm.size());
         }
-        sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt, ws.fd, scale_n, ws.gred(), ws.loss_part.p,
-                              ws.st.p, s);
+        mark(1, [&] {
+            sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt, ws.fd, scale_n, ws.gred(),
+                                  ws.loss_part.p, ws.st.p, s);
+        });
+        mark(2, [&] {
+            sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.gred(), ws.m.p, ws.v.p, hp, r->bc_table.p,
+                              make_double2(0, 0), true, scale_n, ws.pack.p, ws.gtab.p, s);
+        });
+        mark(5, [&] {
+            sadk::launch_advance(ws.st.p, np, 1, r->loss_hist.p, r->active_hist.p, ws.loss_part.p, nbw, ws.otops.p, s);
+        });
+    };
+    for (int t = 1; t <= c.iters; t++) {
+        const bool rf = (t - 1) % c.refresh_every == 0;
         bool ev_d = budget && t >= c.densify_start && t <= c.densify_end && t % c.densify_every == 0;
         bool ev_p = budget && t >= c.prune_start && t <= c.prune_end && t % c.prune_every == 0;
         if (ev_p && !c.prune_during_densify && t <= c.densify_end) ev_p = false;
         bool ev = ev_d || ev_p;
-        if (ev) stats_device(ws);
-        sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.gred(), ws.m.p, ws.v.p, hp, r->bc_table.p, make_double2(0, 0),
-                          true, scale_n, ev ? nullptr : ws.pack.p, ev ? nullptr : ws.gtab.p, s);
-        if (ev_p) prune_device(ws, c.prune_pct * sched);
-        if (ev_d) densify_device(ws, c.densify_pct * sched, c);
-        if (ev) {
+        if (!ev && use_graphs) {
+            const int c0 = ws.cur;
+            cudaGraphExec_t& gx = r->plain[c0][rf ? 1 : 0];
+            if (!gx) {
+                cudaGraph_t g = nullptr;
+                uint64_t l0 = sadk::launch_counter();
+                ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
+                plain_iteration(rf);
+                ck(cudaStreamEndCapture(s, &g), "end capture");
+                ck(cudaGraphInstantiate(&gx, g, 0), "graph instantiate");
+                cudaGraphDestroy(g);
+                r->plain_launches[c0][rf ? 1 : 0] = sadk::launch_counter() - l0;
+                ws.cur = c0;
+            }
+            ck(cudaGraphLaunch(gx, s), "graph launch");
+            sadk::add_launches(r->plain_launches[c0][rf ? 1 : 0]);
+            if (rf && (warm.size() & 1)) ws.cur = 1 - c0;
+            continue;
+        }
+        if (!ev) {
+            plain_iteration(rf);
+            continue;
+        }
+        int npass = 0;
+        if (rf) {
+            mark(0, [&] { passes_device(ws, warm, c.inject, c.seed, fp64, 0); });
+            npass += static_cast<int>(warm.size());
+        }
+        mark(1, [&] {
+            sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt, ws.fd, scale_n, ws.gred(),
+                                  ws.loss_part.p, ws.st.p, s);
+        });
+        mark(3, [&] { stats_device(ws); });
+        mark(2, [&] {
+            sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.gred(), ws.m.p, ws.v.p, hp, r->bc_table.p,
+                              make_double2(0, 0), true, scale_n, nullptr, nullptr, s);
+        });
+        mark(3, [&] {
+            if (ev_p) prune_device(ws, c.prune_pct * sched);
+            if (ev_d) densify_device(ws, c.densify_pct * sched, c);
             ws.compute_active();
             build_tables(ws, fp64, true, true, false);
             ws.cur = 0;
             sadk::launch_jfa_seed(ws.sites(), ws.st.p, ws.ids[0].p, ws.fd, scale_n, s);
-            passes_device(ws, full4, c.inject, c.seed, fp64, static_cast<uint32_t>(npass));
-            npass += static_cast<int>(full4.size());
-        }
-        sadk::launch_advance(ws.st.p, npass, 1, r->loss_hist.p, r->active_hist.p, ws.loss_part.p, nbw, ws.otops.p, s);
+        });
+        mark(0, [&] { passes_device(ws, full4, c.inject, c.seed, fp64, static_cast<uint32_t>(npass)); });
+        npass += static_cast<int>(full4.size());
+        mark(2, [&] {
+            sadk::launch_advance(ws.st.p, npass, 1, r->loss_hist.p, r->active_hist.p, ws.loss_part.p, nbw, ws.otops.p,
+                                 s);
+        });
     }
     // final full refresh (train.cpp:287)
     const auto fin = full_refresh_passes(ws.fd.gw, ws.fd.gh, c.final_passes);
@@ -1396,6 +1480,15 @@ static void fit_loop(sad_fit_run* r) {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     r->total_ms = ms;
+    for (double& p : r->phase_ms) p = 0;
+    for (auto& m : r->marks) {
+        float pm = 0;
+        cudaEventElapsedTime(&pm, m.second.first, m.second.second);
+        if (m.first < 8) r->phase_ms[m.first] += pm;
+    }
+    if (r->profile)
+        std::fprintf(stderr, "phases ms: propagate %.1f fwd_bwd %.1f adam %.1f events %.1f advance %.1f\n",
+                     r->phase_ms[0], r->phase_ms[1], r->phase_ms[2], r->phase_ms[3], r->phase_ms[5]);
 
     DevState fs = ws.get_state();
     r->n_sites = static_cast<size_t>(fs.n_sites);
@@ -1543,6 +1636,10 @@ void* sad_host_alloc(size_t bytes) {
 
 void sad_host_free(void* p) {
     if (p) cudaFreeHost(p);
+}
+
+sad_status sad_fit_set_profiling(sad_fit_run* r, int on) {
+    return guard([&] { r->profile = on != 0; });
 }
 
 sad_status sad_fit_timing(sad_fit_run* r, double* total, double* ph) {
