@@ -316,13 +316,33 @@ class Backend:
     def fit_store(self, sites: SiteStore, target: ImageBuffer, cfg: TrainConfig) -> FitResult:
         return self._fit(target, cfg, sites)
 
+    def _fit_run(self, w, h, c):
+        """Resident fit runs are cached per (shape, config): repeated fits reuse the device workspace
+        (sites, field, record pools, graphs) instead of reallocating ~hundreds of MB per call."""
+        if not hasattr(self, "_runs"):
+            self._runs = {}
+        key = (w, h, bytes(c))
+        run = self._runs.get(key)
+        if run is None:
+            while len(self._runs) >= 2:
+                _, old = self._runs.popitem()
+                self.lib.sad_fit_destroy(old)
+            run = _P()
+            self._call("fit_create", C.c_int(w), C.c_int(h), C.byref(c), C.byref(run))
+            self._runs[key] = run
+        return run
+
+    def close(self):
+        for run in getattr(self, "_runs", {}).values():
+            self.lib.sad_fit_destroy(run)
+        self._runs = {}
+
     def _fit(self, target: ImageBuffer, cfg: TrainConfig, init: Optional[SiteStore]) -> FitResult:
         c = cfg.to_c()
         w, h = target.width, target.height
         if self.kind == "gpu":
-            run = _P()
-            self._call("fit_create", C.c_int(w), C.c_int(h), C.byref(c), C.byref(run))
-            try:
+            run = self._fit_run(w, h, c)
+            if True:
                 self._call("fit_set_target", run, _ptr(target.data))
                 if init is None:
                     self._call("fit_run_init", run)
@@ -336,13 +356,11 @@ class Backend:
                 res = self._fit_collect(w, h, cfg, int(n.value), int(nh.value), float(sc.value),
                                         lambda sv, fv, hist: self._call("fit_download", run, sv, fv, hist))
                 tot = C.c_double()
-                ph = (C.c_double * 4)()
+                ph = (C.c_double * 8)()
                 self._call("fit_timing", run, C.byref(tot), ph)
                 res.timing = {"total_ms": tot.value, "propagate_ms": ph[0], "fwd_bwd_ms": ph[1],
                               "adam_ms": ph[2], "events_ms": ph[3]}
                 return res
-            finally:
-                self.lib.sad_fit_destroy(run)
         if self.kind == "ref":
             hd = _P()
             if init is None:

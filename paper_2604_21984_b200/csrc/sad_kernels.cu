@@ -797,7 +797,11 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, const
         sm.cnt[u] = 0;  // aliases hkey: safe after the barrier
         const uint32_t site = sm.site_of_local[u];
         uint32_t slot = static_cast<uint32_t>(atomicAdd(red.cnt + site, 1));
-        if (slot >= static_cast<uint32_t>(red.maxt)) {  // overflow record from the pool, linked per site
+        const uint32_t scap = red.roff ? static_cast<uint32_t>(red.rcap[site]) : static_cast<uint32_t>(red.maxt);
+        if (red.roff && slot < scap && red.roff[site] + slot >= red.psize) slot = scap;  // pool bound
+        if (slot < scap) {
+            if (red.roff) slot = 0x80000000u | slot;  // adaptive-layout record
+        } else {  // overflow record from the pool, linked per site
             int r = atomicAdd(red.otop, 1);
             if (r < red.ocap) red.onext[r] = atomicExch(red.head + site, r);
             slot = r < red.ocap ? static_cast<uint32_t>(red.maxt + r) : 0xffffffffu;
@@ -924,7 +928,10 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, const
         for (int c = c0; c < c1 && c < NCK; c++) dd_merge(t, sm.carry[c * NCH + ch]);
         const uint32_t site = sm.site_of_local[u];
         const uint32_t slot = sm.slot_of_local[u];
-        if (slot < static_cast<uint32_t>(red.maxt)) {
+        if (slot & 0x80000000u && slot != 0xffffffffu) {
+            red.part[(static_cast<size_t>(red.roff[site]) + (slot & 0x7fffffffu)) * red.stride + ch] =
+                make_double2(t.hi, t.lo);
+        } else if (slot < static_cast<uint32_t>(red.maxt) && !red.roff) {
             red.part[(static_cast<size_t>(site) * red.maxt + slot) * red.stride + ch] = make_double2(t.hi, t.lo);
         } else if (slot != 0xffffffffu) {
             red.opart[static_cast<size_t>(slot - red.maxt) * red.stride + ch] = make_double2(t.hi, t.lo);
@@ -1336,6 +1343,10 @@ __device__ __forceinline__ DD red_total(const RedTarget& red, int id, int ch, in
     double2 o = red.over[static_cast<size_t>(ch) * red.cap + id];
     DD acc{o.x, o.y};
     const double2* rec = red.part + static_cast<size_t>(id) * red.maxt * red.stride + ch;
+    if (red.roff) {
+        rec = red.part + static_cast<size_t>(red.roff[id]) * red.stride + ch;
+        if (n > red.rcap[id]) n = red.rcap[id];
+    }
     for (int s = 0; s < n; s++) {
         double2 r = rec[static_cast<size_t>(s) * red.stride];
         dd_merge(acc, DD{r.x, r.y});
@@ -1538,14 +1549,17 @@ __device__ __forceinline__ void clamp_site(double* p, int cap, int id, const Ada
     }
 }
 
-// One 16-lane group per site: lane k < 10 merges the gradient records of slot k, applies the Adam
-// update of that parameter and its clamp; dir is renormalised from both lanes' values exchanged by
-// shuffle; lane 0 then rebuilds the site's candidate snapshot and backward table.
+// One 16-lane group per site.  The site's gradient records (one per tile that touched it) are
+// merged in parallel — lane j takes records j, j+16, ... for all ten channels, then a 16-lane
+// butterfly of double-double merges (order independent) leaves every lane with the totals.  Lane
+// k < 10 then applies the Adam update of parameter k and its clamp; dir is renormalised from both
+// lanes' values exchanged by shuffle; lanes 0-4 rebuild the site's candidate snapshot and backward
+// table.  With the adaptive record layout, lane 0 also plans the next pass's record capacity.
 template <typename T>
 __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarget grads, double* __restrict__ m,
                                               double* __restrict__ v, AdamHyper hp,
                                               const double2* __restrict__ bc_table, double2 bc_now, int zero_grads,
-                                              double scale, Q4<T>* pack, Q4<T>* gtab) {
+                                              double scale, Q4<T>* pack, Q4<T>* gtab, int32_t* rcap_next) {
     const int lane16 = threadIdx.x & 15;
     const int id = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
     const unsigned gmask = 0xffffu << (threadIdx.x & 16);
@@ -1553,15 +1567,73 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
     const bool live = id < st->n_sites;
     const int k = lane16;
     unsigned long long skipped = 0;
+    // ---- gradient totals (all lanes of the group take part in the shuffles)
+    DD acc[10];
+#pragma unroll
+    for (int ch = 0; ch < 10; ch++) acc[ch] = DD{0.0, 0.0};
+    int claimed = 0;
+    if (live) {
+        claimed = grads.cnt[id];
+        int n, base;
+        if (grads.roff) {
+            n = claimed < grads.rcap[id] ? claimed : grads.rcap[id];
+            base = grads.roff[id];
+        } else {
+            n = claimed < grads.maxt ? claimed : grads.maxt;
+            base = id * grads.maxt;
+        }
+        if (grads.roff && static_cast<long long>(base) + n > grads.psize)
+            n = static_cast<int>(grads.psize - base > 0 ? grads.psize - base : 0);
+        for (int j = lane16; j < n; j += 32) {  // two records in flight per lane
+            const bool two = j + 16 < n;
+            const double2* r0 = grads.part + (static_cast<size_t>(base) + j) * grads.stride;
+            const double2* r1 = grads.part + (static_cast<size_t>(base) + (two ? j + 16 : j)) * grads.stride;
+            double2 a[10], b[10];
+#pragma unroll
+            for (int ch = 0; ch < 10; ch++) {
+                a[ch] = r0[ch];
+                b[ch] = r1[ch];
+            }
+#pragma unroll
+            for (int ch = 0; ch < 10; ch++) {
+                dd_merge(acc[ch], DD{a[ch].x, a[ch].y});
+                if (two) dd_merge(acc[ch], DD{b[ch].x, b[ch].y});
+            }
+        }
+        if (lane16 == 0)
+            for (int r = grads.head[id]; r >= 0; r = grads.onext[r]) {
+#pragma unroll
+                for (int ch = 0; ch < 10; ch++) {
+                    double2 o = grads.opart[static_cast<size_t>(r) * grads.stride + ch];
+                    dd_merge(acc[ch], DD{o.x, o.y});
+                }
+            }
+        if (lane16 < 10) {
+            double2 o = grads.over[static_cast<size_t>(lane16) * cap + id];  // CAS-fallback totals
+            DD mine{o.x, o.y};
+#pragma unroll
+            for (int ch = 0; ch < 10; ch++)
+                if (ch == lane16) dd_merge(acc[ch], mine);
+        }
+    }
+#pragma unroll
+    for (int d = 8; d >= 1; d >>= 1) {
+#pragma unroll
+        for (int ch = 0; ch < 10; ch++) {
+            DD o{__shfl_xor_sync(gmask, acc[ch].hi, d, 16), __shfl_xor_sync(gmask, acc[ch].lo, d, 16)};
+            dd_merge(acc[ch], o);
+        }
+    }
+    DD g = acc[0];
+#pragma unroll
+    for (int ch = 1; ch < 10; ch++)
+        if (k == ch) g = acc[ch];
     if (live) {
         const bool upd = s.active[id] && !s.frozen[id];
         double p = 0.0;
         if (k < 10) p = s.p[static_cast<size_t>(k) * cap + id];
         if (upd && k < 10) {
             const double2 bc = bc_table ? bc_table[st->t + 1] : bc_now;
-            int nrec = grads.cnt[id];
-            if (nrec > grads.maxt) nrec = grads.maxt;
-            DD g = red_total(grads, id, k, nrec);
             double gv = g.hi + g.lo;
             if (!isfinite(gv)) {
                 skipped++;
@@ -1601,65 +1673,77 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
             if (k == 0) grads.cnt[id] = 0;
             if (k == 1) grads.head[id] = -1;
         }
+        if (rcap_next && k == 0) {
+            // next pass's record capacity: last count plus headroom (active sites only)
+            int want = s.active[id] ? claimed + (claimed >> 2) + 2 : 0;
+            rcap_next[id] = want < 4096 ? want : 4096;
+        }
     } else {
         __shfl_sync(gmask, 0.0, (threadIdx.x & 16) + 7);
         __shfl_sync(gmask, 0.0, (threadIdx.x & 16) + 8);
+        if (rcap_next && k == 0 && id < cap) rcap_next[id] = 0;
     }
     if (skipped) atomicAdd(reinterpret_cast<unsigned long long*>(&st->skipped), skipped);
     __syncwarp();
-    if (live && lane16 == 0 && (pack || gtab)) {
-        // same derivations as k_tables (score_table.hpp:20-46, grad.cpp:84-110)
+    if (live && lane16 < 5 && (pack || gtab)) {
+        // same derivations as k_tables (score_table.hpp:20-46, grad.cpp:84-110), one output quad per lane
         const double* pp = s.p;
-        bool act = s.active[id] != 0;
-        double x = pp[0 * cap + id], y = pp[1 * cap + id], lt = pp[2 * cap + id], r = pp[3 * cap + id];
-        double ux = pp[7 * cap + id], uy = pp[8 * cap + id], an = pp[9 * cap + id];
-        if (pack) {
-            Q4<T> a, b;
-            if (!act) {
-                a = {T(0), T(0), T(0), T(0)};
-                b = {T(1), T(0), T(1), T(0)};
-            } else {
-                double hx = half_rt(x), hy = half_rt(y), hlt = half_rt(lt), hr = half_rt(r);
+        const bool act = s.active[id] != 0;
+        const double x = pp[0 * cap + id], y = pp[1 * cap + id], lt = pp[2 * cap + id], r = pp[3 * cap + id];
+        const double ux = pp[7 * cap + id], uy = pp[8 * cap + id], an = pp[9 * cap + id];
+        if (lane16 == 0 && pack) {
+            Q4<T> a{T(0), T(0), T(0), T(0)};
+            if (act) a = {static_cast<T>(half_rt(x)), static_cast<T>(half_rt(y)), static_cast<T>(exp(half_rt(lt))),
+                          static_cast<T>(half_rt(r))};
+            pack[2 * id] = a;
+        } else if (lane16 == 1 && pack) {
+            Q4<T> b{T(1), T(0), T(1), T(0)};
+            if (act) {
                 double hux = half_rt(ux), huy = half_rt(uy), han = half_rt(an);
                 double ea = exp(han), ia = exp(-han);
                 double vx = -huy, vy = hux;
-                a = {static_cast<T>(hx), static_cast<T>(hy), static_cast<T>(exp(hlt)), static_cast<T>(hr)};
                 b = {static_cast<T>(ea * hux * hux + ia * vx * vx), static_cast<T>(ea * hux * huy + ia * vx * vy),
                      static_cast<T>(ea * huy * huy + ia * vy * vy), T(1)};
             }
-            pack[2 * id] = a;
             pack[2 * id + 1] = b;
-        }
-        if (gtab) {
-            Q4<T> a, b, c;
-            if (!act) {
-                a = {T(0), T(0), T(0), T(0)};
-                b = {T(1), T(1), T(1), T(0)};
-                c = {T(0), T(0), T(0), T(0)};
-            } else {
-                a = {static_cast<T>(x), static_cast<T>(y), static_cast<T>(exp(lt)), static_cast<T>(r)};
-                b = {static_cast<T>(exp(an)), static_cast<T>(exp(-an)), static_cast<T>(ux), static_cast<T>(uy)};
-                c = {static_cast<T>(pp[4 * cap + id]), static_cast<T>(pp[5 * cap + id]),
-                     static_cast<T>(pp[6 * cap + id]), T(1)};
-            }
+        } else if (lane16 == 2 && gtab) {
+            Q4<T> a{T(0), T(0), T(0), T(0)};
+            if (act) a = {static_cast<T>(x), static_cast<T>(y), static_cast<T>(exp(lt)), static_cast<T>(r)};
             gtab[3 * id] = a;
+        } else if (lane16 == 3 && gtab) {
+            Q4<T> b{T(1), T(1), T(1), T(0)};
+            if (act) b = {static_cast<T>(exp(an)), static_cast<T>(exp(-an)), static_cast<T>(ux), static_cast<T>(uy)};
             gtab[3 * id + 1] = b;
+        } else if (lane16 == 4 && gtab) {
+            Q4<T> c{T(0), T(0), T(0), T(0)};
+            if (act) c = {static_cast<T>(pp[4 * cap + id]), static_cast<T>(pp[5 * cap + id]),
+                          static_cast<T>(pp[6 * cap + id]), T(1)};
             gtab[3 * id + 2] = c;
         }
     }
 }
 
-void launch_adam(bool fp64, const SitesDev& s, DevState* st, const RedTarget& grads, double* m, double* v, const AdamHyper& hp,
-                 const double2* bc_table, double2 bc_now, bool zero_grads, double scale, void* pack, void* gtab,
-                 cudaStream_t stream) {
+void launch_adam(bool fp64, const SitesDev& s, DevState* st, const RedTarget& grads, double* m, double* v,
+                 const AdamHyper& hp, const double2* bc_table, double2 bc_now, bool zero_grads, double scale,
+                 void* pack, void* gtab, int32_t* rcap_next, cudaStream_t stream) {
     int grid = (s.cap + 7) / 8;  // 8 sites (16 lanes each) per 128-thread block
     if (grid < 1) grid = 1;
     if (fp64)
         k_adam<double><<<grid, 128, 0, stream>>>(s, st, grads, m, v, hp, bc_table, bc_now, zero_grads ? 1 : 0, scale,
-                                                 (Q4<double>*)pack, (Q4<double>*)gtab);
+                                                 (Q4<double>*)pack, (Q4<double>*)gtab, rcap_next);
     else
         k_adam<float><<<grid, 128, 0, stream>>>(s, st, grads, m, v, hp, bc_table, bc_now, zero_grads ? 1 : 0, scale,
-                                                (Q4<float>*)pack, (Q4<float>*)gtab);
+                                                (Q4<float>*)pack, (Q4<float>*)gtab, rcap_next);
+    SAD_LAUNCHED();
+}
+
+__global__ void k_fill_i32(int32_t* p, int n, int32_t v) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+void launch_fill_i32(int32_t* p, int n, int32_t v, cudaStream_t stream) {
+    k_fill_i32<<<(n + 255) / 256, 256, 0, stream>>>(p, n, v);
     SAD_LAUNCHED();
 }
 

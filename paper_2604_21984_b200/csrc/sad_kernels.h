@@ -58,6 +58,11 @@ struct RedTarget {
     double2* opart; // [ocap][stride]
     int32_t* otop;  // pool allocation counter (reset per pass)
     int ocap;
+    // adaptive layout (when roff != nullptr): site records live at part[roff[site] + slot] for
+    // slot < rcap[site] (capacity planned from the previous pass's count), pool of `psize` records
+    const int32_t* roff;
+    int32_t* rcap;
+    long long psize;
 };
 
 struct FieldDims {
@@ -120,9 +125,13 @@ void launch_finalize(const RedTarget& red, int n_ch, const DevState* st, cudaStr
 // ---------------------------------------------------------------- optimiser
 // Adam (+ clamp_project) over all slots < n_sites; optionally zeroes grads and rebuilds pack/gtab.
 // bc: (1 - beta1^t, 1 - beta2^t) table indexed by the new t, or nullptr to use bc_now.
+// With grads.roff set, Adam also writes next pass's record capacities to rcap_next (then
+// launch_plan_records turns them into offsets).
 void launch_adam(bool fp64, const SitesDev& s, DevState* st, const RedTarget& grads, double* m, double* v,
                  const AdamHyper& hp, const double2* bc_table, double2 bc_now, bool zero_grads, double scale,
-                 void* pack, void* gtab, cudaStream_t stream);
+                 void* pack, void* gtab, int32_t* rcap_next, cudaStream_t stream);
+// Initial record plan: rcap = per_site for every slot (offsets follow from a scan).
+void launch_fill_i32(int32_t* p, int n, int32_t v, cudaStream_t stream);
 void launch_clamp(const SitesDev& s, const DevState* st, const AdamHyper& hp, cudaStream_t stream);
 
 // ---------------------------------------------------------------- budget events

@@ -6,6 +6,7 @@
 #include "sad_kernels.h"
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
@@ -320,10 +321,38 @@ struct Workspace {
     DBuf<double2> gopart, sopart;
     int ocap = 0;
     sadk::RedTarget gred() {
-        return sadk::RedTarget{grads.p, gpart.p, gcnt.p, cap, maxt, 11, ghead.p, gnext.p, gopart.p, otops.p, ocap};
+        return sadk::RedTarget{grads.p, gpart.p, gcnt.p, cap, maxt, 11, ghead.p, gnext.p, gopart.p, otops.p, ocap,
+                               nullptr, nullptr, 0};
     }
     sadk::RedTarget sred() {
-        return sadk::RedTarget{stats.p, spart.p, scnt.p, cap, maxt, 8, shead.p, snext.p, sopart.p, otops.p + 1, ocap};
+        return sadk::RedTarget{stats.p, spart.p, scnt.p, cap, maxt, 8, shead.p, snext.p, sopart.p, otops.p + 1, ocap,
+                               nullptr, nullptr, 0};
+    }
+    // Adaptive gradient-record layout of the resident fit (see RedTarget): per-site capacity planned
+    // from the previous pass, offsets by an exclusive scan, one pool.
+    DBuf<double2> apool;
+    DBuf<int32_t> roff, rcap;
+    long long apsize = 0;
+    sadk::RedTarget gred_adaptive() {
+        sadk::RedTarget t = gred();
+        t.roff = roff.p;
+        t.rcap = rcap.p;
+        t.part = apool.p;
+        t.psize = apsize;
+        return t;
+    }
+    void ensure_adaptive(size_t tiles) {
+        long long want = 16ll * cap + 64ll * static_cast<long long>(tiles);
+        if (apsize < want || !apool.p) {
+            apool.ensure(static_cast<size_t>(want) * 11);
+            apsize = want;
+        }
+        roff.ensure(cap);
+        rcap.ensure(cap);
+    }
+    void plan_records() {  // roff = exclusive_scan(rcap)
+        size_t bytes = cub_tmp.n;
+        ck(cub::DeviceScan::ExclusiveSum(cub_tmp.p, bytes, rcap.p, roff.p, cap, stream), "DeviceScan");
     }
     // overflow pool sized from the number of reduction tiles (each tile adds at most its bucket count)
     void ensure_pool(size_t tiles) {
@@ -425,7 +454,10 @@ struct Workspace {
                                         0, 64, stream);
         thrust::counting_iterator<uint32_t> it(0);
         cub::DeviceSelect::Flagged(nullptr, b, it, flags.p, act.p, &st.p->n_active, static_cast<int>(items), stream);
-        cub_tmp.ensure(std::max(a, b) + 256);
+        size_t c = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, c, static_cast<int32_t*>(nullptr), static_cast<int32_t*>(nullptr),
+                                      static_cast<int>(items), stream);
+        cub_tmp.ensure(std::max({a, b, c}) + 256);
     }
 
     void ensure_field(int w_, int h_, int k, int cell) {
@@ -1074,7 +1106,7 @@ sad_status sad_adam_step(sad_ctx* c, sad_sites_view* s, const double* grads, sad
         double2 bc = make_double2(1.0 - std::pow(cfg->beta1, static_cast<double>(t)),
                                   1.0 - std::pow(cfg->beta2, static_cast<double>(t)));
         sadk::launch_adam(false, ws.sites(), ws.st.p, ws.gred(), ws.m.p, ws.v.p, adam_hyper(*cfg, w, h), nullptr, bc,
-                          false, 1.0, nullptr, nullptr, ws.stream);
+                          false, 1.0, nullptr, nullptr, nullptr, ws.stream);
         ck(cudaMemcpyAsync(m.data(), ws.m.p, m.size() * 8, cudaMemcpyDeviceToHost, ws.stream), "D2H");
         ck(cudaMemcpyAsync(v.data(), ws.v.p, v.size() * 8, cudaMemcpyDeviceToHost, ws.stream), "D2H");
         DevState st = ws.get_state();
@@ -1348,6 +1380,11 @@ static void fit_loop(sad_fit_run* r) {
     init.n_sites = st0.n_sites;
     init.n_active = sta.n_active;
     ws.set_state(init);
+    ws.ensure_adaptive(static_cast<size_t>(sadk::backward_blocks(fp64, ws.fd)));
+    sadk::launch_fill_i32(ws.rcap.p, ws.cap, 16, s);
+    ws.plan_records();
+    ck(cudaMemsetAsync(ws.gcnt.p, 0, sizeof(int32_t) * ws.cap, s), "memset gcnt");
+    ck(cudaMemsetAsync(ws.ghead.p, 0xff, sizeof(int32_t) * ws.cap, s), "memset ghead");
 
     const sadk::AdamHyper hp = adam_hyper(c, w, h);
     const auto full4 = full_refresh_passes(ws.fd.gw, ws.fd.gh, 4);
@@ -1398,12 +1435,13 @@ static void fit_loop(sad_fit_run* r) {
             np = static_cast<int>(warm.size());
         }
         mark(1, [&] {
-            sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt, ws.fd, scale_n, ws.gred(),
+            sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt, ws.fd, scale_n, ws.gred_adaptive(),
                                   ws.loss_part.p, ws.st.p, s);
         });
         mark(2, [&] {
-            sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.gred(), ws.m.p, ws.v.p, hp, r->bc_table.p,
-                              make_double2(0, 0), true, scale_n, ws.pack.p, ws.gtab.p, s);
+            sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.gred_adaptive(), ws.m.p, ws.v.p, hp, r->bc_table.p,
+                              make_double2(0, 0), true, scale_n, ws.pack.p, ws.gtab.p, ws.rcap.p, s);
+            ws.plan_records();
         });
         mark(5, [&] {
             sadk::launch_advance(ws.st.p, np, 1, r->loss_hist.p, r->active_hist.p, ws.loss_part.p, nbw, ws.otops.p, s);
@@ -1444,13 +1482,14 @@ static void fit_loop(sad_fit_run* r) {
             npass += static_cast<int>(warm.size());
         }
         mark(1, [&] {
-            sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt, ws.fd, scale_n, ws.gred(),
+            sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt, ws.fd, scale_n, ws.gred_adaptive(),
                                   ws.loss_part.p, ws.st.p, s);
         });
         mark(3, [&] { stats_device(ws); });
         mark(2, [&] {
-            sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.gred(), ws.m.p, ws.v.p, hp, r->bc_table.p,
-                              make_double2(0, 0), true, scale_n, nullptr, nullptr, s);
+            sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.gred_adaptive(), ws.m.p, ws.v.p, hp, r->bc_table.p,
+                              make_double2(0, 0), true, scale_n, nullptr, nullptr, ws.rcap.p, s);
+            ws.plan_records();
         });
         mark(3, [&] {
             if (ev_p) prune_device(ws, c.prune_pct * sched);
@@ -1589,7 +1628,7 @@ sad_status sad_fit_bench(sad_fit_run* r, int which, int reps, double* ms_per_lau
                 ck(cudaMemsetAsync(ws.gcnt.p, 0, sizeof(int32_t) * ws.cap, s), "memset");
                 ck(cudaMemsetAsync(ws.ghead.p, 0xff, sizeof(int32_t) * ws.cap, s), "memset");
                 ck(cudaMemsetAsync(ws.otops.p, 0, sizeof(int32_t), s), "memset");
-                sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt, ws.fd, sn, ws.gred(),
+                sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt, ws.fd, sn, ws.gred_adaptive(),
                                       ws.loss_part.p, ws.st.p, s);
                 break;
             case 6:
@@ -1600,8 +1639,12 @@ sad_status sad_fit_bench(sad_fit_run* r, int which, int reps, double* ms_per_lau
             case 2: sadk::launch_render(false, ws.ids[ws.cur].p, ws.rtab.p, ws.fd, sn, ws.px_f.p, ws.st.p, s); break;
             case 3: passes_device(ws, {sad_pass_spec{16, 1}}, c.inject, c.seed, fp64, 0); break;
             case 4:
-                sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.gred(), ws.m.p, ws.v.p, hp, nullptr,
-                                  make_double2(1.0, 1.0), true, sn, ws.pack.p, ws.gtab.p, s);
+                // one fwd+bwd then Adam, as in the fit (records present); the fwd+bwd share is timed apart
+                sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt, ws.fd, sn, ws.gred_adaptive(),
+                                      ws.loss_part.p, ws.st.p, s);
+                sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.gred_adaptive(), ws.m.p, ws.v.p, hp, nullptr,
+                                  make_double2(1.0, 1.0), true, sn, ws.pack.p, ws.gtab.p, ws.rcap.p, s);
+                ws.plan_records();
                 break;
             case 5: stats_device(ws); break;
             default: fail(SAD_EINVAL, "bench: unknown kernel");
@@ -1625,6 +1668,11 @@ sad_status sad_fit_bench(sad_fit_run* r, int which, int reps, double* ms_per_lau
             sad_status rc = sad_fit_bench(r, 6, reps, &base);
             if (rc == SAD_OK) *ms_per_launch = std::max(0.0, *ms_per_launch - base);
         }
+        if (which == 4) {  // Adam (+ record plan) = (fwd+bwd, Adam, plan) - fwd+bwd
+            double base = 0;
+            sad_status rc = sad_fit_bench(r, 1, reps, &base);
+            if (rc == SAD_OK) *ms_per_launch = std::max(0.0, *ms_per_launch - base);
+        }
     });
 }
 
@@ -1645,7 +1693,7 @@ sad_status sad_fit_set_profiling(sad_fit_run* r, int on) {
 sad_status sad_fit_timing(sad_fit_run* r, double* total, double* ph) {
     return guard([&] {
         *total = r->total_ms;
-        for (int i = 0; i < 4; i++) ph[i] = r->phase_ms[i];
+        for (int i = 0; i < 4; i++) ph[i] = r->phase_ms[i];  // ph holds 4 phases (header contract)
     });
 }
 
