@@ -47,6 +47,10 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--ref-iters", type=int, default=30, help="iterations per reference-arm sample")
     p.add_argument("--cpu-iters", type=int, default=60, help="iterations of the cpu_baseline sample")
+    p.add_argument("--mode", default="config2", choices=["config2", "config3"],
+                   help="config3: 2048x2048 / 100k-site fit + 1e6 random point queries (own JSON line)")
+    p.add_argument("--c3-iters", type=int, default=300)
+    p.add_argument("--no-roofline-2048", action="store_true")
     return p.parse_args()
 
 
@@ -170,6 +174,122 @@ def run_reference(a):
 
 
 # ---------------------------------------------------------------------------- B200 arm
+KBENCH = {"propagate_warm": 0, "fwd_bwd": 1, "render": 2, "propagate_flood": 3}
+
+
+def kernel_table(G, run, npx, n_act, N, reps=50):
+    """CUDA-event timings of the hot kernels on a fitted, device-resident state, with their
+    algorithmic bytes per launch (propagate 64 B/cell + 32 B/site; fwd+bwd 44 B/px +
+    124 B/site; render 44 B/px + 40 B/site)."""
+    bytes_per = {"propagate_warm": 64 * npx + 32 * n_act, "fwd_bwd": 44 * npx + 124 * N,
+                 "render": 44 * npx + 40 * N, "propagate_flood": 64 * npx + 32 * n_act}
+    out = {}
+    for nm, which in KBENCH.items():
+        t = C.c_double()
+        G._call("fit_bench", run, C.c_int(which), C.c_int(reps), C.byref(t))
+        out[nm] = {"ms": t.value, "bytes": bytes_per[nm], "GBps": bytes_per[nm] / (t.value * 1e-3) / 1e9}
+    return out
+
+
+def hbm_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        return float(json.load(open(path)).get("hbm_gbs", 6650.0)), "MEASURED_PEAKS.json hbm_gbs (burst copy)"
+    return 6650.0, "fallback 6650 GB/s (B200_PROFILING.md)"
+
+
+def roofline_2048(G, iters=200, n_sites=100000):
+    """Config-3 sized state (2048x2048, 100k sites): the HBM-relevant operating point."""
+    import paper_2604_21984_b200 as sad
+    from paper_2604_21984_b200.synth import synthetic_image
+    W = H = 2048
+    cfg = sad.TrainConfig(iters=iters, n_sites=n_sites, fp64=False)
+    run = C.c_void_p()
+    cc = cfg.to_c()
+    G._call("fit_create", C.c_int(W), C.c_int(H), C.byref(cc), C.byref(run))
+    try:
+        img = synthetic_image(W, H, 3)
+        G._call("fit_set_target", run, img.ctypes.data_as(C.POINTER(C.c_double)))
+        G._call("fit_run_init", run)
+        tot, ph = C.c_double(), (C.c_double * 8)()
+        G._call("fit_timing", run, C.byref(tot), ph)
+        kt = kernel_table(G, run, W * H, n_sites, n_sites)
+    finally:
+        G.lib.sad_fit_destroy(run)
+    peak, src = hbm_peak()
+    for v in kt.values():
+        v["frac_hbm"] = v["GBps"] / peak
+    return {"workload": f"2048x2048, {n_sites} sites, {iters}-iteration fit state", "fit_ms_per_iter": tot.value / iters,
+            "kernels": kt, "peak_gbs": peak, "peak_source": src}
+
+
+def run_config3(a):
+    """Config 3: 2048x2048 synthetic image, 100k sites, fit, then 1e6 random point queries."""
+    import torch
+    import paper_2604_21984_b200 as sad
+    from paper_2604_21984_b200 import api
+    from paper_2604_21984_b200.synth import Rng, synthetic_image
+    stream = torch.cuda.Stream()  # explicit stream shared by the library and the timing events
+    torch.cuda.set_stream(stream)
+    lib = api.load_library()
+    ctx = C.c_void_p()
+    if lib.sad_ctx_create(C.c_int(0), C.c_void_p(stream.cuda_stream), C.byref(ctx)):
+        raise RuntimeError(lib.sad_last_error().decode())
+    G = api.Backend(lib, "sad_", "gpu", ctx=ctx)
+    W = H = 2048
+    cfg = sad.TrainConfig(iters=a.c3_iters, n_sites=100000, fp64=False)
+    run = C.c_void_p()
+    cc = cfg.to_c()
+    G._call("fit_create", C.c_int(W), C.c_int(H), C.byref(cc), C.byref(run))
+    img = synthetic_image(W, H, 3)
+    G._call("fit_set_target", run, img.ctypes.data_as(C.POINTER(C.c_double)))
+    G._call("fit_run_init", run)  # warm-up
+    ms = []
+    for _ in range(max(a.steps, 1)):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        G._call("fit_run_init", run)
+        e1.record(stream)
+        e1.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    # 1e6 random point queries, coordinates from seeded_stream(5, 7, 9)
+    nq = 1_000_000
+    rng = Rng(5, 7, 9)
+    xy = np.empty((nq, 2), np.int32)
+    s = np.uint64(rng.s)
+    st = np.zeros(nq * 2, np.uint32)
+    x = int(rng.s)
+    for i in range(nq * 2):  # sequential xorshift32 stream
+        x ^= (x << 13) & 0xFFFFFFFF
+        x ^= x >> 17
+        x ^= (x << 5) & 0xFFFFFFFF
+        st[i] = x
+    xy[:, 0] = st[0::2] % W
+    xy[:, 1] = st[1::2] % H
+    dxy = torch.from_numpy(xy).cuda()
+    dids = torch.empty(nq * 16, dtype=torch.int32, device="cuda")
+    dw = torch.empty(nq * 16, dtype=torch.float64, device="cuda")
+    dn = torch.empty(nq, dtype=torch.int32, device="cuda")
+    args = (run, C.c_void_p(dxy.data_ptr()), C.c_size_t(nq), C.c_void_p(dids.data_ptr()),
+            C.c_void_p(dw.data_ptr()), C.c_void_p(dn.data_ptr()))
+    G._call("fit_point_query", *args)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(5):
+        G._call("fit_point_query", *args)
+    e1.record(stream)
+    e1.synchronize()
+    q_ms = e0.elapsed_time(e1) / 5
+    rf = roofline_2048(G, iters=a.c3_iters)
+    G.lib.sad_fit_destroy(run)
+    out = {"metric": METRIC, "mode": "config3", "value": nq / (q_ms * 1e-3), "unit": "point queries/s",
+           "fit_ms": float(np.mean(ms)), "fit_iters_per_s": a.c3_iters / (np.mean(ms) * 1e-3),
+           "config": {"workload": f"config3: 2048x2048 synthetic, n_sites=100000, {a.c3_iters}-iteration fit, "
+                                  f"then 1e6 random point queries (seeded_stream(5,7,9)) on the fitted field"},
+           "reference_pixel_weights_ms_per_query": 3.07, "roofline_2048": rf}
+    print(json.dumps(out), flush=True)
+
+
 def psnr(a, b):
     m = float(np.mean((a - b) ** 2))
     return 99.0 if m <= 0 else min(99.0, 10 * math.log10(1.0 / m))
@@ -186,7 +306,8 @@ def run_b200(a):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # explicit stream shared by the library and the timing events
+    torch.cuda.set_stream(stream)
     lib = api.load_library()
     ctx = C.c_void_p()
     rc = lib.sad_ctx_create(C.c_int(local), C.c_void_p(stream.cuda_stream), C.byref(ctx))
@@ -198,7 +319,8 @@ def run_b200(a):
 
     W, H = a.width, a.height
     npx = W * H
-    seeds = [1 + rank * a.images_per_gpu + i for i in range(a.images_per_gpu)]
+    from paper_2604_21984_b200 import shard
+    seeds = shard.image_seeds(a.images_per_gpu, world, rank)
     imgs = [synthetic_image(W, H, s) for s in seeds]
     cfgs = [train_config(a, s) for s in seeds]
     dev_t = [torch.from_numpy(im).cuda() for im in imgs]
@@ -256,14 +378,10 @@ def run_b200(a):
     last_train_psnr = res.history[-1].psnr if res.history else None
 
     # per-kernel timings on the fitted state (CUDA events on the same stream)
-    kern = {}
-    names = {0: "propagate_warm", 1: "fwd_bwd", 2: "render", 3: "propagate_flood"}
-    for which, nm in names.items():
-        out = C.c_double()
-        G._call("fit_bench", runs[0], C.c_int(which), C.c_int(100), C.byref(out))
-        kern[nm] = out.value
     n_act = res.sites.active_count()
     N = res.sites.size()
+    kt = kernel_table(G, runs[0], npx, n_act, N, reps=100)
+    kern = {k: v["ms"] for k, v in kt.items()}
     ev = sum(1 for t in range(1, a.iters + 1)
              if (20 <= t <= 3000 and t % 20 == 0) or (100 <= t <= 3000 and t % 40 == 0))
     flood_per = len(G.full_refresh_passes(W, H, 0))
@@ -317,6 +435,9 @@ def run_b200(a):
         except Exception as e:  # oracle not built on this box
             cpu = {"value": None, "unit": "iters/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 
+    rf2048 = None
+    if rank == 0 and not a.no_roofline_2048:
+        rf2048 = roofline_2048(G)
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": a.steps,
@@ -327,7 +448,7 @@ def run_b200(a):
             "e2e": {"value": e2e_val, "unit": "iters/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "encode_seconds": e2e_s / (a.steps * a.images_per_gpu)},
             "gpu_launches": launches, "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu,
-            "clocks": clk,
+            "clocks": clk, "roofline_2048": rf2048,
         }
         print(json.dumps(out), flush=True)
     for run in runs:
@@ -341,6 +462,8 @@ def main():
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+    elif a.mode == "config3":
+        run_config3(a)
     else:
         run_b200(a)
 

@@ -216,6 +216,20 @@ sad_status sad_bpp_target_count(double bpp, int width, int height, uint64_t* out
 sad_status sad_simulate_schedule(int n0, double scale, const sad_train_config* cfg, int* out);
 sad_status sad_plan_schedule(int n0, uint64_t target, const sad_train_config* cfg, double* out);
 
+/* ---------------------------------------------------------------- codec.hpp (decode path) */
+/* write_file (codec.cpp:147-177) into memory: out NULL -> only *nbytes = required size. */
+sad_status sad_encode(const sad_sites_view* sites, int width, int height, uint8_t* out, size_t cap, size_t* nbytes);
+/* read_file header checks (codec.cpp:179-205): magic, version, extent, size equation. */
+sad_status sad_decode_header(const uint8_t* buf, size_t n, int* width, int* height, uint32_t* count);
+/* read_file + unpack_site (codec.cpp:115-140, 179-222); sites.capacity >= count. */
+sad_status sad_decode(const uint8_t* buf, size_t n, sad_sites_view* sites, int* width, int* height);
+/* bpp (codec.cpp:142-145) */
+sad_status sad_bpp(size_t count, int width, int height, double* out);
+/* Decode pipeline: bytes -> sites -> refresh(Full, passes) on the device -> render_image into out_rgb
+ * (3*W*H host doubles); optionally returns the decoded sites (capacity >= count). */
+sad_status sad_decode_render(sad_ctx* ctx, const uint8_t* buf, size_t n, int k, int passes, int inject,
+                             uint64_t seed, int fp64, double* out_rgb, sad_sites_view* out_sites);
+
 /* ---------------------------------------------------------------- resident fit (train.cpp:221-311) */
 /* Allocates every device buffer for a W x H fit.  `n_init` = 0 lets fit() choose (bpp / n_sites). */
 sad_status sad_fit_create(sad_ctx* ctx, int width, int height, const sad_train_config* cfg,
@@ -242,6 +256,10 @@ sad_status sad_fit_set_profiling(sad_fit_run* run, int on);
  * run's stream.  which: 0 warm propagate pass, 1 fused fwd+bwd, 2 render, 3 Box3 flood pass
  * (step 16), 4 Adam, 5 stats.  Evidence for the roofline numbers; not part of the reference API. */
 sad_status sad_fit_bench(sad_fit_run* run, int which, int reps, double* ms_per_launch);
+/* Batched point queries (pixel_weights, render.cpp:93-105) against the fitted field; all pointers
+ * are DEVICE pointers: xy is n_q (x, y) pairs, ids/w receive 16 entries per query, n the counts. */
+sad_status sad_fit_point_query(sad_fit_run* run, const int32_t* d_xy, size_t n_q, uint32_t* d_ids, double* d_w,
+                               int32_t* d_n);
 /* Pinned host memory for zero-staging transfers (cudaMallocHost / cudaFreeHost). */
 void* sad_host_alloc(size_t bytes);
 void sad_host_free(void* p);

@@ -8,6 +8,7 @@
 // when threads > 1 (types.cpp:71-80 vs candidates.cpp:99); results are thread-count invariant
 // (test_candidates.cpp:294-303), so the replica returns exactly what sad::fit returns.
 #include "sad/budget.hpp"
+#include "sad/codec.hpp"
 #include "sad/candidates.hpp"
 #include "sad/grad.hpp"
 #include "sad/half.hpp"
@@ -20,6 +21,8 @@
 #include "../include/sad_b200.h"
 
 #include <chrono>
+#include <cstdio>
+#include <unistd.h>
 #include <cmath>
 #include <cstring>
 #include <stdexcept>
@@ -526,6 +529,50 @@ int sadref_plan_schedule(int n0, uint64_t target, const sad_train_config* c, dou
 
 double sadref_mse(const double* a, const double* b, int w, int h) {
     return mse(to_image(a, w, h), to_image(b, w, h));
+}
+
+// ---- codec (write_file / read_file go through a temporary file: the reference API is file based)
+int sadref_encode(const sad_sites_view* sv, int w, int h, uint8_t* out, size_t cap, size_t* nbytes) {
+    return guard([&] {
+        SiteStore st = to_store(sv);
+        char path[] = "/tmp/sadref_XXXXXX";
+        int fd = mkstemp(path);
+        if (fd < 0) throw std::runtime_error("mkstemp");
+        close(fd);
+        write_file(path, st, w, h);
+        FILE* f = std::fopen(path, "rb");
+        std::vector<uint8_t> b;
+        int ch;
+        while ((ch = std::fgetc(f)) != EOF) b.push_back(static_cast<uint8_t>(ch));
+        std::fclose(f);
+        std::remove(path);
+        *nbytes = b.size();
+        if (out) {
+            if (cap < b.size()) throw std::invalid_argument("encode: buffer too small");
+            std::memcpy(out, b.data(), b.size());
+        }
+    });
+}
+
+int sadref_decode(const uint8_t* buf, size_t n, sad_sites_view* sv, int* w, int* h) {
+    return guard([&] {
+        char path[] = "/tmp/sadref_XXXXXX";
+        int fd = mkstemp(path);
+        if (fd < 0) throw std::runtime_error("mkstemp");
+        FILE* f = fdopen(fd, "wb");
+        std::fwrite(buf, 1, n, f);
+        std::fclose(f);
+        try {
+            DecodedFile d = read_file(path);
+            std::remove(path);
+            *w = d.width;
+            *h = d.height;
+            if (from_store(d.sites, sv)) throw std::invalid_argument(g_err);
+        } catch (...) {
+            std::remove(path);
+            throw;
+        }
+    });
 }
 
 // ---- fit (library sad::fit when threads == 1, else the pre-warmed replica)

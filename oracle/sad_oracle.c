@@ -1004,3 +1004,109 @@ done:
     free(stats);
     return rc;
 }
+
+/* ------------------------------------------------------------------ codec.cpp (decode path) */
+static double cclamp(double v, double lo, double hi) { return v < lo ? lo : (hi < v ? hi : v); }
+static uint32_t un_enc(double v, double lo, double sc, uint32_t mx) {
+    return (uint32_t)lround(cclamp((v - lo) / sc, 0.0, 1.0) * mx);
+}
+static double un_dec(uint32_t c, double lo, double sc, uint32_t mx) { return lo + ((double)c / mx) * sc; }
+static void le32w(uint8_t* p, uint32_t v) { for (int i = 0; i < 4; i++) p[i] = (uint8_t)(v >> (8 * i)); }
+static uint32_t le32r(const uint8_t* p) { return p[0] | (p[1] << 8) | (p[2] << 16) | ((uint32_t)p[3] << 24); }
+static void f32w(uint8_t* p, double v) { float f = (float)v; uint32_t u; memcpy(&u, &f, 4); le32w(p, u); }
+static double f32r(const uint8_t* p) { uint32_t u = le32r(p); float f; memcpy(&f, &u, 4); return f; }
+
+/* compute_ranges (codec.cpp:53-88) */
+static void cover(double lo, double hi, double* mn_o, double* sc_o) {
+    float mn = (float)lo;
+    if ((double)mn > lo) mn = nextafterf(mn, -INFINITY);
+    double span = hi - (double)mn;
+    float sc = (float)(span < 1e-6 ? 1e-6 : span);
+    while ((double)mn + (double)sc < hi) sc = nextafterf(sc, INFINITY);
+    *mn_o = mn;
+    *sc_o = sc;
+}
+
+/* write_file (codec.cpp:147-177) into memory */
+int sado_encode(const sad_sites_view* s, int w, int h, uint8_t* out, size_t cap, size_t* nbytes) {
+    if (w < 1 || h < 1) return fail(SAD_EINVAL, "write: empty extent");
+    size_t cnt = 0;
+    for (size_t i = 0; i < s->size; i++) cnt += s->active[i] != 0;
+    *nbytes = 58 + 16 * cnt;
+    if (!out) return SAD_OK;
+    if (cap < *nbytes) return fail(SAD_ENOMEM, "encode: buffer too small");
+    double q[10] = {0, 1e-6, 0, 1e-6, 0, 0, 0, 1e-6, 1e-6, 1e-6}; /* lt min/scale, r min/scale, cmin[3], cscale[3] */
+    double lo[5], hi[5];
+    int any = 0;
+    for (size_t i = 0; i < s->size; i++) {
+        if (!s->active[i]) continue;
+        double v[5] = {s->log_tau[i], s->radius[i], s->col_r[i], s->col_g[i], s->col_b[i]};
+        for (int k = 0; k < 5; k++) {
+            if (!any) lo[k] = hi[k] = v[k];
+            else { if (v[k] < lo[k]) lo[k] = v[k]; if (hi[k] < v[k]) hi[k] = v[k]; }
+        }
+        any = 1;
+    }
+    if (any) {
+        cover(lo[0], hi[0], &q[0], &q[1]);
+        cover(lo[1], hi[1], &q[2], &q[3]);
+        for (int c = 0; c < 3; c++) cover(lo[2 + c], hi[2 + c], &q[4 + c], &q[7 + c]);
+    }
+    memcpy(out, "SADF", 4);
+    out[4] = 1; out[5] = 0;
+    le32w(out + 6, (uint32_t)w); le32w(out + 10, (uint32_t)h); le32w(out + 14, (uint32_t)cnt);
+    for (int k = 0; k < 10; k++) f32w(out + 18 + 4 * k, q[k]);
+    double wd = w > 1 ? w - 1.0 : 1.0, hd = h > 1 ? h - 1.0 : 1.0;
+    uint8_t* r = out + 58;
+    for (size_t i = 0; i < s->size; i++) {
+        if (!s->active[i]) continue;
+        le32w(r, un_enc(s->x[i], 0, wd, 32767) | (un_enc(s->y[i], 0, hd, 32767) << 15) | (1u << 31));
+        le32w(r + 4, un_enc(s->col_r[i], q[4], q[7], 2047) | (un_enc(s->col_g[i], q[5], q[8], 2047) << 11) |
+                         (un_enc(s->col_b[i], q[6], q[9], 1023) << 22));
+        le32w(r + 8, un_enc(s->log_tau[i], q[0], q[1], 65535) | (un_enc(s->radius[i], q[2], q[3], 65535) << 16));
+        double ang = atan2(s->dir_y[i], s->dir_x[i]);
+        le32w(r + 12, un_enc(ang, -3.14159265358979323846, 2.0 * 3.14159265358979323846, 65535) |
+                          ((uint32_t)sado_float_to_half((float)s->aniso[i]) << 16));
+        r += 16;
+    }
+    return SAD_OK;
+}
+
+/* read_file + unpack_site (codec.cpp:115-140, 179-222) */
+int sado_decode(const uint8_t* b, size_t n, sad_sites_view* s, int* w, int* h) {
+    char msg[96];
+    if (n < 18) { snprintf(msg, sizeof msg, "file truncated at byte %zu, need %zu", n, (size_t)18); return fail(SAD_EFORMAT, msg); }
+    if (memcmp(b, "SADF", 4)) return fail(SAD_EFORMAT, "bad magic, not a site file");
+    if ((b[4] | (b[5] << 8)) != 1) return fail(SAD_EFORMAT, "unknown format version");
+    uint32_t ww = le32r(b + 6), hh = le32r(b + 10), cnt = le32r(b + 14);
+    if (ww < 1 || hh < 1 || ww > (1u << 24) || hh > (1u << 24)) return fail(SAD_EFORMAT, "unreasonable image extent in header");
+    size_t need = 58 + 16 * (size_t)cnt;
+    if (n != need) { snprintf(msg, sizeof msg, "file truncated at byte %zu, need %zu", n, need); return fail(SAD_EFORMAT, msg); }
+    if (s->capacity < cnt) return fail(SAD_ENOMEM, "decode: capacity");
+    double q[10];
+    for (int k = 0; k < 10; k++) q[k] = f32r(b + 18 + 4 * k);
+    *w = (int)ww; *h = (int)hh;
+    double wd = ww > 1 ? ww - 1.0 : 1.0, hd = hh > 1 ? hh - 1.0 : 1.0;
+    for (uint32_t i = 0; i < cnt; i++) {
+        const uint8_t* r = b + 58 + 16 * (size_t)i;
+        uint32_t w0 = le32r(r), w1 = le32r(r + 4), w2 = le32r(r + 8), w3 = le32r(r + 12);
+        site_t p = {0, 0, 7.5, 1.0, 0, 0, 0, 1.0, 0, 0, 1, 0};
+        if (!(w0 >> 31)) {
+            p.active = 0; p.x = -1.0; p.y = -1.0;
+        } else {
+            p.x = un_dec(w0 & 0x7fffu, 0, wd, 32767);
+            p.y = un_dec((w0 >> 15) & 0x7fffu, 0, hd, 32767);
+            p.cr = cclamp(un_dec(w1 & 0x7ffu, q[4], q[7], 2047), 0, 1);
+            p.cg = cclamp(un_dec((w1 >> 11) & 0x7ffu, q[5], q[8], 2047), 0, 1);
+            p.cb = cclamp(un_dec(w1 >> 22, q[6], q[9], 1023), 0, 1);
+            p.log_tau = un_dec(w2 & 0xffffu, q[0], q[1], 65535);
+            p.radius = un_dec(w2 >> 16, q[2], q[3], 65535);
+            double ang = un_dec(w3 & 0xffffu, -3.14159265358979323846, 2.0 * 3.14159265358979323846, 65535);
+            p.dx = cos(ang); p.dy = sin(ang);
+            p.aniso = (double)sado_half_to_float((uint16_t)(w3 >> 16));
+        }
+        site_set(s, i, &p);
+    }
+    s->size = cnt;
+    return SAD_OK;
+}

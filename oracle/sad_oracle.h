@@ -51,6 +51,8 @@ int sado_simulate_schedule(int n0, double scale, const sad_train_config* cfg, in
 int sado_plan_schedule(int n0, uint64_t target, const sad_train_config* cfg, double* out);
 /* fit: `init` NULL -> fit() (init_sites), else fit_store().  `out` sites/field must be sized by
  * the caller from sado_fit_capacity(); history holds cfg->iters rows. */
+int sado_encode(const sad_sites_view* s, int w, int h, uint8_t* out, size_t cap, size_t* nbytes);
+int sado_decode(const uint8_t* buf, size_t n, sad_sites_view* s, int* w, int* h);
 int sado_fit_capacity(int w, int h, const sad_train_config* cfg, size_t n_init, size_t* cap);
 int sado_fit(const double* tgt, int w, int h, const sad_train_config* cfg,
              const sad_sites_view* init, sad_sites_view* out_sites, sad_field_view* out_field,

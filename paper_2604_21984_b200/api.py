@@ -309,6 +309,56 @@ class Backend:
         self._call("plan_schedule", C.c_int(n0), C.c_uint64(target), C.byref(c), C.byref(out))
         return out.value
 
+    # ------------------------------------------------------------------ codec.hpp (decode path)
+    def encode_sites(self, sites: SiteStore, width: int, height: int) -> bytes:
+        """write_file (codec.cpp:147-177) into memory: the `.sad` container bytes."""
+        sv, keep = sites._view()
+        n = C.c_size_t()
+        self._call("encode", C.byref(sv), C.c_int(width), C.c_int(height), None, C.c_size_t(0), C.byref(n))
+        buf = (C.c_uint8 * n.value)()
+        self._call("encode", C.byref(sv), C.c_int(width), C.c_int(height), buf, C.c_size_t(n.value), C.byref(n))
+        return bytes(buf)
+
+    def decode_sites(self, data: bytes):
+        """read_file (codec.cpp:179-222): returns (width, height, SiteStore)."""
+        count = max((len(data) - 58) // 16, 0) if len(data) >= 58 else 0
+        st = SiteStore(0)
+        sv, keep = st._view(capacity=count + 1)
+        buf = (C.c_uint8 * len(data)).from_buffer_copy(data)
+        w, h = C.c_int(), C.c_int()
+        self._call("decode", buf, C.c_size_t(len(data)), C.byref(sv), C.byref(w), C.byref(h))
+        st._absorb(sv, keep)
+        return w.value, h.value, st
+
+    def write_file(self, path: str, sites: SiteStore, width: int, height: int):
+        with open(path, "wb") as f:
+            f.write(self.encode_sites(sites, width, height))
+
+    def read_file(self, path: str):
+        with open(path, "rb") as f:
+            return self.decode_sites(f.read())
+
+    def decode_render(self, data: bytes, k: int = 8, passes: int = 16, inject: int = 4, seed: int = 1,
+                      fp64: bool = False):
+        """Decode pipeline on the device: bytes -> sites -> refresh(Full, passes) -> render_image.
+        Returns (ImageBuffer, SiteStore)."""
+        if self.kind != "gpu":
+            w, h, st = self.decode_sites(data)
+            f = CandidateField()
+            f.resize(w, h, k)
+            self.refresh(st, f, RefreshMode.Full, passes, inject, seed, RunOpts(fp64=fp64))
+            return self.render_image(st, f, RunOpts(fp64=fp64)), st
+        buf = (C.c_uint8 * len(data)).from_buffer_copy(data)
+        w, h, cnt = C.c_int(), C.c_int(), C.c_uint32()
+        self._call("decode_header", buf, C.c_size_t(len(data)), C.byref(w), C.byref(h), C.byref(cnt))
+        img = ImageBuffer(w.value, h.value)
+        st = SiteStore(0)
+        sv, keep = st._view(capacity=cnt.value + 1)
+        self._call("decode_render", buf, C.c_size_t(len(data)), C.c_int(k), C.c_int(passes), C.c_int(inject),
+                   C.c_uint64(seed), C.c_int(int(fp64)), _ptr(img.data), C.byref(sv))
+        st._absorb(sv, keep)
+        return img, st
+
     # ------------------------------------------------------------------ fit (train.cpp:221-311)
     def fit(self, target: ImageBuffer, cfg: TrainConfig) -> FitResult:
         return self._fit(target, cfg, None)
@@ -423,6 +473,7 @@ class Backend:
 _NO_CTX = {"jump_step", "full_refresh_passes", "schedule_passes", "bpp_target_count", "simulate_schedule",
            "plan_schedule", "fit_set_target", "fit_set_target_device", "fit_run_init", "fit_run_store",
            "fit_info", "fit_download", "fit_render_device", "fit_timing", "fit_bench", "fit_set_profiling",
+           "fit_point_query", "encode", "decode", "decode_header", "bpp",
            "last_error"}
 
 # ---------------------------------------------------------------------- product binding

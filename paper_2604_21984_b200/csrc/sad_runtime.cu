@@ -24,6 +24,7 @@ using sadk::DevState;
 namespace {
 
 thread_local std::string g_err;
+bool g_cuda_used = false;  // a context exists: launch errors are worth checking
 
 struct SadFail {
     int code;
@@ -40,6 +41,10 @@ template <typename F>
 sad_status guard(F&& f) {
     try {
         f();
+        if (g_cuda_used) {
+            cudaError_t le = cudaGetLastError();  // kernel launch failures (no synchronisation)
+            if (le != cudaSuccess) fail(SAD_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(le));
+        }
         return SAD_OK;
     } catch (const SadFail& e) {
         g_err = e.msg;
@@ -776,6 +781,7 @@ struct sad_fit_run {
 extern "C" {
 
 const char* sad_last_error(void) { return g_err.c_str(); }
+void sad_internal_set_error(const char* msg) { g_err = msg; }
 int sad_abi_version(void) { return SAD_ABI_VERSION; }
 
 void sad_default_config(sad_train_config* c) {
@@ -803,6 +809,7 @@ sad_status sad_ctx_create(int device, void* stream, sad_ctx** out) {
         if (prop.major != 10) fail(SAD_ECUDA, "libsad_b200 is built for sm_100a (B200); device is sm_" +
                                                   std::to_string(prop.major) + std::to_string(prop.minor));
         auto* c = new sad_ctx();
+        g_cuda_used = true;
         c->device = device;
         if (stream) {
             c->stream = static_cast<cudaStream_t>(stream);
@@ -1672,6 +1679,78 @@ sad_status sad_fit_bench(sad_fit_run* r, int which, int reps, double* ms_per_lau
             double base = 0;
             sad_status rc = sad_fit_bench(r, 1, reps, &base);
             if (rc == SAD_OK) *ms_per_launch = std::max(0.0, *ms_per_launch - base);
+        }
+    });
+}
+
+// Batched random-access decode against the fitted, device-resident field (pixel_weights semantics,
+// render.cpp:93-105, with the table built once instead of per query).  xy/ids/w/n are DEVICE
+// pointers (n_q queries; ids/w hold 16 entries per query).
+sad_status sad_fit_point_query(sad_fit_run* r, const int32_t* d_xy, size_t n_q, uint32_t* d_ids, double* d_w,
+                               int32_t* d_n) {
+    return guard([&] {
+        if (!r->done) fail(SAD_EINVAL, "fit: not run");
+        Workspace& ws = r->ws;
+        build_tables(ws, true, false, false, true);
+        sadk::launch_pixel_weights(ws.ids[ws.cur].p, ws.rtab_d.p, ws.fd, norm_scale(r->w, r->h), d_xy,
+                                   static_cast<int>(n_q), d_ids, d_w, d_n, ws.stream);
+    });
+}
+
+// Decode pipeline (SPEC decode: read_file -> refresh(Full, passes) -> render_image): bytes -> sites on
+// the host (exact) -> device full refresh -> device render into out_rgb (host, 3*W*H doubles).
+sad_status sad_decode_render(sad_ctx* c, const uint8_t* buf, size_t n, int k, int passes, int inject, uint64_t seed,
+                             int fp64, double* out_rgb, sad_sites_view* out_sites) {
+    return guard([&] {
+        int w = 0, h = 0;
+        uint32_t count = 0;
+        sad_status rc = sad_decode_header(buf, n, &w, &h, &count);
+        if (rc != SAD_OK) fail(rc, sad_last_error());
+        std::vector<double> p(10 * static_cast<size_t>(count) + 10);
+        std::vector<uint8_t> fl(2 * static_cast<size_t>(count) + 2);
+        sad_sites_view v{};
+        v.capacity = count + 1;
+        double** arr[10] = {&v.x, &v.y, &v.log_tau, &v.radius, &v.col_r, &v.col_g, &v.col_b, &v.dir_x, &v.dir_y, &v.aniso};
+        for (int i = 0; i < 10; i++) *arr[i] = p.data() + static_cast<size_t>(i) * (count + 1);
+        v.active = fl.data();
+        v.frozen = fl.data() + count + 1;
+        rc = sad_decode(buf, n, &v, &w, &h);
+        if (rc != SAD_OK) fail(rc, sad_last_error());
+        Workspace& ws = c->ws;
+        upload_sites(ws, &v);
+        ws.ensure_field(w, h, k, 1);
+        ws.cur = 0;
+        ws.patch_state(offsetof(DevState, pass_index), static_cast<uint32_t>(0));
+        ws.compute_active();
+        build_tables(ws, fp64 != 0, true, false, fp64 == 0);
+        double sn = norm_scale(w, h);
+        sadk::launch_jfa_seed(ws.sites(), ws.st.p, ws.ids[0].p, ws.fd, sn, ws.stream);
+        passes_device(ws, full_refresh_passes(ws.fd.gw, ws.fd.gh, passes), inject, seed, fp64 != 0, 0);
+        size_t npx = 3 * static_cast<size_t>(w) * h;
+        if (fp64) {
+            build_tables(ws, true, false, false, true);
+            ws.px_d.ensure(npx);
+            sadk::launch_render(true, ws.ids[ws.cur].p, ws.rtab_d.p, ws.fd, sn, ws.px_d.p, ws.st.p, ws.stream);
+            ck(cudaMemcpyAsync(out_rgb, ws.px_d.p, npx * 8, cudaMemcpyDeviceToHost, ws.stream), "D2H render");
+        } else {
+            ws.px_f.ensure(npx);
+            sadk::launch_render(false, ws.ids[ws.cur].p, ws.rtab.p, ws.fd, sn, ws.px_f.p, ws.st.p, ws.stream);
+            std::vector<float> tmp(npx);
+            ck(cudaMemcpyAsync(tmp.data(), ws.px_f.p, npx * 4, cudaMemcpyDeviceToHost, ws.stream), "D2H render");
+            ck(cudaStreamSynchronize(ws.stream), "sync");
+            for (size_t i = 0; i < npx; i++) out_rgb[i] = tmp[i];
+        }
+        check_err(ws, "render");
+        if (out_sites) {
+            if (out_sites->capacity < count) fail(SAD_ENOMEM, "decode: sites view capacity too small");
+            double** dst[10] = {&out_sites->x, &out_sites->y, &out_sites->log_tau, &out_sites->radius,
+                                &out_sites->col_r, &out_sites->col_g, &out_sites->col_b, &out_sites->dir_x,
+                                &out_sites->dir_y, &out_sites->aniso};
+            for (int i = 0; i < 10; i++) std::memcpy(*dst[i], *arr[i], 8 * count);
+            std::memcpy(out_sites->active, v.active, count);
+            std::memcpy(out_sites->frozen, v.frozen, count);
+            out_sites->size = count;
+            out_sites->generation = v.generation;
         }
     });
 }
