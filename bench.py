@@ -44,6 +44,7 @@ def parse():
     p.add_argument("--bpp", type=float, default=2.0)
     p.add_argument("--iters", type=int, default=4000)
     p.add_argument("--images-per-gpu", type=int, default=1)
+    p.add_argument("--serial", action="store_true", help="fit a rank's images one after another")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--ref-iters", type=int, default=30, help="iterations per reference-arm sample")
     p.add_argument("--cpu-iters", type=int, default=60, help="iterations of the cpu_baseline sample")
@@ -60,7 +61,8 @@ def config_dict(a):
                     f"(full fit() incl. device init_sites, {a.iters} iterations with densify/prune events, "
                     f"final refresh(Full,16)), fp32 kernels",
         "width": a.width, "height": a.height, "target_bpp": a.bpp, "iters": a.iters,
-        "images_per_gpu": a.images_per_gpu, "k": 8, "inject": 4,
+        "images_per_gpu": a.images_per_gpu, "concurrent_images": a.images_per_gpu > 1 and not a.serial,
+        "k": 8, "inject": 4,
         "l2": "flushed (256 MiB write) between timed steps",
     }
 
@@ -324,18 +326,48 @@ def run_b200(a):
     imgs = [synthetic_image(W, H, s) for s in seeds]
     cfgs = [train_config(a, s) for s in seeds]
     dev_t = [torch.from_numpy(im).cuda() for im in imgs]
+    torch.cuda.synchronize()
+    # Several images per GPU (config 4) run concurrently: one context + stream + host thread each,
+    # so the latency-bound kernels of independent fits overlap on the SMs.
+    conc = a.images_per_gpu > 1 and not a.serial
+    streams = [torch.cuda.Stream() for _ in cfgs] if conc else [stream] * len(cfgs)
+    backends = []
+    for st_i in streams:
+        if st_i is stream:
+            backends.append(G)
+            continue
+        cx = C.c_void_p()
+        if lib.sad_ctx_create(C.c_int(local), C.c_void_p(st_i.cuda_stream), C.byref(cx)):
+            raise RuntimeError(lib.sad_last_error().decode())
+        backends.append(api.Backend(lib, "sad_", "gpu", ctx=cx))
     runs = []
-    for cfg in cfgs:
+    for cfg, B in zip(cfgs, backends):
         run = C.c_void_p()
         cc = cfg.to_c()
-        G._call("fit_create", C.c_int(W), C.c_int(H), C.byref(cc), C.byref(run))
+        B._call("fit_create", C.c_int(W), C.c_int(H), C.byref(cc), C.byref(run))
         runs.append(run)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
+    def fit_one(i):
+        backends[i]._call("fit_set_target_device", runs[i], C.c_void_p(dev_t[i].data_ptr()))
+        backends[i]._call("fit_run_init", runs[i])
+
     def step():
-        for run, t in zip(runs, dev_t):
-            G._call("fit_set_target_device", run, C.c_void_p(t.data_ptr()))
-            G._call("fit_run_init", run)
+        if not conc:
+            for i in range(len(runs)):
+                fit_one(i)
+            return
+        ev0 = torch.cuda.Event()
+        ev0.record(stream)
+        for st_i in streams:
+            st_i.wait_event(ev0)
+        th = [threading.Thread(target=fit_one, args=(i,)) for i in range(len(runs))]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        for st_i in streams:
+            stream.wait_stream(st_i)
 
     for _ in range(a.warmup):
         step()
@@ -344,7 +376,7 @@ def run_b200(a):
         torch.distributed.barrier()
     clocks = ClockSampler(local)
     clocks.start()
-    launches0 = lib.sad_ctx_launch_count(ctx)
+    launches0 = lib.sad_ctx_launch_count(ctx)  # process-wide counter (all contexts)
     ms = []
     for _ in range(a.steps):
         flush.zero_()

@@ -1118,10 +1118,17 @@ __global__ void __launch_bounds__(BwdTile<T>::TW * BwdTile<T>::TH)
 #pragma unroll
         for (int i = 0; i < KM; i++) {
             const int e = i * TPX + tid;
-            if (!ok[i]) {
+            // A kept candidate whose softmax weight underflowed to exactly 0 contributes +-0 to every
+            // channel (all terms are products with w or A = w * finite): dropping it leaves every
+            // compensated sum, and the non-finite count, bit-identical — and shrinks the reduction.
+            if (!ok[i] || w[i] == T(0)) {
                 sm.key[e] = kEmpty;
                 continue;
             }
+#if SAD_EXPERIMENT == 3
+            atomicAdd(&g_phase_clk[13], 1ull);
+            if (w[i] == T(0)) atomicAdd(&g_phase_clk[14], 1ull);
+#endif
             const uint32_t id = cid[i];
             const Q4<T> a = gtab[3 * id], b = gtab[3 * id + 1], c = gtab[3 * id + 2];
             T dc0 = c.x - ch0, dc1 = c.y - ch1, dc2 = c.z - ch2;

@@ -11,7 +11,7 @@ from paper_2604_21984_b200.synth import synthetic_image  # noqa: E402
 
 api.LIB_PATH = os.path.abspath(sys.argv[1])
 G = sad.gpu_backend(0)
-cfg = sad.TrainConfig(iters=200, target_bpp=2.0, fp64=False)
+cfg = sad.TrainConfig(iters=int(os.environ.get('ITERS', 200)), target_bpp=2.0, fp64=False)
 run = C.c_void_p()
 cc = cfg.to_c()
 G._call("fit_create", C.c_int(768), C.c_int(512), C.byref(cc), C.byref(run))
@@ -30,3 +30,4 @@ tot = sum(buf[i] for i in range(9))
 for i, nm in enumerate(names):
     print(f"{nm:24s} {buf[i] / blocks:10.0f} cycles/block  {100.0 * buf[i] / tot:5.1f}%")
 print(f"us/launch (event) {out.value * 1e3:.1f}  CAS-fallback site records: {buf[15] / 21:.0f} per launch")
+print(f"entries kept {buf[13] / 21:.0f} per launch, with w == 0: {100.0 * buf[14] / max(buf[13], 1):.1f}%")
