@@ -244,13 +244,10 @@ struct TopKReg {
 // Deduplication is streaming: a candidate already in the running list is skipped, which yields
 // the reference's set-based result because the list's K-th key only ever improves.
 template <typename T, int KM, bool EXACT, bool BOX>
-__global__ void __launch_bounds__(256) k_propagate(const uint32_t* __restrict__ prev, uint32_t* __restrict__ next,
-                                                   const Q4<T>* __restrict__ pack, const uint32_t* __restrict__ act,
-                                                   const DevState* __restrict__ st, FieldDims f, int step, int inject,
-                                                   uint64_t seed, uint32_t pass_offset, T s) {
-    const int gx = blockIdx.x * blockDim.x + threadIdx.x;
-    const int gy = blockIdx.y * blockDim.y + threadIdx.y;
-    if (gx >= f.gw || gy >= f.gh) return;
+__device__ __forceinline__ void propagate_cell(const uint32_t* __restrict__ prev, uint32_t* __restrict__ next,
+                                               const Q4<T>* __restrict__ pack, const uint32_t* __restrict__ act,
+                                               const DevState* __restrict__ st, const FieldDims& f, int gx, int gy,
+                                               int step, int inject, uint64_t seed, uint32_t pass_offset, T s) {
     const int k = EXACT ? KM : f.k;
     const T cx = static_cast<T>(gx * static_cast<double>(f.cell) + (f.cell - 1) * 0.5);
     const T cy = static_cast<T>(gy * static_cast<double>(f.cell) + (f.cell - 1) * 0.5);
@@ -319,14 +316,38 @@ __global__ void __launch_bounds__(256) k_propagate(const uint32_t* __restrict__ 
     }
 }
 
-// Axial (step-s, 5-list) pass specialised for K = 8.  Same result as k_propagate, fewer divergent
-// slots: the cell's own list is scored and ordered with an 8-input sorting network (the insertion
-// sort of TopK::consider yields the same order for distinct, finite keys), the neighbour entries
-// that are not in it and the injected ids are compacted into a per-thread shared-memory queue, and
-// only the queue is scored and inserted.  The TopK result over a set of distinct candidates is
-// independent of feed order (strict total order), and a repeated candidate is either already in the
-// list (skipped) or worse than the current K-th (rejected), so the map is identical.  Own lists with
-// a repeated id or a non-finite logit (never produced by the fit) take the generic streaming path.
+template <typename T, int KM, bool EXACT, bool BOX>
+__global__ void __launch_bounds__(256) k_propagate(const uint32_t* __restrict__ prev, uint32_t* __restrict__ next,
+                                                   const Q4<T>* __restrict__ pack, const uint32_t* __restrict__ act,
+                                                   const DevState* __restrict__ st, FieldDims f, int step, int inject,
+                                                   uint64_t seed, uint32_t pass_offset, T s) {
+    const int gx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gy = blockIdx.y * blockDim.y + threadIdx.y;
+    if (gx >= f.gw || gy >= f.gh) return;
+    propagate_cell<T, KM, EXACT, BOX>(prev, next, pack, act, st, f, gx, gy, step, inject, seed, pass_offset, s);
+}
+
+// Rare-path fallback of the key kernels below (a NaN logit or a repeated id in the own list): the
+// cell is recomputed by the streaming kernel body in the reference's feed order.
+template <bool BOX>
+__device__ __noinline__ void propagate_cell_slow(const uint32_t* __restrict__ prev, uint32_t* __restrict__ next,
+                                                 const Q4<float>* __restrict__ pack, const uint32_t* __restrict__ act,
+                                                 const DevState* __restrict__ st, FieldDims f, int gx, int gy, int step,
+                                                 int inject, uint64_t seed, uint32_t pass_offset, float s) {
+    propagate_cell<float, 8, true, BOX>(prev, next, pack, act, st, f, gx, gy, step, inject, seed, pass_offset, s);
+}
+
+// Propagate pass specialised for K = 8 (Axial: 4 neighbour lists; Box3: 8).  Same map as
+// k_propagate, fewer divergent slots: the cell's own list is scored and ordered with an 8-input
+// sorting network (the insertion sort of TopK::consider yields the same order for distinct, finite
+// keys); the neighbour entries not already in the running list go, four lists at a time, into a
+// per-thread shared-memory queue (the injected ids join the last round), and only the queue is
+// scored and inserted.  The TopK result over a set of distinct candidates does not depend on feed
+// order (strict total order), and a repeated candidate is either in the list (skipped) or worse
+// than the current K-th (the K-th key only improves), so the map equals the reference's
+// first-appearance pool (candidates.cpp:108-135).  Own lists with a repeated id or a non-finite
+// logit take the generic streaming path.  List loads are issued two lists at a time and the queue
+// drain prefetches the next candidate's table rows while the current one is scored.
 constexpr int kAxQ = 36;  // 4 neighbour lists x 8 + 4 injected (larger inject: generic kernel)
 
 template <typename T>
@@ -341,11 +362,15 @@ __device__ __forceinline__ void cex(T& la, uint32_t& ia, T& lb, uint32_t& ib) {
     ia = ti;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(256) k_propagate_ax8(const uint32_t* __restrict__ prev, uint32_t* __restrict__ next,
-                                                       const Q4<T>* __restrict__ pack, const uint32_t* __restrict__ act,
-                                                       const DevState* __restrict__ st, FieldDims f, int step,
-                                                       int inject, uint64_t seed, uint32_t pass_offset, T s) {
+// kAxialOff / kBoxOff (candidates.cpp:88-90), offsets 1..8
+__device__ __forceinline__ int off_x(int o) { return (o == 1 || o == 5 || o == 6) ? 1 : ((o == 2 || o == 7 || o == 8) ? -1 : 0); }
+__device__ __forceinline__ int off_y(int o) { return (o == 3 || o == 5 || o == 7) ? 1 : ((o == 4 || o == 6 || o == 8) ? -1 : 0); }
+
+template <typename T, bool BOX>
+__global__ void __launch_bounds__(256) k_propagate_k8(const uint32_t* __restrict__ prev, uint32_t* __restrict__ next,
+                                                      const Q4<T>* __restrict__ pack, const uint32_t* __restrict__ act,
+                                                      const DevState* __restrict__ st, FieldDims f, int step,
+                                                      int inject, uint64_t seed, uint32_t pass_offset, T s) {
     __shared__ uint32_t q[kAxQ * 256];
     const int tid = threadIdx.y * blockDim.x + threadIdx.x;
     const int gx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -412,21 +437,263 @@ __global__ void __launch_bounds__(256) k_propagate_ax8(const uint32_t* __restric
         }
     }
 
-    // ---- neighbour entries not already in the list, then injected ids, into the queue
-    int nq = 0;
+    const int n_act = st->n_active;
+    constexpr int NG = BOX ? 2 : 1;
 #pragma unroll 1
-    for (int o = 1; o < 5; o++) {
-        int nx = gx + (o == 1 ? step : (o == 2 ? -step : 0));
-        int ny = gy + (o == 3 ? step : (o == 4 ? -step : 0));
-        if (nx < 0 || ny < 0 || nx >= f.gw || ny >= f.gh) continue;
+    for (int g = 0; g < NG; g++) {
+        // ---- neighbour entries not already in the list (two lists per load batch)
+        int nq = 0;
+#pragma unroll 1
+        for (int pr = 0; pr < 2; pr++) {
+            uint4 u[4];
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int o = 1 + 4 * g + 2 * pr + h;
+                const int nx = gx + off_x(o) * step, ny = gy + off_y(o) * step;
+                if (nx >= 0 && ny >= 0 && nx < f.gw && ny < f.gh) {
+                    const uint4* lst = reinterpret_cast<const uint4*>(prev + 8 * (static_cast<size_t>(ny) * f.gw + nx));
+                    u[2 * h] = __ldg(lst);
+                    u[2 * h + 1] = __ldg(lst + 1);
+                } else {
+                    u[2 * h] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+                    u[2 * h + 1] = u[2 * h];
+                }
+            }
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const uint32_t v[8] = {u[2 * h].x, u[2 * h].y, u[2 * h].z, u[2 * h].w,
+                                       u[2 * h + 1].x, u[2 * h + 1].y, u[2 * h + 1].z, u[2 * h + 1].w};
+                bool end = false;
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    end = end || v[i] == kEmpty;
+                    if (!end && !sel.contains(v[i])) q[nq++ * 256 + tid] = v[i];
+                }
+            }
+        }
+        if (g == NG - 1 && inject > 0 && n_act > 0) {
+            uint32_t rs = seeded_state(seed, st->pass_index + pass_offset,
+                                       static_cast<uint32_t>(gy) * static_cast<uint32_t>(f.gw) + static_cast<uint32_t>(gx));
+            for (int j = 0; j < inject; j++)
+                q[nq++ * 256 + tid] = __ldg(act + xs_next(rs) % static_cast<uint32_t>(n_act));
+        }
+        // ---- score and insert the queue; the next entry's rows are in flight meanwhile
+        if (nq > 0) {
+            uint32_t c = q[tid];
+            Q4<T> b = pack[2 * c + 1], a = pack[2 * c];
+#pragma unroll 1
+            for (int j = 0; j < nq; j++) {
+                const uint32_t cn = j + 1 < nq ? q[(j + 1) * 256 + tid] : c;
+                const Q4<T> bn = pack[2 * cn + 1], an = pack[2 * cn];
+                if (b.w != T(0) && !sel.contains(c)) {
+                    const T l = score_logit(a, b, cx, cy, s);
+                    if (!sel.full_reject(l, c)) sel.consider(c, l);
+                }
+                c = cn;
+                a = an;
+                b = bn;
+            }
+        }
+    }
+    uint4* out = reinterpret_cast<uint4*>(next + 8 * (static_cast<size_t>(gy) * f.gw + gx));
+    out[0] = make_uint4(sel.id[0], sel.id[1], sel.id[2], sel.id[3]);
+    out[1] = make_uint4(sel.id[4], sel.id[5], sel.id[6], sel.id[7]);
+}
+
+#ifndef SAD_PROP_MINB
+#define SAD_PROP_MINB 4
+#endif
+// ---------------------------------------------------------------------- K = 8, fp32, 64-bit keys
+// A list entry (logit l, id c) is one u64 key: the order-preserving bits of l (with -0 folded onto
+// +0, so equal logits tie exactly as in TopK) in the high word and ~c in the low word.  Larger key
+// <=> better under (logit desc, id asc), every real key is > 0 (the most negative finite float maps
+// to 0x00800000), and an empty slot is key 0 whose low word decodes to kEmpty.  `better` becomes
+// one 64-bit compare, the K-th rejection test one compare, and the sorted insertion eight compares
+// plus selects with no position search.  Only a NaN logit (no order) or a repeated id in the own
+// list leaves this representation; such a cell is recomputed by propagate_cell_slow.
+__device__ __forceinline__ uint64_t list_key(float l, uint32_t c) {
+    uint32_t u = __float_as_uint(__fadd_rn(l, 0.0f));
+    u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    return (static_cast<uint64_t>(u) << 32) | static_cast<uint32_t>(~c);
+}
+
+struct KeyList8 {
+    uint64_t k[8];
+    __device__ __forceinline__ bool contains(uint32_t c) const {
+        const uint32_t nc = ~c;
+        bool d = false;
+#pragma unroll
+        for (int i = 0; i < 8; i++) d |= (static_cast<uint32_t>(k[i]) == nc);
+        return d;
+    }
+    // x must beat k[7] and must not be in the list
+    __device__ __forceinline__ void insert(uint64_t x) {
+        bool b[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) b[i] = x > k[i];
+#pragma unroll
+        for (int i = 7; i >= 1; i--) k[i] = b[i - 1] ? k[i - 1] : (b[i] ? x : k[i]);
+        k[0] = b[0] ? x : k[0];
+    }
+    __device__ __forceinline__ void consider(uint32_t c, uint64_t x) {
+        if (x > k[7] && !contains(c)) insert(x);
+    }
+};
+
+__device__ __forceinline__ void kcex(uint64_t& a, uint64_t& b) {  // a <- max, b <- min
+    const uint64_t hi = a > b ? a : b, lo = a > b ? b : a;
+    a = hi;
+    b = lo;
+}
+
+// Own list -> sorted keys.  Returns false when the slow path is needed (NaN logit, repeated id).
+__device__ __forceinline__ bool own_keys(const uint32_t* __restrict__ prev, const Q4<float>* __restrict__ pack,
+                                         const FieldDims& f, int gx, int gy, float cx, float cy, float s,
+                                         KeyList8& L) {
+    const uint4* own = reinterpret_cast<const uint4*>(prev + 8 * (static_cast<size_t>(gy) * f.gw + gx));
+    const uint4 o0 = __ldg(own), o1 = __ldg(own + 1);
+    const uint32_t oid[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+    bool stop = false, ok = true;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        stop = stop || oid[i] == kEmpty;
+        L.k[i] = 0;
+        if (!stop) {
+            const Q4<float> a = pack[2 * oid[i]], b = pack[2 * oid[i] + 1];
+            if (b.w != 0.0f) {
+                const float l = score_logit(a, b, cx, cy, s);
+                ok &= (l == l);
+                L.k[i] = list_key(l, oid[i]);
+            }
+        }
+    }
+    // Batcher odd-even merge sort (descending), 19 comparators
+    kcex(L.k[0], L.k[1]); kcex(L.k[2], L.k[3]); kcex(L.k[4], L.k[5]); kcex(L.k[6], L.k[7]);
+    kcex(L.k[0], L.k[2]); kcex(L.k[1], L.k[3]); kcex(L.k[4], L.k[6]); kcex(L.k[5], L.k[7]);
+    kcex(L.k[1], L.k[2]); kcex(L.k[5], L.k[6]);
+    kcex(L.k[0], L.k[4]); kcex(L.k[1], L.k[5]); kcex(L.k[2], L.k[6]); kcex(L.k[3], L.k[7]);
+    kcex(L.k[2], L.k[4]); kcex(L.k[3], L.k[5]);
+    kcex(L.k[1], L.k[2]); kcex(L.k[3], L.k[4]); kcex(L.k[5], L.k[6]);
+    // a repeated id has a repeated key, adjacent after sorting
+#pragma unroll
+    for (int i = 0; i < 7; i++) ok &= !(L.k[i] != 0 && L.k[i] == L.k[i + 1]);
+    return ok;
+}
+
+__device__ __forceinline__ void store_keys(uint32_t* __restrict__ next, const FieldDims& f, int gx, int gy,
+                                           const KeyList8& L) {
+    uint4* out = reinterpret_cast<uint4*>(next + 8 * (static_cast<size_t>(gy) * f.gw + gx));
+    out[0] = make_uint4(~static_cast<uint32_t>(L.k[0]), ~static_cast<uint32_t>(L.k[1]), ~static_cast<uint32_t>(L.k[2]),
+                        ~static_cast<uint32_t>(L.k[3]));
+    out[1] = make_uint4(~static_cast<uint32_t>(L.k[4]), ~static_cast<uint32_t>(L.k[5]), ~static_cast<uint32_t>(L.k[6]),
+                        ~static_cast<uint32_t>(L.k[7]));
+}
+
+// Streaming variant (Box3 floods): every neighbour entry is scored first, then tested against the
+// K-th key, and only the survivors are deduplicated against the list — at flood steps most entries
+// are new sites, so dedup-first would be wasted work.
+template <bool BOX>
+__global__ void __launch_bounds__(256, SAD_PROP_MINB) k_prop8_stream(const uint32_t* __restrict__ prev, uint32_t* __restrict__ next,
+                                                      const Q4<float>* __restrict__ pack,
+                                                      const uint32_t* __restrict__ act, const DevState* __restrict__ st,
+                                                      FieldDims f, int step, int inject, uint64_t seed,
+                                                      uint32_t pass_offset, float s) {
+    const int gx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gy = blockIdx.y * blockDim.y + threadIdx.y;
+    if (gx >= f.gw || gy >= f.gh) return;
+    const float cx = static_cast<float>(gx * static_cast<double>(f.cell) + (f.cell - 1) * 0.5);
+    const float cy = static_cast<float>(gy * static_cast<double>(f.cell) + (f.cell - 1) * 0.5);
+    KeyList8 L;
+    bool ok = own_keys(prev, pack, f, gx, gy, cx, cy, s, L);
+    auto feed = [&](uint32_t c) {
+        const Q4<float> b = pack[2 * c + 1], a = pack[2 * c];
+        if (b.w == 0.0f) return;
+        const float l = score_logit(a, b, cx, cy, s);
+        ok &= (l == l);
+        L.consider(c, list_key(l, c));
+    };
+    constexpr int NOFF = BOX ? 9 : 5;
+    // the next neighbour list is in flight while the current one is scored
+    auto load = [&](int o, uint4& u0, uint4& u1) {
+        const int nx = gx + off_x(o) * step, ny = gy + off_y(o) * step;
+        if (nx < 0 || ny < 0 || nx >= f.gw || ny >= f.gh) {
+            u0 = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+            u1 = u0;
+            return;
+        }
         const uint4* lst = reinterpret_cast<const uint4*>(prev + 8 * (static_cast<size_t>(ny) * f.gw + nx));
-        uint4 u0 = __ldg(lst), u1 = __ldg(lst + 1);
-        uint32_t v[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
-        bool end = false;
+        u0 = __ldg(lst);
+        u1 = __ldg(lst + 1);
+    };
+    uint4 u0, u1;
+    load(1, u0, u1);
+#pragma unroll 1
+    for (int o = 1; o < NOFF; o++) {
+        const uint32_t v[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+        if (o + 1 < NOFF) load(o + 1, u0, u1);
 #pragma unroll
         for (int i = 0; i < 8; i++) {
-            end = end || v[i] == kEmpty;
-            if (!end && !sel.contains(v[i])) q[nq++ * 256 + tid] = v[i];
+            if (v[i] == kEmpty) break;
+            feed(v[i]);
+        }
+    }
+    const int n_act = st->n_active;
+    if (inject > 0 && n_act > 0) {
+        uint32_t rs = seeded_state(seed, st->pass_index + pass_offset,
+                                   static_cast<uint32_t>(gy) * static_cast<uint32_t>(f.gw) + static_cast<uint32_t>(gx));
+#pragma unroll 1
+        for (int j = 0; j < inject; j++) feed(__ldg(act + xs_next(rs) % static_cast<uint32_t>(n_act)));
+    }
+    if (ok)
+        store_keys(next, f, gx, gy, L);
+    else
+        propagate_cell_slow<BOX>(prev, next, pack, act, st, f, gx, gy, step, inject, seed, pass_offset, s);
+}
+
+// Queue variant (warm Axial passes): most neighbour entries are already in the own list, so they are
+// filtered by id first and only the rest (plus the injected ids) go through a per-thread shared
+// queue that is scored convergently, with the next entry's table rows prefetched.
+__global__ void __launch_bounds__(256, SAD_PROP_MINB) k_prop8_queue(const uint32_t* __restrict__ prev, uint32_t* __restrict__ next,
+                                                     const Q4<float>* __restrict__ pack,
+                                                     const uint32_t* __restrict__ act, const DevState* __restrict__ st,
+                                                     FieldDims f, int step, int inject, uint64_t seed,
+                                                     uint32_t pass_offset, float s) {
+    __shared__ uint32_t q[kAxQ * 256];
+    const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+    const int gx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gy = blockIdx.y * blockDim.y + threadIdx.y;
+    if (gx >= f.gw || gy >= f.gh) return;
+    const float cx = static_cast<float>(gx * static_cast<double>(f.cell) + (f.cell - 1) * 0.5);
+    const float cy = static_cast<float>(gy * static_cast<double>(f.cell) + (f.cell - 1) * 0.5);
+    KeyList8 L;
+    bool ok = own_keys(prev, pack, f, gx, gy, cx, cy, s, L);
+    int nq = 0;
+#pragma unroll 1
+    for (int pr = 0; pr < 2; pr++) {
+        uint4 u[4];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int o = 1 + 2 * pr + h;
+            const int nx = gx + off_x(o) * step, ny = gy + off_y(o) * step;
+            if (nx >= 0 && ny >= 0 && nx < f.gw && ny < f.gh) {
+                const uint4* lst = reinterpret_cast<const uint4*>(prev + 8 * (static_cast<size_t>(ny) * f.gw + nx));
+                u[2 * h] = __ldg(lst);
+                u[2 * h + 1] = __ldg(lst + 1);
+            } else {
+                u[2 * h] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+                u[2 * h + 1] = u[2 * h];
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const uint32_t v[8] = {u[2 * h].x, u[2 * h].y, u[2 * h].z, u[2 * h].w,
+                                   u[2 * h + 1].x, u[2 * h + 1].y, u[2 * h + 1].z, u[2 * h + 1].w};
+            bool end = false;
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                end = end || v[i] == kEmpty;
+                if (!end && !L.contains(v[i])) q[nq++ * 256 + tid] = v[i];
+            }
         }
     }
     const int n_act = st->n_active;
@@ -435,21 +702,27 @@ __global__ void __launch_bounds__(256) k_propagate_ax8(const uint32_t* __restric
                                    static_cast<uint32_t>(gy) * static_cast<uint32_t>(f.gw) + static_cast<uint32_t>(gx));
         for (int j = 0; j < inject; j++) q[nq++ * 256 + tid] = __ldg(act + xs_next(rs) % static_cast<uint32_t>(n_act));
     }
-    // ---- score and insert the queue
+    if (nq > 0) {
+        uint32_t c = q[tid];
+        Q4<float> b = pack[2 * c + 1], a = pack[2 * c];
 #pragma unroll 1
-    for (int j = 0; j < nq; j++) {
-        const uint32_t c = q[j * 256 + tid];
-        if (sel.contains(c)) continue;
-        const Q4<T> b = pack[2 * c + 1];
-        if (b.w == T(0)) continue;
-        const Q4<T> a = pack[2 * c];
-        T l = score_logit(a, b, cx, cy, s);
-        if (sel.full_reject(l, c)) continue;
-        sel.consider(c, l);
+        for (int j = 0; j < nq; j++) {
+            const uint32_t cn = j + 1 < nq ? q[(j + 1) * 256 + tid] : c;
+            const Q4<float> bn = pack[2 * cn + 1], an = pack[2 * cn];
+            if (b.w != 0.0f) {
+                const float l = score_logit(a, b, cx, cy, s);
+                ok &= (l == l);
+                L.consider(c, list_key(l, c));
+            }
+            c = cn;
+            a = an;
+            b = bn;
+        }
     }
-    uint4* out = reinterpret_cast<uint4*>(next + 8 * (static_cast<size_t>(gy) * f.gw + gx));
-    out[0] = make_uint4(sel.id[0], sel.id[1], sel.id[2], sel.id[3]);
-    out[1] = make_uint4(sel.id[4], sel.id[5], sel.id[6], sel.id[7]);
+    if (ok)
+        store_keys(next, f, gx, gy, L);
+    else
+        propagate_cell_slow<false>(prev, next, pack, act, st, f, gx, gy, step, inject, seed, pass_offset, s);
 }
 
 template <typename T, int KM, bool EXACT>
@@ -472,16 +745,27 @@ static void propagate_t(const uint32_t* prev, uint32_t* next, const void* pack, 
 void launch_propagate(bool fp64, const uint32_t* prev, uint32_t* next, const void* pack, const uint32_t* act,
                       const DevState* st, const FieldDims& f, uint32_t step, int box, int inject, uint64_t seed,
                       uint32_t pass_offset, double scale, cudaStream_t stream) {
-    if (f.k == 8 && !box && inject <= 4) {
+    if (f.k == 8 && !fp64) {
         dim3 block(32, 8);
         dim3 grid((f.gw + 31) / 32, (f.gh + 7) / 8);
-        if (fp64)
-            k_propagate_ax8<double><<<grid, block, 0, stream>>>(prev, next, (const Q4<double>*)pack, act, st, f,
-                                                                (int)step, inject, seed, pass_offset, scale);
+        const float sf = static_cast<float>(scale);
+        if (box)
+            k_prop8_stream<true><<<grid, block, 0, stream>>>(prev, next, (const Q4<float>*)pack, act, st, f, (int)step,
+                                                             inject, seed, pass_offset, sf);
+        else if (inject <= 4)
+            k_prop8_queue<<<grid, block, 0, stream>>>(prev, next, (const Q4<float>*)pack, act, st, f, (int)step, inject,
+                                                      seed, pass_offset, sf);
         else
-            k_propagate_ax8<float><<<grid, block, 0, stream>>>(prev, next, (const Q4<float>*)pack, act, st, f,
-                                                               (int)step, inject, seed, pass_offset,
-                                                               static_cast<float>(scale));
+            k_prop8_stream<false><<<grid, block, 0, stream>>>(prev, next, (const Q4<float>*)pack, act, st, f,
+                                                              (int)step, inject, seed, pass_offset, sf);
+        SAD_LAUNCHED();
+        return;
+    }
+    if (f.k == 8 && inject <= 4 && !box) {
+        dim3 block(32, 8);
+        dim3 grid((f.gw + 31) / 32, (f.gh + 7) / 8);
+        k_propagate_k8<double, false><<<grid, block, 0, stream>>>(prev, next, (const Q4<double>*)pack, act, st, f,
+                                                                 (int)step, inject, seed, pass_offset, scale);
         SAD_LAUNCHED();
         return;
     }

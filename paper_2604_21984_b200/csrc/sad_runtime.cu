@@ -1614,7 +1614,8 @@ sad_status sad_fit_render_device(sad_fit_run* r, float* out) {
 }
 
 // Micro-benchmark of one kernel on the fitted, device-resident state (roofline evidence).
-// which: 0 warm propagate pass, 1 fused fwd+bwd, 2 render, 3 Box3 flood pass (step 16), 4 Adam, 5 stats.
+// which: 0 warm propagate pass, 1 fused fwd+bwd, 2 render, 3 Box3 flood pass (step 16), 4 Adam, 5 stats,
+// 6 record-counter memsets, 7 event full refresh (seed + floods + 4 Axial passes).
 sad_status sad_fit_bench(sad_fit_run* r, int which, int reps, double* ms_per_launch) {
     return guard([&] {
         if (!r->done) fail(SAD_EINVAL, "fit: not run");
@@ -1654,6 +1655,11 @@ sad_status sad_fit_bench(sad_fit_run* r, int which, int reps, double* ms_per_lau
                 ws.plan_records();
                 break;
             case 5: stats_device(ws); break;
+            case 7:  // one event refresh: seed + ceil(log2) Box3 floods + 4 Axial passes
+                ws.cur = 0;
+                sadk::launch_jfa_seed(ws.sites(), ws.st.p, ws.ids[0].p, ws.fd, sn, s);
+                passes_device(ws, full_refresh_passes(ws.fd.gw, ws.fd.gh, 4), c.inject, c.seed, fp64, 0);
+                break;
             default: fail(SAD_EINVAL, "bench: unknown kernel");
             }
         };

@@ -79,6 +79,44 @@ def test_propagate_pass_box_step(G, R):
     assert np.array_equal(fg.ids, fr.ids)
 
 
+@pytest.mark.parametrize("stencil,step", [(sad.Stencil.Axial, 1), (sad.Stencil.Box3, 4), (sad.Stencil.Box3, 1)])
+def test_propagate_fallback_cells(G, R, stencil, step):
+    """Own lists holding a repeated id take the K=8 kernels' exact streaming fallback; the map must
+    still equal the reference's first-appearance pool result (candidates.cpp:108-135)."""
+    w, h = 40, 32
+    st = random_sites(w, h, 80, 17)
+    fg, fr = _field(w, h), _field(w, h)
+    G.refresh(st, fg, sad.RefreshMode.Full, 2, 4, 5, F32)
+    R.refresh(st, fr, sad.RefreshMode.Full, 2, 4, 5, F32)
+    assert np.array_equal(fg.ids, fr.ids)
+    ids = fg.ids.reshape(-1, 8).copy()
+    rows = np.random.default_rng(3).choice(ids.shape[0], 300, replace=False)
+    full = rows[ids[rows, 3] != sad.CandidateField.kEmpty]
+    ids[full, 3] = ids[full, 0]
+    ids[rows[:40], 1] = ids[rows[:40], 0]
+    fg.ids = ids.reshape(-1).copy()
+    fr.ids = ids.reshape(-1).copy()
+    for B, f in ((G, fg), (R, fr)):
+        B.propagate_pass(st, f, sad.PassSpec(step, stencil), 4, 31, F32)
+    assert np.array_equal(fg.ids, fr.ids)
+
+
+def test_propagate_nan_site(G, R):
+    """A site with a NaN coordinate gives NaN logits (no order); cells that see it are recomputed
+    in the reference's feed order, and the rest of the map is unaffected."""
+    w, h = 40, 32
+    st = random_sites(w, h, 80, 23)
+    fg, fr = _field(w, h), _field(w, h)
+    G.refresh(st, fg, sad.RefreshMode.Full, 2, 4, 5, F32)
+    R.refresh(st, fr, sad.RefreshMode.Full, 2, 4, 5, F32)
+    st.x[11] = np.nan
+    st.bump()
+    for B, f in ((G, fg), (R, fr)):
+        B.propagate_pass(st, f, sad.PassSpec(1, sad.Stencil.Axial), 4, 31, F32)
+        B.propagate_pass(st, f, sad.PassSpec(2, sad.Stencil.Box3), 4, 32, F32)
+    assert np.array_equal(fg.ids, fr.ids)
+
+
 @pytest.mark.parametrize("k,cell", [(1, 1), (3, 1), (12, 1), (16, 1), (8, 2), (5, 3)])
 def test_refresh_other_k_and_cell(G, R, k, cell):
     st = random_model(40, 30, 70, 4)

@@ -14,7 +14,8 @@ import paper_2604_21984_b200 as sad  # noqa: E402
 from paper_2604_21984_b200 import api  # noqa: E402
 from paper_2604_21984_b200.synth import synthetic_image  # noqa: E402
 
-KERNELS = {"propagate_warm": 0, "fwd_bwd": 1, "render": 2, "propagate_flood": 3, "adam": 4, "stats": 5}
+KERNELS = {"propagate_warm": 0, "fwd_bwd": 1, "render": 2, "propagate_flood": 3, "adam": 4, "stats": 5,
+           "memsets": 6, "refresh_full": 7}
 
 p = argparse.ArgumentParser()
 p.add_argument("--kernel", default="fwd_bwd", choices=list(KERNELS))
