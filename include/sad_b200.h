@@ -174,6 +174,12 @@ sad_status sad_pixel_weights(sad_ctx* ctx, const sad_sites_view* sites, const sa
 sad_status sad_render_id_map(sad_ctx* ctx, const sad_sites_view* sites, const sad_field_view* field,
                              uint32_t* out);
 
+/* tau_diffusion (train.hpp:43-44, train.cpp:171-213).  grads: n*11 doubles in/out; only the logtau
+ * column (slot 2) of pixel owners changes.  lambda == 0 is a no-op; lambda outside [0,1] -> EINVAL;
+ * a stale field -> ESTALE; an empty candidate list -> EEMPTY (render_id_map). */
+sad_status sad_tau_diffusion(sad_ctx* ctx, const sad_sites_view* sites, const sad_field_view* field, double lambda,
+                             double* grads);
+
 /* ---------------------------------------------------------------- grad.hpp */
 /* backward_image (grad.hpp:96-98, grad.cpp:364-372).  grads: n*11 doubles (value of each Accum). */
 sad_status sad_backward_image(sad_ctx* ctx, const sad_sites_view* sites, const sad_field_view* field,

@@ -20,6 +20,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <cstring>
 #include <vector>
 
 namespace sad::b200 {
@@ -232,6 +233,28 @@ inline void adam_step(Context& g, SiteStore& st, const GradBuffer& gb, AdamState
     s.store_into(st);
     a.t = av.t;
     a.skipped = av.skipped;
+}
+
+// tau_diffusion (train.hpp:43-44): owners' logtau accumulators are reset to the mixed value
+inline void tau_diffusion(Context& g, const SiteStore& st, const CandidateField& f, double lambda, GradBuffer& gb,
+                          const RunOpts& = {}) {
+    if (lambda == 0) return;
+    if (lambda < 0 || lambda > 1) throw std::invalid_argument("tau_diffusion: lambda out of [0,1]");
+    if (gb.size() != st.size()) throw std::invalid_argument("tau_diffusion: size mismatch");
+    detail::SitesView s(st);
+    sad_field_view v = detail::field_view(f);
+    std::vector<double> buf(std::max<size_t>(st.size(), 1) * kChannels);
+    for (size_t id = 0; id < st.size(); id++)
+        for (int c = 0; c < kChannels; c++) buf[id * kChannels + c] = gb.grad(c, static_cast<uint32_t>(id));
+    std::vector<double> before(buf);
+    check(sad_tau_diffusion(g.get(), &s.v, &v, lambda, buf.data()));
+    for (size_t id = 0; id < st.size(); id++) {
+        const size_t i = id * kChannels + kGradLogTau;
+        if (std::memcmp(&buf[i], &before[i], sizeof(double)) == 0) continue;
+        Accum& a = gb.at(kGradLogTau, static_cast<uint32_t>(id));
+        a.reset();
+        a.add(buf[i]);
+    }
 }
 
 // accumulate_stats (budget.hpp:29-30)

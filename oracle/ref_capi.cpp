@@ -378,6 +378,24 @@ int sadref_backward_image(const sad_sites_view* sv, const sad_field_view* fv, co
     });
 }
 
+int sadref_tau_diffusion(const sad_sites_view* sv, const sad_field_view* fv, double lambda, double* grads) {
+    return guard([&] {
+        SiteStore st = to_store(sv);
+        CandidateField f = to_field(fv);
+        size_t n = st.size();
+        GradBuffer gb;
+        gb.resize(n);
+        for (size_t id = 0; id < n; id++)
+            for (int s = 0; s < kChannels; s++) {
+                Accum a;
+                a.add(grads[id * 11 + s]);
+                gb.at(s, static_cast<uint32_t>(id)) = a;
+            }
+        tau_diffusion(st, f, lambda, gb, RunOpts{});
+        grads_out(gb, n, grads);
+    });
+}
+
 int sadref_image_loss(const sad_sites_view* sv, const sad_field_view* fv, const double* tgt, int fp64,
                       double* loss) {
     return guard([&] {

@@ -350,6 +350,64 @@ int sado_image_loss(const sad_sites_view* s, const sad_field_view* f, const doub
     return fp64 ? loss_d(s, f, tgt, loss) : loss_f(s, f, tgt, loss);
 }
 
+/* tau_diffusion (train.cpp:171-213): every pixel owner's logtau gradient becomes
+ * (1 - lambda) g0[o] + lambda * (sequential ascending-id sum of g0 over its unique co-candidates) / count,
+ * stored through a reset Accum (reset + add). */
+static int cmp_u64(const void* a, const void* b) {
+    uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+    return x < y ? -1 : (x > y);
+}
+
+int sado_tau_diffusion(const sad_sites_view* s, const sad_field_view* f, double lambda, double* grads) {
+    if (lambda == 0) return SAD_OK;
+    if (lambda < 0 || lambda > 1) return fail(SAD_EINVAL, "tau_diffusion: lambda out of [0,1]");
+    size_t np = (size_t)f->width * f->height;
+    uint32_t* owner = (uint32_t*)malloc(4 * np + 4);
+    int rc = sado_render_id_map(s, f, owner);
+    if (rc) {
+        free(owner);
+        return rc;
+    }
+    uint64_t* e = (uint64_t*)malloc(8 * np * f->k + 8);
+    size_t ne = 0;
+    for (int py = 0; py < f->height; py++)
+        for (int px = 0; px < f->width; px++) {
+            uint64_t o = owner[(size_t)py * f->width + px];
+            const uint32_t* lst = f->ids + (size_t)f->k * ((size_t)(py / f->cell) * f->gw + px / f->cell);
+            for (int i = 0; i < f->k; i++) {
+                uint32_t id = lst[i];
+                if (id == SAD_EMPTY_ID) break;
+                if (!s->active[id]) continue;
+                e[ne++] = (o << 32) | id;
+            }
+        }
+    qsort(e, ne, 8, cmp_u64); /* (owner, id) pair order == u64 order */
+    size_t nu = 0;
+    for (size_t i = 0; i < ne; i++)
+        if (nu == 0 || e[nu - 1] != e[i]) e[nu++] = e[i];
+    double* g0 = (double*)malloc(8 * s->size + 8);
+    for (size_t i = 0; i < s->size; i++) g0[i] = grads[i * 11 + 2];
+    size_t i = 0;
+    while (i < nu) {
+        uint32_t o = (uint32_t)(e[i] >> 32);
+        double sum = 0;
+        int cnt = 0;
+        while (i < nu && (uint32_t)(e[i] >> 32) == o) {
+            sum += g0[(uint32_t)e[i]];
+            cnt++;
+            i++;
+        }
+        double mixed = (1.0 - lambda) * g0[o] + lambda * (sum / cnt);
+        accum_t a = {0.0, 0.0};
+        accum_add(&a, mixed);
+        grads[(size_t)o * 11 + 2] = accum_value(&a);
+    }
+    free(g0);
+    free(e);
+    free(owner);
+    return SAD_OK;
+}
+
 /* ------------------------------------------------------------------ train.cpp */
 static inline double mx(double a, double b) { return (a < b) ? b : a; } /* std::max */
 static inline double mn(double a, double b) { return (b < a) ? b : a; } /* std::min */
@@ -970,6 +1028,8 @@ int sado_fit(const double* tgt, int w, int h, const sad_train_config* cfg, const
             rc = fail(SAD_ENUMERIC, "fit: non-finite loss");
             goto done;
         }
+        if (c.tau_diffusion_lambda > 0)
+            if ((rc = sado_tau_diffusion(st, f, c.tau_diffusion_lambda, gb))) goto done;
         int ev_d = budget && t >= c.densify_start && t <= c.densify_end && t % c.densify_every == 0;
         int ev_p = budget && t >= c.prune_start && t <= c.prune_end && t % c.prune_every == 0;
         if (ev_p && !c.prune_during_densify && t <= c.densify_end) ev_p = 0;

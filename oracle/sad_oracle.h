@@ -36,6 +36,7 @@ int sado_backward_image(const sad_sites_view* s, const sad_field_view* f, const 
                         int with_removal, double* grads, uint64_t* nonfinite, double* loss);
 int sado_image_loss(const sad_sites_view* s, const sad_field_view* f, const double* tgt, int fp64,
                     double* loss);
+int sado_tau_diffusion(const sad_sites_view* s, const sad_field_view* f, double lambda, double* grads);
 int sado_adam_step(sad_sites_view* s, const double* grads, sad_adam_view* a, int w, int h,
                    const sad_train_config* cfg);
 int sado_clamp_project(sad_sites_view* s, int w, int h, const sad_train_config* cfg);

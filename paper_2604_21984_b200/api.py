@@ -232,6 +232,24 @@ class Backend:
         sites._absorb(sv, keep)
         adam._absorb(av, akeep)
 
+    def tau_diffusion(self, sites: SiteStore, field: CandidateField, lam: float, g: GradBuffer,
+                      opts: RunOpts = RunOpts()):
+        """tau_diffusion (train.hpp:43-44, train.cpp:171-213): mixes each pixel owner's logtau gradient
+        with the mean over its co-candidates; other channels and non-owners are untouched."""
+        if lam == 0:
+            return
+        if lam < 0 or lam > 1:
+            raise InvalidArgument("tau_diffusion: lambda out of [0,1]")
+        if g.size() != sites.size():
+            raise InvalidArgument("tau_diffusion: size mismatch")
+        sv, keep = sites._view()
+        fv = field._view()
+        gd = np.ascontiguousarray(g.data, dtype=np.float64).reshape(-1).copy()
+        if gd.size == 0:
+            gd = np.zeros(11)
+        self._call("tau_diffusion", C.byref(sv), C.byref(fv), C.c_double(lam), _ptr(gd))
+        g.data = gd[: sites.size() * 11].reshape(-1, 11).copy()
+
     def clamp_project(self, sites: SiteStore, width, height, cfg: TrainConfig):
         sv, keep = sites._view()
         c = cfg.to_c()

@@ -1846,20 +1846,10 @@ __device__ __forceinline__ void clamp_site(double* p, int cap, int id, const Ada
 // k < 10 then applies the Adam update of parameter k and its clamp; dir is renormalised from both
 // lanes' values exchanged by shuffle; lanes 0-4 rebuild the site's candidate snapshot and backward
 // table.  With the adaptive record layout, lane 0 also plans the next pass's record capacity.
-template <typename T>
-__global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarget grads, double* __restrict__ m,
-                                              double* __restrict__ v, AdamHyper hp,
-                                              const double2* __restrict__ bc_table, double2 bc_now, int zero_grads,
-                                              double scale, Q4<T>* pack, Q4<T>* gtab, int32_t* rcap_next) {
-    const int lane16 = threadIdx.x & 15;
-    const int id = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
-    const unsigned gmask = 0xffffu << (threadIdx.x & 16);
-    const int cap = s.cap;
-    const bool live = id < st->n_sites;
-    const int k = lane16;
-    unsigned long long skipped = 0;
-    // ---- gradient totals (all lanes of the group take part in the shuffles)
-    DD acc[10];
+// The ten channel totals of site `id`, merged by its 16-lane group (shared by k_adam and
+// k_site_totals so both see bit-identical values).  Returns the site's claimed record count.
+__device__ __forceinline__ int merge_site(const RedTarget& grads, int id, bool live, int lane16, unsigned gmask,
+                                          int cap, DD (&acc)[10]) {
 #pragma unroll
     for (int ch = 0; ch < 10; ch++) acc[ch] = DD{0.0, 0.0};
     int claimed = 0;
@@ -1915,6 +1905,52 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
             dd_merge(acc[ch], o);
         }
     }
+    return claimed;
+}
+
+// Gradient values (Accum::value) of every site and channel into tot[ch * cap + id], plus a copy of the
+// logtau column in g0 — the inputs of tau_diffusion inside the fit.
+__global__ void __launch_bounds__(128) k_site_totals(RedTarget grads, const DevState* __restrict__ st, int cap,
+                                                     double* __restrict__ tot, double* __restrict__ g0) {
+    const int lane16 = threadIdx.x & 15;
+    const int id = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
+    const unsigned gmask = 0xffffu << (threadIdx.x & 16);
+    const bool live = id < st->n_sites;
+    DD acc[10];
+    merge_site(grads, id, live, lane16, gmask, cap, acc);
+    if (!live) return;
+    DD g = acc[0];
+#pragma unroll
+    for (int ch = 1; ch < 10; ch++)
+        if (lane16 == ch) g = acc[ch];
+    if (lane16 < 10) tot[static_cast<size_t>(lane16) * cap + id] = g.hi + g.lo;
+    if (lane16 == 2) g0[id] = g.hi + g.lo;
+}
+
+void launch_site_totals(const RedTarget& grads, const DevState* st, int cap, double* tot, double* g0,
+                        cudaStream_t stream) {
+    int grid = (cap + 7) / 8;
+    if (grid < 1) grid = 1;
+    k_site_totals<<<grid, 128, 0, stream>>>(grads, st, cap, tot, g0);
+    SAD_LAUNCHED();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarget grads, double* __restrict__ m,
+                                              double* __restrict__ v, AdamHyper hp,
+                                              const double2* __restrict__ bc_table, double2 bc_now, int zero_grads,
+                                              double scale, Q4<T>* pack, Q4<T>* gtab, int32_t* rcap_next,
+                                              const double* __restrict__ totals) {
+    const int lane16 = threadIdx.x & 15;
+    const int id = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
+    const unsigned gmask = 0xffffu << (threadIdx.x & 16);
+    const int cap = s.cap;
+    const bool live = id < st->n_sites;
+    const int k = lane16;
+    unsigned long long skipped = 0;
+    // ---- gradient totals (all lanes of the group take part in the shuffles)
+    DD acc[10];
+    const int claimed = merge_site(grads, id, live && !totals, lane16, gmask, cap, acc);
     DD g = acc[0];
 #pragma unroll
     for (int ch = 1; ch < 10; ch++)
@@ -1925,7 +1961,7 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
         if (k < 10) p = s.p[static_cast<size_t>(k) * cap + id];
         if (upd && k < 10) {
             const double2 bc = bc_table ? bc_table[st->t + 1] : bc_now;
-            double gv = g.hi + g.lo;
+            double gv = totals ? totals[static_cast<size_t>(k) * cap + id] : g.hi + g.lo;
             if (!isfinite(gv)) {
                 skipped++;
             } else {
@@ -1966,7 +2002,8 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
         }
         if (rcap_next && k == 0) {
             // next pass's record capacity: last count plus headroom (active sites only)
-            int want = s.active[id] ? claimed + (claimed >> 2) + 2 : 0;
+            const int cl = totals ? grads.cnt[id] : claimed;
+            int want = s.active[id] ? cl + (cl >> 2) + 2 : 0;
             rcap_next[id] = want < 4096 ? want : 4096;
         }
     } else {
@@ -2016,15 +2053,81 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
 
 void launch_adam(bool fp64, const SitesDev& s, DevState* st, const RedTarget& grads, double* m, double* v,
                  const AdamHyper& hp, const double2* bc_table, double2 bc_now, bool zero_grads, double scale,
-                 void* pack, void* gtab, int32_t* rcap_next, cudaStream_t stream) {
+                 void* pack, void* gtab, int32_t* rcap_next, cudaStream_t stream, const double* totals) {
     int grid = (s.cap + 7) / 8;  // 8 sites (16 lanes each) per 128-thread block
     if (grid < 1) grid = 1;
     if (fp64)
         k_adam<double><<<grid, 128, 0, stream>>>(s, st, grads, m, v, hp, bc_table, bc_now, zero_grads ? 1 : 0, scale,
-                                                 (Q4<double>*)pack, (Q4<double>*)gtab, rcap_next);
+                                                 (Q4<double>*)pack, (Q4<double>*)gtab, rcap_next, totals);
     else
         k_adam<float><<<grid, 128, 0, stream>>>(s, st, grads, m, v, hp, bc_table, bc_now, zero_grads ? 1 : 0, scale,
-                                                (Q4<float>*)pack, (Q4<float>*)gtab, rcap_next);
+                                                (Q4<float>*)pack, (Q4<float>*)gtab, rcap_next, totals);
+    SAD_LAUNCHED();
+}
+
+// ====================================================================== tau_diffusion (train.cpp:171-213)
+// Edge keys (owner << nb | id) for every pixel's active candidates (owner from render_id_map); the
+// sentinel (all ones in 2·nb bits) marks no edge and sorts last.  nb is chosen so that no valid id
+// equals the all-ones id field.
+__global__ void k_tau_edges(const uint32_t* __restrict__ ids, const uint32_t* __restrict__ owner,
+                            const uint8_t* __restrict__ active, FieldDims f, int nb, uint64_t* __restrict__ keys) {
+    const int px = blockIdx.x * blockDim.x + threadIdx.x;
+    const int py = blockIdx.y;
+    if (px >= f.width) return;
+    const size_t pix = static_cast<size_t>(py) * f.width + px;
+    const uint64_t sentinel = (nb >= 32) ? ~0ull : ((1ull << (2 * nb)) - 1);
+    const uint32_t o = owner[pix];
+    const uint32_t* lst = ids + static_cast<size_t>(f.k) * (static_cast<size_t>(py / f.cell) * f.gw + px / f.cell);
+    uint64_t* out = keys + pix * f.k;
+    bool end = o == kEmpty;
+    for (int i = 0; i < f.k; i++) {
+        const uint32_t id = lst[i];
+        end = end || id == kEmpty;
+        out[i] = (end || !active[id]) ? sentinel : ((static_cast<uint64_t>(o) << nb) | id);
+    }
+}
+
+void launch_tau_edges(const uint32_t* ids, const uint32_t* owner, const uint8_t* active, const FieldDims& f, int nb,
+                      uint64_t* keys, cudaStream_t stream) {
+    dim3 grid((f.width + 127) / 128, f.height);
+    k_tau_edges<<<grid, 128, 0, stream>>>(ids, owner, active, f, nb, keys);
+    SAD_LAUNCHED();
+}
+
+// One thread per owner segment of the sorted unique edges: the co-candidate sum runs sequentially in
+// ascending id order exactly as the reference loop, then the mixed value goes through a reset Accum
+// (Accum::add on {0, 0}, accum.hpp) into out[owner].
+__global__ void k_tau_mix(const uint64_t* __restrict__ uniq, const int* __restrict__ count, int nb,
+                          const double* __restrict__ g0, double lambda, double* __restrict__ out) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = *count;
+    if (e >= n) return;
+    const uint64_t sentinel = (nb >= 32) ? ~0ull : ((1ull << (2 * nb)) - 1);
+    const uint64_t key = uniq[e];
+    if (key == sentinel) return;
+    const uint64_t o = key >> nb;
+    if (e > 0 && (uniq[e - 1] >> nb) == o) return;
+    const uint64_t mask = (1ull << nb) - 1;
+    double sum = 0.0;
+    int cnt = 0;
+    for (int j = e; j < n; j++) {
+        const uint64_t kj = uniq[j];
+        if (kj == sentinel || (kj >> nb) != o) break;
+        sum += g0[kj & mask];
+        cnt++;
+    }
+    const double mixed = (1.0 - lambda) * g0[o] + lambda * (sum / cnt);
+    const double hi = 0.0 + mixed;
+    const double bb = hi - 0.0;
+    const double err = (0.0 - (hi - bb)) + (mixed - bb);
+    out[o] = hi + (0.0 + err);
+}
+
+void launch_tau_mix(const uint64_t* uniq, const int* count, int max_items, int nb, const double* g0, double lambda,
+                    double* out, cudaStream_t stream) {
+    int grid = (max_items + 255) / 256;
+    if (grid < 1) grid = 1;
+    k_tau_mix<<<grid, 256, 0, stream>>>(uniq, count, nb, g0, lambda, out);
     SAD_LAUNCHED();
 }
 

@@ -129,7 +129,14 @@ void launch_finalize(const RedTarget& red, int n_ch, const DevState* st, cudaStr
 // launch_plan_records turns them into offsets).
 void launch_adam(bool fp64, const SitesDev& s, DevState* st, const RedTarget& grads, double* m, double* v,
                  const AdamHyper& hp, const double2* bc_table, double2 bc_now, bool zero_grads, double scale,
-                 void* pack, void* gtab, int32_t* rcap_next, cudaStream_t stream);
+                 void* pack, void* gtab, int32_t* rcap_next, cudaStream_t stream, const double* totals = nullptr);
+// tau_diffusion pieces (train.cpp:171-213)
+void launch_site_totals(const RedTarget& grads, const DevState* st, int cap, double* tot, double* g0,
+                        cudaStream_t stream);
+void launch_tau_edges(const uint32_t* ids, const uint32_t* owner, const uint8_t* active, const FieldDims& f, int nb,
+                      uint64_t* keys, cudaStream_t stream);
+void launch_tau_mix(const uint64_t* uniq, const int* count, int max_items, int nb, const double* g0, double lambda,
+                    double* out, cudaStream_t stream);
 // Initial record plan: rcap = per_site for every slot (offsets follow from a scan).
 void launch_fill_i32(int32_t* p, int n, int32_t v, cudaStream_t stream);
 void launch_clamp(const SitesDev& s, const DevState* st, const AdamHyper& hp, cudaStream_t stream);

@@ -316,6 +316,17 @@ struct Workspace {
         DBuf<int32_t> nsel;
         DBuf<char> tmp;
     } ib;
+    // tau_diffusion scratch (train.cpp:171-213): W*H*k edge keys, owner map, per-site totals
+    struct TauBufs {
+        size_t ne = 0;
+        int nb = 0, tcap = 0;
+        DBuf<uint64_t> k0, k1;
+        DBuf<int32_t> count;
+        DBuf<uint32_t> owner;
+        DBuf<double> tot, g0;
+        DBuf<char> tmp;
+        size_t tmp_bytes = 0;
+    } tb;
 
     ~Workspace() {
         if (hst) cudaFreeHost(hst);
@@ -620,6 +631,53 @@ void passes_device(Workspace& ws, const std::vector<sad_pass_spec>& seq, int inj
 void build_tables(Workspace& ws, bool fp64, bool pack, bool gtab, bool rtab) {
     sadk::launch_tables(fp64, ws.sites(), ws.st.p, norm_scale(ws.fd.width, ws.fd.height), pack ? ws.pack.p : nullptr,
                         gtab ? ws.gtab.p : nullptr, rtab ? (fp64 ? ws.rtab_d.p : ws.rtab.p) : nullptr, ws.stream);
+}
+
+// ------------------------------------------------------------------ tau_diffusion (train.cpp:171-213)
+// Sizes are fixed per (W, H, k, capacity): W*H*k edge keys of 2*nb bits, with nb such that every
+// valid id is below the all-ones id field.  Everything stays on the stream (graph capturable).
+void ensure_tau(Workspace& ws) {
+    auto& tb = ws.tb;
+    const size_t np = static_cast<size_t>(ws.fd.width) * ws.fd.height;
+    const size_t ne = np * static_cast<size_t>(ws.fd.k);
+    int nb = 1;
+    while (nb < 32 && ((1ull << nb) - 1) < static_cast<unsigned long long>(ws.cap)) nb++;
+    if (tb.ne == ne && tb.nb == nb && tb.tcap == ws.cap) return;
+    if (ne > static_cast<size_t>(INT32_MAX)) fail(SAD_EINVAL, "tau_diffusion: too many edges");
+    tb.k0.ensure(ne);
+    tb.k1.ensure(ne);
+    tb.owner.ensure(np);
+    tb.count.ensure(1);
+    tb.tot.ensure(10 * static_cast<size_t>(ws.cap));
+    tb.g0.ensure(ws.cap);
+    size_t b1 = 0, b2 = 0;
+    ck(cub::DeviceRadixSort::SortKeys(nullptr, b1, tb.k0.p, tb.k1.p, static_cast<int>(ne), 0, 2 * nb, ws.stream),
+       "tau sort size");
+    ck(cub::DeviceSelect::Unique(nullptr, b2, tb.k1.p, tb.k0.p, tb.count.p, static_cast<int>(ne), ws.stream),
+       "tau unique size");
+    tb.tmp_bytes = std::max<size_t>(std::max(b1, b2), 16);
+    tb.tmp.ensure(tb.tmp_bytes);
+    tb.ne = ne;
+    tb.nb = nb;
+    tb.tcap = ws.cap;
+}
+
+// Owner map (render_id_map, double ScoreTable) -> edge keys -> radix sort -> unique -> per-owner mix
+// into out[] (non-owners keep what out already holds).  g0 is the logtau column before mixing.
+void tau_device(Workspace& ws, double lambda, double* out, const double* g0) {
+    auto& tb = ws.tb;
+    build_tables(ws, true, false, false, true);
+    sadk::launch_id_map(ws.ids[ws.cur].p, ws.rtab_d.p, ws.fd, norm_scale(ws.fd.width, ws.fd.height), tb.owner.p,
+                        ws.st.p, ws.stream);
+    sadk::launch_tau_edges(ws.ids[ws.cur].p, tb.owner.p, ws.active.p, ws.fd, tb.nb, tb.k0.p, ws.stream);
+    size_t bytes = tb.tmp_bytes;
+    ck(cub::DeviceRadixSort::SortKeys(tb.tmp.p, bytes, tb.k0.p, tb.k1.p, static_cast<int>(tb.ne), 0, 2 * tb.nb,
+                                      ws.stream),
+       "tau sort");
+    bytes = tb.tmp_bytes;
+    ck(cub::DeviceSelect::Unique(tb.tmp.p, bytes, tb.k1.p, tb.k0.p, tb.count.p, static_cast<int>(tb.ne), ws.stream),
+       "tau unique");
+    sadk::launch_tau_mix(tb.k0.p, tb.count.p, static_cast<int>(tb.ne), tb.nb, g0, lambda, out, ws.stream);
 }
 
 sadk::AdamHyper adam_hyper(const sad_train_config& c, int w, int h) {
@@ -1017,6 +1075,30 @@ sad_status sad_render_id_map(sad_ctx* c, const sad_sites_view* s, const sad_fiel
     });
 }
 
+sad_status sad_tau_diffusion(sad_ctx* c, const sad_sites_view* s, const sad_field_view* f, double lambda,
+                             double* grads) {
+    return guard([&] {
+        if (lambda == 0) return;
+        if (lambda < 0 || lambda > 1) fail(SAD_EINVAL, "tau_diffusion: lambda out of [0,1]");
+        if (!grads) fail(SAD_EINVAL, "tau_diffusion: null gradient buffer");
+        check_synced(s, f);
+        Workspace& ws = c->ws;
+        upload_sites(ws, s);
+        upload_field(ws, f);
+        ensure_tau(ws);
+        const size_t n = s->size;
+        std::vector<double> g0(n + 1), o(n + 1);
+        for (size_t i = 0; i < n; i++) g0[i] = grads[i * 11 + 2];
+        ck(cudaMemcpyAsync(ws.tb.g0.p, g0.data(), 8 * n, cudaMemcpyHostToDevice, ws.stream), "H2D g0");
+        ck(cudaMemcpyAsync(ws.tb.tot.p, g0.data(), 8 * n, cudaMemcpyHostToDevice, ws.stream), "H2D g0");
+        tau_device(ws, lambda, ws.tb.tot.p, ws.tb.g0.p);
+        ck(cudaMemcpyAsync(o.data(), ws.tb.tot.p, 8 * n, cudaMemcpyDeviceToHost, ws.stream), "D2H tau");
+        ck(cudaStreamSynchronize(ws.stream), "tau_diffusion");
+        check_err(ws, "render");
+        for (size_t i = 0; i < n; i++) grads[i * 11 + 2] = o[i];
+    });
+}
+
 // ====================================================================== grad
 static void backward_call(sad_ctx* c, const sad_sites_view* s, const sad_field_view* f, const double* img, int fp64,
                           int mode, double* grads, uint64_t* nonfinite, double* loss) {
@@ -1388,6 +1470,16 @@ static void fit_loop(sad_fit_run* r) {
     init.n_active = sta.n_active;
     ws.set_state(init);
     ws.ensure_adaptive(static_cast<size_t>(sadk::backward_blocks(fp64, ws.fd)));
+    // tau_diffusion (train.cpp:251-252): only lambda > 0 runs it, and lambda > 1 fails on iteration 1
+    const bool tau = c.tau_diffusion_lambda > 0;
+    if (tau && c.iters >= 1 && c.tau_diffusion_lambda > 1) fail(SAD_EINVAL, "tau_diffusion: lambda out of [0,1]");
+    if (tau) ensure_tau(ws);
+    const double* totals = tau ? ws.tb.tot.p : nullptr;
+    auto tau_step = [&] {
+        if (!tau) return;
+        sadk::launch_site_totals(ws.gred_adaptive(), ws.st.p, ws.cap, ws.tb.tot.p, ws.tb.g0.p, s);
+        tau_device(ws, c.tau_diffusion_lambda, ws.tb.tot.p + 2 * static_cast<size_t>(ws.cap), ws.tb.g0.p);
+    };
     sadk::launch_fill_i32(ws.rcap.p, ws.cap, 16, s);
     ws.plan_records();
     ck(cudaMemsetAsync(ws.gcnt.p, 0, sizeof(int32_t) * ws.cap, s), "memset gcnt");
@@ -1444,10 +1536,11 @@ static void fit_loop(sad_fit_run* r) {
         mark(1, [&] {
             sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt, ws.fd, scale_n, ws.gred_adaptive(),
                                   ws.loss_part.p, ws.st.p, s);
+            tau_step();
         });
         mark(2, [&] {
             sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.gred_adaptive(), ws.m.p, ws.v.p, hp, r->bc_table.p,
-                              make_double2(0, 0), true, scale_n, ws.pack.p, ws.gtab.p, ws.rcap.p, s);
+                              make_double2(0, 0), true, scale_n, ws.pack.p, ws.gtab.p, ws.rcap.p, s, totals);
             ws.plan_records();
         });
         mark(5, [&] {
@@ -1491,11 +1584,12 @@ static void fit_loop(sad_fit_run* r) {
         mark(1, [&] {
             sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt, ws.fd, scale_n, ws.gred_adaptive(),
                                   ws.loss_part.p, ws.st.p, s);
+            tau_step();
         });
         mark(3, [&] { stats_device(ws); });
         mark(2, [&] {
             sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.gred_adaptive(), ws.m.p, ws.v.p, hp, r->bc_table.p,
-                              make_double2(0, 0), true, scale_n, nullptr, nullptr, ws.rcap.p, s);
+                              make_double2(0, 0), true, scale_n, nullptr, nullptr, ws.rcap.p, s, totals);
             ws.plan_records();
         });
         mark(3, [&] {

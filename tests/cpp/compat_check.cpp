@@ -72,6 +72,14 @@ int main() {
         for (int c = 0; c < kChannels; c++) same = same && ga.grad(c, id) == gb.grad(c, id);
     expect(same, "backward_image fp32 loss and gradients bit-identical");
 
+    GradBuffer ta = ga, tb = ga;
+    tau_diffusion(st, a, 0.4, ta);
+    b200::tau_diffusion(gpu, st, b, 0.4, tb);
+    bool tsame = true;
+    for (uint32_t id = 0; id < st.size(); id++)
+        for (int c = 0; c < kChannels; c++) tsame = tsame && ta.grad(c, id) == tb.grad(c, id);
+    expect(tsame, "tau_diffusion bit-identical");
+
     SiteStore sa = st, sb = st;
     AdamState ma, mb;
     TrainConfig cfg;
