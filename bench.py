@@ -48,9 +48,11 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--ref-iters", type=int, default=30, help="iterations per reference-arm sample")
     p.add_argument("--cpu-iters", type=int, default=60, help="iterations of the cpu_baseline sample")
-    p.add_argument("--mode", default="config2", choices=["config2", "config3"],
-                   help="config3: 2048x2048 / 100k-site fit + 1e6 random point queries (own JSON line)")
+    p.add_argument("--mode", default="config2", choices=["config2", "config3", "config5"],
+                   help="config3: 2048x2048 / 100k-site fit + 1e6 random point queries; config5: 8192x8192 "
+                        "2-BPP fit on one GPU (each its own JSON line)")
     p.add_argument("--c3-iters", type=int, default=300)
+    p.add_argument("--c5-iters", type=int, default=100)
     p.add_argument("--no-roofline-2048", action="store_true")
     return p.parse_args()
 
@@ -292,6 +294,58 @@ def run_config3(a):
     print(json.dumps(out), flush=True)
 
 
+def run_config5(a):
+    """Config 5: one 8192x8192 image at 2 BPP (n0 = 1,677,722 sites) fitted on one GPU.  Two fits of
+    different length give the marginal cost per iteration (the densify/prune events of the default
+    schedule included, one every 20 iterations from t = 20); the whole short fit (device init, initial
+    full refresh, iterations, final refresh(Full, 16)) is reported too."""
+    import torch
+    import paper_2604_21984_b200 as sad
+    from paper_2604_21984_b200 import api
+    from paper_2604_21984_b200.synth import synthetic_image
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    lib = api.load_library()
+    ctx = C.c_void_p()
+    if lib.sad_ctx_create(C.c_int(0), C.c_void_p(stream.cuda_stream), C.byref(ctx)):
+        raise RuntimeError(lib.sad_last_error().decode())
+    G = api.Backend(lib, "sad_", "gpu", ctx=ctx)
+    W = H = 8192
+    img = synthetic_image(W, H, 5)
+    res = {}
+    for iters in (max(a.c5_iters // 2, 20), a.c5_iters):
+        cfg = sad.TrainConfig(iters=iters, target_bpp=2.0, fp64=False)
+        run = C.c_void_p()
+        cc = cfg.to_c()
+        G._call("fit_create", C.c_int(W), C.c_int(H), C.byref(cc), C.byref(run))
+        G._call("fit_set_target", run, img.ctypes.data_as(C.POINTER(C.c_double)))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        G._call("fit_run_init", run)
+        e1.record(stream)
+        e1.synchronize()
+        info = sad_fit_info(G, run)
+        res[iters] = (e0.elapsed_time(e1), info)
+        G.lib.sad_fit_destroy(run)
+    (i0, (t0, _)), (i1, (t1, info1)) = sorted(res.items())
+    per_iter = (t1 - t0) / (i1 - i0)
+    out = {"metric": "fit iterations/s", "mode": "config5", "value": 1e3 / per_iter, "unit": "iters/s",
+           "ms_per_iter_marginal": per_iter, "fit_ms": {str(k): v[0] for k, v in res.items()},
+           "final_site_slots": info1["n_sites"], "schedule_scale": info1["schedule_scale"], "n_gpus": 1,
+           "config": {"workload": f"config5: 8192x8192 synthetic (seed 5), target 2.0 BPP (n0 1,677,722), fp32; "
+                                  f"marginal per-iteration time between a {i0}- and a {i1}-iteration fit "
+                                  f"(default event schedule)"},
+           "reference_cpu_s_per_warm_pass_8_threads": 9.32, "reference_cpu_initial_refresh_s": 393.7}
+    print(json.dumps(out), flush=True)
+
+
+def sad_fit_info(G, run):
+    """A few scalars of a finished fit (sad_fit_info)."""
+    n, nh, sc = C.c_size_t(), C.c_int(), C.c_double()
+    G._call("fit_info", run, C.byref(n), C.byref(nh), C.byref(sc))
+    return {"n_sites": n.value, "n_history": nh.value, "schedule_scale": sc.value}
+
+
 def psnr(a, b):
     m = float(np.mean((a - b) ** 2))
     return 99.0 if m <= 0 else min(99.0, 10 * math.log10(1.0 / m))
@@ -496,6 +550,8 @@ def main():
         run_reference(a)
     elif a.mode == "config3":
         run_config3(a)
+    elif a.mode == "config5":
+        run_config5(a)
     else:
         run_b200(a)
 
