@@ -993,16 +993,20 @@ void launch_pixel_weights(const uint32_t* ids, const void* rtab_d, const FieldDi
 //      independent double-double chains — balanced work, high ILP); a bucket split across threads
 //      is finished by its first thread, which merges the carries of the following threads;
 //   5. each (site, tile) total is one record, claimed with one atomicAdd per site (RedTarget).
-template <typename CT, int NCH, int TPX, int KM>
-struct TileRed {
+template <typename CT, int NCH, int TPX, int KM, int NT = TPX>
+struct TileRed {  // TPX pixels, KM slots each, NT threads (TPX or 2 * TPX)
     static constexpr int E = TPX * KM;  // entries per tile
-    static constexpr int HT = E;        // hash slots (load factor <= 1)
-    static constexpr int ES = E + 1;    // padded row stride: channel rows land on distinct banks
-    static constexpr int PT = KM;       // sorted positions per thread in step 4
-    union {
-        CT c[NCH * ES];
-        DD carry[2 * TPX * NCH];  // step 4 chunk partials, written after every read of c[]
-    };
+    static constexpr int UMAX = E / 4;  // distinct sites per tile kept in shared memory (rest: DD atomics)
+    static constexpr int HT = E / 2;    // hash slots (load factor <= 1/2 up to UMAX sites)
+    static constexpr int ES = E + 16 / static_cast<int>(sizeof(CT));  // row stride: 16-byte aligned rows
+    static constexpr int PT = KM;       // sorted positions per chunk in step 4
+    static constexpr int CA = NCH / 2, CB = NCH - CA;  // step 4 runs in two channel halves
+    // step 4 writes the chunk partials of channels [0, CA) over rows [0, CA) and those of [CA, NCH)
+    // over rows [CA, NCH): each half's rows are dead once its sums are read
+    static_assert(CA * ES * sizeof(CT) >= 2 * TPX * CA * sizeof(DD), "chunk partials (half A) do not fit");
+    static_assert(CB * ES * sizeof(CT) >= 2 * TPX * CB * sizeof(DD), "chunk partials (half B) do not fit");
+    static_assert((CA * ES * sizeof(CT)) % 16 == 0, "half B rows must stay 16-byte aligned");
+    alignas(16) CT c[NCH * ES];
     union {
         uint32_t key[E];  // site id per entry (steps 1-2)
         struct {
@@ -1012,15 +1016,15 @@ struct TileRed {
     };
     union {
         uint32_t hkey[HT];  // hash keys (step 2)
-        uint32_t cnt[E];    // bucket sizes (step 3)
+        uint32_t cnt[UMAX];  // bucket sizes (step 3)
     };
     uint16_t local_of_entry[E];
     uint16_t local_of_slot[HT];
-    uint32_t start[E];
-    uint32_t site_of_local[E];
-    uint32_t slot_of_local[E];
+    uint32_t start[UMAX];
+    uint32_t site_of_local[UMAX];
+    uint32_t slot_of_local[UMAX];
     int n_local;
-    DD warp_part[TPX / 32];
+    DD warp_part[NT / 32];
 };
 
 template <typename CT>
@@ -1046,38 +1050,44 @@ __device__ __forceinline__ void write_record(const RedTarget& red, uint32_t site
     }
 }
 
-template <typename CT, int NCH, int TPX, int KM>
-__device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, const RedTarget& red) {
-    using R = TileRed<CT, NCH, TPX, KM>;
+template <typename CT, int NCH, int TPX, int KM, int NT>
+__device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM, NT>& sm, const RedTarget& red) {
+    using R = TileRed<CT, NCH, TPX, KM, NT>;
+    static_assert(NT == TPX || NT == 2 * TPX, "thread count");
+    constexpr bool TWO = NT < 2 * TPX;  // each thread sums chunks tid and tid + NT (else only tid)
     const int tid = threadIdx.x;
 #if SAD_EXPERIMENT == 3
     long long _t0 = clock64();
 #endif
     // 2. hash insert (site ids are < 2^31; table keys start as kEmpty)
-    for (int e = tid; e < R::E; e += TPX) {
+    for (int e = tid; e < R::E; e += NT) {
         uint32_t key = sm.key[e];
         if (key == kEmpty) continue;
         uint32_t h = (key * 2654435761u) & (R::HT - 1);
-        while (true) {
+        uint16_t got = 0xffffu;  // stays 0xffff if the table is full: the entry goes to the atomic path
+        for (int probe = 0; probe < R::HT; probe++) {
             uint32_t prev = atomicCAS(&sm.hkey[h], kEmpty, key);
-            if (prev == kEmpty || prev == key) break;
+            if (prev == kEmpty || prev == key) {
+                got = static_cast<uint16_t>(h);
+                break;
+            }
             h = (h + 1) & (R::HT - 1);
         }
-        sm.local_of_entry[e] = static_cast<uint16_t>(h);
+        sm.local_of_entry[e] = got;
     }
     __syncthreads();
     PH(1);
-    for (int h = tid; h < R::HT; h += TPX) {
+    for (int h = tid; h < R::HT; h += NT) {
         uint32_t key = sm.hkey[h];
         if (key != kEmpty) {
             int loc = atomicAdd(&sm.n_local, 1);
-            sm.local_of_slot[h] = static_cast<uint16_t>(loc);
-            sm.site_of_local[loc] = key;
+            sm.local_of_slot[h] = static_cast<uint16_t>(loc < R::UMAX ? loc : 0xffff);
+            if (loc < R::UMAX) sm.site_of_local[loc] = key;
         }
     }
     __syncthreads();
-    const int U = sm.n_local;
-    for (int u = tid; u < U; u += TPX) {
+    const int U = sm.n_local < R::UMAX ? sm.n_local : R::UMAX;
+    for (int u = tid; u < U; u += NT) {
         sm.cnt[u] = 0;  // aliases hkey: safe after the barrier
         const uint32_t site = sm.site_of_local[u];
         uint32_t slot = static_cast<uint32_t>(atomicAdd(red.cnt + site, 1));
@@ -1095,11 +1105,20 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, const
     __syncthreads();
     PH(2);
     // 3. bucket counts (entries with key == kEmpty get bucket 0xffff)
-    for (int e = tid; e < R::E; e += TPX) {
+    for (int e = tid; e < R::E; e += NT) {
         uint16_t loc = 0xffffu;
-        if (sm.key[e] != kEmpty) {
-            loc = sm.local_of_slot[sm.local_of_entry[e]];
-            atomicAdd(&sm.cnt[loc], 1u);
+        const uint32_t key = sm.key[e];
+        if (key != kEmpty) {
+            const uint16_t hs = sm.local_of_entry[e];
+            loc = hs == 0xffffu ? static_cast<uint16_t>(0xffffu) : sm.local_of_slot[hs];
+            if (loc != 0xffffu) {
+                atomicAdd(&sm.cnt[loc], 1u);
+            } else {  // more than UMAX distinct sites in this tile: exact DD merge straight into `over`
+#pragma unroll
+                for (int ch = 0; ch < NCH; ch++)
+                    dd_atomic_merge(red.over + static_cast<size_t>(ch) * red.cap + key,
+                                    DD{static_cast<double>(sm.c[ch * R::ES + e]), 0.0});
+            }
         }
         sm.local_of_entry[e] = loc;
     }
@@ -1124,16 +1143,16 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, const
     }
     __syncthreads();  // key[] is dead from here: its storage becomes order/posloc
     PH(3);
-    for (int e = tid; e < R::E; e += TPX) {
+    for (int e = tid; e < R::E; e += NT) {
         int loc = sm.local_of_entry[e];
         if (loc == 0xffff) continue;
         int pos = static_cast<int>(atomicAdd(&sm.start[loc], 1u));
         sm.srt.order[pos] = static_cast<uint16_t>(e);
     }
     __syncthreads();
-    for (int u = tid; u < U; u += TPX) sm.start[u] -= sm.cnt[u];  // cursor back to the bucket start
+    for (int u = tid; u < U; u += NT) sm.start[u] -= sm.cnt[u];  // cursor back to the bucket start
     PH(4);
-    // 4. buckets split into chunks of PT sorted entries; thread t sums chunks t and t + TPX for all
+    // 4. buckets split into chunks of PT sorted entries; thread t sums chunks t and t + NT for all
     //    channels (convergent fixed-trip loops, NCH independent double-double chains)
     const int U2 = U;
     uint16_t* chunk_base = sm.local_of_slot;  // dead after counting: chunk index of each bucket's first chunk
@@ -1156,17 +1175,18 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, const
         if (tid == 0) n_chunks = carry;
     }
     __syncthreads();
-    for (int u = tid; u < U2; u += TPX) {
+    for (int u = tid; u < U2; u += NT) {
         int c0 = chunk_base[u], nc = static_cast<int>((sm.cnt[u] + R::PT - 1) / R::PT);
         for (int c = c0; c < c0 + nc; c++) chunk_bucket[c] = static_cast<uint16_t>(u);
     }
     __syncthreads();
     const int NC = n_chunks;
     PH(5);
-    DD acc0[NCH], acc1[NCH];
-    auto sum_chunk = [&](int c, DD* acc) {
+    // Two channel halves: each thread holds its two chunks' partials for CB channels at a time (half
+    // the registers of a single pass), and each half's partials overwrite that half's dead rows.
+    auto sum_chunk = [&](int c, int ch0, int nch, DD* acc) {
 #pragma unroll
-        for (int ch = 0; ch < NCH; ch++) acc[ch] = DD{0.0, 0.0};
+        for (int ch = 0; ch < R::CB; ch++) acc[ch] = DD{0.0, 0.0};
         const int u = chunk_bucket[c];
         const int off = (c - chunk_base[u]) * R::PT;
         const int n = static_cast<int>(sm.cnt[u]) - off;
@@ -1176,40 +1196,53 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, const
             if (j < n) {
                 const int e = sm.srt.order[b + j];
 #pragma unroll
-                for (int ch = 0; ch < NCH; ch++) dd_add(acc[ch], static_cast<double>(sm.c[ch * R::ES + e]));
+                for (int ch = 0; ch < R::CB; ch++)
+                    if (ch < nch) dd_add(acc[ch], static_cast<double>(sm.c[(ch0 + ch) * R::ES + e]));
             }
         }
     };
-    if (tid < NC) sum_chunk(tid, acc0);
-    if (tid + TPX < NC) sum_chunk(tid + TPX, acc1);
-    // chunks beyond 2*TPX (more than ~TPX distinct sites in one tile): merged straight into `over`
-    for (int c = tid + 2 * TPX; c < NC; c += TPX) {
-        DD tmp[NCH];
-        sum_chunk(c, tmp);
-        const uint32_t site = sm.site_of_local[chunk_bucket[c]];
+    DD* const carry_a = reinterpret_cast<DD*>(sm.c);
+    DD* const carry_b = reinterpret_cast<DD*>(sm.c + R::CA * R::ES);
+    auto half = [&](int ch0, int nch, DD* carry) {
+        DD acc0[R::CB], acc1[R::CB];
+        if (tid < NC) sum_chunk(tid, ch0, nch, acc0);
+        if (TWO && tid + NT < NC) sum_chunk(tid + NT, ch0, nch, acc1);
+        // chunks beyond 2*TPX (more than ~TPX distinct sites in one tile): merged straight into `over`
+        for (int c = tid + 2 * TPX; c < NC; c += NT) {
+            DD tmp[R::CB];
+            sum_chunk(c, ch0, nch, tmp);
+            const uint32_t site = sm.site_of_local[chunk_bucket[c]];
 #pragma unroll
-        for (int ch = 0; ch < NCH; ch++) dd_atomic_merge(red.over + static_cast<size_t>(ch) * red.cap + site, tmp[ch]);
-    }
-    __syncthreads();  // every read of c[] is done: its storage becomes the chunk partials
+            for (int ch = 0; ch < R::CB; ch++)
+                if (ch < nch) dd_atomic_merge(red.over + static_cast<size_t>(ch0 + ch) * red.cap + site, tmp[ch]);
+        }
+        __syncthreads();  // every read of this half's rows is done: they become its chunk partials
+        if (tid < NC) {
+#pragma unroll
+            for (int ch = 0; ch < R::CB; ch++)
+                if (ch < nch) carry[tid * nch + ch] = acc0[ch];
+        }
+        if (TWO && tid + NT < NC) {
+#pragma unroll
+            for (int ch = 0; ch < R::CB; ch++)
+                if (ch < nch) carry[(tid + NT) * nch + ch] = acc1[ch];
+        }
+    };
+    half(0, R::CA, carry_a);
     PH(6);
-    if (tid < NC) {
-#pragma unroll
-        for (int ch = 0; ch < NCH; ch++) sm.carry[tid * NCH + ch] = acc0[ch];
-    }
-    if (tid + TPX < NC) {
-#pragma unroll
-        for (int ch = 0; ch < NCH; ch++) sm.carry[(tid + TPX) * NCH + ch] = acc1[ch];
-    }
+    half(R::CA, R::CB, carry_b);
     __syncthreads();
     PH(7);
     // 5. per (site, channel): merge the site's chunks and store the record (or CAS on slot overflow)
     const int NCK = NC < 2 * TPX ? NC : 2 * TPX;
-    for (int item = tid; item < U2 * NCH; item += TPX) {
+    for (int item = tid; item < U2 * NCH; item += NT) {
         const int u = item / NCH, ch = item - u * NCH;
         const int c0 = chunk_base[u];
         const int c1 = c0 + static_cast<int>((sm.cnt[u] + R::PT - 1) / R::PT);
         DD t{0.0, 0.0};
-        for (int c = c0; c < c1 && c < NCK; c++) dd_merge(t, sm.carry[c * NCH + ch]);
+        const DD* cp = ch < R::CA ? carry_a + ch : carry_b + (ch - R::CA);
+        const int cs = ch < R::CA ? R::CA : R::CB;
+        for (int c = c0; c < c1 && c < NCK; c++) dd_merge(t, cp[c * cs]);
         const uint32_t site = sm.site_of_local[u];
         const uint32_t slot = sm.slot_of_local[u];
         if (slot & 0x80000000u && slot != 0xffffffffu) {
@@ -1229,10 +1262,10 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM>& sm, const
     PH(8);
 }
 
-template <typename CT, int NCH, int TPX, int KM>
-__device__ __forceinline__ void tile_init(TileRed<CT, NCH, TPX, KM>& sm) {
-    using R = TileRed<CT, NCH, TPX, KM>;
-    for (int h = threadIdx.x; h < R::HT; h += TPX) sm.hkey[h] = kEmpty;
+template <typename CT, int NCH, int TPX, int KM, int NT>
+__device__ __forceinline__ void tile_init(TileRed<CT, NCH, TPX, KM, NT>& sm) {
+    using R = TileRed<CT, NCH, TPX, KM, NT>;
+    for (int h = threadIdx.x; h < R::HT; h += NT) sm.hkey[h] = kEmpty;
     if (threadIdx.x == 0) sm.n_local = 0;
 }
 
@@ -1478,6 +1511,255 @@ __global__ void __launch_bounds__(BwdTile<T>::TW * BwdTile<T>::TH)
     if (threadIdx.x == 0 && nf) atomicAdd(reinterpret_cast<unsigned long long*>(&st->nonfinite), nf);
 }
 
+// fp32 variant with two lanes per pixel (256 threads per 16x8 tile): lane h of a pixel takes list
+// slots [h*KM/2, (h+1)*KM/2).  Everything order-sensitive keeps the reference's sequential order: the
+// sentinel of lane 0 ends lane 1's list, the running max is combined in slot order, and the float
+// sums of the softmax denominator and of the blended colour are continued by lane 1 from lane 0's
+// partial (one shuffle each way), so every rounding equals the one-thread loop of k_backward.  The
+// shuffles run for every lane (pairs whose pixel is outside or empty compute unused values), and the
+// tile reduction then runs on all 256 threads.
+#ifndef SAD_BWD2_MINB
+#define SAD_BWD2_MINB 4
+#endif
+template <int KM, int MODE>
+__global__ void __launch_bounds__(256, SAD_BWD2_MINB) k_backward2(const uint32_t* __restrict__ ids, const Q4<float>* __restrict__ gtab,
+                                                   const float* __restrict__ tgt, FieldDims f, float s, float inv_hw2,
+                                                   RedTarget red, double2* __restrict__ loss_part, DevState* st) {
+    using T = float;
+    constexpr int TW = 16, TH = 8, TPX = TW * TH, NT = 2 * TPX, H = KM / 2;
+    constexpr int NCH = MODE == 1 ? 11 : 10;
+    constexpr unsigned FULL = 0xffffffffu;
+    using Red = TileRed<T, NCH, TPX, KM, NT>;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    Red& sm = *reinterpret_cast<Red*>(smraw);
+    tile_init(sm);
+
+    const int tid = threadIdx.x;
+    const int pix = tid >> 1, half = tid & 1;
+    const int px = blockIdx.x * TW + (pix % TW);
+    const int py = blockIdx.y * TH + (pix / TW);
+    const bool inside = px < f.width && py < f.height;
+    constexpr T kTiny = T(1e-12);
+
+    uint32_t cid[H];
+    T dxs[H], dys[H], ud[H], vd[H], nrm[H], lg[H];
+    bool ok[H];
+    bool any = false;
+    T best = T(0);
+    unsigned long long nonfinite = 0;
+    DD loss{0.0, 0.0};
+    {
+        uint32_t idv[H];
+        const uint32_t* lst = ids + static_cast<size_t>(f.k) * (static_cast<size_t>(py / f.cell) * f.gw + px / f.cell);
+        bool has_empty = false;
+#pragma unroll
+        for (int j = 0; j < H; j++) {
+            const int i = half * H + j;
+            idv[j] = (inside && i < f.k) ? lst[i] : kEmpty;
+            has_empty = has_empty || idv[j] == kEmpty;
+        }
+        const bool partner_empty = __shfl_xor_sync(FULL, has_empty, 1);
+        const T fx = static_cast<T>(px), fy = static_cast<T>(py);
+        bool stop = !inside || (half == 1 && partner_empty);
+#pragma unroll
+        for (int j = 0; j < H; j++) {
+            const uint32_t id = idv[j];
+            stop = stop || id == kEmpty;
+            cid[j] = id;
+            ok[j] = false;
+            dxs[j] = dys[j] = ud[j] = vd[j] = nrm[j] = lg[j] = T(0);
+            if (!stop) {
+                const Q4<T> a = gtab[3 * id], b = gtab[3 * id + 1];
+                const T act = gtab[3 * id + 2].w;
+                T dx = fx - a.x, dy = fy - a.y;
+                T pa = b.z * dx + b.w * dy;
+                T pb = b.z * dy - b.w * dx;
+                T q = b.x * pa * pa + b.y * pb * pb;
+                if (q < T(0)) q = T(0);
+                T m = tsqrt(q);
+                T l = -a.z * (m * s - a.w * s);
+                ok[j] = act != T(0) && c_finite(l);
+                dxs[j] = dx;
+                dys[j] = dy;
+                ud[j] = pa;
+                vd[j] = pb;
+                nrm[j] = m;
+                lg[j] = l;
+                if (ok[j] && (!any || l > best)) best = l;
+                any = any || ok[j];
+            }
+        }
+    }
+    // running max in slot order: lane 1's candidates come after lane 0's
+    const bool pany = __shfl_xor_sync(FULL, any, 1);
+    const T pbest = __shfl_xor_sync(FULL, best, 1);
+    const bool a0 = half == 0 ? any : pany, a1 = half == 0 ? pany : any;
+    const T b0 = half == 0 ? best : pbest, b1 = half == 0 ? pbest : best;
+    best = a0 ? ((a1 && b1 > b0) ? b1 : b0) : b1;
+    const bool any_all = a0 || a1;
+    if (inside && !any_all && half == 0) atomicOr(&st->err, 1);
+
+    // softmax denominator: lane 0 sums its slots from 0, lane 1 continues from lane 0's sum
+    T w[H];
+    T wpart = T(0);
+#pragma unroll
+    for (int j = 0; j < H; j++) {
+        w[j] = T(0);
+        if (ok[j]) w[j] = texp(lg[j] - best);
+    }
+    if (half == 0) {
+#pragma unroll
+        for (int j = 0; j < H; j++)
+            if (ok[j]) wpart += w[j];
+    }
+    const T from0 = __shfl_xor_sync(FULL, wpart, 1);
+    if (half == 1) {
+        wpart = from0;
+#pragma unroll
+        for (int j = 0; j < H; j++)
+            if (ok[j]) wpart += w[j];
+    }
+    const T from1 = __shfl_xor_sync(FULL, wpart, 1);
+    const T wsum = half == 0 ? from1 : wpart;
+    const T invw = trcp(wsum);
+    // blended colour, same hand-over
+    Q4<T> col[H];
+    T c0 = T(0), c1 = T(0), c2 = T(0);
+#pragma unroll
+    for (int j = 0; j < H; j++) {
+        col[j] = Q4<T>{T(0), T(0), T(0), T(0)};
+        if (ok[j]) {
+            w[j] *= invw;
+            col[j] = gtab[3 * cid[j] + 2];
+        }
+    }
+    if (half == 0) {
+#pragma unroll
+        for (int j = 0; j < H; j++)
+            if (ok[j]) {
+                c0 += w[j] * col[j].x;
+                c1 += w[j] * col[j].y;
+                c2 += w[j] * col[j].z;
+            }
+    }
+    {
+        const T r0 = __shfl_xor_sync(FULL, c0, 1), r1 = __shfl_xor_sync(FULL, c1, 1), r2 = __shfl_xor_sync(FULL, c2, 1);
+        if (half == 1) {
+            c0 = r0;
+            c1 = r1;
+            c2 = r2;
+#pragma unroll
+            for (int j = 0; j < H; j++)
+                if (ok[j]) {
+                    c0 += w[j] * col[j].x;
+                    c1 += w[j] * col[j].y;
+                    c2 += w[j] * col[j].z;
+                }
+        }
+        const T s0 = __shfl_xor_sync(FULL, c0, 1), s1 = __shfl_xor_sync(FULL, c1, 1), s2 = __shfl_xor_sync(FULL, c2, 1);
+        if (half == 0) {
+            c0 = s0;
+            c1 = s1;
+            c2 = s2;
+        }
+    }
+    const T ch0 = c0, ch1 = c1, ch2 = c2;
+    if (any_all) {
+        T g0, g1, g2, t0 = T(0), t1 = T(0), t2 = T(0), pl = T(0);
+        const T* tp = tgt + 3 * (static_cast<size_t>(py) * f.width + px);
+        if (MODE != 2) {
+            t0 = tp[0];
+            t1 = tp[1];
+            t2 = tp[2];
+            T e0 = ch0 - t0, e1 = ch1 - t1, e2 = ch2 - t2;
+            pl = e0 * e0 + e1 * e1 + e2 * e2;
+            if (half == 0) {
+                double plv = static_cast<double>(pl);
+                if (!c_finite(pl)) {
+                    nonfinite++;
+                    plv = 0;
+                }
+                dd_add(loss, plv);
+            }
+            g0 = inv_hw2 * e0;
+            g1 = inv_hw2 * e1;
+            g2 = inv_hw2 * e2;
+        } else {
+            g0 = tp[0];
+            g1 = tp[1];
+            g2 = tp[2];
+        }
+#pragma unroll
+        for (int j = 0; j < H; j++) {
+            const int e = (half * H + j) * TPX + pix;
+            if (!ok[j] || w[j] == T(0)) {  // zero weight: +-0 in every channel (see k_backward)
+                sm.key[e] = kEmpty;
+                continue;
+            }
+            const uint32_t id = cid[j];
+            const Q4<T> a = gtab[3 * id], b = gtab[3 * id + 1];
+            const Q4<T> c = col[j];
+            T dc0 = c.x - ch0, dc1 = c.y - ch1, dc2 = c.z - ch2;
+            T A = w[j] * (g0 * dc0 + g1 * dc1 + g2 * dc2);
+            T ts = a.z * s;
+            T v[11];
+            v[4] = w[j] * g0;
+            v[5] = w[j] * g1;
+            v[6] = w[j] * g2;
+            v[2] = A * lg[j];
+            v[3] = A * ts;
+            if (nrm[j] > kTiny) {
+                T inv_n = trcp(nrm[j]);
+                T eau = b.x * ud[j];
+                T iav = b.y * vd[j];
+                T coef = A * ts * inv_n;
+                v[0] = coef * (eau * b.z - iav * b.w);
+                v[1] = coef * (eau * b.w + iav * b.z);
+                v[7] = -coef * (eau * dxs[j] + iav * dys[j]);
+                v[8] = -coef * (eau * dys[j] - iav * dxs[j]);
+                v[9] = -A * ts * T(0.5) * inv_n * (eau * ud[j] - iav * vd[j]);
+            } else {
+                v[0] = v[1] = v[7] = v[8] = v[9] = T(0);
+            }
+            if (MODE == 1) {
+                if (w[j] >= T(1) - T(1e-6)) {
+                    v[10] = static_cast<T>(1e6);
+                } else {
+                    T inv_rest = trcp(T(1) - w[j]);
+                    T r0 = (ch0 - w[j] * c.x) * inv_rest - t0;
+                    T r1 = (ch1 - w[j] * c.y) * inv_rest - t1;
+                    T r2 = (ch2 - w[j] * c.z) * inv_rest - t2;
+                    v[10] = r0 * r0 + r1 * r1 + r2 * r2 - pl;
+                }
+            }
+            sm.key[e] = id;
+            bool bad = false;
+#pragma unroll
+            for (int t = 0; t < NCH; t++) bad |= !c_finite(v[t]);
+            if (bad) {
+#pragma unroll
+                for (int t = 0; t < NCH; t++)
+                    if (!c_finite(v[t])) {
+                        v[t] = T(0);
+                        nonfinite++;
+                    }
+            }
+#pragma unroll
+            for (int t = 0; t < NCH; t++) sm.c[t * Red::ES + e] = v[t];
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < H; j++) sm.key[(half * H + j) * TPX + pix] = kEmpty;
+    }
+    __syncthreads();
+    tile_reduce(sm, red);
+    __syncthreads();
+    if (MODE != 2) block_dd_store<NT>(loss, sm.warp_part, loss_part + blockIdx.y * gridDim.x + blockIdx.x);
+    __syncthreads();
+    unsigned long long nf = block_sum_u64<NT>(nonfinite, reinterpret_cast<unsigned long long*>(sm.warp_part));
+    if (threadIdx.x == 0 && nf) atomicAdd(reinterpret_cast<unsigned long long*>(&st->nonfinite), nf);
+}
+
 int backward_blocks(bool fp64, const FieldDims& f) {
     int tw = fp64 ? BwdTile<double>::TW : BwdTile<float>::TW, th = fp64 ? BwdTile<double>::TH : BwdTile<float>::TH;
     return ((f.width + tw - 1) / tw) * ((f.height + th - 1) / th);
@@ -1489,19 +1771,33 @@ static void backward_attr() {
     constexpr int NCH = MODE == 1 ? 11 : 10;
     cudaFuncSetAttribute(k_backward<T, KM, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(TileRed<T, NCH, TW * TH, KM>));
+    if (sizeof(T) == 4)
+        cudaFuncSetAttribute(k_backward2<KM, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(TileRed<float, NCH, 128, KM, 256>));
 }
+
+// SAD_BWD1=1 selects the one-lane-per-pixel fp32 kernel (A/B and regression checks)
+static const bool g_bwd1 = getenv("SAD_BWD1") != nullptr;
 
 template <typename T, int KM, int MODE>
 static void backward_t(const uint32_t* ids, const void* gtab, const void* tgt, const FieldDims& f, double scale,
                        const RedTarget& red, double2* loss_part, DevState* st, cudaStream_t stream) {
     constexpr int TW = BwdTile<T>::TW, TH = BwdTile<T>::TH;
     constexpr int NCH = MODE == 1 ? 11 : 10;
-    size_t smem = sizeof(TileRed<T, NCH, TW * TH, KM>);
-    auto kern = k_backward<T, KM, MODE>;
     dim3 grid((f.width + TW - 1) / TW, (f.height + TH - 1) / TH);
     T inv_hw2 = static_cast<T>(2.0 / (static_cast<double>(f.width) * f.height));
-    kern<<<grid, TW * TH, smem, stream>>>(ids, (const Q4<T>*)gtab, (const T*)tgt, f, static_cast<T>(scale), inv_hw2,
-                                          red, loss_part, st);
+    if (sizeof(T) == 4 && !g_bwd1) {
+        static_assert(BwdTile<float>::TW == 16 && BwdTile<float>::TH == 8, "k_backward2 tile");
+        size_t smem = sizeof(TileRed<float, NCH, 128, KM, 256>);
+        k_backward2<KM, MODE><<<grid, 256, smem, stream>>>(ids, (const Q4<float>*)gtab, (const float*)tgt, f,
+                                                           static_cast<float>(scale), static_cast<float>(inv_hw2), red,
+                                                           loss_part, st);
+    } else {
+        size_t smem = sizeof(TileRed<T, NCH, TW * TH, KM>);
+        auto kern = k_backward<T, KM, MODE>;
+        kern<<<grid, TW * TH, smem, stream>>>(ids, (const Q4<T>*)gtab, (const T*)tgt, f, static_cast<T>(scale),
+                                              inv_hw2, red, loss_part, st);
+    }
     SAD_LAUNCHED();
 }
 

@@ -24,7 +24,7 @@ out = C.c_double()
 G._call("fit_bench", run, C.c_int(1), C.c_int(20), C.byref(out))
 G.lib.sad_exp_phase(buf, 0)
 names = ["phase1(fwd+bwd math)", "hash insert", "compact+slot claim", "count+scan", "scatter", "chunk scan+fill",
-         "chunk dd sums", "carry store", "merge+records"]
+         "dd sums half A (+store)", "dd sums half B (+store)", "merge+records"]
 blocks = 21 * 3072  # 1 warm-up + 20 timed launches
 tot = sum(buf[i] for i in range(9))
 for i, nm in enumerate(names):
