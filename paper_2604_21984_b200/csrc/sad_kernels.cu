@@ -2142,10 +2142,28 @@ __device__ __forceinline__ void clamp_site(double* p, int cap, int id, const Ada
 // k < 10 then applies the Adam update of parameter k and its clamp; dir is renormalised from both
 // lanes' values exchanged by shuffle; lanes 0-4 rebuild the site's candidate snapshot and backward
 // table.  With the adaptive record layout, lane 0 also plans the next pass's record capacity.
+#ifndef SAD_ADAM_TWO
+#define SAD_ADAM_TWO 0
+#endif
 // The ten channel totals of site `id`, merged by its 16-lane group (shared by k_adam and
-// k_site_totals so both see bit-identical values).  Returns the site's claimed record count.
+// k_site_totals so both see bit-identical values).  Lanes first sum disjoint record subsets for all
+// channels, then a reduce-scatter (10 -> 5 -> 4 -> 2 -> 1 channels per lane; exact double-double
+// merges, so the grouping does not matter) leaves lane l with the total of channel
+// lane_channel(l) = 5 * bit3(l) + (l & 7) when (l & 7) < 5, else none (-1).  Returns the claimed
+// record count.
+__device__ __forceinline__ int lane_channel(int lane16) {
+    const int loc = lane16 & 7;
+    return loc < 5 ? 5 * ((lane16 >> 3) & 1) + loc : -1;
+}
+__device__ __forceinline__ int channel_lane(int ch) { return ch < 5 ? ch : ch + 3; }
+
+__device__ __forceinline__ DD shfl_xor_dd(unsigned mask, const DD& v, int d) {
+    return DD{__shfl_xor_sync(mask, v.hi, d, 16), __shfl_xor_sync(mask, v.lo, d, 16)};
+}
+
 __device__ __forceinline__ int merge_site(const RedTarget& grads, int id, bool live, int lane16, unsigned gmask,
-                                          int cap, DD (&acc)[10]) {
+                                          int cap, DD& mine) {
+    DD acc[10];
 #pragma unroll
     for (int ch = 0; ch < 10; ch++) acc[ch] = DD{0.0, 0.0};
     int claimed = 0;
@@ -2161,6 +2179,7 @@ __device__ __forceinline__ int merge_site(const RedTarget& grads, int id, bool l
         }
         if (grads.roff && static_cast<long long>(base) + n > grads.psize)
             n = static_cast<int>(grads.psize - base > 0 ? grads.psize - base : 0);
+#if SAD_ADAM_TWO
         for (int j = lane16; j < n; j += 32) {  // two records in flight per lane
             const bool two = j + 16 < n;
             const double2* r0 = grads.part + (static_cast<size_t>(base) + j) * grads.stride;
@@ -2177,6 +2196,16 @@ __device__ __forceinline__ int merge_site(const RedTarget& grads, int id, bool l
                 if (two) dd_merge(acc[ch], DD{b[ch].x, b[ch].y});
             }
         }
+#else
+        for (int j = lane16; j < n; j += 16) {  // one record per lane and step: most sites have <= 16
+            const double2* r0 = grads.part + (static_cast<size_t>(base) + j) * grads.stride;
+            double2 a[10];
+#pragma unroll
+            for (int ch = 0; ch < 10; ch++) a[ch] = r0[ch];
+#pragma unroll
+            for (int ch = 0; ch < 10; ch++) dd_merge(acc[ch], DD{a[ch].x, a[ch].y});
+        }
+#endif
         if (lane16 == 0)
             for (int r = grads.head[id]; r >= 0; r = grads.onext[r]) {
 #pragma unroll
@@ -2193,14 +2222,35 @@ __device__ __forceinline__ int merge_site(const RedTarget& grads, int id, bool l
                 if (ch == lane16) dd_merge(acc[ch], mine);
         }
     }
+    const bool b3 = lane16 & 8, b2 = lane16 & 4, b1 = lane16 & 2, b0 = lane16 & 1;
+    const DD z{0.0, 0.0};
+    DD a5[5];  // channel 5*b3 + j
 #pragma unroll
-    for (int d = 8; d >= 1; d >>= 1) {
-#pragma unroll
-        for (int ch = 0; ch < 10; ch++) {
-            DD o{__shfl_xor_sync(gmask, acc[ch].hi, d, 16), __shfl_xor_sync(gmask, acc[ch].lo, d, 16)};
-            dd_merge(acc[ch], o);
-        }
+    for (int j = 0; j < 5; j++) {
+        DD keep = b3 ? acc[5 + j] : acc[j];
+        const DD o = shfl_xor_dd(gmask, b3 ? acc[j] : acc[5 + j], 8);
+        dd_merge(keep, o);
+        a5[j] = keep;
     }
+    DD a4[4];  // channel 5*b3 + 4*b2 + j (local index 4*b2 + j < 5)
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        const DD hi_part = j + 4 < 5 ? a5[j + 4 < 5 ? j + 4 : 0] : z;
+        DD keep = b2 ? hi_part : a5[j];
+        const DD o = shfl_xor_dd(gmask, b2 ? a5[j] : hi_part, 4);
+        dd_merge(keep, o);
+        a4[j] = keep;
+    }
+    DD a2[2];  // channel 5*b3 + 4*b2 + 2*b1 + j
+#pragma unroll
+    for (int j = 0; j < 2; j++) {
+        DD keep = b1 ? a4[2 + j] : a4[j];
+        const DD o = shfl_xor_dd(gmask, b1 ? a4[j] : a4[2 + j], 2);
+        dd_merge(keep, o);
+        a2[j] = keep;
+    }
+    mine = b0 ? a2[1] : a2[0];
+    dd_merge(mine, shfl_xor_dd(gmask, b0 ? a2[0] : a2[1], 1));
     return claimed;
 }
 
@@ -2212,15 +2262,12 @@ __global__ void __launch_bounds__(128) k_site_totals(RedTarget grads, const DevS
     const int id = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
     const unsigned gmask = 0xffffu << (threadIdx.x & 16);
     const bool live = id < st->n_sites;
-    DD acc[10];
-    merge_site(grads, id, live, lane16, gmask, cap, acc);
-    if (!live) return;
-    DD g = acc[0];
-#pragma unroll
-    for (int ch = 1; ch < 10; ch++)
-        if (lane16 == ch) g = acc[ch];
-    if (lane16 < 10) tot[static_cast<size_t>(lane16) * cap + id] = g.hi + g.lo;
-    if (lane16 == 2) g0[id] = g.hi + g.lo;
+    DD g;
+    merge_site(grads, id, live, lane16, gmask, cap, g);
+    const int ch = lane_channel(lane16);
+    if (!live || ch < 0) return;
+    tot[static_cast<size_t>(ch) * cap + id] = g.hi + g.lo;
+    if (ch == 2) g0[id] = g.hi + g.lo;
 }
 
 void launch_site_totals(const RedTarget& grads, const DevState* st, int cap, double* tot, double* g0,
@@ -2245,17 +2292,15 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
     const int k = lane16;
     unsigned long long skipped = 0;
     // ---- gradient totals (all lanes of the group take part in the shuffles)
-    DD acc[10];
-    const int claimed = merge_site(grads, id, live && !totals, lane16, gmask, cap, acc);
-    DD g = acc[0];
-#pragma unroll
-    for (int ch = 1; ch < 10; ch++)
-        if (k == ch) g = acc[ch];
+    DD g;
+    const int claimed = merge_site(grads, id, live && !totals, lane16, gmask, cap, g);
+    const int kc = lane_channel(lane16);  // the parameter this lane updates (-1: none)
     if (live) {
         const bool upd = s.active[id] && !s.frozen[id];
         double p = 0.0;
-        if (k < 10) p = s.p[static_cast<size_t>(k) * cap + id];
-        if (upd && k < 10) {
+        if (kc >= 0) p = s.p[static_cast<size_t>(kc) * cap + id];
+        if (upd && kc >= 0) {
+            const int k = kc;
             const double2 bc = bc_table ? bc_table[st->t + 1] : bc_now;
             double gv = totals ? totals[static_cast<size_t>(k) * cap + id] : g.hi + g.lo;
             if (!isfinite(gv)) {
@@ -2283,14 +2328,14 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
             default: break;
             }
         }
-        const double nx = __shfl_sync(gmask, p, (threadIdx.x & 16) + 7);
-        const double ny = __shfl_sync(gmask, p, (threadIdx.x & 16) + 8);
-        if (upd && (k == 7 || k == 8)) {
+        const double nx = __shfl_sync(gmask, p, (threadIdx.x & 16) + channel_lane(7));
+        const double ny = __shfl_sync(gmask, p, (threadIdx.x & 16) + channel_lane(8));
+        if (upd && (kc == 7 || kc == 8)) {
             double norm = __dsqrt_rn(nx * nx + ny * ny);
-            if (!(norm > 1e-12) || !isfinite(norm)) p = k == 7 ? 1.0 : 0.0;
-            else p = (k == 7 ? nx : ny) / norm;
+            if (!(norm > 1e-12) || !isfinite(norm)) p = kc == 7 ? 1.0 : 0.0;
+            else p = (kc == 7 ? nx : ny) / norm;
         }
-        if (upd && k < 10) s.p[static_cast<size_t>(k) * cap + id] = p;
+        if (upd && kc >= 0) s.p[static_cast<size_t>(kc) * cap + id] = p;
         if (zero_grads) {
             if (k < 11) grads.over[static_cast<size_t>(k) * cap + id] = make_double2(0.0, 0.0);
             if (k == 0) grads.cnt[id] = 0;
@@ -2303,8 +2348,8 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
             rcap_next[id] = want < 4096 ? want : 4096;
         }
     } else {
-        __shfl_sync(gmask, 0.0, (threadIdx.x & 16) + 7);
-        __shfl_sync(gmask, 0.0, (threadIdx.x & 16) + 8);
+        __shfl_sync(gmask, 0.0, (threadIdx.x & 16) + channel_lane(7));
+        __shfl_sync(gmask, 0.0, (threadIdx.x & 16) + channel_lane(8));
         if (rcap_next && k == 0 && id < cap) rcap_next[id] = 0;
     }
     if (skipped) atomicAdd(reinterpret_cast<unsigned long long*>(&st->skipped), skipped);
