@@ -485,8 +485,14 @@ def run_b200(a):
                        "share_of_fit": counts[nm] * t / fit_ms}
     dom = max((k for k in kernels if counts[k] > 0), key=lambda k: kernels[k]["share_of_fit"])
     ach = kernels[dom]["GBps"]
-    roofline = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
-                "kernel": dom, "algorithmic_bytes_per_launch": bytes_per[dom],
+    # DRAM traffic per launch of the dominant kernel from the committed ncu --set full capture
+    traffic, traffic_src = None, None
+    tf = os.path.join(ROOT, "profiles", "r1b_ncu_fwd_bwd_traffic.json")
+    if dom == "fwd_bwd" and os.path.exists(tf):
+        tj = json.load(open(tf))
+        traffic, traffic_src = tj["traffic_bytes"], f"{os.path.relpath(tf, ROOT)} ({tj['capture']})"
+    roofline = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
+                "traffic_source": traffic_src, "kernel": dom, "algorithmic_bytes_per_launch": bytes_per[dom],
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6650 GB/s",
                 "note": "768x512 working set is L2-resident; HBM fraction is judged at 2048^2 (see DESIGN.md)"}
 

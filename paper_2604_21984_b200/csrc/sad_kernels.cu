@@ -2694,10 +2694,13 @@ void launch_flag_active(const SitesDev& s, const DevState* st, uint8_t* flags, c
 }
 
 // ====================================================================== loop bookkeeping
-__global__ void k_advance(DevState* st, int passes, int adam_steps, double2* loss_hist, int32_t* active_hist,
-                          const double2* __restrict__ loss_part, int n_part, int32_t* otop) {
+// End-of-iteration bookkeeping: loss = exact (double-double) sum of the per-tile partials, history
+// rows, pass index and Adam step.  1024 threads and two shuffle trees keep the serial part short.
+__global__ void __launch_bounds__(1024) k_advance(DevState* st, int passes, int adam_steps, double2* loss_hist,
+                                                  int32_t* active_hist, const double2* __restrict__ loss_part,
+                                                  int n_part, int32_t* otop) {
     if (otop && threadIdx.x == 0) *otop = 0;
-    __shared__ DD parts[8];
+    __shared__ DD parts[32];
     DD acc{0.0, 0.0};
     if (loss_hist)
         for (int i = threadIdx.x; i < n_part; i += blockDim.x) dd_merge(acc, DD{loss_part[i].x, loss_part[i].y});
@@ -2708,8 +2711,14 @@ __global__ void k_advance(DevState* st, int passes, int adam_steps, double2* los
     }
     if ((threadIdx.x & 31) == 0) parts[threadIdx.x >> 5] = acc;
     __syncthreads();
+    if (threadIdx.x >= 32) return;
+    acc = threadIdx.x < static_cast<int>(blockDim.x >> 5) ? parts[threadIdx.x] : DD{0.0, 0.0};
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+        DD o{__shfl_down_sync(0xffffffffu, acc.hi, d), __shfl_down_sync(0xffffffffu, acc.lo, d)};
+        dd_merge(acc, o);
+    }
     if (threadIdx.x != 0) return;
-    for (int w = 1; w < 8; w++) dd_merge(acc, parts[w]);
     if (loss_hist) {
         loss_hist[st->iter] = make_double2(acc.hi, acc.lo);
         if (active_hist) active_hist[st->iter] = st->n_active;
@@ -2721,7 +2730,7 @@ __global__ void k_advance(DevState* st, int passes, int adam_steps, double2* los
 
 void launch_advance(DevState* st, int passes, int adam_steps, double2* loss_hist, int32_t* active_hist,
                     const double2* loss_part, int n_part, int32_t* otop, cudaStream_t stream) {
-    k_advance<<<1, 256, 0, stream>>>(st, passes, adam_steps, loss_hist, active_hist, loss_part, n_part, otop);
+    k_advance<<<1, 1024, 0, stream>>>(st, passes, adam_steps, loss_hist, active_hist, loss_part, n_part, otop);
     SAD_LAUNCHED();
 }
 
