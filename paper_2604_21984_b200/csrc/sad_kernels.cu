@@ -653,6 +653,7 @@ __global__ void __launch_bounds__(256, SAD_PROP_MINB) k_prop8_stream(const uint3
 // Queue variant (warm Axial passes): most neighbour entries are already in the own list, so they are
 // filtered by id first and only the rest (plus the injected ids) go through a per-thread shared
 // queue that is scored convergently, with the next entry's table rows prefetched.
+template <bool BOX>
 __global__ void __launch_bounds__(256, SAD_PROP_MINB) k_prop8_queue(const uint32_t* __restrict__ prev, uint32_t* __restrict__ next,
                                                      const Q4<float>* __restrict__ pack,
                                                      const uint32_t* __restrict__ act, const DevState* __restrict__ st,
@@ -667,62 +668,67 @@ __global__ void __launch_bounds__(256, SAD_PROP_MINB) k_prop8_queue(const uint32
     const float cy = static_cast<float>(gy * static_cast<double>(f.cell) + (f.cell - 1) * 0.5);
     KeyList8 L;
     bool ok = own_keys(prev, pack, f, gx, gy, cx, cy, s, L);
-    int nq = 0;
-#pragma unroll 1
-    for (int pr = 0; pr < 2; pr++) {
-        uint4 u[4];
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const int o = 1 + 2 * pr + h;
-            const int nx = gx + off_x(o) * step, ny = gy + off_y(o) * step;
-            if (nx >= 0 && ny >= 0 && nx < f.gw && ny < f.gh) {
-                const uint4* lst = reinterpret_cast<const uint4*>(prev + 8 * (static_cast<size_t>(ny) * f.gw + nx));
-                u[2 * h] = __ldg(lst);
-                u[2 * h + 1] = __ldg(lst + 1);
-            } else {
-                u[2 * h] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
-                u[2 * h + 1] = u[2 * h];
-            }
-        }
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const uint32_t v[8] = {u[2 * h].x, u[2 * h].y, u[2 * h].z, u[2 * h].w,
-                                   u[2 * h + 1].x, u[2 * h + 1].y, u[2 * h + 1].z, u[2 * h + 1].w};
-            bool end = false;
-#pragma unroll
-            for (int i = 0; i < 8; i++) {
-                end = end || v[i] == kEmpty;
-                if (!end && !L.contains(v[i])) q[nq++ * 256 + tid] = v[i];
-            }
-        }
-    }
     const int n_act = st->n_active;
-    if (inject > 0 && n_act > 0) {
-        uint32_t rs = seeded_state(seed, st->pass_index + pass_offset,
-                                   static_cast<uint32_t>(gy) * static_cast<uint32_t>(f.gw) + static_cast<uint32_t>(gx));
-        for (int j = 0; j < inject; j++) q[nq++ * 256 + tid] = __ldg(act + xs_next(rs) % static_cast<uint32_t>(n_act));
-    }
-    if (nq > 0) {
-        uint32_t c = q[tid];
-        Q4<float> b = pack[2 * c + 1], a = pack[2 * c];
+    constexpr int NG = BOX ? 2 : 1;  // groups of four neighbour lists (Box3: axial, then diagonal)
 #pragma unroll 1
-        for (int j = 0; j < nq; j++) {
-            const uint32_t cn = j + 1 < nq ? q[(j + 1) * 256 + tid] : c;
-            const Q4<float> bn = pack[2 * cn + 1], an = pack[2 * cn];
-            if (b.w != 0.0f) {
-                const float l = score_logit(a, b, cx, cy, s);
-                ok &= (l == l);
-                L.consider(c, list_key(l, c));
+    for (int g = 0; g < NG; g++) {
+        int nq = 0;
+#pragma unroll 1
+        for (int pr = 0; pr < 2; pr++) {
+            uint4 u[4];
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int o = 1 + 4 * g + 2 * pr + h;
+                const int nx = gx + off_x(o) * step, ny = gy + off_y(o) * step;
+                if (nx >= 0 && ny >= 0 && nx < f.gw && ny < f.gh) {
+                    const uint4* lst = reinterpret_cast<const uint4*>(prev + 8 * (static_cast<size_t>(ny) * f.gw + nx));
+                    u[2 * h] = __ldg(lst);
+                    u[2 * h + 1] = __ldg(lst + 1);
+                } else {
+                    u[2 * h] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+                    u[2 * h + 1] = u[2 * h];
+                }
             }
-            c = cn;
-            a = an;
-            b = bn;
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const uint32_t v[8] = {u[2 * h].x, u[2 * h].y, u[2 * h].z, u[2 * h].w,
+                                       u[2 * h + 1].x, u[2 * h + 1].y, u[2 * h + 1].z, u[2 * h + 1].w};
+                bool end = false;
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    end = end || v[i] == kEmpty;
+                    if (!end && !L.contains(v[i])) q[nq++ * 256 + tid] = v[i];
+                }
+            }
+        }
+        if (g == NG - 1 && inject > 0 && n_act > 0) {
+            uint32_t rs = seeded_state(seed, st->pass_index + pass_offset,
+                                       static_cast<uint32_t>(gy) * static_cast<uint32_t>(f.gw) + static_cast<uint32_t>(gx));
+            for (int j = 0; j < inject; j++)
+                q[nq++ * 256 + tid] = __ldg(act + xs_next(rs) % static_cast<uint32_t>(n_act));
+        }
+        if (nq > 0) {
+            uint32_t c = q[tid];
+            Q4<float> b = pack[2 * c + 1], a = pack[2 * c];
+#pragma unroll 1
+            for (int j = 0; j < nq; j++) {
+                const uint32_t cn = j + 1 < nq ? q[(j + 1) * 256 + tid] : c;
+                const Q4<float> bn = pack[2 * cn + 1], an = pack[2 * cn];
+                if (b.w != 0.0f) {
+                    const float l = score_logit(a, b, cx, cy, s);
+                    ok &= (l == l);
+                    L.consider(c, list_key(l, c));
+                }
+                c = cn;
+                a = an;
+                b = bn;
+            }
         }
     }
     if (ok)
         store_keys(next, f, gx, gy, L);
     else
-        propagate_cell_slow<false>(prev, next, pack, act, st, f, gx, gy, step, inject, seed, pass_offset, s);
+        propagate_cell_slow<BOX>(prev, next, pack, act, st, f, gx, gy, step, inject, seed, pass_offset, s);
 }
 
 template <typename T, int KM, bool EXACT>
@@ -742,6 +748,9 @@ static void propagate_t(const uint32_t* prev, uint32_t* next, const void* pack, 
     SAD_LAUNCHED();
 }
 
+// largest Box3 step that uses the dedup-first queue kernel (SAD_BOX_QUEUE_STEP overrides, for A/B)
+static const int g_box_queue_max_step = getenv("SAD_BOX_QUEUE_STEP") ? atoi(getenv("SAD_BOX_QUEUE_STEP")) : 4;
+
 void launch_propagate(bool fp64, const uint32_t* prev, uint32_t* next, const void* pack, const uint32_t* act,
                       const DevState* st, const FieldDims& f, uint32_t step, int box, int inject, uint64_t seed,
                       uint32_t pass_offset, double scale, cudaStream_t stream) {
@@ -749,12 +758,17 @@ void launch_propagate(bool fp64, const uint32_t* prev, uint32_t* next, const voi
         dim3 block(32, 8);
         dim3 grid((f.gw + 31) / 32, (f.gh + 7) / 8);
         const float sf = static_cast<float>(scale);
-        if (box)
+        // Box3 floods at small steps see mostly ids already in the cell's list: dedup first (queue);
+        // at larger steps most entries are new sites: score first (stream)
+        if (box && (inject > 4 || step > g_box_queue_max_step))
             k_prop8_stream<true><<<grid, block, 0, stream>>>(prev, next, (const Q4<float>*)pack, act, st, f, (int)step,
                                                              inject, seed, pass_offset, sf);
+        else if (box)
+            k_prop8_queue<true><<<grid, block, 0, stream>>>(prev, next, (const Q4<float>*)pack, act, st, f, (int)step,
+                                                            inject, seed, pass_offset, sf);
         else if (inject <= 4)
-            k_prop8_queue<<<grid, block, 0, stream>>>(prev, next, (const Q4<float>*)pack, act, st, f, (int)step, inject,
-                                                      seed, pass_offset, sf);
+            k_prop8_queue<false><<<grid, block, 0, stream>>>(prev, next, (const Q4<float>*)pack, act, st, f, (int)step,
+                                                             inject, seed, pass_offset, sf);
         else
             k_prop8_stream<false><<<grid, block, 0, stream>>>(prev, next, (const Q4<float>*)pack, act, st, f,
                                                               (int)step, inject, seed, pass_offset, sf);
@@ -1945,23 +1959,31 @@ __device__ __forceinline__ DD red_total(const RedTarget& red, int id, int ch, in
     return acc;
 }
 
+// One 16-lane group per site, lane ch < NCH merges channel ch (records, overflow list, CAS totals);
+// the counters are reset after the whole group has read them.
 template <int NCH>
-__global__ void k_finalize(RedTarget red, const DevState* __restrict__ st) {
-    const int id = blockIdx.x * blockDim.x + threadIdx.x;
-    if (id >= st->n_sites) return;
-    int n = red.cnt[id];
+__global__ void __launch_bounds__(128) k_finalize(RedTarget red, const DevState* __restrict__ st) {
+    static_assert(NCH <= 16, "channels per group");
+    const int lane16 = threadIdx.x & 15;
+    const int id = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
+    const unsigned gmask = 0xffffu << (threadIdx.x & 16);
+    const bool live = id < st->n_sites;
+    int n = live ? red.cnt[id] : 0;
     if (n > red.maxt) n = red.maxt;
-#pragma unroll 1
-    for (int ch = 0; ch < NCH; ch++) {
-        DD t = red_total(red, id, ch, n);
-        red.over[static_cast<size_t>(ch) * red.cap + id] = make_double2(t.hi, t.lo);
+    if (live && lane16 < NCH) {
+        const DD t = red_total(red, id, lane16, n);
+        red.over[static_cast<size_t>(lane16) * red.cap + id] = make_double2(t.hi, t.lo);
     }
-    red.cnt[id] = 0;
-    red.head[id] = -1;
+    __syncwarp(gmask);
+    if (live && lane16 == 0) {
+        red.cnt[id] = 0;
+        red.head[id] = -1;
+    }
 }
 
 void launch_finalize(const RedTarget& red, int n_ch, const DevState* st, cudaStream_t stream) {
-    int grid = (red.cap + 127) / 128;
+    int grid = (red.cap + 7) / 8;  // 8 sites (16 lanes each) per block
+    if (grid < 1) grid = 1;
     if (n_ch == 8) k_finalize<8><<<grid, 128, 0, stream>>>(red, st);
     else if (n_ch == 10) k_finalize<10><<<grid, 128, 0, stream>>>(red, st);
     else k_finalize<11><<<grid, 128, 0, stream>>>(red, st);

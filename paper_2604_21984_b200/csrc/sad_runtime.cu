@@ -1740,6 +1740,11 @@ sad_status sad_fit_bench(sad_fit_run* r, int which, int reps, double* ms_per_lau
                 break;
             case 2: sadk::launch_render(false, ws.ids[ws.cur].p, ws.rtab.p, ws.fd, sn, ws.px_f.p, ws.st.p, s); break;
             case 3: passes_device(ws, {sad_pass_spec{16, 1}}, c.inject, c.seed, fp64, 0); break;
+            case 8: {  // one Box3 pass at SAD_BENCH_STEP (default 1) on the fitted field
+                const char* e = getenv("SAD_BENCH_STEP");
+                passes_device(ws, {sad_pass_spec{static_cast<uint32_t>(e ? atoi(e) : 1), 1}}, c.inject, c.seed, fp64, 0);
+                break;
+            }
             case 4:
                 // one fwd+bwd then Adam, as in the fit (records present); the fwd+bwd share is timed apart
                 sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt, ws.fd, sn, ws.gred_adaptive(),
