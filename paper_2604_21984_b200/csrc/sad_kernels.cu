@@ -2305,7 +2305,9 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
                                               double* __restrict__ v, AdamHyper hp,
                                               const double2* __restrict__ bc_table, double2 bc_now, int zero_grads,
                                               double scale, Q4<T>* pack, Q4<T>* gtab, int32_t* rcap_next,
-                                              const double* __restrict__ totals) {
+                                              const double* __restrict__ totals, int32_t* roff_next,
+                                              int32_t* pool_top) {
+    __shared__ int32_t s_want[8], s_base;
     const int lane16 = threadIdx.x & 15;
     const int id = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
     const unsigned gmask = 0xffffu << (threadIdx.x & 16);
@@ -2367,12 +2369,31 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
             // next pass's record capacity: last count plus headroom (active sites only)
             const int cl = totals ? grads.cnt[id] : claimed;
             int want = s.active[id] ? cl + (cl >> 2) + 2 : 0;
-            rcap_next[id] = want < 4096 ? want : 4096;
+            want = want < 4096 ? want : 4096;
+            rcap_next[id] = want;
+            if (roff_next) s_want[threadIdx.x >> 4] = want;
         }
     } else {
         __shfl_sync(gmask, 0.0, (threadIdx.x & 16) + channel_lane(7));
         __shfl_sync(gmask, 0.0, (threadIdx.x & 16) + channel_lane(8));
         if (rcap_next && k == 0 && id < cap) rcap_next[id] = 0;
+        if (rcap_next && k == 0) s_want[threadIdx.x >> 4] = 0;
+    }
+    // record slices for the next pass: a block-wide prefix of the 8 capacities and one pool claim per
+    // block (the layout is order dependent, the merged totals are not)
+    if (rcap_next && roff_next) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int tot = 0;
+            for (int g = 0; g < 8; g++) {
+                const int w = s_want[g];
+                s_want[g] = tot;
+                tot += w;
+            }
+            s_base = atomicAdd(pool_top, tot);
+        }
+        __syncthreads();
+        if (k == 0 && id < cap) roff_next[id] = s_base + s_want[threadIdx.x >> 4];
     }
     if (skipped) atomicAdd(reinterpret_cast<unsigned long long*>(&st->skipped), skipped);
     __syncwarp();
@@ -2416,15 +2437,18 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
 
 void launch_adam(bool fp64, const SitesDev& s, DevState* st, const RedTarget& grads, double* m, double* v,
                  const AdamHyper& hp, const double2* bc_table, double2 bc_now, bool zero_grads, double scale,
-                 void* pack, void* gtab, int32_t* rcap_next, cudaStream_t stream, const double* totals) {
+                 void* pack, void* gtab, int32_t* rcap_next, cudaStream_t stream, const double* totals,
+                 int32_t* roff_next, int32_t* pool_top) {
     int grid = (s.cap + 7) / 8;  // 8 sites (16 lanes each) per 128-thread block
     if (grid < 1) grid = 1;
     if (fp64)
         k_adam<double><<<grid, 128, 0, stream>>>(s, st, grads, m, v, hp, bc_table, bc_now, zero_grads ? 1 : 0, scale,
-                                                 (Q4<double>*)pack, (Q4<double>*)gtab, rcap_next, totals);
+                                                 (Q4<double>*)pack, (Q4<double>*)gtab, rcap_next, totals, roff_next,
+                                                 pool_top);
     else
         k_adam<float><<<grid, 128, 0, stream>>>(s, st, grads, m, v, hp, bc_table, bc_now, zero_grads ? 1 : 0, scale,
-                                                (Q4<float>*)pack, (Q4<float>*)gtab, rcap_next, totals);
+                                                (Q4<float>*)pack, (Q4<float>*)gtab, rcap_next, totals, roff_next,
+                                                pool_top);
     SAD_LAUNCHED();
 }
 
@@ -2721,7 +2745,10 @@ void launch_flag_active(const SitesDev& s, const DevState* st, uint8_t* flags, c
 __global__ void __launch_bounds__(1024) k_advance(DevState* st, int passes, int adam_steps, double2* loss_hist,
                                                   int32_t* active_hist, const double2* __restrict__ loss_part,
                                                   int n_part, int32_t* otop) {
-    if (otop && threadIdx.x == 0) *otop = 0;
+    if (otop && threadIdx.x == 0) {
+        otop[0] = 0;  // gradient overflow pool
+        otop[2] = 0;  // gradient record pool (claimed by the next k_adam)
+    }
     __shared__ DD parts[32];
     DD acc{0.0, 0.0};
     if (loss_hist)

@@ -378,8 +378,8 @@ struct Workspace {
         snext.ensure(want);
         gopart.ensure(want * 11);
         sopart.ensure(want * 8);
-        otops.ensure(2);
-        ck(cudaMemsetAsync(otops.p, 0, 2 * sizeof(int32_t), stream), "memset otop");
+        otops.ensure(3);  // [0] gradient overflow top, [1] stats overflow top, [2] gradient record pool top
+        ck(cudaMemsetAsync(otops.p, 0, 3 * sizeof(int32_t), stream), "memset otop");
         ocap = static_cast<int>(want);
     }
     void zero_red(bool g) {
@@ -1540,8 +1540,8 @@ static void fit_loop(sad_fit_run* r) {
         });
         mark(2, [&] {
             sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.gred_adaptive(), ws.m.p, ws.v.p, hp, r->bc_table.p,
-                              make_double2(0, 0), true, scale_n, ws.pack.p, ws.gtab.p, ws.rcap.p, s, totals);
-            ws.plan_records();
+                              make_double2(0, 0), true, scale_n, ws.pack.p, ws.gtab.p, ws.rcap.p, s, totals,
+                              ws.roff.p, ws.otops.p + 2);
         });
         mark(5, [&] {
             sadk::launch_advance(ws.st.p, np, 1, r->loss_hist.p, r->active_hist.p, ws.loss_part.p, nbw, ws.otops.p, s);
@@ -1589,8 +1589,8 @@ static void fit_loop(sad_fit_run* r) {
         mark(3, [&] { stats_device(ws); });
         mark(2, [&] {
             sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.gred_adaptive(), ws.m.p, ws.v.p, hp, r->bc_table.p,
-                              make_double2(0, 0), true, scale_n, nullptr, nullptr, ws.rcap.p, s, totals);
-            ws.plan_records();
+                              make_double2(0, 0), true, scale_n, nullptr, nullptr, ws.rcap.p, s, totals,
+                              ws.roff.p, ws.otops.p + 2);
         });
         mark(3, [&] {
             if (ev_p) prune_device(ws, c.prune_pct * sched);
