@@ -1101,20 +1101,24 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM, NT>& sm, c
     }
     __syncthreads();
     const int U = sm.n_local < R::UMAX ? sm.n_local : R::UMAX;
-    for (int u = tid; u < U; u += NT) {
-        sm.cnt[u] = 0;  // aliases hkey: safe after the barrier
-        const uint32_t site = sm.site_of_local[u];
-        uint32_t slot = static_cast<uint32_t>(atomicAdd(red.cnt + site, 1));
-        const uint32_t scap = red.roff ? static_cast<uint32_t>(red.rcap[site]) : static_cast<uint32_t>(red.maxt);
-        if (red.roff && slot < scap && red.roff[site] + slot >= red.psize) slot = scap;  // pool bound
-        if (slot < scap) {
-            if (red.roff) slot = 0x80000000u | slot;  // adaptive-layout record
-        } else {  // overflow record from the pool, linked per site
-            int r = atomicAdd(red.otop, 1);
-            if (r < red.ocap) red.onext[r] = atomicExch(red.head + site, r);
-            slot = r < red.ocap ? static_cast<uint32_t>(red.maxt + r) : 0xffffffffu;
+    // Record slot claims: one global atomicAdd per (site, tile), issued here and consumed only before
+    // step 5, so their latency overlaps steps 3-4.  Step 5 then stores without global loads.
+    constexpr int RU = (R::UMAX + NT - 1) / NT;
+    uint32_t c_raw[RU], c_cap[RU];
+    int32_t c_off[RU];
+#pragma unroll
+    for (int r = 0; r < RU; r++) {
+        const int u = tid + r * NT;
+        c_raw[r] = 0;
+        c_cap[r] = 0;
+        c_off[r] = 0;
+        if (u < U) {
+            sm.cnt[u] = 0;  // aliases hkey: safe after the barrier
+            const uint32_t site = sm.site_of_local[u];
+            c_raw[r] = static_cast<uint32_t>(atomicAdd(red.cnt + site, 1));
+            c_cap[r] = red.roff ? static_cast<uint32_t>(red.rcap[site]) : static_cast<uint32_t>(red.maxt);
+            c_off[r] = red.roff ? red.roff[site] : 0;
         }
-        sm.slot_of_local[u] = slot;
     }
     __syncthreads();
     PH(2);
@@ -1245,6 +1249,27 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM, NT>& sm, c
     half(0, R::CA, carry_a);
     PH(6);
     half(R::CA, R::CB, carry_b);
+    // record code per local site: bits 31-30 = 00 record index into part, 01 overflow record into opart,
+    // 11 pool exhausted (exact DD CAS into over)
+#pragma unroll
+    for (int r = 0; r < RU; r++) {
+        const int u = tid + r * NT;
+        if (u < U) {
+            const uint32_t site = sm.site_of_local[u];
+            uint32_t slot = c_raw[r];
+            const uint32_t scap = c_cap[r];
+            if (red.roff && slot < scap && static_cast<long long>(c_off[r]) + slot >= red.psize) slot = scap;  // pool bound
+            uint32_t code;
+            if (slot < scap) {
+                code = red.roff ? static_cast<uint32_t>(c_off[r]) + slot : site * static_cast<uint32_t>(red.maxt) + slot;
+            } else {  // overflow record from the pool, linked per site
+                const int ro = atomicAdd(red.otop, 1);
+                if (ro < red.ocap) red.onext[ro] = atomicExch(red.head + site, ro);
+                code = ro < red.ocap ? (0x40000000u | static_cast<uint32_t>(ro)) : 0xc0000000u;
+            }
+            sm.slot_of_local[u] = code;
+        }
+    }
     __syncthreads();
     PH(7);
     // 5. per (site, channel): merge the site's chunks and store the record (or CAS on slot overflow)
@@ -1258,14 +1283,11 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM, NT>& sm, c
         const int cs = ch < R::CA ? R::CA : R::CB;
         for (int c = c0; c < c1 && c < NCK; c++) dd_merge(t, cp[c * cs]);
         const uint32_t site = sm.site_of_local[u];
-        const uint32_t slot = sm.slot_of_local[u];
-        if (slot & 0x80000000u && slot != 0xffffffffu) {
-            red.part[(static_cast<size_t>(red.roff[site]) + (slot & 0x7fffffffu)) * red.stride + ch] =
-                make_double2(t.hi, t.lo);
-        } else if (slot < static_cast<uint32_t>(red.maxt) && !red.roff) {
-            red.part[(static_cast<size_t>(site) * red.maxt + slot) * red.stride + ch] = make_double2(t.hi, t.lo);
-        } else if (slot != 0xffffffffu) {
-            red.opart[static_cast<size_t>(slot - red.maxt) * red.stride + ch] = make_double2(t.hi, t.lo);
+        const uint32_t code = sm.slot_of_local[u];
+        if ((code >> 30) == 0u) {
+            red.part[static_cast<size_t>(code) * red.stride + ch] = make_double2(t.hi, t.lo);
+        } else if ((code >> 30) == 1u) {
+            red.opart[static_cast<size_t>(code & 0x3fffffffu) * red.stride + ch] = make_double2(t.hi, t.lo);
         } else {  // pool exhausted
 #if SAD_EXPERIMENT == 3
             if (ch == 0) atomicAdd(&g_phase_clk[15], 1ull);
@@ -1546,6 +1568,9 @@ __global__ void __launch_bounds__(256, SAD_BWD2_MINB) k_backward2(const uint32_t
     using Red = TileRed<T, NCH, TPX, KM, NT>;
     extern __shared__ __align__(16) unsigned char smraw[];
     Red& sm = *reinterpret_cast<Red*>(smraw);
+#if SAD_EXPERIMENT == 3
+    long long _t0 = clock64();
+#endif
     tile_init(sm);
 
     const int tid = threadIdx.x;
@@ -1766,6 +1791,7 @@ __global__ void __launch_bounds__(256, SAD_BWD2_MINB) k_backward2(const uint32_t
         for (int j = 0; j < H; j++) sm.key[(half * H + j) * TPX + pix] = kEmpty;
     }
     __syncthreads();
+    PH(0);
     tile_reduce(sm, red);
     __syncthreads();
     if (MODE != 2) block_dd_store<NT>(loss, sm.warp_part, loss_part + blockIdx.y * gridDim.x + blockIdx.x);
