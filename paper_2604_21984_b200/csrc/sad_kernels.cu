@@ -2124,6 +2124,10 @@ __global__ void __launch_bounds__(64) k_stats(const uint32_t* __restrict__ ids, 
 
 // Opt-in shared-memory sizes of the tile-reduction kernels; called once per context, before any
 // launch can be captured into a CUDA graph.
+template <int KM>
+__global__ void k_stats2(const uint32_t* __restrict__ ids, const Q4<double>* __restrict__ rtab,
+                         const double* __restrict__ tgt, FieldDims f, double s, RedTarget red, DevState* st);
+
 void prepare_kernels() {
     backward_attr<float, 8, 0>();
     backward_attr<float, 8, 1>();
@@ -2141,17 +2145,202 @@ void prepare_kernels() {
                          (int)sizeof(TileRed<double, 8, 64, 8>));
     cudaFuncSetAttribute(k_stats<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(TileRed<double, 8, 64, 16>));
+    cudaFuncSetAttribute(k_stats2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(TileRed<double, 8, 64, 8, 128>));
+    cudaFuncSetAttribute(k_stats2<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(TileRed<double, 8, 64, 16, 128>));
 }
+
+// Two lanes per pixel (128 threads per 8x8 tile), same hand-over of the order-sensitive double sums
+// as k_backward2: lane 0 sums its slots' softmax weights / colours from zero, lane 1 continues from
+// lane 0's partial.  Skipped slots (inactive, non-finite logit) do not take part, exactly as the
+// reference's compacted candidate loop (budget.cpp:60-100).
+template <int KM>
+__global__ void __launch_bounds__(128) k_stats2(const uint32_t* __restrict__ ids, const Q4<double>* __restrict__ rtab,
+                                               const double* __restrict__ tgt, FieldDims f, double s, RedTarget red,
+                                               DevState* st) {
+    constexpr int TW = 8, TH = 8, TPX = 64, NT = 128, NCH = 8, H = KM / 2;
+    constexpr unsigned FULL = 0xffffffffu;
+    using Red = TileRed<double, NCH, TPX, KM, NT>;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    Red& sm = *reinterpret_cast<Red*>(smraw);
+    tile_init(sm);
+    const int tid = threadIdx.x;
+    const int pix = tid >> 1, half = tid & 1;
+    const int px = blockIdx.x * TW + (pix % TW);
+    const int py = blockIdx.y * TH + (pix / TW);
+    const bool inside = px < f.width && py < f.height;
+    uint32_t cid[H];
+    double lg[H];
+    bool ok[H];
+    bool any = false;
+    double best = 0;
+    {
+        uint32_t idv[H];
+        const uint32_t* lst = ids + static_cast<size_t>(f.k) * (static_cast<size_t>(py / f.cell) * f.gw + px / f.cell);
+        bool has_empty = false;
+#pragma unroll
+        for (int j = 0; j < H; j++) {
+            const int i = half * H + j;
+            idv[j] = (inside && i < f.k) ? lst[i] : kEmpty;
+            has_empty = has_empty || idv[j] == kEmpty;
+        }
+        const bool partner_empty = __shfl_xor_sync(FULL, has_empty, 1);
+        bool stop = !inside || (half == 1 && partner_empty);
+#pragma unroll
+        for (int j = 0; j < H; j++) {
+            const uint32_t id = idv[j];
+            stop = stop || id == kEmpty;
+            cid[j] = id;
+            ok[j] = false;
+            lg[j] = 0;
+            if (!stop) {
+                const Q4<double> a = rtab[3 * id], b = rtab[3 * id + 1];
+                if (b.w != 0.0) {
+                    const double l = score_logit(a, b, static_cast<double>(px), static_cast<double>(py), s);
+                    if (isfinite(l)) {
+                        ok[j] = true;
+                        lg[j] = l;
+                        if (!any || l > best) best = l;
+                        any = true;
+                    }
+                }
+            }
+        }
+    }
+    const bool pany = __shfl_xor_sync(FULL, any, 1);
+    const double pbest = __shfl_xor_sync(FULL, best, 1);
+    const bool a0 = half == 0 ? any : pany, a1 = half == 0 ? pany : any;
+    const double b0 = half == 0 ? best : pbest, b1 = half == 0 ? pbest : best;
+    best = a0 ? ((a1 && b1 > b0) ? b1 : b0) : b1;
+    const bool any_all = a0 || a1;
+
+    double w[H];
+    double wpart = 0;
+#pragma unroll
+    for (int j = 0; j < H; j++) w[j] = ok[j] ? exp(lg[j] - best) : 0.0;
+    if (half == 0) {
+#pragma unroll
+        for (int j = 0; j < H; j++)
+            if (ok[j]) wpart += w[j];
+    }
+    const double from0 = __shfl_xor_sync(FULL, wpart, 1);
+    if (half == 1) {
+        wpart = from0;
+#pragma unroll
+        for (int j = 0; j < H; j++)
+            if (ok[j]) wpart += w[j];
+    }
+    const double from1 = __shfl_xor_sync(FULL, wpart, 1);
+    const double invw = 1.0 / (half == 0 ? from1 : wpart);
+    Q4<double> col[H];
+    double c0 = 0, c1 = 0, c2 = 0;
+#pragma unroll
+    for (int j = 0; j < H; j++) {
+        col[j] = Q4<double>{0, 0, 0, 0};
+        if (ok[j]) {
+            w[j] *= invw;
+            col[j] = rtab[3 * cid[j] + 2];
+        }
+    }
+    if (half == 0) {
+#pragma unroll
+        for (int j = 0; j < H; j++)
+            if (ok[j]) {
+                c0 += w[j] * col[j].x;
+                c1 += w[j] * col[j].y;
+                c2 += w[j] * col[j].z;
+            }
+    }
+    {
+        const double r0 = __shfl_xor_sync(FULL, c0, 1), r1 = __shfl_xor_sync(FULL, c1, 1),
+                     r2 = __shfl_xor_sync(FULL, c2, 1);
+        if (half == 1) {
+            c0 = r0;
+            c1 = r1;
+            c2 = r2;
+#pragma unroll
+            for (int j = 0; j < H; j++)
+                if (ok[j]) {
+                    c0 += w[j] * col[j].x;
+                    c1 += w[j] * col[j].y;
+                    c2 += w[j] * col[j].z;
+                }
+        }
+        const double s0 = __shfl_xor_sync(FULL, c0, 1), s1 = __shfl_xor_sync(FULL, c1, 1),
+                     s2 = __shfl_xor_sync(FULL, c2, 1);
+        if (half == 0) {
+            c0 = s0;
+            c1 = s1;
+            c2 = s2;
+        }
+    }
+    if (any_all) {
+        const double* tp = tgt + 3 * (static_cast<size_t>(py) * f.width + px);
+        const double e0 = c0 - tp[0], e1 = c1 - tp[1], e2 = c2 - tp[2];
+        const double r2 = e0 * e0 + e1 * e1 + e2 * e2;
+        const double fx = px, fy = py;
+#pragma unroll
+        for (int j = 0; j < H; j++) {
+            const int e = (half * H + j) * TPX + pix;
+            if (!ok[j]) {
+                sm.key[e] = kEmpty;
+                continue;
+            }
+            const Q4<double> c = col[j];
+            const double rho = w[j] * r2;
+            double v[8];
+            v[0] = w[j];
+            v[1] = rho;
+            v[2] = rho * fx;
+            v[3] = rho * fy;
+            v[4] = rho * fx * fx;
+            v[5] = rho * fx * fy;
+            v[6] = rho * fy * fy;
+            if (w[j] >= 1.0 - 1e-6) {
+                v[7] = 1e6;
+            } else {
+                const double ir = 1.0 / (1.0 - w[j]);
+                const double q0 = (c0 - w[j] * c.x) * ir - tp[0];
+                const double q1 = (c1 - w[j] * c.y) * ir - tp[1];
+                const double q2 = (c2 - w[j] * c.z) * ir - tp[2];
+                v[7] = q0 * q0 + q1 * q1 + q2 * q2 - r2;
+            }
+            sm.key[e] = cid[j];
+#pragma unroll
+            for (int t = 0; t < NCH; t++) sm.c[t * Red::ES + e] = isfinite(v[t]) ? v[t] : 0.0;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < H; j++) sm.key[(half * H + j) * TPX + pix] = kEmpty;
+    }
+    __syncthreads();
+    tile_reduce(sm, red);
+    __syncthreads();
+    unsigned long long v = block_sum_u64<NT>((half == 0 && any_all) ? 1ull : 0ull,
+                                             reinterpret_cast<unsigned long long*>(sm.warp_part));
+    if (threadIdx.x == 0 && v) atomicAdd(reinterpret_cast<unsigned long long*>(&st->valid), v);
+}
+
+static const bool g_stats1 = getenv("SAD_STATS1") != nullptr;
 
 void launch_stats(const uint32_t* ids, const void* rtab_d, const double* tgt, const FieldDims& f, double scale,
                   const RedTarget& red, DevState* st, cudaStream_t stream) {
     dim3 grid((f.width + 7) / 8, (f.height + 7) / 8);
-    if (f.k <= 8) {
-        size_t smem = sizeof(TileRed<double, 8, 64, 8>);
-        k_stats<8><<<grid, 64, smem, stream>>>(ids, (const Q4<double>*)rtab_d, tgt, f, scale, red, st);
+    if (g_stats1) {  // one lane per pixel (A/B)
+        if (f.k <= 8)
+            k_stats<8><<<grid, 64, sizeof(TileRed<double, 8, 64, 8>), stream>>>(ids, (const Q4<double>*)rtab_d, tgt, f,
+                                                                                scale, red, st);
+        else
+            k_stats<16><<<grid, 64, sizeof(TileRed<double, 8, 64, 16>), stream>>>(ids, (const Q4<double>*)rtab_d, tgt,
+                                                                                  f, scale, red, st);
     } else {
-        size_t smem = sizeof(TileRed<double, 8, 64, 16>);
-        k_stats<16><<<grid, 64, smem, stream>>>(ids, (const Q4<double>*)rtab_d, tgt, f, scale, red, st);
+        if (f.k <= 8)
+            k_stats2<8><<<grid, 128, sizeof(TileRed<double, 8, 64, 8, 128>), stream>>>(ids, (const Q4<double>*)rtab_d,
+                                                                                       tgt, f, scale, red, st);
+        else
+            k_stats2<16><<<grid, 128, sizeof(TileRed<double, 8, 64, 16, 128>), stream>>>(
+                ids, (const Q4<double>*)rtab_d, tgt, f, scale, red, st);
     }
     SAD_LAUNCHED();
 }
