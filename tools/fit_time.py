@@ -16,7 +16,12 @@ p.add_argument("--height", type=int, default=512)
 p.add_argument("--bpp", type=float, default=2.0)
 p.add_argument("--iters", type=int, default=4000)
 p.add_argument("--reps", type=int, default=3)
+p.add_argument("--lib", default=None, help="alternative libsad_b200.so (A/B)")
+p.add_argument("--no-e2e", action="store_true")
 a = p.parse_args()
+if a.lib:
+    from paper_2604_21984_b200 import api
+    api.LIB_PATH = os.path.abspath(a.lib)
 G = sad.gpu_backend(0)
 cfg = sad.TrainConfig(iters=a.iters, target_bpp=a.bpp, fp64=False)
 img = synthetic_image(a.width, a.height, 1)
@@ -38,7 +43,7 @@ for i in range(a.reps):
     print(f"resident fit {i}: wall {1e3 * (t1 - t0):.1f} ms, device {tot.value:.1f} ms, phases "
           f"propagate {ph[0]:.1f} fwd_bwd {ph[1]:.1f} adam+adv {ph[2]:.1f} events {ph[3]:.1f} ms")
 G.lib.sad_fit_destroy(run)
-for i in range(a.reps):
+for i in range(0 if a.no_e2e else a.reps):
     t0 = time.perf_counter()
     r = G.fit(sad.ImageBuffer(a.width, a.height, img), cfg)
     print(f"e2e fit {i}: {1e3 * (time.perf_counter() - t0):.1f} ms  psnr_last {r.history[-1].psnr:.3f}")
