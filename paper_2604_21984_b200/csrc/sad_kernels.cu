@@ -10,13 +10,15 @@
 #ifndef SAD_EXPERIMENT
 #define SAD_EXPERIMENT 0
 #endif
-#if SAD_EXPERIMENT == 3
+#if SAD_EXPERIMENT == 3 || SAD_EXPERIMENT == 4
 __device__ unsigned long long g_phase_clk[16];
-#define PH(i) do { __syncthreads(); if (threadIdx.x == 0) { long long _c = clock64(); atomicAdd(&g_phase_clk[i], (unsigned long long)(_c - _t0)); _t0 = _c; } } while (0)
 extern "C" void sad_exp_phase(unsigned long long* out, int reset) {
     if (reset) { unsigned long long z[16] = {0}; cudaMemcpyToSymbol(g_phase_clk, z, sizeof z); }
     else cudaMemcpyFromSymbol(out, g_phase_clk, 16 * sizeof(unsigned long long));
 }
+#endif
+#if SAD_EXPERIMENT == 3
+#define PH(i) do { __syncthreads(); if (threadIdx.x == 0) { long long _c = clock64(); atomicAdd(&g_phase_clk[i], (unsigned long long)(_c - _t0)); _t0 = _c; } } while (0)
 #else
 #define PH(i) do { } while (0)
 #endif
@@ -536,6 +538,11 @@ struct KeyList8 {
         k[0] = b[0] ? x : k[0];
     }
     __device__ __forceinline__ void consider(uint32_t c, uint64_t x) {
+#if SAD_EXPERIMENT == 4
+        atomicAdd(&g_phase_clk[0], 1ull);
+        if (x > k[7]) atomicAdd(&g_phase_clk[1], 1ull);
+        if (x > k[7] && !contains(c)) atomicAdd(&g_phase_clk[2], 1ull);
+#endif
         if (x > k[7] && !contains(c)) insert(x);
     }
 };
@@ -1024,8 +1031,7 @@ struct TileRed {  // TPX pixels, KM slots each, NT threads (TPX or 2 * TPX)
     union {
         uint32_t key[E];  // site id per entry (steps 1-2)
         struct {
-            uint16_t order[E];   // entry of each sorted position (steps 3-4)
-            uint16_t posloc[E];  // bucket of each sorted position
+            uint16_t order[E];  // entry of each sorted position (steps 3-4)
         } srt;
     };
     union {
@@ -1050,18 +1056,6 @@ __device__ __forceinline__ bool c_finite<float>(float x) {
 template <>
 __device__ __forceinline__ bool c_finite<double>(double x) {
     return isfinite(x);
-}
-
-template <int NCH>
-__device__ __forceinline__ void write_record(const RedTarget& red, uint32_t site, uint32_t slot, const DD* acc) {
-    if (slot < static_cast<uint32_t>(red.maxt)) {
-        double2* rec = red.part + (static_cast<size_t>(site) * red.maxt + slot) * red.stride;
-#pragma unroll
-        for (int ch = 0; ch < NCH; ch++) rec[ch] = make_double2(acc[ch].hi, acc[ch].lo);
-    } else {
-#pragma unroll
-        for (int ch = 0; ch < NCH; ch++) dd_atomic_merge(red.over + static_cast<size_t>(ch) * red.cap + site, acc[ch]);
-    }
 }
 
 template <typename CT, int NCH, int TPX, int KM, int NT>
