@@ -442,6 +442,8 @@ def run_b200(a):
         e1.synchronize()
         ms.append(e0.elapsed_time(e1))
     torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
     launches = int(lib.sad_ctx_launch_count(ctx) - launches0)
     clk = clocks.stop()
     tot_ms = sum(ms)
