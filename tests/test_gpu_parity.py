@@ -186,6 +186,39 @@ def test_backward_matches(G, R, fp64, removal):
         assert frac > 0.999, f"only {frac:.5f} of fp32 gradient entries bit-identical"
 
 
+@pytest.mark.parametrize("w,h,k,cell", [(37, 29, 1, 1), (37, 29, 3, 1), (50, 34, 8, 1), (40, 30, 12, 1),
+                                         (40, 30, 16, 2), (23, 17, 5, 3)])
+def test_tiles_ragged_and_other_k(G, R, w, h, k, cell):
+    """The fp32 two-lanes-per-pixel backward and stats kernels on image sizes that are not multiples of
+    their 16x8 / 8x8 tiles, with lists shorter than 8 (lane 1 partly or wholly past the list end) and
+    K = 16 (the 16-slot instantiations).  fp32 loss and gradients must be bit-identical."""
+    st = random_model(w, h, 45, 17 + k)
+    st.deactivate(2)
+    tgt = random_target(w, h, 5 + k)
+    f = _field(w, h, k, cell)
+    R.refresh(st, f, sad.RefreshMode.Full, 3, 4, 11, F32)
+    for removal in (False, True):
+        gg, gr = sad.GradBuffer(), sad.GradBuffer()
+        lg = G.backward_image(st, f, tgt, gg, F32, removal)
+        lr = R.backward_image(st, f, tgt, gr, F32, removal)
+        assert lg == lr
+        assert np.array_equal(gg.data, gr.data)
+        assert gg.nonfinite == gr.nonfinite
+    dl = random_target(w, h, 3)
+    dl.data -= 0.5
+    gg, gr = sad.GradBuffer(), sad.GradBuffer()
+    G.backward_pixel_grad(st, f, dl, gg, F32)
+    R.backward_pixel_grad(st, f, dl, gr, F32)
+    assert np.array_equal(gg.data[:, :10], gr.data[:, :10])
+    assert G.image_loss(st, f, tgt, F32) == R.image_loss(st, f, tgt, F32)
+    assert np.array_equal(G.render_image(st, f, F32).data, R.render_image(st, f, F32).data)
+    assert np.array_equal(G.render_id_map(st, f), R.render_id_map(st, f))
+    sg = G.accumulate_stats(st, f, tgt)
+    sr = R.accumulate_stats(st, f, tgt)
+    assert sg.valid_pixels == sr.valid_pixels
+    assert np.allclose(sg.data, sr.data, rtol=1e-12, atol=1e-12)
+
+
 def test_loss_identity_and_pixgrad(G, R):
     """test_grad.cpp:116-128: image_loss == backward loss; adjoint entry point parity."""
     st = random_model(64, 64, 60, 7)
