@@ -2515,13 +2515,16 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
                                               const double2* __restrict__ bc_table, double2 bc_now, int zero_grads,
                                               double scale, Q4<T>* pack, Q4<T>* gtab, int32_t* rcap_next,
                                               const double* __restrict__ totals, int32_t* roff_next,
-                                              int32_t* pool_top) {
+                                              int32_t* pool_top, const uint32_t* __restrict__ act) {
     __shared__ int32_t s_want[8], s_base;
     const int lane16 = threadIdx.x & 15;
-    const int id = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
+    const int grp = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
     const unsigned gmask = 0xffffu << (threadIdx.x & 16);
     const int cap = s.cap;
-    const bool live = id < st->n_sites;
+    // with `act` (plain iterations) the groups walk the ascending active list: inactive sites have no
+    // records, no update and keep their tables, so skipping them is exact
+    const bool live = act ? grp < st->n_active : grp < st->n_sites;
+    const int id = act ? (live ? static_cast<int>(act[grp]) : cap) : grp;
     const int k = lane16;
     unsigned long long skipped = 0;
     // ---- gradient totals (all lanes of the group take part in the shuffles)
@@ -2585,7 +2588,7 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
     } else {
         __shfl_sync(gmask, 0.0, (threadIdx.x & 16) + channel_lane(7));
         __shfl_sync(gmask, 0.0, (threadIdx.x & 16) + channel_lane(8));
-        if (rcap_next && k == 0 && id < cap) rcap_next[id] = 0;
+        if (rcap_next && k == 0 && id < cap) rcap_next[id] = 0;  // (act: id == cap, nothing written)
         if (rcap_next && k == 0) s_want[threadIdx.x >> 4] = 0;
     }
     // record slices for the next pass: a block-wide prefix of the 8 capacities and one pool claim per
@@ -2647,17 +2650,17 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
 void launch_adam(bool fp64, const SitesDev& s, DevState* st, const RedTarget& grads, double* m, double* v,
                  const AdamHyper& hp, const double2* bc_table, double2 bc_now, bool zero_grads, double scale,
                  void* pack, void* gtab, int32_t* rcap_next, cudaStream_t stream, const double* totals,
-                 int32_t* roff_next, int32_t* pool_top) {
+                 int32_t* roff_next, int32_t* pool_top, const uint32_t* act) {
     int grid = (s.cap + 7) / 8;  // 8 sites (16 lanes each) per 128-thread block
     if (grid < 1) grid = 1;
     if (fp64)
         k_adam<double><<<grid, 128, 0, stream>>>(s, st, grads, m, v, hp, bc_table, bc_now, zero_grads ? 1 : 0, scale,
                                                  (Q4<double>*)pack, (Q4<double>*)gtab, rcap_next, totals, roff_next,
-                                                 pool_top);
+                                                 pool_top, act);
     else
         k_adam<float><<<grid, 128, 0, stream>>>(s, st, grads, m, v, hp, bc_table, bc_now, zero_grads ? 1 : 0, scale,
                                                 (Q4<float>*)pack, (Q4<float>*)gtab, rcap_next, totals, roff_next,
-                                                pool_top);
+                                                pool_top, act);
     SAD_LAUNCHED();
 }
 

@@ -130,7 +130,7 @@ void launch_finalize(const RedTarget& red, int n_ch, const DevState* st, cudaStr
 void launch_adam(bool fp64, const SitesDev& s, DevState* st, const RedTarget& grads, double* m, double* v,
                  const AdamHyper& hp, const double2* bc_table, double2 bc_now, bool zero_grads, double scale,
                  void* pack, void* gtab, int32_t* rcap_next, cudaStream_t stream, const double* totals = nullptr,
-                 int32_t* roff_next = nullptr, int32_t* pool_top = nullptr);
+                 int32_t* roff_next = nullptr, int32_t* pool_top = nullptr, const uint32_t* act = nullptr);
 // tau_diffusion pieces (train.cpp:171-213)
 void launch_site_totals(const RedTarget& grads, const DevState* st, int cap, double* tot, double* g0,
                         cudaStream_t stream);

@@ -1432,6 +1432,9 @@ static int capacity_bound(const sad_train_config& c, int n0, double scale, bool 
     return static_cast<int>(n) + 1;
 }
 
+// SAD_ADAM_ALL=1: plain-iteration Adam over every slot (A/B)
+static const bool g_adam_all = getenv("SAD_ADAM_ALL") != nullptr;
+
 // fit_impl (train.cpp:221-291), resident in HBM.
 static void fit_loop(sad_fit_run* r) {
     Workspace& ws = r->ws;
@@ -1539,9 +1542,11 @@ static void fit_loop(sad_fit_run* r) {
             tau_step();
         });
         mark(2, [&] {
+            // plain iterations: active sites only (event iterations below run every slot, which also
+            // zeroes the record capacity of pruned slots before densify can reuse them)
             sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.gred_adaptive(), ws.m.p, ws.v.p, hp, r->bc_table.p,
                               make_double2(0, 0), true, scale_n, ws.pack.p, ws.gtab.p, ws.rcap.p, s, totals,
-                              ws.roff.p, ws.otops.p + 2);
+                              ws.roff.p, ws.otops.p + 2, g_adam_all ? nullptr : ws.act.p);
         });
         mark(5, [&] {
             sadk::launch_advance(ws.st.p, np, 1, r->loss_hist.p, r->active_hist.p, ws.loss_part.p, nbw, ws.otops.p, s);
