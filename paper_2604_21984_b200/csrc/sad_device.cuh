@@ -101,6 +101,9 @@ template <> __device__ __forceinline__ float tsqrt<float>(float x) { return __fs
 template <> __device__ __forceinline__ double tsqrt<double>(double x) { return __dsqrt_rn(x); }
 
 template <typename T> __device__ __forceinline__ bool tfinite(T x) { return isfinite(static_cast<double>(x)); }
+template <> __device__ __forceinline__ bool tfinite<float>(float x) {  // exponent field not all ones
+    return (__float_as_uint(x) & 0x7f800000u) != 0x7f800000u;
+}
 
 // IEEE round-to-nearest reciprocal: the same value as T(1) / x, with a shorter instruction sequence.
 template <typename T> __device__ __forceinline__ T trcp(T x);

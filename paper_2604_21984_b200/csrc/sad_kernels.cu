@@ -110,6 +110,13 @@ void launch_tables(bool fp64, const SitesDev& s, const DevState* st, double scal
     SAD_LAUNCHED();
 }
 
+// Candidate cell of pixel (px, py) (CandidateField::cell_x/cell_y, types.hpp:95-101); the fit's cell
+// size is 1, so the two integer divisions are skipped on that (launch-uniform) path.
+__device__ __forceinline__ size_t cell_index(const FieldDims& f, int px, int py) {
+    if (f.cell == 1) return static_cast<size_t>(py) * f.gw + px;
+    return static_cast<size_t>(py / f.cell) * f.gw + px / f.cell;
+}
+
 // ScoreTable<T>::logit (score_table.hpp:48-54), quadratic form, no contraction.
 template <typename T>
 __device__ __forceinline__ T score_logit(const Q4<T>& a, const Q4<T>& b, T px, T py, T s) {
@@ -842,62 +849,71 @@ void launch_exact_topk(bool fp64, const void* rtab, const uint32_t* act, int n_a
 template <typename T, int KM>
 __global__ void __launch_bounds__(256) k_render(const uint32_t* __restrict__ ids, const Q4<T>* __restrict__ rtab,
                                                 FieldDims f, T s, T* __restrict__ out, DevState* st) {
+    // mix_at (render.cpp:19-52): candidates stay in their list slots; `ok` marks the ones the reference
+    // keeps (before the first sentinel, active, finite logit), and every sum runs over the kept slots
+    // in list order, so it rounds exactly like the reference's compacted loop
     const int px = blockIdx.x * blockDim.x + threadIdx.x;
     const int py = blockIdx.y * blockDim.y + threadIdx.y;
     if (px >= f.width || py >= f.height) return;
-    const uint32_t* lst = ids + static_cast<size_t>(f.k) * (static_cast<size_t>(py / f.cell) * f.gw + px / f.cell);
+    const uint32_t* lst = ids + static_cast<size_t>(f.k) * cell_index(f, px, py);
     uint32_t cid[KM];
+    if (KM == 8 && f.k == 8) {
+        const uint4 u0 = __ldg(reinterpret_cast<const uint4*>(lst)), u1 = __ldg(reinterpret_cast<const uint4*>(lst) + 1);
+        cid[0] = u0.x; cid[1] = u0.y; cid[2] = u0.z; cid[3] = u0.w;
+        cid[4] = u1.x; cid[5] = u1.y; cid[6] = u1.z; cid[7] = u1.w;
+    } else {
+#pragma unroll
+        for (int i = 0; i < KM; i++) cid[i] = i < f.k ? __ldg(lst + i) : kEmpty;
+    }
     T lg[KM];
-    int n = 0;
+    bool ok[KM];
+    bool any = false, stop = false;
     T best = T(0);
     const T fx = static_cast<T>(px), fy = static_cast<T>(py);
 #pragma unroll
     for (int i = 0; i < KM; i++) {
-        cid[i] = 0;
+        stop = stop || cid[i] == kEmpty;
+        ok[i] = false;
         lg[i] = T(0);
-    }
-#pragma unroll
-    for (int i = 0; i < KM; i++) {
-        if (i >= f.k) break;
-        uint32_t id = lst[i];
-        if (id == kEmpty) break;
-        Q4<T> a = rtab[3 * id], b = rtab[3 * id + 1];
-        if (b.w == T(0)) continue;
-        T l = score_logit(a, b, fx, fy, s);
-        if (!tfinite(l)) continue;
-#pragma unroll
-        for (int j = 0; j < KM; j++)
-            if (j == n) {
-                cid[j] = id;
-                lg[j] = l;
+        if (!stop) {
+            const Q4<T> a = rtab[3 * cid[i]], b = rtab[3 * cid[i] + 1];
+            if (b.w != T(0)) {
+                const T l = score_logit(a, b, fx, fy, s);
+                if (tfinite(l)) {
+                    ok[i] = true;
+                    lg[i] = l;
+                    if (!any || l > best) best = l;
+                    any = true;
+                }
             }
-        if (n == 0 || l > best) best = l;
-        n++;
+        }
     }
-    T* o = out + 3 * (static_cast<size_t>(py) * f.width + px);
-    if (n == 0) {
+    if (!any) {
         atomicOr(&st->err, 1);
         return;
     }
     T w[KM];
     T sum = T(0);
 #pragma unroll
-    for (int i = 0; i < KM; i++)
-        if (i < n) {
+    for (int i = 0; i < KM; i++) {
+        w[i] = T(0);
+        if (ok[i]) {
             w[i] = texp(lg[i] - best);
             sum += w[i];
         }
-    T inv = trcp(sum);
+    }
+    const T inv = trcp(sum);
     T r = T(0), g = T(0), b = T(0);
 #pragma unroll
     for (int i = 0; i < KM; i++)
-        if (i < n) {
-            T wi = w[i] * inv;
-            Q4<T> c = rtab[3 * cid[i] + 2];
+        if (ok[i]) {
+            const T wi = w[i] * inv;
+            const Q4<T> c = rtab[3 * cid[i] + 2];
             r += wi * c.x;
             g += wi * c.y;
             b += wi * c.z;
         }
+    T* o = out + 3 * (static_cast<size_t>(py) * f.width + px);
     o[0] = r;
     o[1] = g;
     o[2] = b;
@@ -928,7 +944,7 @@ __global__ void k_id_map(const uint32_t* __restrict__ ids, const Q4<double>* __r
     const int px = blockIdx.x * blockDim.x + threadIdx.x;
     const int py = blockIdx.y * blockDim.y + threadIdx.y;
     if (px >= f.width || py >= f.height) return;
-    const uint32_t* lst = ids + static_cast<size_t>(f.k) * (static_cast<size_t>(py / f.cell) * f.gw + px / f.cell);
+    const uint32_t* lst = ids + static_cast<size_t>(f.k) * cell_index(f, px, py);
     uint32_t best = kEmpty;
     double bl = 0;
     for (int i = 0; i < f.k; i++) {
@@ -965,7 +981,7 @@ __global__ void k_pixel_weights(const uint32_t* __restrict__ ids, const Q4<doubl
     int n = 0;
     double best = 0;
     if (px >= 0 && py >= 0 && px < f.width && py < f.height) {
-        const uint32_t* lst = ids + static_cast<size_t>(f.k) * (static_cast<size_t>(py / f.cell) * f.gw + px / f.cell);
+        const uint32_t* lst = ids + static_cast<size_t>(f.k) * cell_index(f, px, py);
         for (int i = 0; i < f.k; i++) {
             uint32_t id = lst[i];
             if (id == kEmpty) break;
@@ -1384,7 +1400,7 @@ __global__ void __launch_bounds__(BwdTile<T>::TW * BwdTile<T>::TH)
     unsigned long long nonfinite = 0;
     DD loss{0.0, 0.0};
     {
-        const uint32_t* lst = ids + static_cast<size_t>(f.k) * (static_cast<size_t>(py / f.cell) * f.gw + px / f.cell);
+        const uint32_t* lst = ids + static_cast<size_t>(f.k) * cell_index(f, px, py);
         const T fx = static_cast<T>(px), fy = static_cast<T>(py);
         bool stop = !inside;
 #pragma unroll
@@ -1583,7 +1599,7 @@ __global__ void __launch_bounds__(256, SAD_BWD2_MINB) k_backward2(const uint32_t
     DD loss{0.0, 0.0};
     {
         uint32_t idv[H];
-        const uint32_t* lst = ids + static_cast<size_t>(f.k) * (static_cast<size_t>(py / f.cell) * f.gw + px / f.cell);
+        const uint32_t* lst = ids + static_cast<size_t>(f.k) * cell_index(f, px, py);
         bool has_empty = false;
 #pragma unroll
         for (int j = 0; j < H; j++) {
@@ -1864,7 +1880,7 @@ __global__ void __launch_bounds__(128) k_loss(const uint32_t* __restrict__ ids, 
     const int py = blockIdx.y * 8 + (tid / 16);
     DD loss{0.0, 0.0};
     if (px < f.width && py < f.height) {
-        const uint32_t* lst = ids + static_cast<size_t>(f.k) * (static_cast<size_t>(py / f.cell) * f.gw + px / f.cell);
+        const uint32_t* lst = ids + static_cast<size_t>(f.k) * cell_index(f, px, py);
         uint32_t cid[KM];
         T lg[KM];
         int n = 0;
@@ -2034,7 +2050,7 @@ __global__ void __launch_bounds__(64) k_stats(const uint32_t* __restrict__ ids, 
     }
     double best = 0;
     if (px < f.width && py < f.height) {
-        const uint32_t* lst = ids + static_cast<size_t>(f.k) * (static_cast<size_t>(py / f.cell) * f.gw + px / f.cell);
+        const uint32_t* lst = ids + static_cast<size_t>(f.k) * cell_index(f, px, py);
 #pragma unroll
         for (int i = 0; i < KM; i++) {
             if (i >= f.k) break;
@@ -2171,7 +2187,7 @@ __global__ void __launch_bounds__(128) k_stats2(const uint32_t* __restrict__ ids
     double best = 0;
     {
         uint32_t idv[H];
-        const uint32_t* lst = ids + static_cast<size_t>(f.k) * (static_cast<size_t>(py / f.cell) * f.gw + px / f.cell);
+        const uint32_t* lst = ids + static_cast<size_t>(f.k) * cell_index(f, px, py);
         bool has_empty = false;
 #pragma unroll
         for (int j = 0; j < H; j++) {
@@ -2676,7 +2692,7 @@ __global__ void k_tau_edges(const uint32_t* __restrict__ ids, const uint32_t* __
     const size_t pix = static_cast<size_t>(py) * f.width + px;
     const uint64_t sentinel = (nb >= 32) ? ~0ull : ((1ull << (2 * nb)) - 1);
     const uint32_t o = owner[pix];
-    const uint32_t* lst = ids + static_cast<size_t>(f.k) * (static_cast<size_t>(py / f.cell) * f.gw + px / f.cell);
+    const uint32_t* lst = ids + static_cast<size_t>(f.k) * cell_index(f, px, py);
     uint64_t* out = keys + pix * f.k;
     bool end = o == kEmpty;
     for (int i = 0; i < f.k; i++) {
