@@ -969,51 +969,102 @@ void launch_id_map(const uint32_t* ids, const void* rtab_d, const FieldDims& f, 
     SAD_LAUNCHED();
 }
 
-// pixel_weights (render.cpp:93-105), batched point queries against a cached double table.
-__global__ void k_pixel_weights(const uint32_t* __restrict__ ids, const Q4<double>* __restrict__ rtab, FieldDims f,
-                                double s, const int32_t* __restrict__ xy, int n_q, uint32_t* __restrict__ oid,
-                                double* __restrict__ ow, int32_t* __restrict__ on) {
-    int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= n_q) return;
-    int px = xy[2 * q], py = xy[2 * q + 1];
-    uint32_t cid[16];
-    double lg[16];
-    int n = 0;
+// pixel_weights (render.cpp:92-116), batched point queries against a cached double table: one thread per query, list slots unrolled (no local-memory
+// arrays), kept candidates compacted in list order at output time; each block stages its 128 queries'
+// 16-slot rows in shared memory (stride 17: conflict-free) and writes them back coalesced.
+template <int KM>
+__global__ void __launch_bounds__(128) k_pixel_weights(const uint32_t* __restrict__ ids,
+                                                       const Q4<double>* __restrict__ rtab, FieldDims f, double s,
+                                                       const int32_t* __restrict__ xy, int n_q,
+                                                       uint32_t* __restrict__ oid, double* __restrict__ ow,
+                                                       int32_t* __restrict__ on) {
+    constexpr int QB = 128, RS = 17;
+    __shared__ uint32_t sid[QB * RS];
+    __shared__ double sw[QB * RS];
+    const int q0 = blockIdx.x * QB;
+    const int q = q0 + threadIdx.x;
+    uint32_t cid[KM];
+    double lg[KM];
+    bool ok[KM];
+    bool any = false;
     double best = 0;
-    if (px >= 0 && py >= 0 && px < f.width && py < f.height) {
-        const uint32_t* lst = ids + static_cast<size_t>(f.k) * cell_index(f, px, py);
-        for (int i = 0; i < f.k; i++) {
-            uint32_t id = lst[i];
-            if (id == kEmpty) break;
-            Q4<double> a = rtab[3 * id], b = rtab[3 * id + 1];
-            if (b.w == 0.0) continue;
-            double l = score_logit(a, b, static_cast<double>(px), static_cast<double>(py), s);
-            if (!isfinite(l)) continue;
-            cid[n] = id;
-            lg[n] = l;
-            if (n == 0 || l > best) best = l;
-            n++;
+#pragma unroll
+    for (int i = 0; i < KM; i++) {
+        cid[i] = kEmpty;
+        lg[i] = 0;
+        ok[i] = false;
+    }
+    if (q < n_q) {
+        const int px = xy[2 * q], py = xy[2 * q + 1];
+        if (px >= 0 && py >= 0 && px < f.width && py < f.height) {
+            const uint32_t* lst = ids + static_cast<size_t>(f.k) * cell_index(f, px, py);
+            bool stop = false;
+#pragma unroll
+            for (int i = 0; i < KM; i++) {
+                const uint32_t id = (!stop && i < f.k) ? __ldg(lst + i) : kEmpty;
+                stop = stop || id == kEmpty;
+                cid[i] = id;
+                if (!stop) {
+                    const Q4<double> a = rtab[3 * id], b = rtab[3 * id + 1];
+                    if (b.w != 0.0) {
+                        const double l = score_logit(a, b, static_cast<double>(px), static_cast<double>(py), s);
+                        if (isfinite(l)) {
+                            ok[i] = true;
+                            lg[i] = l;
+                            if (!any || l > best) best = l;
+                            any = true;
+                        }
+                    }
+                }
+            }
         }
     }
-    double w[16], sum = 0;
-    for (int i = 0; i < n; i++) {
-        w[i] = exp(lg[i] - best);
-        sum += w[i];
+    double w[KM];
+    double sum = 0;
+#pragma unroll
+    for (int i = 0; i < KM; i++) {
+        w[i] = 0;
+        if (ok[i]) {
+            w[i] = exp(lg[i] - best);
+            sum += w[i];
+        }
     }
-    double inv = 1.0 / sum;
+    const double inv = 1.0 / sum;
+    uint32_t* my_id = sid + threadIdx.x * RS;
+    double* my_w = sw + threadIdx.x * RS;
+#pragma unroll
     for (int i = 0; i < 16; i++) {
-        oid[16 * q + i] = i < n ? cid[i] : kEmpty;
-        ow[16 * q + i] = i < n ? w[i] * inv : 0.0;
+        my_id[i] = kEmpty;
+        my_w[i] = 0.0;
     }
-    on[q] = n;
+    int n = 0;
+#pragma unroll
+    for (int i = 0; i < KM; i++)
+        if (ok[i]) {
+            my_id[n] = cid[i];
+            my_w[n] = w[i] * inv;
+            n++;
+        }
+    if (q < n_q) on[q] = n;
+    __syncthreads();
+    const int rows = n_q - q0 < QB ? n_q - q0 : QB;
+    for (int j = threadIdx.x; j < rows * 16; j += QB) {
+        const int r = j >> 4, c = j & 15;
+        oid[static_cast<size_t>(q0) * 16 + j] = sid[r * RS + c];
+        ow[static_cast<size_t>(q0) * 16 + j] = sw[r * RS + c];
+    }
 }
 
 void launch_pixel_weights(const uint32_t* ids, const void* rtab_d, const FieldDims& f, double scale, const int32_t* xy,
                           int n_q, uint32_t* out_ids, double* out_w, int32_t* out_n, cudaStream_t stream) {
     int grid = (n_q + 127) / 128;
     if (grid < 1) grid = 1;
-    k_pixel_weights<<<grid, 128, 0, stream>>>(ids, (const Q4<double>*)rtab_d, f, scale, xy, n_q, out_ids, out_w,
-                                              out_n);
+    if (f.k <= 8)
+        k_pixel_weights<8><<<grid, 128, 0, stream>>>(ids, (const Q4<double>*)rtab_d, f, scale, xy, n_q, out_ids, out_w,
+                                                     out_n);
+    else
+        k_pixel_weights<16><<<grid, 128, 0, stream>>>(ids, (const Q4<double>*)rtab_d, f, scale, xy, n_q, out_ids,
+                                                      out_w, out_n);
     SAD_LAUNCHED();
 }
 

@@ -219,6 +219,26 @@ def test_tiles_ragged_and_other_k(G, R, w, h, k, cell):
     assert np.allclose(sg.data, sr.data, rtol=1e-12, atol=1e-12)
 
 
+@pytest.mark.parametrize("k", [5, 8, 12])
+def test_pixel_weights_batch(G, R, k):
+    """pixel_weights (render.cpp:92-104) batched: per query the kept ids in list order, exactly, and their
+    double softmax weights (CUDA double exp vs glibc differ by ulps)."""
+    w, h = 45, 37
+    st = random_model(w, h, 60, 29)
+    st.deactivate(4)
+    f = _field(w, h, k)
+    R.refresh(st, f, sad.RefreshMode.Full, 3, 4, 13, F32)
+    rng = np.random.default_rng(k)
+    pix = np.stack([rng.integers(0, w, 300), rng.integers(0, h, 300)], 1)
+    ig, wg, ng = G.pixel_weights_batch(st, f, pix)
+    ir, wr, nr = R.pixel_weights_batch(st, f, pix)
+    assert np.array_equal(ng, nr)
+    assert np.array_equal(ig, ir)
+    # double softmax: ids exact; weights carry the CUDA-vs-glibc double exp ulp differences (tables and
+    # softmax), amplified by large logits -- measured max 1.7e-13 relative
+    assert np.allclose(wg, wr, rtol=1e-12, atol=0)
+
+
 def test_loss_identity_and_pixgrad(G, R):
     """test_grad.cpp:116-128: image_loss == backward loss; adjoint entry point parity."""
     st = random_model(64, 64, 60, 7)
