@@ -383,6 +383,21 @@ def test_fit_config1_first_iterations(G, R):
     assert d.max() <= 0.05, d
 
 
+def test_fit_fp64_default_config(G, R):
+    """The reference's TrainConfig defaults to fp64 (types.hpp:162): the all-double GPU fit follows the
+    reference trajectory within the north star's 0.05 dB over the first 20 iterations (CUDA double exp
+    may differ from glibc by an ulp, so bit-identity is not claimed for fp64)."""
+    tgt = synth_target(32, 24, 6)
+    cfg = sad.TrainConfig(iters=30, n_sites=60, seed=3)
+    assert cfg.fp64
+    a = G.fit(tgt, cfg)
+    b = R.fit(tgt, cfg)
+    pa = np.array([r.psnr for r in a.history[:20]])
+    pb = np.array([r.psnr for r in b.history[:20]])
+    assert np.max(np.abs(pa - pb)) <= 0.05
+    assert a.history[0].loss == pytest.approx(b.history[0].loss, rel=1e-12)
+
+
 def test_fit_deterministic(G):
     tgt = ramp_image(32, 32)
     cfg = sad.TrainConfig(iters=40, n_sites=25, seed=11, fp64=False)
