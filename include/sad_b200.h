@@ -144,6 +144,21 @@ sad_status sad_ctx_synchronize(sad_ctx* ctx);
 /* Number of kernel launches this context issued so far (evidence for the bench's gpu_launches). */
 uint64_t sad_ctx_launch_count(const sad_ctx* ctx);
 
+/* ---------------------------------------------------------------- device-resident objects
+ * A context can hold one SiteStore and one CandidateField in HBM.  Every per-call function below
+ * that takes a sites or field view also accepts NULL, meaning "the context's resident object": it is
+ * used in place (no host copy) and results stay on the device (fields produced by jfa_seed /
+ * run_passes / refresh, sites changed by adam_step / clamp_project / init_sites / prune / densify),
+ * with generation, pass_index, synced_generation and refresh_count tracked exactly as for views.
+ * Passing a host view instead replaces the workspace copy and invalidates that resident object. */
+sad_status sad_sites_alloc(sad_ctx* ctx, size_t capacity);            /* empty resident store */
+sad_status sad_sites_upload(sad_ctx* ctx, const sad_sites_view* sites); /* size/generation from the view */
+sad_status sad_sites_download(sad_ctx* ctx, sad_sites_view* sites);     /* capacity must hold `size` */
+sad_status sad_sites_info(sad_ctx* ctx, size_t* size, size_t* capacity, uint64_t* generation);
+sad_status sad_field_alloc(sad_ctx* ctx, int width, int height, int k, int cell); /* CandidateField::resize */
+sad_status sad_field_upload(sad_ctx* ctx, const sad_field_view* field);
+sad_status sad_field_download(sad_ctx* ctx, sad_field_view* field); /* ids: gw*gh*k or NULL (metadata only) */
+
 /* ---------------------------------------------------------------- candidates.hpp */
 /* jump_step (candidates.cpp:27-33) */
 sad_status sad_jump_step(uint32_t t, uint32_t b, uint32_t* out);

@@ -9,4 +9,4 @@ from .types import (AdamState, CandidateField, FitResult, GradBuffer, HistoryRow
                     RefreshMode, RunOpts, Site, SiteStats, SiteStore, StatsResult, Stencil, TrainConfig,
                     history_line, normalization_scale, psnr_from_loss, run_opts, kGradSlots, kChannels)
 from .api import (Backend, CudaError, EmptyList, InvalidArgument, NumericError, StaleField,  # noqa
-                  gpu_backend, load_library, LIB_PATH)
+                  ResidentField, ResidentSites, gpu_backend, load_library, LIB_PATH)

@@ -68,6 +68,11 @@ _P = C.c_void_p
 _dp = C.POINTER(C.c_double)
 
 
+def _ref(x):
+    """byref, or NULL for a resident object (its views are None)."""
+    return None if x is None else C.byref(x)
+
+
 def _ptr(a: np.ndarray, t=C.c_double):
     return a.ctypes.data_as(C.POINTER(t))
 
@@ -98,6 +103,54 @@ class Backend:
     def _thr(self):
         return (C.c_int(self.threads),) if self.kind == "ref" else ()
 
+    # ------------------------------------------------------------------ device-resident objects
+    def sites_alloc(self, capacity: int) -> "ResidentSites":
+        self._call("sites_alloc", C.c_size_t(capacity))
+        return ResidentSites(self)
+
+    def sites_upload(self, sites: SiteStore, capacity: Optional[int] = None) -> "ResidentSites":
+        """Upload into the context's resident store, with room for `capacity` sites (densify appends)."""
+        sv, keep = sites._view(capacity=capacity)
+        self._call("sites_upload", _ref(sv))
+        return ResidentSites(self)
+
+    def sites_download(self) -> SiteStore:
+        n, cap, gen = self._sites_info()
+        out = SiteStore(0)
+        sv, keep = out._view(capacity=max(n, 1))
+        self._call("sites_download", _ref(sv))
+        out._absorb(sv, keep)
+        return out
+
+    def _sites_info(self):
+        n, cap, gen = C.c_size_t(), C.c_size_t(), C.c_uint64()
+        self._call("sites_info", C.byref(n), C.byref(cap), C.byref(gen))
+        return n.value, cap.value, gen.value
+
+    def field_alloc(self, width: int, height: int, k: int, cell: int = 1) -> "ResidentField":
+        self._call("field_alloc", C.c_int(width), C.c_int(height), C.c_int(k), C.c_int(cell))
+        return ResidentField(self)
+
+    def field_upload(self, field: CandidateField) -> "ResidentField":
+        fv = field._view()
+        self._call("field_upload", _ref(fv))
+        return ResidentField(self)
+
+    def field_download(self) -> CandidateField:
+        m = self._field_meta()
+        f = CandidateField()
+        f.resize(m.width, m.height, m.k, m.cell)
+        fv = f._view()
+        self._call("field_download", _ref(fv))
+        f._absorb(fv)
+        return f
+
+    def _field_meta(self):
+        fv = _abi.FieldView()
+        fv.ids = None
+        self._call("field_download", C.byref(fv))
+        return fv
+
     # ------------------------------------------------------------------ candidates.hpp
     def jump_step(self, t: int, b: int) -> int:
         out = C.c_uint32()
@@ -113,7 +166,7 @@ class Backend:
     def jfa_seed(self, sites: SiteStore, field: CandidateField):
         sv, keep = sites._view()
         fv = field._view()
-        self._call("jfa_seed", C.byref(sv), C.byref(fv))
+        self._call("jfa_seed", _ref(sv), _ref(fv))
         field._absorb(fv)
 
     def run_passes(self, sites: SiteStore, field: CandidateField, seq: Sequence[PassSpec], inject: int,
@@ -121,7 +174,7 @@ class Backend:
         sv, keep = sites._view()
         fv = field._view()
         arr = (_abi.PassSpec * max(len(seq), 1))(*[_abi.PassSpec(p.step, int(p.stencil)) for p in seq])
-        self._call("run_passes", C.byref(sv), C.byref(fv), arr, C.c_int(len(seq)), C.c_int(inject),
+        self._call("run_passes", _ref(sv), _ref(fv), arr, C.c_int(len(seq)), C.c_int(inject),
                    C.c_uint64(seed), C.c_int(int(opts.fp64)), *self._thr())
         field._absorb(fv)
 
@@ -132,7 +185,7 @@ class Backend:
                 seed: int, opts: RunOpts = RunOpts()):
         sv, keep = sites._view()
         fv = field._view()
-        self._call("refresh", C.byref(sv), C.byref(fv), C.c_int(int(mode)), C.c_int(passes), C.c_int(inject),
+        self._call("refresh", _ref(sv), _ref(fv), C.c_int(int(mode)), C.c_int(passes), C.c_int(inject),
                    C.c_uint64(seed), C.c_int(int(opts.fp64)), *self._thr())
         field._absorb(fv)
 
@@ -140,7 +193,7 @@ class Backend:
         xy = np.ascontiguousarray(np.asarray(pixels, np.int32).reshape(-1, 2))
         out = np.full(xy.shape[0] * k, _abi.EMPTY_ID, np.uint32)
         sv, keep = sites._view()
-        self._call("exact_topk_batch", C.byref(sv), _ptr(xy, C.c_int32), C.c_size_t(xy.shape[0]), C.c_int(k),
+        self._call("exact_topk_batch", _ref(sv), _ptr(xy, C.c_int32), C.c_size_t(xy.shape[0]), C.c_int(k),
                    C.c_double(scale), C.c_int(int(fp64)), _ptr(out, C.c_uint32))
         return out.reshape(-1, k)
 
@@ -149,7 +202,7 @@ class Backend:
         out = ImageBuffer(field.width, field.height)
         sv, keep = sites._view()
         fv = field._view()
-        args = [C.byref(sv), C.byref(fv), C.c_int(int(opts.fp64))]
+        args = [_ref(sv), _ref(fv), C.c_int(int(opts.fp64))]
         if self.kind == "ref":
             args.append(C.c_int(self.threads))
         self._call("render_image", *args, _ptr(out.data))
@@ -163,7 +216,7 @@ class Backend:
         n = np.zeros(q, np.int32)
         sv, keep = sites._view()
         fv = field._view()
-        self._call("pixel_weights", C.byref(sv), C.byref(fv), _ptr(xy, C.c_int32), C.c_size_t(q),
+        self._call("pixel_weights", _ref(sv), _ref(fv), _ptr(xy, C.c_int32), C.c_size_t(q),
                    _ptr(ids, C.c_uint32), _ptr(w), _ptr(n, C.c_int32))
         return ids.reshape(q, 16), w.reshape(q, 16), n
 
@@ -175,7 +228,7 @@ class Backend:
         out = np.zeros(field.width * field.height, np.uint32)
         sv, keep = sites._view()
         fv = field._view()
-        self._call("render_id_map", C.byref(sv), C.byref(fv), _ptr(out, C.c_uint32))
+        self._call("render_id_map", _ref(sv), _ref(fv), _ptr(out, C.c_uint32))
         return out
 
     # ------------------------------------------------------------------ grad.hpp
@@ -189,7 +242,7 @@ class Backend:
         loss = C.c_double()
         sv, keep = sites._view()
         fv = field._view()
-        args = [C.byref(sv), C.byref(fv), _ptr(target.data), C.c_int(int(opts.fp64)), C.c_int(int(with_removal))]
+        args = [_ref(sv), _ref(fv), _ptr(target.data), C.c_int(int(opts.fp64)), C.c_int(int(with_removal))]
         if self.kind == "ref":
             args.append(C.c_int(self.threads))
         self._call("backward_image", *args, _ptr(g), C.byref(nf), C.byref(loss))
@@ -203,7 +256,7 @@ class Backend:
         loss = C.c_double()
         sv, keep = sites._view()
         fv = field._view()
-        self._call("image_loss", C.byref(sv), C.byref(fv), _ptr(target.data), C.c_int(int(opts.fp64)),
+        self._call("image_loss", _ref(sv), _ref(fv), _ptr(target.data), C.c_int(int(opts.fp64)),
                    C.byref(loss))
         return float(loss.value)
 
@@ -213,7 +266,7 @@ class Backend:
         nf = C.c_uint64()
         sv, keep = sites._view()
         fv = field._view()
-        self._call("backward_pixel_grad", C.byref(sv), C.byref(fv), _ptr(dl.data), C.c_int(int(opts.fp64)),
+        self._call("backward_pixel_grad", _ref(sv), _ref(fv), _ptr(dl.data), C.c_int(int(opts.fp64)),
                    _ptr(g), C.byref(nf))
         out.data = g[: sites.size() * 11].reshape(-1, 11).copy()
         out.nonfinite = int(nf.value)
@@ -228,7 +281,7 @@ class Backend:
         if gd.size == 0:
             gd = np.zeros(11)
         c = cfg.to_c()
-        self._call("adam_step", C.byref(sv), _ptr(gd), C.byref(av), C.c_int(width), C.c_int(height), C.byref(c))
+        self._call("adam_step", _ref(sv), _ptr(gd), C.byref(av), C.c_int(width), C.c_int(height), C.byref(c))
         sites._absorb(sv, keep)
         adam._absorb(av, akeep)
 
@@ -247,20 +300,20 @@ class Backend:
         gd = np.ascontiguousarray(g.data, dtype=np.float64).reshape(-1).copy()
         if gd.size == 0:
             gd = np.zeros(11)
-        self._call("tau_diffusion", C.byref(sv), C.byref(fv), C.c_double(lam), _ptr(gd))
+        self._call("tau_diffusion", _ref(sv), _ref(fv), C.c_double(lam), _ptr(gd))
         g.data = gd[: sites.size() * 11].reshape(-1, 11).copy()
 
     def clamp_project(self, sites: SiteStore, width, height, cfg: TrainConfig):
         sv, keep = sites._view()
         c = cfg.to_c()
-        self._call("clamp_project", C.byref(sv), C.c_int(width), C.c_int(height), C.byref(c))
+        self._call("clamp_project", _ref(sv), C.c_int(width), C.c_int(height), C.byref(c))
         sites._absorb(sv, keep)
 
     def init_sites(self, sites: SiteStore, target: ImageBuffer, n: int, cfg: TrainConfig):
         tmp = SiteStore(0)
         sv, keep = tmp._view(capacity=max(n, 1))
         c = cfg.to_c()
-        self._call("init_sites", C.byref(sv), _ptr(target.data), C.c_int(target.width), C.c_int(target.height),
+        self._call("init_sites", _ref(sv), _ptr(target.data), C.c_int(target.width), C.c_int(target.height),
                    C.c_int(n), C.byref(c))
         gen = sites.generation
         sites._absorb(sv, keep)
@@ -275,7 +328,7 @@ class Backend:
         valid = C.c_uint64()
         sv, keep = sites._view()
         fv = field._view()
-        args = [C.byref(sv), C.byref(fv), _ptr(target.data)]
+        args = [_ref(sv), _ref(fv), _ptr(target.data)]
         if self.kind == "ref":
             args.append(C.c_int(self.threads))
         self._call("accumulate_stats", *args, _ptr(buf), C.byref(valid))
@@ -289,7 +342,7 @@ class Backend:
         sv, keep = sites._view()
         sd = np.ascontiguousarray(stats.data.reshape(-1)) if stats.data.size else np.zeros(8)
         n = C.c_int()
-        self._call("prune", C.byref(sv), _ptr(sd), C.c_uint64(stats.valid_pixels), C.c_double(percentile),
+        self._call("prune", _ref(sv), _ptr(sd), C.c_uint64(stats.valid_pixels), C.c_double(percentile),
                    C.byref(n))
         sites._absorb(sv, keep)
         return n.value
@@ -304,7 +357,7 @@ class Backend:
         sd = np.ascontiguousarray(stats.data.reshape(-1)) if stats.data.size else np.zeros(8)
         c = cfg.to_c()
         n = C.c_int()
-        self._call("densify", C.byref(sv), C.byref(av), _ptr(sd), _ptr(target.data), C.c_int(target.width),
+        self._call("densify", _ref(sv), C.byref(av), _ptr(sd), _ptr(target.data), C.c_int(target.width),
                    C.c_int(target.height), C.c_double(percentile), C.byref(c), C.byref(n))
         sites._absorb(sv, keep)
         adam._absorb(av, akeep)
@@ -332,9 +385,9 @@ class Backend:
         """write_file (codec.cpp:147-177) into memory: the `.sad` container bytes."""
         sv, keep = sites._view()
         n = C.c_size_t()
-        self._call("encode", C.byref(sv), C.c_int(width), C.c_int(height), None, C.c_size_t(0), C.byref(n))
+        self._call("encode", _ref(sv), C.c_int(width), C.c_int(height), None, C.c_size_t(0), C.byref(n))
         buf = (C.c_uint8 * n.value)()
-        self._call("encode", C.byref(sv), C.c_int(width), C.c_int(height), buf, C.c_size_t(n.value), C.byref(n))
+        self._call("encode", _ref(sv), C.c_int(width), C.c_int(height), buf, C.c_size_t(n.value), C.byref(n))
         return bytes(buf)
 
     def decode_sites(self, data: bytes):
@@ -344,7 +397,7 @@ class Backend:
         sv, keep = st._view(capacity=count + 1)
         buf = (C.c_uint8 * len(data)).from_buffer_copy(data)
         w, h = C.c_int(), C.c_int()
-        self._call("decode", buf, C.c_size_t(len(data)), C.byref(sv), C.byref(w), C.byref(h))
+        self._call("decode", buf, C.c_size_t(len(data)), _ref(sv), C.byref(w), C.byref(h))
         st._absorb(sv, keep)
         return w.value, h.value, st
 
@@ -373,7 +426,7 @@ class Backend:
         st = SiteStore(0)
         sv, keep = st._view(capacity=cnt.value + 1)
         self._call("decode_render", buf, C.c_size_t(len(data)), C.c_int(k), C.c_int(passes), C.c_int(inject),
-                   C.c_uint64(seed), C.c_int(int(fp64)), _ptr(img.data), C.byref(sv))
+                   C.c_uint64(seed), C.c_int(int(fp64)), _ptr(img.data), _ref(sv))
         st._absorb(sv, keep)
         return img, st
 
@@ -416,7 +469,7 @@ class Backend:
                     self._call("fit_run_init", run)
                 else:
                     sv, keep = init._view()
-                    self._call("fit_run_store", run, C.byref(sv))
+                    self._call("fit_run_store", run, _ref(sv))
                 n = C.c_size_t()
                 nh = C.c_int()
                 sc = C.c_double()
@@ -435,7 +488,7 @@ class Backend:
                 self._call("fit", _ptr(target.data), C.c_int(w), C.c_int(h), C.byref(c), None, C.byref(hd))
             else:
                 sv, keep = init._view()
-                self._call("fit", _ptr(target.data), C.c_int(w), C.c_int(h), C.byref(c), C.byref(sv), C.byref(hd))
+                self._call("fit", _ptr(target.data), C.c_int(w), C.c_int(h), C.byref(c), _ref(sv), C.byref(hd))
             try:
                 n = C.c_size_t()
                 nh = C.c_int()
@@ -462,12 +515,12 @@ class Backend:
         hist = (_abi.HistoryRowC * max(cfg.iters, 1))()
         sc = C.c_double()
         if init is None:
-            self._call("fit", _ptr(target.data), C.c_int(w), C.c_int(h), C.byref(c), None, C.byref(sv), C.byref(fv),
+            self._call("fit", _ptr(target.data), C.c_int(w), C.c_int(h), C.byref(c), None, _ref(sv), _ref(fv),
                        hist, C.byref(sc))
         else:
             iv, ikeep = init._view()
-            self._call("fit", _ptr(target.data), C.c_int(w), C.c_int(h), C.byref(c), C.byref(iv), C.byref(sv),
-                       C.byref(fv), hist, C.byref(sc))
+            self._call("fit", _ptr(target.data), C.c_int(w), C.c_int(h), C.byref(c), C.byref(iv), _ref(sv),
+                       _ref(fv), hist, C.byref(sc))
         out._absorb(sv, keep)
         f._absorb(fv)
         rows = [HistoryRow(r.iter, r.loss, r.psnr, r.active_sites, r.ms) for r in hist[: cfg.iters]]
@@ -480,7 +533,7 @@ class Backend:
         f.resize(w, h, cfg.k)
         fv = f._view()
         hist = (_abi.HistoryRowC * max(nh, 1))()
-        download(C.byref(sv), C.byref(fv), hist)
+        download(_ref(sv), _ref(fv), hist)
         sv.size = n
         st._absorb(sv, keep)
         f._absorb(fv)
@@ -526,3 +579,43 @@ def gpu_backend(device: int = 0) -> Backend:
                 raise CudaError("sad_ctx_create: " + lib.sad_last_error().decode(errors="replace"))
             _gpu = Backend(lib, "sad_", "gpu", ctx=ctx)
         return _gpu
+
+
+class ResidentSites:
+    """The context's device-resident SiteStore (sad_sites_alloc / sad_sites_upload): pass it
+    wherever a SiteStore is expected to run on the device copy without host transfers."""
+
+    def __init__(self, backend: "Backend"):
+        self._B = backend
+
+    def _view(self, capacity=None):
+        return None, None
+
+    def _absorb(self, v, bufs):
+        pass
+
+    def size(self) -> int:
+        return self._B._sites_info()[0]
+
+    @property
+    def generation(self) -> int:
+        return self._B._sites_info()[2]
+
+
+class ResidentField:
+    """The context's device-resident CandidateField (sad_field_alloc / sad_field_upload)."""
+
+    def __init__(self, backend: "Backend"):
+        self._B = backend
+
+    def _view(self):
+        return None
+
+    def _absorb(self, v):
+        pass
+
+    def __getattr__(self, name):
+        if name in ("width", "height", "cell", "gw", "gh", "k", "synced_generation", "refresh_count",
+                    "pass_index"):
+            return getattr(self._B._field_meta(), name)
+        raise AttributeError(name)

@@ -798,13 +798,57 @@ void init_sites_device(Workspace& ws, int w, int h, int n, const sad_train_confi
 }  // namespace
 
 // ====================================================================== context
+// Device-resident SiteStore / CandidateField of a context: uploaded once, used by the
+// per-call functions when they get NULL views, downloaded on request.  A call with a host view
+// replaces the workspace copy and so invalidates the corresponding resident object.
+struct Resident {
+    bool sites = false, field = false;
+    size_t n = 0, capacity = 0;
+    uint64_t generation = 0;
+    sad_field_view fmeta{};  // ids unused
+};
+
 struct sad_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own = false;
     Workspace ws;
     uint64_t launches0 = 0;
+    Resident res;
 };
+
+// Resolve a sites argument: a host view is uploaded; NULL selects the resident store (its size and
+// generation are returned through `meta` for the staleness checks).
+static const sad_sites_view* sites_arg(sad_ctx* c, const sad_sites_view* s, sad_sites_view& meta, int extra_cap = 0) {
+    if (s) {
+        upload_sites(c->ws, s, extra_cap);
+        c->res.sites = false;
+        return s;
+    }
+    if (!c->res.sites) fail(SAD_EINVAL, "no resident sites: pass a view or call sad_sites_upload first");
+    if (extra_cap > 0) c->ws.ensure_cap(static_cast<int>(c->res.n) + extra_cap);
+    meta = sad_sites_view{};
+    meta.size = c->res.n;
+    meta.capacity = c->res.capacity;
+    meta.generation = c->res.generation;
+    return &meta;
+}
+
+// Resolve a field argument: a host view is (optionally) uploaded; NULL selects the resident field.
+static sad_field_view* field_arg(sad_ctx* c, sad_field_view* f, bool upload);
+static const sad_field_view* field_arg(sad_ctx* c, const sad_field_view* f) {
+    return field_arg(c, const_cast<sad_field_view*>(f), true);
+}
+static sad_field_view* field_arg(sad_ctx* c, sad_field_view* f, bool upload) {
+    if (f) {
+        check_field(f);
+        if (upload) upload_field(c->ws, f);
+        c->res.field = false;
+        return f;
+    }
+    if (!c->res.field) fail(SAD_EINVAL, "no resident field: pass a view or call sad_field_upload / sad_field_alloc");
+    return &c->res.fmeta;
+}
 
 struct sad_fit_run {
     sad_ctx* ctx = nullptr;
@@ -899,6 +943,98 @@ sad_status sad_ctx_synchronize(sad_ctx* c) {
 uint64_t sad_ctx_launch_count(const sad_ctx* c) { return sadk::launch_counter() - (c ? c->launches0 : 0); }
 
 // ====================================================================== candidates
+// ====================================================================== device-resident objects
+sad_status sad_sites_alloc(sad_ctx* c, size_t capacity) {
+    return guard([&] {
+        if (capacity > static_cast<size_t>(INT32_MAX / 2)) fail(SAD_EINVAL, "too many sites");
+        c->ws.ensure_cap(static_cast<int>(std::max<size_t>(capacity, 1)));
+        c->ws.patch_state(offsetof(DevState, n_sites), 0);
+        c->res.sites = true;
+        c->res.n = 0;
+        c->res.capacity = capacity;
+        c->res.generation = 0;
+    });
+}
+
+sad_status sad_sites_upload(sad_ctx* c, const sad_sites_view* s) {
+    return guard([&] {
+        if (!s) fail(SAD_EINVAL, "null sites view");
+        upload_sites(c->ws, s, static_cast<int>(s->capacity > s->size ? s->capacity - s->size : 0));
+        c->res.sites = true;
+        c->res.n = s->size;
+        c->res.capacity = std::max(s->capacity, s->size);
+        c->res.generation = s->generation;
+    });
+}
+
+sad_status sad_sites_download(sad_ctx* c, sad_sites_view* s) {
+    return guard([&] {
+        if (!s) fail(SAD_EINVAL, "null sites view");
+        if (!c->res.sites) fail(SAD_EINVAL, "no resident sites");
+        download_sites(c->ws, s, c->res.n);
+        s->generation = c->res.generation;
+    });
+}
+
+sad_status sad_sites_info(sad_ctx* c, size_t* size, size_t* capacity, uint64_t* generation) {
+    return guard([&] {
+        if (!c->res.sites) fail(SAD_EINVAL, "no resident sites");
+        if (size) *size = c->res.n;
+        if (capacity) *capacity = c->res.capacity;
+        if (generation) *generation = c->res.generation;
+    });
+}
+
+sad_status sad_field_alloc(sad_ctx* c, int width, int height, int k, int cell) {
+    return guard([&] {
+        if (width < 1 || height < 1) fail(SAD_EINVAL, "CandidateField: empty image");
+        if (k < 1 || k > 16) fail(SAD_EINVAL, "CandidateField: k out of range");
+        if (cell < 1) fail(SAD_EINVAL, "CandidateField: bad cell size");
+        Workspace& ws = c->ws;
+        ws.ensure_field(width, height, k, cell);
+        ws.cur = 0;
+        const size_t n = static_cast<size_t>(ws.fd.gw) * ws.fd.gh * k;
+        ck(cudaMemsetAsync(ws.ids[0].p, 0xff, 4 * n, ws.stream), "memset field");
+        sad_field_view& m = c->res.fmeta;  // CandidateField::resize (types.cpp:89-101)
+        m = sad_field_view{};
+        m.width = width;
+        m.height = height;
+        m.cell = cell;
+        m.gw = ws.fd.gw;
+        m.gh = ws.fd.gh;
+        m.k = k;
+        m.synced_generation = ~0ull;
+        c->res.field = true;
+    });
+}
+
+sad_status sad_field_upload(sad_ctx* c, const sad_field_view* f) {
+    return guard([&] {
+        upload_field(c->ws, f);
+        c->res.fmeta = *f;
+        c->res.fmeta.ids = nullptr;
+        c->res.field = true;
+    });
+}
+
+sad_status sad_field_download(sad_ctx* c, sad_field_view* f) {
+    return guard([&] {
+        if (!f) fail(SAD_EINVAL, "null field view");
+        if (!c->res.field) fail(SAD_EINVAL, "no resident field");
+        const sad_field_view& m = c->res.fmeta;
+        f->width = m.width;
+        f->height = m.height;
+        f->cell = m.cell;
+        f->gw = m.gw;
+        f->gh = m.gh;
+        f->k = m.k;
+        if (f->ids) download_field(c->ws, f);  // ids == NULL: metadata only
+        f->synced_generation = m.synced_generation;
+        f->refresh_count = m.refresh_count;
+        f->pass_index = m.pass_index;
+    });
+}
+
 sad_status sad_jump_step(uint32_t t, uint32_t b, uint32_t* out) {
     return guard([&] { *out = jump_step(t, b); });
 }
@@ -921,36 +1057,36 @@ sad_status sad_schedule_passes(int gw, int gh, int total, sad_pass_spec* out, in
     });
 }
 
-sad_status sad_jfa_seed(sad_ctx* c, const sad_sites_view* s, sad_field_view* f) {
+sad_status sad_jfa_seed(sad_ctx* c, const sad_sites_view* s_in, sad_field_view* f_in) {
     return guard([&] {
         Workspace& ws = c->ws;
-        upload_sites(ws, s);
-        check_field(f);
+        sad_sites_view sm;
+        const sad_sites_view* s = sites_arg(c, s_in, sm);
+        sad_field_view* f = field_arg(c, f_in, false);
         ws.ensure_field(f->width, f->height, f->k, f->cell);
         ws.cur = 0;
         sadk::launch_jfa_seed(ws.sites(), ws.st.p, ws.ids[0].p, ws.fd, norm_scale(f->width, f->height), ws.stream);
-        download_field(ws, f);
+        if (f_in) download_field(ws, f);
         f->synced_generation = s->generation;
     });
 }
 
-static void run_passes_call(sad_ctx* c, const sad_sites_view* s, sad_field_view* f, const std::vector<sad_pass_spec>& seq,
-                            int inject, uint64_t seed, int fp64, bool full) {
+static void run_passes_call(sad_ctx* c, const sad_sites_view* s_in, sad_field_view* f_in,
+                            const std::vector<sad_pass_spec>& seq, int inject, uint64_t seed, int fp64, bool full) {
     Workspace& ws = c->ws;
-    upload_sites(ws, s);
+    sad_sites_view sm;
+    const sad_sites_view* s = sites_arg(c, s_in, sm);
+    sad_field_view* f = field_arg(c, f_in, !full);
     if (full) {
-        check_field(f);
         ws.ensure_field(f->width, f->height, f->k, f->cell);
         ws.cur = 0;
         sadk::launch_jfa_seed(ws.sites(), ws.st.p, ws.ids[0].p, ws.fd, norm_scale(f->width, f->height), ws.stream);
-    } else {
-        upload_field(ws, f);
     }
     ws.patch_state(offsetof(DevState, pass_index), f->pass_index);
     ws.compute_active();
     build_tables(ws, fp64 != 0, true, false, false);
     passes_device(ws, seq, inject, seed, fp64 != 0, 0);
-    download_field(ws, f);
+    if (f_in) download_field(ws, f);
     f->pass_index += static_cast<uint32_t>(seq.size());
     f->synced_generation = s->generation;
 }
@@ -958,21 +1094,21 @@ static void run_passes_call(sad_ctx* c, const sad_sites_view* s, sad_field_view*
 sad_status sad_run_passes(sad_ctx* c, const sad_sites_view* s, sad_field_view* f, const sad_pass_spec* seq, int n_pass,
                           int inject, uint64_t seed, int fp64) {
     return guard([&] {
-        check_field(f);
         std::vector<sad_pass_spec> v(seq, seq + std::max(n_pass, 0));
         run_passes_call(c, s, f, v, inject, seed, fp64, false);
     });
 }
 
-sad_status sad_refresh(sad_ctx* c, const sad_sites_view* s, sad_field_view* f, int mode, int passes, int inject,
+sad_status sad_refresh(sad_ctx* c, const sad_sites_view* s, sad_field_view* f_in, int mode, int passes, int inject,
                        uint64_t seed, int fp64) {
     return guard([&] {
-        check_field(f);
+        sad_field_view* f = f_in ? f_in : field_arg(c, nullptr, false);
+        if (f_in) check_field(f_in);
         if (mode == SAD_REFRESH_FULL) {
-            run_passes_call(c, s, f, full_refresh_passes(f->gw, f->gh, passes), inject, seed, fp64, true);
+            run_passes_call(c, s, f_in, full_refresh_passes(f->gw, f->gh, passes), inject, seed, fp64, true);
         } else {
             std::vector<sad_pass_spec> v(static_cast<size_t>(passes < 0 ? 0 : passes), sad_pass_spec{1, 0});
-            run_passes_call(c, s, f, v, inject, seed, fp64, false);
+            run_passes_call(c, s, f_in, v, inject, seed, fp64, false);
         }
         f->refresh_count++;
     });
@@ -983,7 +1119,8 @@ sad_status sad_exact_topk_batch(sad_ctx* c, const sad_sites_view* s, const int32
     return guard([&] {
         if (k < 1 || k > 16) fail(SAD_EINVAL, "exact_topk: k out of range");
         Workspace& ws = c->ws;
-        upload_sites(ws, s);
+        sad_sites_view sm;
+        sites_arg(c, s, sm);
         ws.compute_active();
         // tables use the probe scale supplied by the caller
         sadk::launch_tables(fp64 != 0, ws.sites(), ws.st.p, scale, nullptr, nullptr, fp64 ? ws.rtab_d.p : ws.rtab.p,
@@ -1002,12 +1139,13 @@ sad_status sad_exact_topk_batch(sad_ctx* c, const sad_sites_view* s, const int32
 }
 
 // ====================================================================== render
-sad_status sad_render_image(sad_ctx* c, const sad_sites_view* s, const sad_field_view* f, int fp64, double* out) {
+sad_status sad_render_image(sad_ctx* c, const sad_sites_view* s_in, const sad_field_view* f_in, int fp64, double* out) {
     return guard([&] {
-        check_synced(s, f);
         Workspace& ws = c->ws;
-        upload_sites(ws, s);
-        upload_field(ws, f);
+        sad_sites_view sm;
+        const sad_sites_view* s = sites_arg(c, s_in, sm);
+        const sad_field_view* f = field_arg(c, f_in);
+        check_synced(s, f);
         build_tables(ws, fp64 != 0, false, false, true);
         size_t n = 3 * static_cast<size_t>(f->width) * f->height;
         if (fp64) {
@@ -1028,16 +1166,17 @@ sad_status sad_render_image(sad_ctx* c, const sad_sites_view* s, const sad_field
     });
 }
 
-sad_status sad_pixel_weights(sad_ctx* c, const sad_sites_view* s, const sad_field_view* f, const int32_t* xy,
+sad_status sad_pixel_weights(sad_ctx* c, const sad_sites_view* s_in, const sad_field_view* f_in, const int32_t* xy,
                              size_t n_q, uint32_t* ids, double* w, int32_t* n) {
     return guard([&] {
+        Workspace& ws = c->ws;
+        sad_sites_view sm;
+        const sad_sites_view* s = sites_arg(c, s_in, sm);
+        const sad_field_view* f = field_arg(c, f_in);
         check_synced(s, f);
         for (size_t q = 0; q < n_q; q++)
             if (xy[2 * q] < 0 || xy[2 * q + 1] < 0 || xy[2 * q] >= f->width || xy[2 * q + 1] >= f->height)
                 fail(SAD_EINVAL, "pixel_weights: pixel out of bounds");
-        Workspace& ws = c->ws;
-        upload_sites(ws, s);
-        upload_field(ws, f);
         build_tables(ws, true, false, false, true);
         DBuf<int32_t> dxy, dn;
         DBuf<uint32_t> did;
@@ -1058,12 +1197,13 @@ sad_status sad_pixel_weights(sad_ctx* c, const sad_sites_view* s, const sad_fiel
     });
 }
 
-sad_status sad_render_id_map(sad_ctx* c, const sad_sites_view* s, const sad_field_view* f, uint32_t* out) {
+sad_status sad_render_id_map(sad_ctx* c, const sad_sites_view* s_in, const sad_field_view* f_in, uint32_t* out) {
     return guard([&] {
-        check_synced(s, f);
         Workspace& ws = c->ws;
-        upload_sites(ws, s);
-        upload_field(ws, f);
+        sad_sites_view sm;
+        const sad_sites_view* s = sites_arg(c, s_in, sm);
+        const sad_field_view* f = field_arg(c, f_in);
+        check_synced(s, f);
         build_tables(ws, true, false, false, true);
         DBuf<uint32_t> d;
         size_t n = static_cast<size_t>(f->width) * f->height;
@@ -1075,16 +1215,17 @@ sad_status sad_render_id_map(sad_ctx* c, const sad_sites_view* s, const sad_fiel
     });
 }
 
-sad_status sad_tau_diffusion(sad_ctx* c, const sad_sites_view* s, const sad_field_view* f, double lambda,
+sad_status sad_tau_diffusion(sad_ctx* c, const sad_sites_view* s_in, const sad_field_view* f_in, double lambda,
                              double* grads) {
     return guard([&] {
         if (lambda == 0) return;
         if (lambda < 0 || lambda > 1) fail(SAD_EINVAL, "tau_diffusion: lambda out of [0,1]");
         if (!grads) fail(SAD_EINVAL, "tau_diffusion: null gradient buffer");
-        check_synced(s, f);
         Workspace& ws = c->ws;
-        upload_sites(ws, s);
-        upload_field(ws, f);
+        sad_sites_view sm;
+        const sad_sites_view* s = sites_arg(c, s_in, sm);
+        const sad_field_view* f = field_arg(c, f_in);
+        check_synced(s, f);
         ensure_tau(ws);
         const size_t n = s->size;
         std::vector<double> g0(n + 1), o(n + 1);
@@ -1100,12 +1241,13 @@ sad_status sad_tau_diffusion(sad_ctx* c, const sad_sites_view* s, const sad_fiel
 }
 
 // ====================================================================== grad
-static void backward_call(sad_ctx* c, const sad_sites_view* s, const sad_field_view* f, const double* img, int fp64,
-                          int mode, double* grads, uint64_t* nonfinite, double* loss) {
-    check_synced(s, f);
+static void backward_call(sad_ctx* c, const sad_sites_view* s_in, const sad_field_view* f_in, const double* img,
+                          int fp64, int mode, double* grads, uint64_t* nonfinite, double* loss) {
     Workspace& ws = c->ws;
-    upload_sites(ws, s);
-    upload_field(ws, f);
+    sad_sites_view sm;
+    const sad_sites_view* s = sites_arg(c, s_in, sm);
+    const sad_field_view* f = field_arg(c, f_in);
+    check_synced(s, f);
     size_t npx = static_cast<size_t>(f->width) * f->height;
     ws.ensure_target(npx);
     ck(cudaMemcpyAsync(ws.tgt_d.p, img, 24 * npx, cudaMemcpyHostToDevice, ws.stream), "H2D target");
@@ -1144,13 +1286,14 @@ sad_status sad_backward_pixel_grad(sad_ctx* c, const sad_sites_view* s, const sa
     return guard([&] { backward_call(c, s, f, dl, fp64, 2, grads, nonfinite, nullptr); });
 }
 
-sad_status sad_image_loss(sad_ctx* c, const sad_sites_view* s, const sad_field_view* f, const double* tgt, int fp64,
-                          double* loss) {
+sad_status sad_image_loss(sad_ctx* c, const sad_sites_view* s_in, const sad_field_view* f_in, const double* tgt,
+                          int fp64, double* loss) {
     return guard([&] {
-        check_synced(s, f);
         Workspace& ws = c->ws;
-        upload_sites(ws, s);
-        upload_field(ws, f);
+        sad_sites_view sm;
+        const sad_sites_view* s = sites_arg(c, s_in, sm);
+        const sad_field_view* f = field_arg(c, f_in);
+        check_synced(s, f);
         upload_target(ws, tgt, f->width, f->height);
         build_tables(ws, fp64 != 0, false, true, false);
         ws.zero_state_field(offsetof(DevState, loss), sizeof(double2));
@@ -1168,13 +1311,14 @@ sad_status sad_image_loss(sad_ctx* c, const sad_sites_view* s, const sad_field_v
 }
 
 // ====================================================================== train
-sad_status sad_adam_step(sad_ctx* c, sad_sites_view* s, const double* grads, sad_adam_view* a, int w, int h,
+sad_status sad_adam_step(sad_ctx* c, sad_sites_view* s_in, const double* grads, sad_adam_view* a, int w, int h,
                          const sad_train_config* cfg) {
     return guard([&] {
         Workspace& ws = c->ws;
+        sad_sites_view sm;
+        const sad_sites_view* s = sites_arg(c, s_in, sm);
         size_t n = s->size;
         if (a->sites != n && n > a->capacity) fail(SAD_ENOMEM, "adam capacity");
-        upload_sites(ws, s);
         // grads (n*11 values) -> (hi=value, lo=0) accumulators; moments -> slot-major
         std::vector<double2> g(static_cast<size_t>(11) * ws.cap, make_double2(0, 0));
         std::vector<double> m(static_cast<size_t>(10) * ws.cap, 0.0), v(static_cast<size_t>(10) * ws.cap, 0.0);
@@ -1199,7 +1343,7 @@ sad_status sad_adam_step(sad_ctx* c, sad_sites_view* s, const double* grads, sad
         ck(cudaMemcpyAsync(m.data(), ws.m.p, m.size() * 8, cudaMemcpyDeviceToHost, ws.stream), "D2H");
         ck(cudaMemcpyAsync(v.data(), ws.v.p, v.size() * 8, cudaMemcpyDeviceToHost, ws.stream), "D2H");
         DevState st = ws.get_state();
-        download_sites(ws, s, n);
+        if (s_in) download_sites(ws, s_in, n);
         for (size_t id = 0; id < n; id++)
             for (int k = 0; k < 10; k++) {
                 a->m[id * 10 + k] = m[k * ws.cap + id];
@@ -1208,17 +1352,25 @@ sad_status sad_adam_step(sad_ctx* c, sad_sites_view* s, const double* grads, sad
         a->sites = n;
         a->t = t;
         a->skipped += st.skipped;
-        s->generation += 2;  // adam_step and clamp_project each bump (train.cpp:167, 136)
+        // adam_step and clamp_project each bump (train.cpp:167, 136)
+        if (s_in) s_in->generation += 2;
+        else c->res.generation += 2;
     });
 }
 
-sad_status sad_clamp_project(sad_ctx* c, sad_sites_view* s, int w, int h, const sad_train_config* cfg) {
+sad_status sad_clamp_project(sad_ctx* c, sad_sites_view* s_in, int w, int h, const sad_train_config* cfg) {
     return guard([&] {
         Workspace& ws = c->ws;
-        upload_sites(ws, s);
+        sad_sites_view sm;
+        sites_arg(c, s_in, sm);
         sadk::launch_clamp(ws.sites(), ws.st.p, adam_hyper(*cfg, w, h), ws.stream);
-        download_sites(ws, s, s->size);
-        s->generation += 1;
+        if (s_in) {
+            download_sites(ws, s_in, s_in->size);
+            s_in->generation += 1;
+        } else {
+            ck(cudaStreamSynchronize(ws.stream), "clamp");
+            c->res.generation += 1;
+        }
     });
 }
 
@@ -1228,24 +1380,34 @@ sad_status sad_init_sites(sad_ctx* c, sad_sites_view* s, const double* tgt, int 
         size_t np = static_cast<size_t>(w) * h;
         if (w < 1 || h < 1) fail(SAD_EINVAL, "init_sites: empty image");
         if (n < 1 || static_cast<size_t>(n) > np) fail(SAD_EINVAL, "init_sites: count out of range");
-        if (static_cast<size_t>(n) > s->capacity) fail(SAD_ENOMEM, "sites view capacity too small");
+        if (s && static_cast<size_t>(n) > s->capacity) fail(SAD_ENOMEM, "sites view capacity too small");
         Workspace& ws = c->ws;
         ws.ensure_cap(n);
         upload_target(ws, tgt, w, h);
         init_sites_device(ws, w, h, n, *cfg);
-        download_sites(ws, s, static_cast<size_t>(n));
-        s->generation += 1 + static_cast<uint64_t>(n);
+        if (s) {  // host view
+            download_sites(ws, s, static_cast<size_t>(n));
+            s->generation += 1 + static_cast<uint64_t>(n);
+            c->res.sites = false;
+        } else {  // into the resident store
+            ck(cudaStreamSynchronize(ws.stream), "init_sites");
+            c->res.generation += 1 + static_cast<uint64_t>(n);
+            c->res.n = static_cast<size_t>(n);
+            c->res.capacity = std::max(c->res.capacity, static_cast<size_t>(ws.cap));
+            c->res.sites = true;
+        }
     });
 }
 
 // ====================================================================== budget
-sad_status sad_accumulate_stats(sad_ctx* c, const sad_sites_view* s, const sad_field_view* f, const double* tgt,
-                                double* stats, uint64_t* valid) {
+sad_status sad_accumulate_stats(sad_ctx* c, const sad_sites_view* s_in, const sad_field_view* f_in,
+                                const double* tgt, double* stats, uint64_t* valid) {
     return guard([&] {
-        if (f->synced_generation != s->generation) fail(SAD_ESTALE, "stats: candidate field is stale");
         Workspace& ws = c->ws;
-        upload_sites(ws, s);
-        upload_field(ws, f);
+        sad_sites_view sm;
+        const sad_sites_view* s = sites_arg(c, s_in, sm);
+        const sad_field_view* f = field_arg(c, f_in);
+        if (f->synced_generation != s->generation) fail(SAD_ESTALE, "stats: candidate field is stale");
         upload_target(ws, tgt, f->width, f->height);
         stats_device(ws);
         size_t n = s->size;
@@ -1267,32 +1429,40 @@ static void upload_stats(Workspace& ws, const double* stats, size_t n, uint64_t 
     ws.patch_state(offsetof(DevState, valid), valid);
 }
 
-sad_status sad_prune(sad_ctx* c, sad_sites_view* s, const double* stats, uint64_t valid, double pct, int* removed) {
+sad_status sad_prune(sad_ctx* c, sad_sites_view* s_in, const double* stats, uint64_t valid, double pct,
+                     int* removed) {
     return guard([&] {
         *removed = 0;
         if (pct <= 0) return;
         if (pct > 1) fail(SAD_EINVAL, "prune: percentile out of (0,1]");
         Workspace& ws = c->ws;
-        upload_sites(ws, s);
+        sad_sites_view sm;
+        const sad_sites_view* s = sites_arg(c, s_in, sm);
         upload_stats(ws, stats, s->size, valid);
         prune_device(ws, pct);
         DevState st = ws.get_state();
-        download_sites(ws, s, s->size);
         *removed = st.done;
-        s->generation += static_cast<uint64_t>(st.done);
+        if (s_in) {
+            download_sites(ws, s_in, s_in->size);
+            s_in->generation += static_cast<uint64_t>(st.done);
+        } else {
+            c->res.generation += static_cast<uint64_t>(st.done);
+        }
     });
 }
 
-sad_status sad_densify(sad_ctx* c, sad_sites_view* s, sad_adam_view* a, const double* stats, const double* tgt, int w,
-                       int h, double pct, const sad_train_config* cfg, int* done) {
+sad_status sad_densify(sad_ctx* c, sad_sites_view* s_in, sad_adam_view* a, const double* stats, const double* tgt,
+                       int w, int h, double pct, const sad_train_config* cfg, int* done) {
     return guard([&] {
         *done = 0;
         if (pct <= 0) return;
         if (pct > 1) fail(SAD_EINVAL, "densify: percentile out of (0,1]");
         Workspace& ws = c->ws;
-        size_t n = s->size;
-        int room = static_cast<int>(std::min(s->capacity, a->capacity)) - static_cast<int>(n);
-        upload_sites(ws, s, std::max(room, 0));
+        const size_t cap_s = s_in ? s_in->capacity : c->res.capacity;
+        size_t n = s_in ? s_in->size : c->res.n;
+        int room = static_cast<int>(std::min(cap_s, a->capacity)) - static_cast<int>(n);
+        sad_sites_view sm;
+        const sad_sites_view* s = sites_arg(c, s_in, sm, std::max(room, 0));
         upload_stats(ws, stats, n, 0);
         upload_target(ws, tgt, w, h);
         std::vector<double> m(static_cast<size_t>(10) * ws.cap, 0.0), v(static_cast<size_t>(10) * ws.cap, 0.0);
@@ -1316,7 +1486,8 @@ sad_status sad_densify(sad_ctx* c, sad_sites_view* s, sad_adam_view* a, const do
         if (nn > s->capacity || nn > a->capacity) fail(SAD_ENOMEM, "densify: sites capacity");
         ck(cudaMemcpyAsync(m.data(), ws.m.p, m.size() * 8, cudaMemcpyDeviceToHost, ws.stream), "D2H");
         ck(cudaMemcpyAsync(v.data(), ws.v.p, v.size() * 8, cudaMemcpyDeviceToHost, ws.stream), "D2H");
-        download_sites(ws, s, nn);
+        if (s_in) download_sites(ws, s_in, nn);
+        else ck(cudaStreamSynchronize(ws.stream), "densify");
         size_t rows = std::max(nn, a->sites);
         for (size_t id = 0; id < rows; id++)
             for (int k = 0; k < 10; k++) {
@@ -1325,7 +1496,12 @@ sad_status sad_densify(sad_ctx* c, sad_sites_view* s, sad_adam_view* a, const do
             }
         a->sites = rows;
         *done = st.done;
-        s->generation += 2 * static_cast<uint64_t>(st.done);
+        if (s_in) {
+            s_in->generation += 2 * static_cast<uint64_t>(st.done);
+        } else {
+            c->res.generation += 2 * static_cast<uint64_t>(st.done);
+            c->res.n = nn;
+        }
     });
 }
 

@@ -1,0 +1,94 @@
+"""Device-resident SiteStore / CandidateField (sad_sites_{alloc,upload,download},
+sad_field_{alloc,upload,download}): a refresh -> render -> backward -> Adam -> event chain run on the
+context's resident objects (NULL views across the C ABI, no host copies in between) gives bit-for-bit
+the results of the host-view calls, with the reference's generation / pass-index bookkeeping."""
+import numpy as np
+import pytest
+
+import paper_2604_21984_b200 as sad
+from tests.fixtures import random_model, random_target
+
+pytestmark = pytest.mark.gpu
+F32 = sad.RunOpts(fp64=False)
+
+
+def _field(w, h, k=8):
+    f = sad.CandidateField()
+    f.resize(w, h, k)
+    return f
+
+
+def test_resident_chain_matches_host_views():
+    G = sad.gpu_backend(0)
+    w, h = 64, 48
+    st = random_model(w, h, 90, 7)
+    tgt = random_target(w, h, 8)
+    cfg = sad.TrainConfig()
+    # host-view path
+    f = _field(w, h)
+    G.refresh(st, f, sad.RefreshMode.Full, 4, 4, 7, F32)
+    G.refresh(st, f, sad.RefreshMode.WarmStart, 2, 4, 9, F32)
+    img = G.render_image(st, f, F32).data
+    g_host = sad.GradBuffer()
+    l_host = G.backward_image(st, f, tgt, g_host, F32, False)
+    st_host = st.copy()
+    a_host = sad.AdamState(st.size())
+    G.adam_step(st_host, g_host, a_host, w, h, cfg)
+
+    # resident path
+    S = G.sites_upload(st)
+    F = G.field_alloc(w, h, 8)
+    assert S.size() == st.size() and S.generation == st.generation
+    G.refresh(S, F, sad.RefreshMode.Full, 4, 4, 7, F32)
+    G.refresh(S, F, sad.RefreshMode.WarmStart, 2, 4, 9, F32)
+    fd = G.field_download()
+    assert np.array_equal(fd.ids, f.ids)
+    assert (fd.pass_index, fd.refresh_count, fd.synced_generation) == (f.pass_index, f.refresh_count,
+                                                                        f.synced_generation)
+    assert np.array_equal(G.render_image(S, F, F32).data, img)
+    g_res = sad.GradBuffer()
+    assert G.backward_image(S, F, tgt, g_res, F32, False) == l_host
+    assert np.array_equal(g_res.data, g_host.data)
+    a_res = sad.AdamState(st.size())
+    G.adam_step(S, g_res, a_res, w, h, cfg)
+    sd = G.sites_download()
+    for p in ("x", "y", "log_tau", "radius", "col_r", "dir_x", "dir_y", "aniso", "active"):
+        assert np.array_equal(getattr(sd, p), getattr(st_host, p)), p
+    assert sd.generation == st_host.generation
+    assert np.array_equal(a_res.m, a_host.m) and a_res.t == a_host.t
+    # sites moved: the resident field is stale for them, exactly like the reference's check_synced
+    with pytest.raises(sad.StaleField):
+        G.render_image(S, F, F32)
+
+
+def test_resident_events_and_invalidation():
+    G = sad.gpu_backend(0)
+    w, h = 48, 48
+    st = random_model(w, h, 40, 11)
+    tgt = random_target(w, h, 12)
+    cfg = sad.TrainConfig()
+    f = _field(w, h)
+    G.refresh(st, f, sad.RefreshMode.Full, 4, 4, 7, F32)
+    stats = G.accumulate_stats(st, f, tgt)
+    a, ma = st.copy(), sad.AdamState(st.size())
+    G.prune(a, stats, 0.2)
+    G.densify(a, ma, stats, tgt, 0.5, cfg)
+
+    S = G.sites_upload(st)
+    F = G.field_upload(f)
+    rs = G.accumulate_stats(S, F, tgt)
+    assert rs.valid_pixels == stats.valid_pixels and np.array_equal(rs.data, stats.data)
+    mb = sad.AdamState(st.size())
+    G.prune(S, rs, 0.2)
+    # densify appends: re-upload the pruned store with room for the children
+    cur = G.sites_download()
+    S = G.sites_upload(cur, capacity=2 * cur.size())
+    nd = G.densify(S, mb, rs, tgt, 0.5, cfg)
+    sd = G.sites_download()
+    assert nd > 0 and sd.size() == a.size()
+    for p in ("x", "y", "log_tau", "radius", "active"):
+        assert np.array_equal(getattr(sd, p), getattr(a, p)), p
+    # a host-view call replaces the workspace copy: the resident sites are gone
+    G.render_image(st, f, F32)
+    with pytest.raises(sad.InvalidArgument):
+        G.render_image(S, F, F32)
