@@ -251,6 +251,19 @@ sad_status sad_bpp(size_t count, int width, int height, double* out);
 sad_status sad_decode_render(sad_ctx* ctx, const uint8_t* buf, size_t n, int k, int passes, int inject,
                              uint64_t seed, int fp64, double* out_rgb, sad_sites_view* out_sites);
 
+/* ---------------------------------------------------------------- fit / fit_store in one call
+ * fit (train.hpp:62-63, train.cpp:295-311) and fit_store (train.hpp:66-68): target upload, the whole
+ * resident loop, result download.  out_sites->capacity >= sad_fit_capacity(); out_field (optional)
+ * needs an ids buffer of W*H*k (cell 1; metadata is filled in); history (optional) holds cfg->iters
+ * rows; schedule_scale (optional) receives FitResult::schedule_scale. */
+sad_status sad_fit_capacity(int width, int height, const sad_train_config* cfg, size_t n_init, size_t* capacity);
+sad_status sad_fit(sad_ctx* ctx, const double* target_rgb, int width, int height, const sad_train_config* cfg,
+                   sad_sites_view* out_sites, sad_field_view* out_field, sad_history_row* history,
+                   double* schedule_scale);
+sad_status sad_fit_store(sad_ctx* ctx, const double* target_rgb, int width, int height,
+                         const sad_sites_view* initial_sites, const sad_train_config* cfg, sad_sites_view* out_sites,
+                         sad_field_view* out_field, sad_history_row* history, double* schedule_scale);
+
 /* ---------------------------------------------------------------- resident fit (train.cpp:221-311) */
 /* Allocates every device buffer for a W x H fit.  `n_init` = 0 lets fit() choose (bpp / n_sites). */
 sad_status sad_fit_create(sad_ctx* ctx, int width, int height, const sad_train_config* cfg,

@@ -437,6 +437,36 @@ class Backend:
     def fit_store(self, sites: SiteStore, target: ImageBuffer, cfg: TrainConfig) -> FitResult:
         return self._fit(target, cfg, sites)
 
+    def fit_oneshot(self, target: ImageBuffer, cfg: TrainConfig, init: Optional[SiteStore] = None) -> FitResult:
+        """sad_fit / sad_fit_store: the single C call an FFI binding would make (no cached run)."""
+        c = cfg.to_c()
+        cap = C.c_size_t()
+        self._call("fit_capacity", C.c_int(target.width), C.c_int(target.height), C.byref(c),
+                   C.c_size_t(init.size() if init is not None else 0), C.byref(cap))
+        sc = C.c_double()
+        n_hist = max(cfg.iters, 1)
+
+        def run(sv, fv, hist):
+            if init is None:
+                self._call("fit", _ptr(target.data), C.c_int(target.width), C.c_int(target.height), C.byref(c),
+                           sv, fv, hist, C.byref(sc))
+            else:
+                iv, ikeep = init._view()
+                self._call("fit_store", _ptr(target.data), C.c_int(target.width), C.c_int(target.height),
+                           _ref(iv), C.byref(c), sv, fv, hist, C.byref(sc))
+
+        st = SiteStore(0)
+        sv, keep = st._view(capacity=max(int(cap.value), 1))
+        f = CandidateField()
+        f.resize(target.width, target.height, cfg.k)
+        fv = f._view()
+        hist = (_abi.HistoryRowC * n_hist)()
+        run(_ref(sv), _ref(fv), hist)
+        st._absorb(sv, keep)
+        f._absorb(fv)
+        rows = [HistoryRow(r.iter, r.loss, r.psnr, r.active_sites, r.ms) for r in hist[:cfg.iters]]
+        return FitResult(st, f, rows, sc.value)
+
     def _fit_run(self, w, h, c):
         """Resident fit runs are cached per (shape, config): repeated fits reuse the device workspace
         (sites, field, record pools, graphs) instead of reallocating ~hundreds of MB per call."""
@@ -544,7 +574,7 @@ class Backend:
 _NO_CTX = {"jump_step", "full_refresh_passes", "schedule_passes", "bpp_target_count", "simulate_schedule",
            "plan_schedule", "fit_set_target", "fit_set_target_device", "fit_run_init", "fit_run_store",
            "fit_info", "fit_download", "fit_render_device", "fit_timing", "fit_bench", "fit_set_profiling",
-           "fit_point_query", "encode", "decode", "decode_header", "bpp",
+           "fit_point_query", "fit_capacity", "encode", "decode", "decode_header", "bpp",
            "last_error"}
 
 # ---------------------------------------------------------------------- product binding

@@ -17,6 +17,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <memory>
 #include <vector>
 
 using sadk::DevState;
@@ -1877,6 +1878,52 @@ sad_status sad_fit_download(sad_fit_run* r, sad_sites_view* s, sad_field_view* f
             f->refresh_count = 0;
         }
         if (hist) std::copy(r->hist.begin(), r->hist.end(), hist);
+    });
+}
+
+// ---- one-shot fit / fit_store (train.hpp:62-68, train.cpp:295-311) over the resident run
+sad_status sad_fit_capacity(int w, int h, const sad_train_config* cfg, size_t n_init, size_t* cap) {
+    return guard([&] {
+        if (!cfg || !cap) fail(SAD_EINVAL, "null argument");
+        sad_train_config v = *cfg;
+        validate(v, w, h);
+        const int n0 = n_init ? static_cast<int>(n_init) : initial_count(v, w, h);
+        *cap = static_cast<size_t>(capacity_bound(v, n0, 1.0, v.target_bpp > 0));  // schedule scale <= 1
+    });
+}
+
+static void fit_once(sad_ctx* c, const double* rgb, int w, int h, const sad_train_config* cfg,
+                     const sad_sites_view* init, sad_sites_view* out_sites, sad_field_view* out_field,
+                     sad_history_row* hist, double* scale) {
+    auto chk = [](sad_status st) {
+        if (st != SAD_OK) fail(st, sad_last_error());
+    };
+    if (!rgb || !cfg || !out_sites) fail(SAD_EINVAL, "null argument");
+    sad_fit_run* r = nullptr;
+    chk(sad_fit_create(c, w, h, cfg, &r));
+    std::unique_ptr<sad_fit_run, void (*)(sad_fit_run*)> hold(r, sad_fit_destroy);
+    chk(sad_fit_set_target(r, rgb));
+    chk(init ? sad_fit_run_store(r, init) : sad_fit_run_init(r));
+    size_t n = 0;
+    int nh = 0;
+    double sc = 0;
+    chk(sad_fit_info(r, &n, &nh, &sc));
+    if (out_sites->capacity < n) fail(SAD_ENOMEM, "fit: output sites capacity (see sad_fit_capacity)");
+    chk(sad_fit_download(r, out_sites, out_field, hist));
+    if (scale) *scale = sc;
+}
+
+sad_status sad_fit(sad_ctx* c, const double* rgb, int w, int h, const sad_train_config* cfg, sad_sites_view* out_sites,
+                   sad_field_view* out_field, sad_history_row* hist, double* scale) {
+    return guard([&] { fit_once(c, rgb, w, h, cfg, nullptr, out_sites, out_field, hist, scale); });
+}
+
+sad_status sad_fit_store(sad_ctx* c, const double* rgb, int w, int h, const sad_sites_view* init,
+                         const sad_train_config* cfg, sad_sites_view* out_sites, sad_field_view* out_field,
+                         sad_history_row* hist, double* scale) {
+    return guard([&] {
+        if (!init) fail(SAD_EINVAL, "fit_store: null initial sites");
+        fit_once(c, rgb, w, h, cfg, init, out_sites, out_field, hist, scale);
     });
 }
 

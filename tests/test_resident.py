@@ -92,3 +92,32 @@ def test_resident_events_and_invalidation():
     G.render_image(st, f, F32)
     with pytest.raises(sad.InvalidArgument):
         G.render_image(S, F, F32)
+
+
+def test_oneshot_fit_and_fit_store():
+    """sad_fit / sad_fit_store (one C call, what a cgo/JNI binding uses) equal the run-based API."""
+    from tests.fixtures import synth_target
+    G = sad.gpu_backend(0)
+    tgt = synth_target(40, 32, 5)
+    cfg = sad.TrainConfig(iters=60, target_bpp=4.0, fp64=False, seed=5, densify_start=10, densify_every=10,
+                          prune_start=20, prune_every=20)
+    a = G.fit(tgt, cfg)
+    b = G.fit_oneshot(tgt, cfg)
+    assert [sad.history_line(r) for r in a.history] == [sad.history_line(r) for r in b.history]
+    assert a.schedule_scale == b.schedule_scale
+    assert np.array_equal(a.field.ids, b.field.ids) and a.field.pass_index == b.field.pass_index
+    for p in ("x", "y", "log_tau", "active"):
+        assert np.array_equal(getattr(a.sites, p), getattr(b.sites, p)), p
+    init = a.sites
+    c = G.fit_store(init, tgt, sad.TrainConfig(iters=20, fp64=False, seed=2))
+    d = G.fit_oneshot(tgt, sad.TrainConfig(iters=20, fp64=False, seed=2), init=init)
+    assert [sad.history_line(r) for r in c.history] == [sad.history_line(r) for r in d.history]
+    assert np.array_equal(c.sites.x, d.sites.x)
+    # an undersized output store is refused
+    import ctypes as C
+    st = sad.SiteStore(0)
+    sv, keep = st._view(capacity=1)
+    cc = cfg.to_c()
+    with pytest.raises(sad.api.CapacityError):
+        G._call("fit", tgt.data.ctypes.data_as(C.POINTER(C.c_double)), C.c_int(40), C.c_int(32), C.byref(cc),
+                C.byref(sv), None, None, None)
