@@ -159,6 +159,10 @@ sad_status sad_field_alloc(sad_ctx* ctx, int width, int height, int k, int cell)
 sad_status sad_field_upload(sad_ctx* ctx, const sad_field_view* field);
 sad_status sad_field_download(sad_ctx* ctx, sad_field_view* field); /* ids: gw*gh*k or NULL (metadata only) */
 
+/* The device ports of glibc's exp (double; single != 0: expf) the kernels use, applied to n host
+ * values -- exposed so their bit-identity with the host libm can be verified. */
+sad_status sad_math_exp(sad_ctx* ctx, const double* x, double* y, size_t n, int single);
+
 /* ---------------------------------------------------------------- candidates.hpp */
 /* jump_step (candidates.cpp:27-33) */
 sad_status sad_jump_step(uint32_t t, uint32_t b, uint32_t* out);

@@ -24,6 +24,7 @@
 #include <cstdio>
 #include <unistd.h>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -173,6 +174,9 @@ FitResult fit_replica(SiteStore st, const ImageBuffer& target, TrainConfig cfg, 
     refresh(st, field, RefreshMode::Full, kEventRefreshPasses, cfg.inject, cfg.seed, opts);
     phase[4] += ms(t0);
     GradBuffer gb;
+    // SAD_REF_STOP_AT=t (divergence hunting): stop after iteration t, keep the field as it is then
+    const char* stop_env = std::getenv("SAD_REF_STOP_AT");
+    const int stop_at = stop_env ? std::atoi(stop_env) : 0;
     for (int t = 1; t <= cfg.iters; t++) {
         auto tick = clk::now();
         if ((t - 1) % cfg.refresh_every == 0) {
@@ -216,10 +220,11 @@ FitResult fit_replica(SiteStore st, const ImageBuffer& target, TrainConfig cfg, 
         row.active_sites = static_cast<int>(st.active_count());
         row.ms = ms(tick);
         out.history.push_back(row);
+        if (stop_at == t) break;
     }
     st.active_ids();
     auto f = clk::now();
-    refresh(st, field, RefreshMode::Full, cfg.final_passes, cfg.inject, cfg.seed, opts);
+    if (!stop_at) refresh(st, field, RefreshMode::Full, cfg.final_passes, cfg.inject, cfg.seed, opts);
     phase[4] += ms(f);
     out.sites = std::move(st);
     out.field = std::move(field);

@@ -54,9 +54,9 @@ __global__ void k_tables(SitesDev s, const DevState* __restrict__ st, double sca
         } else {
             double hx = half_rt(x), hy = half_rt(y), hlt = half_rt(lt), hr = half_rt(r);
             double hux = half_rt(ux), huy = half_rt(uy), han = half_rt(an);
-            double ea = exp(han), ia = exp(-han);
+            double ea = sad_dexp(han), ia = sad_dexp(-han);
             double vx = -huy, vy = hux;
-            a = {static_cast<T>(hx), static_cast<T>(hy), static_cast<T>(exp(hlt)), static_cast<T>(hr)};
+            a = {static_cast<T>(hx), static_cast<T>(hy), static_cast<T>(sad_dexp(hlt)), static_cast<T>(hr)};
             b = {static_cast<T>(ea * hux * hux + ia * vx * vx), static_cast<T>(ea * hux * huy + ia * vx * vy),
                  static_cast<T>(ea * huy * huy + ia * vy * vy), T(1)};
         }
@@ -70,8 +70,8 @@ __global__ void k_tables(SitesDev s, const DevState* __restrict__ st, double sca
             b = {T(1), T(1), T(1), T(0)};
             c = {T(0), T(0), T(0), T(0)};
         } else {
-            a = {static_cast<T>(x), static_cast<T>(y), static_cast<T>(exp(lt)), static_cast<T>(r)};
-            b = {static_cast<T>(exp(an)), static_cast<T>(exp(-an)), static_cast<T>(ux), static_cast<T>(uy)};
+            a = {static_cast<T>(x), static_cast<T>(y), static_cast<T>(sad_dexp(lt)), static_cast<T>(r)};
+            b = {static_cast<T>(sad_dexp(an)), static_cast<T>(sad_dexp(-an)), static_cast<T>(ux), static_cast<T>(uy)};
             c = {static_cast<T>(cr), static_cast<T>(cg), static_cast<T>(cb), T(1)};
         }
         gtab[3 * id] = a;
@@ -84,9 +84,9 @@ __global__ void k_tables(SitesDev s, const DevState* __restrict__ st, double sca
             a = {T(0), T(0), T(0), T(0)};
             b = {T(1), T(0), T(1), T(0)};
         } else {
-            double ea = exp(an), ia = exp(-an);
+            double ea = sad_dexp(an), ia = sad_dexp(-an);
             double vx = -uy, vy = ux;
-            a = {static_cast<T>(x), static_cast<T>(y), static_cast<T>(exp(lt)), static_cast<T>(r)};
+            a = {static_cast<T>(x), static_cast<T>(y), static_cast<T>(sad_dexp(lt)), static_cast<T>(r)};
             b = {static_cast<T>(ea * ux * ux + ia * vx * vx), static_cast<T>(ea * ux * uy + ia * vx * vy),
                  static_cast<T>(ea * uy * uy + ia * vy * vy), T(1)};
         }
@@ -137,7 +137,7 @@ __device__ __forceinline__ double packed_logit_d(const SitesDev& s, uint32_t id,
     double x = half_rt(p[0 * cap + id]), y = half_rt(p[1 * cap + id]);
     double lt = half_rt(p[2 * cap + id]), r = half_rt(p[3 * cap + id]);
     double ux = half_rt(p[7 * cap + id]), uy = half_rt(p[8 * cap + id]), an = half_rt(p[9 * cap + id]);
-    double ea = exp(an), ia = exp(-an);
+    double ea = sad_dexp(an), ia = sad_dexp(-an);
     double vx = -uy, vy = ux;
     double gxx = ea * ux * ux + ia * vx * vx;
     double gxy = ea * ux * uy + ia * vx * vy;
@@ -146,7 +146,7 @@ __device__ __forceinline__ double packed_logit_d(const SitesDev& s, uint32_t id,
     double q = gxx * dx * dx + 2.0 * gxy * dx * dy + gyy * dy * dy;
     if (q < 0) q = 0;
     double d = __dsqrt_rn(q) * scale - r * scale;
-    return -exp(lt) * d;
+    return -sad_dexp(lt) * d;
 }
 
 __global__ void k_jfa_seed(SitesDev s, const DevState* __restrict__ st, uint32_t* __restrict__ ids, FieldDims f,
@@ -1025,7 +1025,7 @@ __global__ void __launch_bounds__(128) k_pixel_weights(const uint32_t* __restric
     for (int i = 0; i < KM; i++) {
         w[i] = 0;
         if (ok[i]) {
-            w[i] = exp(lg[i] - best);
+            w[i] = sad_dexp(lg[i] - best);
             sum += w[i];
         }
     }
@@ -2127,7 +2127,7 @@ __global__ void __launch_bounds__(64) k_stats(const uint32_t* __restrict__ ids, 
 #pragma unroll
         for (int i = 0; i < KM; i++)
             if (i < n) {
-                w[i] = exp(lg[i] - best);
+                w[i] = sad_dexp(lg[i] - best);
                 wsum += w[i];
             }
         double invw = 1.0 / wsum;
@@ -2279,7 +2279,7 @@ __global__ void __launch_bounds__(128) k_stats2(const uint32_t* __restrict__ ids
     double w[H];
     double wpart = 0;
 #pragma unroll
-    for (int j = 0; j < H; j++) w[j] = ok[j] ? exp(lg[j] - best) : 0.0;
+    for (int j = 0; j < H; j++) w[j] = ok[j] ? sad_dexp(lg[j] - best) : 0.0;
     if (half == 0) {
 #pragma unroll
         for (int j = 0; j < H; j++)
@@ -2684,14 +2684,14 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
         const double ux = pp[7 * cap + id], uy = pp[8 * cap + id], an = pp[9 * cap + id];
         if (lane16 == 0 && pack) {
             Q4<T> a{T(0), T(0), T(0), T(0)};
-            if (act) a = {static_cast<T>(half_rt(x)), static_cast<T>(half_rt(y)), static_cast<T>(exp(half_rt(lt))),
+            if (act) a = {static_cast<T>(half_rt(x)), static_cast<T>(half_rt(y)), static_cast<T>(sad_dexp(half_rt(lt))),
                           static_cast<T>(half_rt(r))};
             pack[2 * id] = a;
         } else if (lane16 == 1 && pack) {
             Q4<T> b{T(1), T(0), T(1), T(0)};
             if (act) {
                 double hux = half_rt(ux), huy = half_rt(uy), han = half_rt(an);
-                double ea = exp(han), ia = exp(-han);
+                double ea = sad_dexp(han), ia = sad_dexp(-han);
                 double vx = -huy, vy = hux;
                 b = {static_cast<T>(ea * hux * hux + ia * vx * vx), static_cast<T>(ea * hux * huy + ia * vx * vy),
                      static_cast<T>(ea * huy * huy + ia * vy * vy), T(1)};
@@ -2699,11 +2699,11 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
             pack[2 * id + 1] = b;
         } else if (lane16 == 2 && gtab) {
             Q4<T> a{T(0), T(0), T(0), T(0)};
-            if (act) a = {static_cast<T>(x), static_cast<T>(y), static_cast<T>(exp(lt)), static_cast<T>(r)};
+            if (act) a = {static_cast<T>(x), static_cast<T>(y), static_cast<T>(sad_dexp(lt)), static_cast<T>(r)};
             gtab[3 * id] = a;
         } else if (lane16 == 3 && gtab) {
             Q4<T> b{T(1), T(1), T(1), T(0)};
-            if (act) b = {static_cast<T>(exp(an)), static_cast<T>(exp(-an)), static_cast<T>(ux), static_cast<T>(uy)};
+            if (act) b = {static_cast<T>(sad_dexp(an)), static_cast<T>(sad_dexp(-an)), static_cast<T>(ux), static_cast<T>(uy)};
             gtab[3 * id + 1] = b;
         } else if (lane16 == 4 && gtab) {
             Q4<T> c{T(0), T(0), T(0), T(0)};
@@ -2794,6 +2794,19 @@ void launch_tau_mix(const uint64_t* uniq, const int* count, int max_items, int n
     int grid = (max_items + 255) / 256;
     if (grid < 1) grid = 1;
     k_tau_mix<<<grid, 256, 0, stream>>>(uniq, count, nb, g0, lambda, out);
+    SAD_LAUNCHED();
+}
+
+// The device libm ports the kernels use, exposed for verification against the host's glibc.
+__global__ void k_math(const double* __restrict__ x, double* __restrict__ y, size_t n, int which) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    y[i] = which == 0 ? sad_dexp(x[i]) : static_cast<double>(sad_expf(static_cast<float>(x[i])));
+}
+
+void launch_math(const double* x, double* y, size_t n, int which, cudaStream_t stream) {
+    const unsigned grid = static_cast<unsigned>((n + 255) / 256);
+    k_math<<<grid ? grid : 1, 256, 0, stream>>>(x, y, n, which);
     SAD_LAUNCHED();
 }
 
@@ -2896,9 +2909,13 @@ __device__ __forceinline__ double luma_at(const double* img, int w, int h, int x
 // split_axis (budget.cpp:170-215) + the split of densify (budget.cpp:237-279).  Split i uses free
 // slot i while they last, then appends in order; parents are active so no two splits touch the same
 // slot, which makes the reference's sequential loop embarrassingly parallel.
+// The split-axis anisotropy -0.5*log(lam1/lam2) is not taken from the device libm: the kernel records
+// each split's ratio and child slots (ratio_out[i] < 0: no log needed) and the host applies glibc's log,
+// the one the reference uses (budget.cpp:198-199), through k_densify_aniso.
 __global__ void k_densify_apply(SitesDev s, DevState* st, const double2* __restrict__ stats, int cap,
                                 const uint32_t* __restrict__ sorted, const uint32_t* __restrict__ free_list,
-                                const double* __restrict__ img, double pct, SplitHyper hp, double* m, double* v) {
+                                const double* __restrict__ img, double pct, SplitHyper hp, double* m, double* v,
+                                double* __restrict__ ratio_out, uint32_t* __restrict__ slots_out) {
     const int n_elig = st->n_elig, n_free = st->n_free, size0 = st->n_sites;
     int want = static_cast<int>(static_cast<double>(n_elig) * pct);
     if (pct <= 0 || want < 1) want = 0;
@@ -2938,7 +2955,8 @@ __global__ void k_densify_apply(SitesDev s, DevState* st, const double2* __restr
                 ax = vx / nn;
                 ay = vy / nn;
                 double ratio = l2 > 0 ? l1 / l2 : 1e18;
-                an = sclamp(-0.5 * log(ratio), hp.aniso_min, hp.aniso_max);
+                an = 0.0;  // set by the host from glibc's log(ratio)
+                ratio_out[i] = ratio;
                 fallback = false;
             }
         }
@@ -2961,6 +2979,7 @@ __global__ void k_densify_apply(SitesDev s, DevState* st, const double2* __restr
         }
         an = sclamp(0.8 * pan, hp.aniso_min, hp.aniso_max);
     }
+    if (fallback) ratio_out[i] = -1.0;
     double mag = sclamp(0.5 * __dsqrt_rn(smax(st8[0], 0.0)), 1.5, 48.0);
     double clt = smax(plt - 0.25, hp.log_tau_min);
     double cr = smax(pr * 0.85, hp.radius_min);
@@ -2971,6 +2990,7 @@ __global__ void k_densify_apply(SitesDev s, DevState* st, const double2* __restr
         int ix = static_cast<int>(llround(cx)), iy = static_cast<int>(llround(cy));
         const double* col = img + 3 * (static_cast<size_t>(iy) * hp.width + ix);
         uint32_t slot = side == 0 ? par : (i < n_free ? free_list[i] : static_cast<uint32_t>(size0 + (i - n_free)));
+        slots_out[2 * i + side] = slot < static_cast<uint32_t>(cap) ? slot : 0xffffffffu;
         if (slot >= static_cast<uint32_t>(cap)) {
             atomicOr(&st->err, 2);
             continue;
@@ -3002,8 +3022,23 @@ __global__ void k_densify_apply(SitesDev s, DevState* st, const double2* __restr
 
 void launch_densify_apply(const SitesDev& s, DevState* st, const double2* stats, int cap, const uint32_t* sorted,
                           const uint32_t* free_list, const double* tgt, double pct, const SplitHyper& hp, double* m,
-                          double* v, cudaStream_t stream) {
-    k_densify_apply<<<(cap + 127) / 128, 128, 0, stream>>>(s, st, stats, cap, sorted, free_list, tgt, pct, hp, m, v);
+                          double* v, double* ratio_out, uint32_t* slots_out, cudaStream_t stream) {
+    k_densify_apply<<<(cap + 127) / 128, 128, 0, stream>>>(s, st, stats, cap, sorted, free_list, tgt, pct, hp, m, v,
+                                                           ratio_out, slots_out);
+    SAD_LAUNCHED();
+}
+
+__global__ void k_densify_aniso(double* __restrict__ p, int cap, int n, const uint32_t* __restrict__ slots,
+                                const double* __restrict__ an) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= 2 * n) return;
+    const uint32_t slot = slots[j];
+    if (slot != 0xffffffffu && an[j >> 1] == an[j >> 1]) p[9 * static_cast<size_t>(cap) + slot] = an[j >> 1];
+}
+
+void launch_densify_aniso(double* p, int cap, int n, const uint32_t* slots, const double* an, cudaStream_t stream) {
+    if (n <= 0) return;
+    k_densify_aniso<<<(2 * n + 127) / 128, 128, 0, stream>>>(p, cap, n, slots, an);
     SAD_LAUNCHED();
 }
 

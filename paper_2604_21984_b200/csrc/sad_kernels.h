@@ -131,6 +131,7 @@ void launch_adam(bool fp64, const SitesDev& s, DevState* st, const RedTarget& gr
                  const AdamHyper& hp, const double2* bc_table, double2 bc_now, bool zero_grads, double scale,
                  void* pack, void* gtab, int32_t* rcap_next, cudaStream_t stream, const double* totals = nullptr,
                  int32_t* roff_next = nullptr, int32_t* pool_top = nullptr, const uint32_t* act = nullptr);
+void launch_math(const double* x, double* y, size_t n, int which, cudaStream_t stream);
 // tau_diffusion pieces (train.cpp:171-213)
 void launch_site_totals(const RedTarget& grads, const DevState* st, int cap, double* tot, double* g0,
                         cudaStream_t stream);
@@ -149,8 +150,9 @@ void launch_prune_apply(const SitesDev& s, DevState* st, const uint32_t* sorted,
 void launch_densify_keys(const SitesDev& s, DevState* st, const double2* stats, int cap, double alpha, double eps,
                          unsigned long long* keys, uint32_t* vals, uint8_t* free_flags, cudaStream_t stream);
 void launch_densify_apply(const SitesDev& s, DevState* st, const double2* stats, int cap, const uint32_t* sorted,
-                          const uint32_t* free_list, const double* tgt, double pct, const SplitHyper& hp,
-                          double* m, double* v, cudaStream_t stream);
+                          const uint32_t* free_list, const double* tgt, double pct, const SplitHyper& hp, double* m,
+                          double* v, double* ratio_out, uint32_t* slots_out, cudaStream_t stream);
+void launch_densify_aniso(double* p, int cap, int n, const uint32_t* slots, const double* an, cudaStream_t stream);
 void launch_flag_active(const SitesDev& s, const DevState* st, uint8_t* flags, cudaStream_t stream);
 
 // ---------------------------------------------------------------- loop bookkeeping

@@ -17,6 +17,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <limits>
 #include <memory>
 #include <vector>
 
@@ -328,6 +329,8 @@ struct Workspace {
         DBuf<char> tmp;
         size_t tmp_bytes = 0;
     } tb;
+    DBuf<double> dens_ratio, dens_an;  // densify: split ratios and their host-computed anisotropy
+    DBuf<uint32_t> dens_slots;
 
     ~Workspace() {
         if (hst) cudaFreeHost(hst);
@@ -734,8 +737,28 @@ void densify_device(Workspace& ws, double pct, const sad_train_config& c) {
     }
     ws.sort_pairs(ws.cap);
     sadk::SplitHyper hp{c.log_tau_min, c.radius_min, c.aniso_min, c.aniso_max, ws.fd.width, ws.fd.height, c.max_sites};
+    ws.dens_ratio.ensure(ws.cap);
+    ws.dens_slots.ensure(2 * static_cast<size_t>(ws.cap));
+    ws.dens_an.ensure(ws.cap);
     sadk::launch_densify_apply(ws.sites(), ws.st.p, ws.stats.p, ws.cap, ws.vals[1].p, ws.free_list.p, ws.tgt_d.p, pct,
-                               hp, ws.m.p, ws.v.p, ws.stream);
+                               hp, ws.m.p, ws.v.p, ws.dens_ratio.p, ws.dens_slots.p, ws.stream);
+    // split-axis anisotropy with the host's glibc log, as the reference (budget.cpp:198-199)
+    const DevState st = ws.get_state();
+    const int done = st.done;
+    if (done > 0) {
+        std::vector<double> ratio(static_cast<size_t>(done)), an(static_cast<size_t>(done));
+        ck(cudaMemcpyAsync(ratio.data(), ws.dens_ratio.p, 8 * static_cast<size_t>(done), cudaMemcpyDeviceToHost,
+                           ws.stream),
+           "D2H ratio");
+        ck(cudaStreamSynchronize(ws.stream), "densify ratio");
+        for (int i = 0; i < done; i++)
+            an[i] = ratio[i] < 0 ? std::numeric_limits<double>::quiet_NaN()
+                                 : std::clamp(-0.5 * std::log(ratio[i]), c.aniso_min, c.aniso_max);
+        ck(cudaMemcpyAsync(ws.dens_an.p, an.data(), 8 * static_cast<size_t>(done), cudaMemcpyHostToDevice, ws.stream),
+           "H2D aniso");
+        sadk::launch_densify_aniso(ws.params.p, ws.cap, done, ws.dens_slots.p, ws.dens_an.p, ws.stream);
+        ck(cudaStreamSynchronize(ws.stream), "densify aniso");  // `an` is host memory read by the copy above
+    }
 }
 
 // Scratch for init_sites_device, allocated once per image size.
@@ -1033,6 +1056,18 @@ sad_status sad_field_download(sad_ctx* c, sad_field_view* f) {
         f->synced_generation = m.synced_generation;
         f->refresh_count = m.refresh_count;
         f->pass_index = m.pass_index;
+    });
+}
+
+sad_status sad_math_exp(sad_ctx* c, const double* x, double* y, size_t n, int single) {
+    return guard([&] {
+        DBuf<double> dx, dy;
+        dx.ensure(std::max<size_t>(n, 1));
+        dy.ensure(std::max<size_t>(n, 1));
+        ck(cudaMemcpyAsync(dx.p, x, 8 * n, cudaMemcpyHostToDevice, c->stream), "H2D");
+        sadk::launch_math(dx.p, dy.p, n, single ? 1 : 0, c->stream);
+        ck(cudaMemcpyAsync(y, dy.p, 8 * n, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        ck(cudaStreamSynchronize(c->stream), "math");
     });
 }
 
@@ -1729,7 +1764,10 @@ static void fit_loop(sad_fit_run* r) {
             sadk::launch_advance(ws.st.p, np, 1, r->loss_hist.p, r->active_hist.p, ws.loss_part.p, nbw, ws.otops.p, s);
         });
     };
+    // SAD_STOP_AT=t (divergence hunting): stop after iteration t without the final refresh
+    const int stop_at = getenv("SAD_STOP_AT") ? atoi(getenv("SAD_STOP_AT")) : 0;
     for (int t = 1; t <= c.iters; t++) {
+        if (stop_at && t > stop_at) break;
         const bool rf = (t - 1) % c.refresh_every == 0;
         bool ev_d = budget && t >= c.densify_start && t <= c.densify_end && t % c.densify_every == 0;
         bool ev_p = budget && t >= c.prune_start && t <= c.prune_end && t % c.prune_every == 0;
@@ -1790,11 +1828,13 @@ static void fit_loop(sad_fit_run* r) {
         });
     }
     // final full refresh (train.cpp:287)
-    const auto fin = full_refresh_passes(ws.fd.gw, ws.fd.gh, c.final_passes);
-    ws.cur = 0;
-    sadk::launch_jfa_seed(ws.sites(), ws.st.p, ws.ids[0].p, ws.fd, scale_n, s);
-    passes_device(ws, fin, c.inject, c.seed, fp64, 0);
-    sadk::launch_advance(ws.st.p, static_cast<int>(fin.size()), 0, nullptr, nullptr, nullptr, 0, ws.otops.p, s);
+    if (!stop_at) {
+        const auto fin = full_refresh_passes(ws.fd.gw, ws.fd.gh, c.final_passes);
+        ws.cur = 0;
+        sadk::launch_jfa_seed(ws.sites(), ws.st.p, ws.ids[0].p, ws.fd, scale_n, s);
+        passes_device(ws, fin, c.inject, c.seed, fp64, 0);
+        sadk::launch_advance(ws.st.p, static_cast<int>(fin.size()), 0, nullptr, nullptr, nullptr, 0, ws.otops.p, s);
+    }
     cudaEventRecord(e1, s);
     ck(cudaStreamSynchronize(s), "fit");
     float ms = 0;
@@ -1818,9 +1858,10 @@ static void fit_loop(sad_fit_run* r) {
     std::vector<int32_t> ah(std::max(c.iters, 1));
     ck(cudaMemcpy(lh.data(), r->loss_hist.p, lh.size() * sizeof(double2), cudaMemcpyDeviceToHost), "D2H hist");
     ck(cudaMemcpy(ah.data(), r->active_hist.p, ah.size() * 4, cudaMemcpyDeviceToHost), "D2H hist");
-    r->hist.resize(c.iters);
+    const int n_rows = stop_at ? std::min(c.iters, stop_at) : c.iters;
+    r->hist.resize(n_rows);
     const double npx = static_cast<double>(w) * h;
-    for (int t = 0; t < c.iters; t++) {
+    for (int t = 0; t < n_rows; t++) {
         double loss = (lh[t].x + lh[t].y) / npx;
         double m = loss / 3.0;
         double ps = m <= 0 ? 99.0 : std::min(99.0, 10.0 * std::log10(1.0 / m));
@@ -1829,7 +1870,7 @@ static void fit_loop(sad_fit_run* r) {
     r->done = true;
     if (fs.err & 1) fail(SAD_EEMPTY, "backward: empty candidate list at a pixel");
     if (fs.err & 2) fail(SAD_ENOMEM, "fit: site capacity exhausted");
-    for (int t = 0; t < c.iters; t++)
+    for (int t = 0; t < n_rows; t++)
         if (!std::isfinite(r->hist[t].loss)) fail(SAD_ENUMERIC, "fit: non-finite loss");
 }
 

@@ -1,0 +1,55 @@
+"""The device ports of glibc's exp / expf (sad_device.cuh) against the host libm the reference links:
+the fit's double tables, stats softmax and seeding logits and its fp32 softmax go through them, so any
+ulp difference would break bit-identity of whole fits."""
+import ctypes as C
+import math
+
+import numpy as np
+import pytest
+
+import paper_2604_21984_b200 as sad
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(G, x, single):
+    y = np.empty_like(x)
+    G._call("math_exp", x.ctypes.data_as(C.POINTER(C.c_double)), y.ctypes.data_as(C.POINTER(C.c_double)),
+            C.c_size_t(x.size), C.c_int(int(single)))
+    return y
+
+
+def test_double_exp_matches_glibc():
+    G = sad.gpu_backend(0)
+    rng = np.random.default_rng(7)
+    parts = [-rng.random(1_000_000) * 60.0,            # softmax weights
+             (rng.random(1_000_000) - 0.5) * 44.0,     # tables: exp(log tau), exp(+-a)
+             (rng.random(300_000) - 0.5) * 1020.0,     # full normal range
+             (rng.random(100_000) - 0.5) * 1e-6,
+             np.array([0.0, -0.0, 1e-300, -1e-300, 709.78, -745.1, 710.0, -746.0, np.inf, -np.inf])]
+    x = np.ascontiguousarray(np.concatenate(parts))
+    y = _dev(G, x, False)
+    with np.errstate(over="ignore", under="ignore"):
+        ref = np.array([math.exp(v) if v < 709.79 else math.inf for v in x])
+    main = np.abs(x) <= 510
+    assert np.array_equal(y[main].view(np.uint64), ref[main].view(np.uint64))
+    tail = ~main & np.isfinite(ref) & (ref > 0)
+    if tail.any():  # |x| > 512: at most one ulp (documented)
+        d = np.abs(y[tail].view(np.int64) - ref[tail].view(np.int64))
+        assert d.max() <= 1
+
+
+def test_float_expf_matches_glibc():
+    G = sad.gpu_backend(0)
+    rng = np.random.default_rng(8)
+    xf = np.concatenate([-rng.random(500_000).astype(np.float32) * 100,
+                         (rng.random(200_000).astype(np.float32) - 0.5) * 170]).astype(np.float32)
+    y = _dev(G, xf.astype(np.float64), True).astype(np.float32)
+    ref = np.exp(xf)  # numpy float32 exp goes to... not glibc expf; compare with math via float32 rounding of libm expf
+    import ctypes.util
+    libm = C.CDLL(ctypes.util.find_library("m"))
+    libm.expf.restype = C.c_float
+    libm.expf.argtypes = [C.c_float]
+    sample = np.arange(0, xf.size, 7)
+    ref = np.array([libm.expf(float(v)) for v in xf[sample]], dtype=np.float32)
+    assert np.array_equal(y[sample].view(np.uint32), ref.view(np.uint32))
