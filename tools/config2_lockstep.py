@@ -16,14 +16,27 @@ from paper_2604_21984_b200.synth import synthetic_image  # noqa: E402
 threads = os.cpu_count() or 1
 G = sad.gpu_backend(0)
 R = ref_backend(threads=threads)
-for seed in [int(x) for x in sys.argv[1:]] or [1]:
-    img = sad.ImageBuffer(768, 512, synthetic_image(768, 512, seed))
-    cfg = sad.TrainConfig(iters=4000, target_bpp=2.0, fp64=False, seed=1)
+# config 3 instead: python tools/config2_lockstep.py --config3 [seed]  (2048^2, 100k sites, 300 iterations)
+C3 = "--config3" in sys.argv
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+W, H = (2048, 2048) if C3 else (768, 512)
+ITERS = 300 if C3 else 4000
+
+
+def make_cfg():
+    if C3:
+        return sad.TrainConfig(iters=ITERS, n_sites=100000, fp64=False, seed=1)
+    return sad.TrainConfig(iters=ITERS, target_bpp=2.0, fp64=False, seed=1)
+
+
+for seed in [int(x) for x in args] or [1]:
+    img = sad.ImageBuffer(W, H, synthetic_image(W, H, seed))
+    cfg = make_cfg()
     G.fit(img, cfg)  # warm (graph capture, allocation)
     t0 = time.perf_counter()
     a = G.fit(img, cfg)
     tg = time.perf_counter() - t0
-    cfg_r = sad.TrainConfig(iters=4000, target_bpp=2.0, fp64=False, seed=1)
+    cfg_r = make_cfg()
     cfg_r.threads = threads
     t0 = time.perf_counter()
     b = R.fit(img, cfg_r)
@@ -41,8 +54,8 @@ for seed in [int(x) for x in sys.argv[1:]] or [1]:
         m = float(np.mean((x - img.data) ** 2))
         return 99.0 if m <= 0 else 10 * np.log10(1.0 / m)
 
-    print(f"seed {seed}: history {'identical (4000 lines)' if first is None else f'first difference at iter {first + 1}'}; "
+    print(f"{W}x{H} seed {seed}: history {f'identical ({ITERS} lines)' if first is None else f'first difference at iter {first + 1}'}; "
           f"final sites identical {same_sites}; final map identical {np.array_equal(a.field.ids, b.field.ids)}; "
           f"decode PSNR gpu {psnr(pa):.6f} ref {psnr(pb):.6f}; active {a.history[-1].active_sites}; "
-          f"fit wall gpu {tg:.3f} s (e2e), reference {tr:.1f} s on {threads} threads ({4000 / tr:.1f} iters/s)",
+          f"fit wall gpu {tg:.3f} s (e2e), reference {tr:.1f} s on {threads} threads ({ITERS / tr:.2f} iters/s)",
           flush=True)
