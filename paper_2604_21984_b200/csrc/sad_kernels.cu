@@ -110,6 +110,12 @@ void launch_tables(bool fp64, const SitesDev& s, const DevState* st, double scal
     SAD_LAUNCHED();
 }
 
+// Rows a kernel covers under the optional FieldDims row range (host and device).
+__host__ __device__ inline int rows_of(const FieldDims& f, int n) {
+    const int hi = f.row1 < n ? f.row1 : n;
+    return hi > f.row0 ? hi - f.row0 : 0;
+}
+
 // Candidate cell of pixel (px, py) (CandidateField::cell_x/cell_y, types.hpp:95-101); the fit's cell
 // size is 1, so the two integer divisions are skipped on that (launch-uniform) path.
 __device__ __forceinline__ size_t cell_index(const FieldDims& f, int px, int py) {
@@ -331,8 +337,8 @@ __global__ void __launch_bounds__(256) k_propagate(const uint32_t* __restrict__ 
                                                    const DevState* __restrict__ st, FieldDims f, int step, int inject,
                                                    uint64_t seed, uint32_t pass_offset, T s) {
     const int gx = blockIdx.x * blockDim.x + threadIdx.x;
-    const int gy = blockIdx.y * blockDim.y + threadIdx.y;
-    if (gx >= f.gw || gy >= f.gh) return;
+    const int gy = blockIdx.y * blockDim.y + threadIdx.y + f.row0;
+    if (gx >= f.gw || gy >= f.gh || gy >= f.row1) return;
     propagate_cell<T, KM, EXACT, BOX>(prev, next, pack, act, st, f, gx, gy, step, inject, seed, pass_offset, s);
 }
 
@@ -383,8 +389,8 @@ __global__ void __launch_bounds__(256) k_propagate_k8(const uint32_t* __restrict
     __shared__ uint32_t q[kAxQ * 256];
     const int tid = threadIdx.y * blockDim.x + threadIdx.x;
     const int gx = blockIdx.x * blockDim.x + threadIdx.x;
-    const int gy = blockIdx.y * blockDim.y + threadIdx.y;
-    if (gx >= f.gw || gy >= f.gh) return;
+    const int gy = blockIdx.y * blockDim.y + threadIdx.y + f.row0;
+    if (gx >= f.gw || gy >= f.gh || gy >= f.row1) return;
     const T cx = static_cast<T>(gx * static_cast<double>(f.cell) + (f.cell - 1) * 0.5);
     const T cy = static_cast<T>(gy * static_cast<double>(f.cell) + (f.cell - 1) * 0.5);
     TopKReg<T, 8, true> sel;
@@ -613,8 +619,8 @@ __global__ void __launch_bounds__(256, SAD_PROP_MINB) k_prop8_stream(const uint3
                                                       FieldDims f, int step, int inject, uint64_t seed,
                                                       uint32_t pass_offset, float s) {
     const int gx = blockIdx.x * blockDim.x + threadIdx.x;
-    const int gy = blockIdx.y * blockDim.y + threadIdx.y;
-    if (gx >= f.gw || gy >= f.gh) return;
+    const int gy = blockIdx.y * blockDim.y + threadIdx.y + f.row0;
+    if (gx >= f.gw || gy >= f.gh || gy >= f.row1) return;
     const float cx = static_cast<float>(gx * static_cast<double>(f.cell) + (f.cell - 1) * 0.5);
     const float cy = static_cast<float>(gy * static_cast<double>(f.cell) + (f.cell - 1) * 0.5);
     KeyList8 L;
@@ -676,8 +682,8 @@ __global__ void __launch_bounds__(256, SAD_PROP_MINB) k_prop8_queue(const uint32
     __shared__ uint32_t q[kAxQ * 256];
     const int tid = threadIdx.y * blockDim.x + threadIdx.x;
     const int gx = blockIdx.x * blockDim.x + threadIdx.x;
-    const int gy = blockIdx.y * blockDim.y + threadIdx.y;
-    if (gx >= f.gw || gy >= f.gh) return;
+    const int gy = blockIdx.y * blockDim.y + threadIdx.y + f.row0;
+    if (gx >= f.gw || gy >= f.gh || gy >= f.row1) return;
     const float cx = static_cast<float>(gx * static_cast<double>(f.cell) + (f.cell - 1) * 0.5);
     const float cy = static_cast<float>(gy * static_cast<double>(f.cell) + (f.cell - 1) * 0.5);
     KeyList8 L;
@@ -750,7 +756,7 @@ static void propagate_t(const uint32_t* prev, uint32_t* next, const void* pack, 
                         const DevState* st, const FieldDims& f, uint32_t step, int box, int inject, uint64_t seed,
                         uint32_t pass_offset, double scale, cudaStream_t stream) {
     dim3 block(32, 8);
-    dim3 grid((f.gw + 31) / 32, (f.gh + 7) / 8);
+    dim3 grid((f.gw + 31) / 32, (rows_of(f, f.gh) + 7) / 8);
     if (box)
         k_propagate<T, KM, EXACT, true><<<grid, block, 0, stream>>>(prev, next, (const Q4<T>*)pack, act, st, f,
                                                                     (int)step, inject, seed, pass_offset,
@@ -770,7 +776,7 @@ void launch_propagate(bool fp64, const uint32_t* prev, uint32_t* next, const voi
                       uint32_t pass_offset, double scale, cudaStream_t stream) {
     if (f.k == 8 && !fp64) {
         dim3 block(32, 8);
-        dim3 grid((f.gw + 31) / 32, (f.gh + 7) / 8);
+        dim3 grid((f.gw + 31) / 32, (rows_of(f, f.gh) + 7) / 8);
         const float sf = static_cast<float>(scale);
         // Box3 floods at small steps see mostly ids already in the cell's list: dedup first (queue);
         // at larger steps most entries are new sites: score first (stream)
@@ -791,7 +797,7 @@ void launch_propagate(bool fp64, const uint32_t* prev, uint32_t* next, const voi
     }
     if (f.k == 8 && inject <= 4 && !box) {
         dim3 block(32, 8);
-        dim3 grid((f.gw + 31) / 32, (f.gh + 7) / 8);
+        dim3 grid((f.gw + 31) / 32, (rows_of(f, f.gh) + 7) / 8);
         k_propagate_k8<double, false><<<grid, block, 0, stream>>>(prev, next, (const Q4<double>*)pack, act, st, f,
                                                                  (int)step, inject, seed, pass_offset, scale);
         SAD_LAUNCHED();
@@ -1436,8 +1442,8 @@ __global__ void __launch_bounds__(BwdTile<T>::TW * BwdTile<T>::TH)
 
     const int tid = threadIdx.x;
     const int px = blockIdx.x * TW + (tid % TW);
-    const int py = blockIdx.y * TH + (tid / TW);
-    const bool inside = px < f.width && py < f.height;
+    const int py = blockIdx.y * TH + (tid / TW) + f.row0;
+    const bool inside = px < f.width && py < f.height && py < f.row1;
     constexpr T kTiny = sizeof(T) == 8 ? T(1e-18) : T(1e-12);
 
     // Candidates stay in their list slots; `ok` marks the ones the reference keeps (active, finite
@@ -1637,8 +1643,8 @@ __global__ void __launch_bounds__(256, SAD_BWD2_MINB) k_backward2(const uint32_t
     const int tid = threadIdx.x;
     const int pix = tid >> 1, half = tid & 1;
     const int px = blockIdx.x * TW + (pix % TW);
-    const int py = blockIdx.y * TH + (pix / TW);
-    const bool inside = px < f.width && py < f.height;
+    const int py = blockIdx.y * TH + (pix / TW) + f.row0;
+    const bool inside = px < f.width && py < f.height && py < f.row1;
     constexpr T kTiny = T(1e-12);
 
     uint32_t cid[H];
@@ -1863,7 +1869,7 @@ __global__ void __launch_bounds__(256, SAD_BWD2_MINB) k_backward2(const uint32_t
 
 int backward_blocks(bool fp64, const FieldDims& f) {
     int tw = fp64 ? BwdTile<double>::TW : BwdTile<float>::TW, th = fp64 ? BwdTile<double>::TH : BwdTile<float>::TH;
-    return ((f.width + tw - 1) / tw) * ((f.height + th - 1) / th);
+    return ((f.width + tw - 1) / tw) * ((rows_of(f, f.height) + th - 1) / th);
 }
 
 template <typename T, int KM, int MODE>
@@ -1885,7 +1891,7 @@ static void backward_t(const uint32_t* ids, const void* gtab, const void* tgt, c
                        const RedTarget& red, double2* loss_part, DevState* st, cudaStream_t stream) {
     constexpr int TW = BwdTile<T>::TW, TH = BwdTile<T>::TH;
     constexpr int NCH = MODE == 1 ? 11 : 10;
-    dim3 grid((f.width + TW - 1) / TW, (f.height + TH - 1) / TH);
+    dim3 grid((f.width + TW - 1) / TW, (rows_of(f, f.height) + TH - 1) / TH);
     T inv_hw2 = static_cast<T>(2.0 / (static_cast<double>(f.width) * f.height));
     if (sizeof(T) == 4 && !g_bwd1) {
         static_assert(BwdTile<float>::TW == 16 && BwdTile<float>::TH == 8, "k_backward2 tile");
@@ -2090,7 +2096,7 @@ __global__ void __launch_bounds__(64) k_stats(const uint32_t* __restrict__ ids, 
     tile_init(sm);
     const int tid = threadIdx.x;
     const int px = blockIdx.x * TW + (tid % TW);
-    const int py = blockIdx.y * TH + (tid / TW);
+    const int py = blockIdx.y * TH + (tid / TW) + f.row0;
     int n = 0;
     uint32_t cid[KM];
     double lg[KM];
@@ -2100,7 +2106,7 @@ __global__ void __launch_bounds__(64) k_stats(const uint32_t* __restrict__ ids, 
         lg[i] = 0;
     }
     double best = 0;
-    if (px < f.width && py < f.height) {
+    if (px < f.width && py < f.height && py < f.row1) {
         const uint32_t* lst = ids + static_cast<size_t>(f.k) * cell_index(f, px, py);
 #pragma unroll
         for (int i = 0; i < KM; i++) {
@@ -2229,8 +2235,8 @@ __global__ void __launch_bounds__(128) k_stats2(const uint32_t* __restrict__ ids
     const int tid = threadIdx.x;
     const int pix = tid >> 1, half = tid & 1;
     const int px = blockIdx.x * TW + (pix % TW);
-    const int py = blockIdx.y * TH + (pix / TW);
-    const bool inside = px < f.width && py < f.height;
+    const int py = blockIdx.y * TH + (pix / TW) + f.row0;
+    const bool inside = px < f.width && py < f.height && py < f.row1;
     uint32_t cid[H];
     double lg[H];
     bool ok[H];
@@ -2387,7 +2393,7 @@ static const bool g_stats1 = getenv("SAD_STATS1") != nullptr;
 
 void launch_stats(const uint32_t* ids, const void* rtab_d, const double* tgt, const FieldDims& f, double scale,
                   const RedTarget& red, DevState* st, cudaStream_t stream) {
-    dim3 grid((f.width + 7) / 8, (f.height + 7) / 8);
+    dim3 grid((f.width + 7) / 8, (rows_of(f, f.height) + 7) / 8);
     if (g_stats1) {  // one lane per pixel (A/B)
         if (f.k <= 8)
             k_stats<8><<<grid, 64, sizeof(TileRed<double, 8, 64, 8>), stream>>>(ids, (const Q4<double>*)rtab_d, tgt, f,

@@ -67,6 +67,9 @@ struct RedTarget {
 
 struct FieldDims {
     int width, height, cell, gw, gh, k;
+    // Optional row range (pixel rows for the pixel kernels, cell rows for propagation; equal at cell 1):
+    // the row-strip partition of a multi-GPU fit computes [row0, row1) only.  Defaults: everything.
+    int row0 = 0, row1 = 1 << 30;
 };
 
 struct AdamHyper {
