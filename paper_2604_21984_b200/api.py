@@ -437,6 +437,54 @@ class Backend:
     def fit_store(self, sites: SiteStore, target: ImageBuffer, cfg: TrainConfig) -> FitResult:
         return self._fit(target, cfg, sites)
 
+    def _collect_run(self, run, w, h, cfg) -> FitResult:
+        n, nh, sc = C.c_size_t(), C.c_int(), C.c_double()
+        self._call("fit_info", run, C.byref(n), C.byref(nh), C.byref(sc))
+        return self._fit_collect(w, h, cfg, int(n.value), int(nh.value), float(sc.value),
+                                 lambda sv, fv, hist: self._call("fit_download", run, sv, fv, hist))
+
+    def fit_strips_loopback(self, target: ImageBuffer, cfg: TrainConfig, world: int) -> List[FitResult]:
+        """Row-strip fit (config 5 partition) with `world` virtual ranks on this device; returns every
+        rank's result (all equal to fit() when the partition is exact)."""
+        c = cfg.to_c()
+        w, h = target.width, target.height
+        runs = []
+        try:
+            for _ in range(world):
+                run = C.c_void_p()
+                self._call("fit_create", C.c_int(w), C.c_int(h), C.byref(c), C.byref(run))
+                runs.append(run)
+                self._call("fit_set_target", run, _ptr(target.data))
+            arr = (C.c_void_p * world)(*[r.value for r in runs])
+            self._call("fit_run_strips_loopback", arr, C.c_int(world))
+            return [self._collect_run(r, w, h, cfg) for r in runs]
+        finally:
+            for r in runs:
+                self.lib.sad_fit_destroy(r)
+
+    def fit_strips(self, target: ImageBuffer, cfg: TrainConfig, rank: int, world: int, nccl_id: bytes,
+                   init: Optional[SiteStore] = None) -> FitResult:
+        """This rank's part of a row-strip multi-GPU fit over NCCL (one process per GPU)."""
+        c = cfg.to_c()
+        w, h = target.width, target.height
+        run = C.c_void_p()
+        self._call("fit_create", C.c_int(w), C.c_int(h), C.byref(c), C.byref(run))
+        try:
+            self._call("fit_set_target", run, _ptr(target.data))
+            idb = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+            sv = None
+            if init is not None:
+                sv, keep = init._view()
+            self._call("fit_run_strips", run, C.c_int(rank), C.c_int(world), idb, _ref(sv))
+            return self._collect_run(run, w, h, cfg)
+        finally:
+            self.lib.sad_fit_destroy(run)
+
+    def nccl_unique_id(self) -> bytes:
+        buf = (C.c_uint8 * 128)()
+        self._call("nccl_unique_id", buf)
+        return bytes(buf)
+
     def fit_oneshot(self, target: ImageBuffer, cfg: TrainConfig, init: Optional[SiteStore] = None) -> FitResult:
         """sad_fit / sad_fit_store: the single C call an FFI binding would make (no cached run)."""
         c = cfg.to_c()
@@ -574,7 +622,7 @@ class Backend:
 _NO_CTX = {"jump_step", "full_refresh_passes", "schedule_passes", "bpp_target_count", "simulate_schedule",
            "plan_schedule", "fit_set_target", "fit_set_target_device", "fit_run_init", "fit_run_store",
            "fit_info", "fit_download", "fit_render_device", "fit_timing", "fit_bench", "fit_set_profiling",
-           "fit_point_query", "fit_capacity", "encode", "decode", "decode_header", "bpp",
+           "fit_point_query", "fit_capacity", "fit_run_strips", "fit_run_strips_loopback", "nccl_unique_id", "encode", "decode", "decode_header", "bpp",
            "last_error"}
 
 # ---------------------------------------------------------------------- product binding

@@ -2582,6 +2582,49 @@ void launch_site_totals(const RedTarget& grads, const DevState* st, int cap, dou
     SAD_LAUNCHED();
 }
 
+// Row-strip fits: each rank's per-site double-double totals of its own records (all ten channels,
+// same merge code as Adam), and the rank-ordered merge of the gathered partials.  Every sum is an
+// exact double-double, so the merged totals equal the single-GPU ones bit for bit.
+__global__ void __launch_bounds__(128) k_site_partials(RedTarget grads, const DevState* __restrict__ st, int cap,
+                                                       double2* __restrict__ out) {
+    const int lane16 = threadIdx.x & 15;
+    const int id = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
+    const unsigned gmask = 0xffffu << (threadIdx.x & 16);
+    const bool live = id < st->n_sites;
+    DD g;
+    merge_site(grads, id, live, lane16, gmask, cap, g);
+    const int ch = lane_channel(lane16);
+    if (id < cap && ch >= 0) out[static_cast<size_t>(ch) * cap + id] = live ? make_double2(g.hi, g.lo) : make_double2(0, 0);
+}
+
+void launch_site_partials(const RedTarget& grads, const DevState* st, int cap, double2* out, cudaStream_t stream) {
+    int grid = (cap + 7) / 8;
+    k_site_partials<<<grid ? grid : 1, 128, 0, stream>>>(grads, st, cap, out);
+    SAD_LAUNCHED();
+}
+
+// parts: world slices of [nch][cap] double2; writes values (hi + lo) and/or the merged double-doubles
+__global__ void k_merge_partials(const double2* __restrict__ parts, int world, int cap, int nch,
+                                 double* __restrict__ values, double2* __restrict__ dd) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    const size_t n = static_cast<size_t>(nch) * cap;
+    if (i >= n) return;
+    DD t{0.0, 0.0};
+    for (int r = 0; r < world; r++) {
+        const double2 v = parts[static_cast<size_t>(r) * n + i];
+        dd_merge(t, DD{v.x, v.y});
+    }
+    if (values) values[i] = t.hi + t.lo;
+    if (dd) dd[i] = make_double2(t.hi, t.lo);
+}
+
+void launch_merge_partials(const double2* parts, int world, int cap, int nch, double* values, double2* dd,
+                           cudaStream_t stream) {
+    const size_t n = static_cast<size_t>(nch) * cap;
+    k_merge_partials<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(parts, world, cap, nch, values, dd);
+    SAD_LAUNCHED();
+}
+
 template <typename T>
 __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarget grads, double* __restrict__ m,
                                               double* __restrict__ v, AdamHyper hp,

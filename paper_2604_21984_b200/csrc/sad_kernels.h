@@ -135,6 +135,10 @@ void launch_adam(bool fp64, const SitesDev& s, DevState* st, const RedTarget& gr
                  void* pack, void* gtab, int32_t* rcap_next, cudaStream_t stream, const double* totals = nullptr,
                  int32_t* roff_next = nullptr, int32_t* pool_top = nullptr, const uint32_t* act = nullptr);
 void launch_math(const double* x, double* y, size_t n, int which, cudaStream_t stream);
+// row-strip fits (multi-GPU config 5)
+void launch_site_partials(const RedTarget& grads, const DevState* st, int cap, double2* out, cudaStream_t stream);
+void launch_merge_partials(const double2* parts, int world, int cap, int nch, double* values, double2* dd,
+                           cudaStream_t stream);
 // tau_diffusion pieces (train.cpp:171-213)
 void launch_site_totals(const RedTarget& grads, const DevState* st, int cap, double* tot, double* g0,
                         cudaStream_t stream);

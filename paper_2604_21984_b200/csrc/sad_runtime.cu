@@ -18,6 +18,9 @@
 #include <stdexcept>
 #include <string>
 #include <limits>
+#include <dlfcn.h>
+#include <functional>
+#include <nccl.h>
 #include <memory>
 #include <vector>
 
@@ -897,6 +900,13 @@ struct sad_fit_run {
     bool profile = false;  // per-phase CUDA-event timing (disables graphs)
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
     uint64_t plain_launches[2][2] = {{0, 0}, {0, 0}};
+    // row-strip multi-GPU fit (config 5): this run's rank, the world size, every rank's first row
+    // (world + 1 bounds), and the buffers of the exact cross-rank merges
+    int rank = 0, world = 1;
+    std::vector<int> strip;
+    DBuf<double2> gpart_self, gpart_all, spart_all, loss_self, loss_all;
+    DBuf<double> tot;
+    DBuf<unsigned long long> valid_all;
     ~sad_fit_run() {
         for (auto& a : plain)
             for (auto& g : a)
@@ -1644,6 +1654,31 @@ static int capacity_bound(const sad_train_config& c, int n0, double scale, bool 
     return static_cast<int>(n) + 1;
 }
 
+// History rows and the end-of-fit checks of a finished run (device loss partials -> HistoryRow).
+static void finish_run(sad_fit_run* r, float ms, int n_rows) {
+    Workspace& ws = r->ws;
+    const sad_train_config& c = r->cfg;
+    DevState fs = ws.get_state();
+    r->n_sites = static_cast<size_t>(fs.n_sites);
+    std::vector<double2> lh(std::max(c.iters, 1));
+    std::vector<int32_t> ah(std::max(c.iters, 1));
+    ck(cudaMemcpy(lh.data(), r->loss_hist.p, lh.size() * sizeof(double2), cudaMemcpyDeviceToHost), "D2H hist");
+    ck(cudaMemcpy(ah.data(), r->active_hist.p, ah.size() * 4, cudaMemcpyDeviceToHost), "D2H hist");
+    r->hist.resize(n_rows);
+    const double npx = static_cast<double>(r->w) * r->h;
+    for (int t = 0; t < n_rows; t++) {
+        double loss = (lh[t].x + lh[t].y) / npx;
+        double m = loss / 3.0;
+        double ps = m <= 0 ? 99.0 : std::min(99.0, 10.0 * std::log10(1.0 / m));
+        r->hist[t] = sad_history_row{t + 1, loss, ps, ah[t], ms / std::max(c.iters, 1)};
+    }
+    r->done = true;
+    if (fs.err & 1) fail(SAD_EEMPTY, "backward: empty candidate list at a pixel");
+    if (fs.err & 2) fail(SAD_ENOMEM, "fit: site capacity exhausted");
+    for (int t = 0; t < n_rows; t++)
+        if (!std::isfinite(r->hist[t].loss)) fail(SAD_ENUMERIC, "fit: non-finite loss");
+}
+
 // SAD_ADAM_ALL=1: plain-iteration Adam over every slot (A/B)
 static const bool g_adam_all = getenv("SAD_ADAM_ALL") != nullptr;
 
@@ -1852,26 +1887,355 @@ static void fit_loop(sad_fit_run* r) {
         std::fprintf(stderr, "phases ms: propagate %.1f fwd_bwd %.1f adam %.1f events %.1f advance %.1f\n",
                      r->phase_ms[0], r->phase_ms[1], r->phase_ms[2], r->phase_ms[3], r->phase_ms[5]);
 
-    DevState fs = ws.get_state();
-    r->n_sites = static_cast<size_t>(fs.n_sites);
-    std::vector<double2> lh(std::max(c.iters, 1));
-    std::vector<int32_t> ah(std::max(c.iters, 1));
-    ck(cudaMemcpy(lh.data(), r->loss_hist.p, lh.size() * sizeof(double2), cudaMemcpyDeviceToHost), "D2H hist");
-    ck(cudaMemcpy(ah.data(), r->active_hist.p, ah.size() * 4, cudaMemcpyDeviceToHost), "D2H hist");
-    const int n_rows = stop_at ? std::min(c.iters, stop_at) : c.iters;
-    r->hist.resize(n_rows);
-    const double npx = static_cast<double>(w) * h;
-    for (int t = 0; t < n_rows; t++) {
-        double loss = (lh[t].x + lh[t].y) / npx;
-        double m = loss / 3.0;
-        double ps = m <= 0 ? 99.0 : std::min(99.0, 10.0 * std::log10(1.0 / m));
-        r->hist[t] = sad_history_row{t + 1, loss, ps, ah[t], ms / std::max(c.iters, 1)};
+    finish_run(r, ms, stop_at ? std::min(c.iters, stop_at) : c.iters);
+}
+
+// ====================================================================== row-strip multi-GPU fit (config 5)
+// one large image split into row strips.  Every rank replicates the sites, tables, target
+// and the whole candidate field, but computes only its strip: propagation rows, backward and stats
+// tiles (FieldDims row range; strips are multiples of the 8-row tiles).  Exchanges per step:
+//   * after every propagation pass: the strips of the new field buffer (owner broadcasts);
+//   * after the backward: every rank's per-site double-double partial totals (10 channels) and its loss
+//     partial, merged in rank order by every rank (exact double-double: equals the single-GPU totals);
+//   * at events: the per-site stats partials (8 channels) and the valid-pixel counts, same merge.
+// Adam, prune, densify, seeding and the tables then run replicated and deterministically, so all ranks
+// hold the same state and the fit is bit-identical to the single-GPU fit.  The transport is NCCL (one
+// process per GPU; loaded with dlopen, no link-time dependency) or a loopback of R virtual ranks on one
+// device (the correctness test of the partition on a single GPU).
+struct StripComm {
+    virtual ~StripComm() = default;
+    virtual int world() const = 0;
+    // rows [strip[q], strip[q+1]) of ids[b] (cell rows of gw*k u32) from rank q to every rank
+    virtual void gather_rows(std::vector<sad_fit_run*>& runs, int b) = 0;
+    // slice q (bytes each) of every rank's `all` <- rank q's `self`
+    virtual void gather(std::vector<sad_fit_run*>& runs, const std::function<const void*(sad_fit_run*)>& self,
+                        const std::function<void*(sad_fit_run*)>& all, size_t bytes) = 0;
+};
+
+struct LoopbackComm : StripComm {
+    int n;
+    explicit LoopbackComm(int world) : n(world) {}
+    int world() const override { return n; }
+    void gather_rows(std::vector<sad_fit_run*>& runs, int b) override {
+        const size_t row = static_cast<size_t>(runs[0]->ws.fd.gw) * runs[0]->ws.fd.k;
+        for (int q = 0; q < n; q++) {
+            const size_t off = row * runs[q]->strip[q], cnt = row * (runs[q]->strip[q + 1] - runs[q]->strip[q]);
+            for (int r = 0; r < n; r++)
+                if (r != q && cnt)
+                    ck(cudaMemcpyAsync(runs[r]->ws.ids[b].p + off, runs[q]->ws.ids[b].p + off, 4 * cnt,
+                                       cudaMemcpyDeviceToDevice, runs[r]->ws.stream),
+                       "loopback rows");
+        }
     }
-    r->done = true;
-    if (fs.err & 1) fail(SAD_EEMPTY, "backward: empty candidate list at a pixel");
-    if (fs.err & 2) fail(SAD_ENOMEM, "fit: site capacity exhausted");
-    for (int t = 0; t < n_rows; t++)
-        if (!std::isfinite(r->hist[t].loss)) fail(SAD_ENUMERIC, "fit: non-finite loss");
+    void gather(std::vector<sad_fit_run*>& runs, const std::function<const void*(sad_fit_run*)>& self,
+                const std::function<void*(sad_fit_run*)>& all, size_t bytes) override {
+        for (int q = 0; q < n; q++)
+            for (int r = 0; r < n; r++)
+                ck(cudaMemcpyAsync(static_cast<char*>(all(runs[r])) + bytes * q, self(runs[q]), bytes,
+                                   cudaMemcpyDeviceToDevice, runs[r]->ws.stream),
+                   "loopback gather");
+    }
+};
+
+struct NcclApi {
+    void* lib = nullptr;
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*groupStart)() = nullptr;
+    ncclResult_t (*groupEnd)() = nullptr;
+    const char* (*errorString)(ncclResult_t) = nullptr;
+    static NcclApi& get() {
+        static NcclApi a;
+        if (!a.lib) {
+            a.lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+            if (!a.lib) fail(SAD_EINVAL, std::string("strips: cannot load libnccl.so.2: ") + dlerror());
+            auto sym = [&](const char* n) {
+                void* f = dlsym(a.lib, n);
+                if (!f) fail(SAD_EINVAL, std::string("strips: NCCL symbol missing: ") + n);
+                return f;
+            };
+            a.getUniqueId = reinterpret_cast<decltype(a.getUniqueId)>(sym("ncclGetUniqueId"));
+            a.commInitRank = reinterpret_cast<decltype(a.commInitRank)>(sym("ncclCommInitRank"));
+            a.commDestroy = reinterpret_cast<decltype(a.commDestroy)>(sym("ncclCommDestroy"));
+            a.allGather = reinterpret_cast<decltype(a.allGather)>(sym("ncclAllGather"));
+            a.broadcast = reinterpret_cast<decltype(a.broadcast)>(sym("ncclBroadcast"));
+            a.groupStart = reinterpret_cast<decltype(a.groupStart)>(sym("ncclGroupStart"));
+            a.groupEnd = reinterpret_cast<decltype(a.groupEnd)>(sym("ncclGroupEnd"));
+            a.errorString = reinterpret_cast<decltype(a.errorString)>(sym("ncclGetErrorString"));
+        }
+        return a;
+    }
+    void check(ncclResult_t rc, const char* what) const {
+        if (rc != ncclSuccess) fail(SAD_ECUDA, std::string(what) + ": " + errorString(rc));
+    }
+};
+
+struct NcclComm : StripComm {
+    NcclApi& api;
+    ncclComm_t comm = nullptr;
+    int n;
+    NcclComm(int rank, int world, const uint8_t* id) : api(NcclApi::get()), n(world) {
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, sizeof(uid));
+        api.check(api.commInitRank(&comm, world, uid, rank), "ncclCommInitRank");
+    }
+    ~NcclComm() override {
+        if (comm) api.commDestroy(comm);
+    }
+    int world() const override { return n; }
+    void gather_rows(std::vector<sad_fit_run*>& runs, int b) override {
+        sad_fit_run* r = runs[0];
+        const size_t row = static_cast<size_t>(r->ws.fd.gw) * r->ws.fd.k;
+        api.check(api.groupStart(), "ncclGroupStart");
+        for (int q = 0; q < n; q++) {
+            const size_t off = row * r->strip[q], cnt = row * (r->strip[q + 1] - r->strip[q]);
+            if (cnt)
+                api.check(api.broadcast(r->ws.ids[b].p + off, r->ws.ids[b].p + off, cnt, ncclUint32, q, comm, r->ws.stream),
+                          "ncclBroadcast");
+        }
+        api.check(api.groupEnd(), "ncclGroupEnd");
+    }
+    void gather(std::vector<sad_fit_run*>& runs, const std::function<const void*(sad_fit_run*)>& self,
+                const std::function<void*(sad_fit_run*)>& all, size_t bytes) override {
+        sad_fit_run* r = runs[0];
+        api.check(api.allGather(self(r), all(r), bytes, ncclChar, comm, r->ws.stream), "ncclAllGather");
+    }
+};
+
+// Row bounds of `world` strips over `rows` rows, each a multiple of the 8-row backward/stats tiles.
+static std::vector<int> strip_bounds(int rows, int world) {
+    const int tiles = (rows + 7) / 8;
+    std::vector<int> b(static_cast<size_t>(world) + 1);
+    for (int q = 0; q <= world; q++) b[q] = std::min(rows, 8 * static_cast<int>(static_cast<long long>(tiles) * q / world));
+    return b;
+}
+
+static void fit_loop_strips(std::vector<sad_fit_run*>& runs, StripComm& T) {
+    const int R = T.world();
+    sad_fit_run* r0 = runs[0];
+    const sad_train_config& c = r0->cfg;
+    const int w = r0->w, h = r0->h;
+    const bool fp64 = c.fp64 != 0;
+    const bool budget = c.target_bpp > 0;
+    const double scale_n = norm_scale(w, h);
+    if (c.tau_diffusion_lambda > 0) fail(SAD_EINVAL, "strips: tau_diffusion is not supported");
+    if (c.k > 16 || r0->ws.fd.cell != 1) fail(SAD_EINVAL, "strips: cell size 1 only");
+    double sched = 1.0;
+    // prologue, per rank (as fit_loop)
+    for (sad_fit_run* r : runs) {
+        Workspace& ws = r->ws;
+        cudaStream_t s = ws.stream;
+        DevState st0 = ws.get_state();
+        ws.compute_active();
+        DevState sta = ws.get_state();
+        r->schedule_scale = 0;
+        if (budget) {
+            if (sta.n_active != r->planned_n0) {
+                r->planned_scale = plan_schedule(sta.n_active, bpp_target_count(c.target_bpp, w, h), c);
+                r->planned_n0 = sta.n_active;
+            }
+            sched = r->planned_scale;
+            r->schedule_scale = sched;
+        }
+        int capn = capacity_bound(c, st0.n_sites, sched, budget);
+        if (capn > ws.cap) {
+            ws.ensure_cap(capn);
+            ws.compute_active();
+            sta = ws.get_state();
+        }
+        ck(cudaMemsetAsync(ws.m.p, 0, sizeof(double) * 10 * ws.cap, s), "memset m");
+        ck(cudaMemsetAsync(ws.v.p, 0, sizeof(double) * 10 * ws.cap, s), "memset v");
+        ws.zero_red(true);
+        DevState init{};
+        init.n_sites = st0.n_sites;
+        init.n_active = sta.n_active;
+        ws.set_state(init);
+        r->strip = strip_bounds(h, R);
+        ws.fd.row0 = r->strip[r->rank];
+        ws.fd.row1 = r->strip[r->rank + 1];
+        ws.ensure_adaptive(static_cast<size_t>(sadk::backward_blocks(fp64, ws.fd)));
+        sadk::launch_fill_i32(ws.rcap.p, ws.cap, 16, s);
+        ws.plan_records();
+        ck(cudaMemsetAsync(ws.gcnt.p, 0, sizeof(int32_t) * ws.cap, s), "memset gcnt");
+        ck(cudaMemsetAsync(ws.ghead.p, 0xff, sizeof(int32_t) * ws.cap, s), "memset ghead");
+        const size_t cap = static_cast<size_t>(ws.cap);
+        r->gpart_self.ensure(10 * cap);
+        r->gpart_all.ensure(static_cast<size_t>(R) * 10 * cap);
+        r->spart_all.ensure(static_cast<size_t>(R) * 8 * cap);
+        r->loss_self.ensure(1);
+        r->loss_all.ensure(R);
+        r->tot.ensure(10 * cap);
+        r->valid_all.ensure(R);
+    }
+    const int cap = r0->ws.cap;
+    const sadk::AdamHyper hp = adam_hyper(c, w, h);
+    const auto full4 = full_refresh_passes(r0->ws.fd.gw, r0->ws.fd.gh, 4);
+    const std::vector<sad_pass_spec> warm(static_cast<size_t>(c.refresh_passes), sad_pass_spec{1, 0});
+    auto tgt_of = [&](sad_fit_run* r) {
+        return fp64 ? static_cast<const void*>(r->ws.tgt_d.p) : static_cast<const void*>(r->ws.tgt_f.p);
+    };
+    auto passes = [&](const std::vector<sad_pass_spec>& seq, uint32_t base) {
+        for (size_t i = 0; i < seq.size(); i++) {
+            for (sad_fit_run* r : runs) {
+                Workspace& ws = r->ws;
+                sadk::launch_propagate(fp64, ws.ids[ws.cur].p, ws.ids[1 - ws.cur].p, ws.pack.p, ws.act.p, ws.st.p, ws.fd,
+                                       seq[i].step, seq[i].stencil, c.inject, c.seed, base + static_cast<uint32_t>(i),
+                                       scale_n, ws.stream);
+            }
+            T.gather_rows(runs, 1 - r0->ws.cur);
+            for (sad_fit_run* r : runs) r->ws.cur = 1 - r->ws.cur;
+        }
+    };
+    auto reseed = [&] {
+        for (sad_fit_run* r : runs) {
+            r->ws.cur = 0;
+            sadk::launch_jfa_seed(r->ws.sites(), r->ws.st.p, r->ws.ids[0].p, r->ws.fd, scale_n, r->ws.stream);
+        }
+    };
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, r0->ws.stream);
+    // initial full refresh
+    for (sad_fit_run* r : runs) build_tables(r->ws, fp64, true, true, false);
+    reseed();
+    passes(full4, 0);
+    for (sad_fit_run* r : runs)
+        sadk::launch_advance(r->ws.st.p, static_cast<int>(full4.size()), 0, nullptr, nullptr, nullptr, 0,
+                             r->ws.otops.p, r->ws.stream);
+    for (int t = 1; t <= c.iters; t++) {
+        const bool rf = (t - 1) % c.refresh_every == 0;
+        bool ev_d = budget && t >= c.densify_start && t <= c.densify_end && t % c.densify_every == 0;
+        bool ev_p = budget && t >= c.prune_start && t <= c.prune_end && t % c.prune_every == 0;
+        if (ev_p && !c.prune_during_densify && t <= c.densify_end) ev_p = false;
+        const bool ev = ev_d || ev_p;
+        int npass = 0;
+        if (rf) {
+            passes(warm, 0);
+            npass += static_cast<int>(warm.size());
+        }
+        // backward on the strips, then the exact cross-rank merge of the site totals and the loss
+        for (sad_fit_run* r : runs) {
+            Workspace& ws = r->ws;
+            sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt_of(r), ws.fd, scale_n, ws.gred_adaptive(),
+                                  ws.loss_part.p, ws.st.p, ws.stream);
+            sadk::launch_loss_reduce(ws.loss_part.p, sadk::backward_blocks(fp64, ws.fd), r->loss_self.p, ws.stream);
+            sadk::launch_site_partials(ws.gred_adaptive(), ws.st.p, cap, r->gpart_self.p, ws.stream);
+        }
+        T.gather(runs, [](sad_fit_run* r) { return static_cast<const void*>(r->gpart_self.p); },
+                 [](sad_fit_run* r) { return static_cast<void*>(r->gpart_all.p); }, 10 * sizeof(double2) * cap);
+        T.gather(runs, [](sad_fit_run* r) { return static_cast<const void*>(r->loss_self.p); },
+                 [](sad_fit_run* r) { return static_cast<void*>(r->loss_all.p); }, sizeof(double2));
+        for (sad_fit_run* r : runs)
+            sadk::launch_merge_partials(r->gpart_all.p, R, cap, 10, r->tot.p, nullptr, r->ws.stream);
+        if (ev) {  // stats (budget.cpp:39-155) on the strips, merged the same way
+            for (sad_fit_run* r : runs) stats_device(r->ws);
+            T.gather(runs, [](sad_fit_run* r) { return static_cast<const void*>(r->ws.stats.p); },
+                     [](sad_fit_run* r) { return static_cast<void*>(r->spart_all.p); }, 8 * sizeof(double2) * cap);
+            T.gather(runs, [](sad_fit_run* r) { return static_cast<const void*>(&r->ws.st.p->valid); },
+                     [](sad_fit_run* r) { return static_cast<void*>(r->valid_all.p); }, sizeof(unsigned long long));
+            for (sad_fit_run* r : runs) {
+                sadk::launch_merge_partials(r->spart_all.p, R, cap, 8, nullptr, r->ws.stats.p, r->ws.stream);
+                std::vector<unsigned long long> va(R);
+                ck(cudaMemcpyAsync(va.data(), r->valid_all.p, 8 * R, cudaMemcpyDeviceToHost, r->ws.stream), "D2H valid");
+                ck(cudaStreamSynchronize(r->ws.stream), "valid");
+                uint64_t vt = 0;
+                for (unsigned long long v : va) vt += v;
+                r->ws.patch_state(offsetof(DevState, valid), vt);
+            }
+        }
+        for (sad_fit_run* r : runs) {
+            Workspace& ws = r->ws;
+            sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.gred_adaptive(), ws.m.p, ws.v.p, hp, r->bc_table.p,
+                              make_double2(0, 0), true, scale_n, ev ? nullptr : ws.pack.p, ev ? nullptr : ws.gtab.p,
+                              ws.rcap.p, ws.stream, r->tot.p, ws.roff.p, ws.otops.p + 2,
+                              (ev || g_adam_all) ? nullptr : ws.act.p);
+        }
+        if (ev) {
+            for (sad_fit_run* r : runs) {
+                Workspace& ws = r->ws;
+                if (ev_p) prune_device(ws, c.prune_pct * sched);
+                if (ev_d) densify_device(ws, c.densify_pct * sched, c);
+                ws.compute_active();
+                build_tables(ws, fp64, true, true, false);
+            }
+            reseed();
+            passes(full4, static_cast<uint32_t>(npass));
+            npass += static_cast<int>(full4.size());
+        }
+        for (sad_fit_run* r : runs)
+            sadk::launch_advance(r->ws.st.p, npass, 1, r->loss_hist.p, r->active_hist.p, r->loss_all.p, R,
+                                 r->ws.otops.p, r->ws.stream);
+    }
+    // final full refresh (train.cpp:287)
+    reseed();
+    passes(full_refresh_passes(r0->ws.fd.gw, r0->ws.fd.gh, c.final_passes), 0);
+    for (sad_fit_run* r : runs)
+        sadk::launch_advance(r->ws.st.p, static_cast<int>(full_refresh_passes(r0->ws.fd.gw, r0->ws.fd.gh, c.final_passes).size()),
+                             0, nullptr, nullptr, nullptr, 0, r->ws.otops.p, r->ws.stream);
+    cudaEventRecord(e1, r0->ws.stream);
+    for (sad_fit_run* r : runs) ck(cudaStreamSynchronize(r->ws.stream), "fit strips");
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    for (sad_fit_run* r : runs) {
+        r->total_ms = ms;
+        r->ws.fd.row0 = 0;  // downloads / renders of the finished run see the whole image
+        r->ws.fd.row1 = 1 << 30;
+        finish_run(r, ms, c.iters);
+    }
+}
+
+static void strips_prepare(sad_fit_run* r, bool init_sites) {
+    if (!r->have_target) fail(SAD_EINVAL, "fit: target not set");
+    if (init_sites) {
+        int n = initial_count(r->cfg, r->w, r->h);
+        r->ws.ensure_cap(n);
+        init_sites_device(r->ws, r->w, r->h, n, r->cfg);
+    }
+}
+
+sad_status sad_nccl_unique_id(uint8_t* out) {
+    return guard([&] {
+        NcclApi& api = NcclApi::get();
+        ncclUniqueId uid;
+        api.check(api.getUniqueId(&uid), "ncclGetUniqueId");
+        std::memcpy(out, &uid, sizeof(uid));
+    });
+}
+
+sad_status sad_fit_run_strips(sad_fit_run* r, int rank, int world, const uint8_t* nccl_id, const sad_sites_view* init) {
+    return guard([&] {
+        if (world < 1 || rank < 0 || rank >= world) fail(SAD_EINVAL, "strips: bad rank / world");
+        if (!nccl_id) fail(SAD_EINVAL, "strips: null NCCL id");
+        if (init) upload_sites(r->ws, init);
+        strips_prepare(r, !init);
+        r->rank = rank;
+        r->world = world;
+        NcclComm comm(rank, world, nccl_id);
+        std::vector<sad_fit_run*> runs{r};
+        fit_loop_strips(runs, comm);
+    });
+}
+
+sad_status sad_fit_run_strips_loopback(sad_fit_run* const* rs, int world) {
+    return guard([&] {
+        if (world < 1 || !rs) fail(SAD_EINVAL, "strips: bad world");
+        std::vector<sad_fit_run*> runs(rs, rs + world);
+        for (int q = 0; q < world; q++) {
+            if (!runs[q] || runs[q]->ws.stream != runs[0]->ws.stream)
+                fail(SAD_EINVAL, "strips loopback: runs must share one context (stream)");
+            strips_prepare(runs[q], true);
+            runs[q]->rank = q;
+            runs[q]->world = world;
+        }
+        LoopbackComm comm(world);
+        fit_loop_strips(runs, comm);
+    });
 }
 
 sad_status sad_fit_run_init(sad_fit_run* r) {
