@@ -1894,7 +1894,8 @@ static void fit_loop(sad_fit_run* r) {
 // one large image split into row strips.  Every rank replicates the sites, tables, target
 // and the whole candidate field, but computes only its strip: propagation rows, backward and stats
 // tiles (FieldDims row range; strips are multiples of the 8-row tiles).  Exchanges per step:
-//   * after every propagation pass: the strips of the new field buffer (owner broadcasts);
+//   * before every propagation pass at jump s: the rows within s of the strip (owner -> reader);
+//     at the end, all strips (owner broadcasts), so every rank holds the whole final field;
 //   * after the backward: every rank's per-site double-double partial totals (10 channels) and its loss
 //     partial, merged in rank order by every rank (exact double-double: equals the single-GPU totals);
 //   * at events: the per-site stats partials (8 channels) and the valid-pixel counts, same merge.
@@ -1907,10 +1908,29 @@ struct StripComm {
     virtual int world() const = 0;
     // rows [strip[q], strip[q+1]) of ids[b] (cell rows of gw*k u32) from rank q to every rank
     virtual void gather_rows(std::vector<sad_fit_run*>& runs, int b) = 0;
+    // before a pass at jump `step`: every rank fetches the rows it will read outside its strip,
+    // [row0 - step, row0) and [row1, row1 + step), from their owners (buffer ids[b])
+    virtual void halo_rows(std::vector<sad_fit_run*>& runs, int b, int step) = 0;
     // slice q (bytes each) of every rank's `all` <- rank q's `self`
     virtual void gather(std::vector<sad_fit_run*>& runs, const std::function<const void*(sad_fit_run*)>& self,
                         const std::function<void*(sad_fit_run*)>& all, size_t bytes) = 0;
 };
+
+// Rows rank `r` reads outside its strip at jump `step` that rank `q` owns: up to two [lo, hi) ranges.
+static int halo_ranges(const std::vector<int>& strip, int r, int q, int step, int out[4]) {
+    const int rows = strip.back();
+    const int need[2][2] = {{std::max(0, strip[r] - step), strip[r]}, {strip[r + 1], std::min(rows, strip[r + 1] + step)}};
+    int n = 0;
+    for (const auto& nd : need) {
+        const int lo = std::max(nd[0], strip[q]), hi = std::min(nd[1], strip[q + 1]);
+        if (hi > lo) {
+            out[2 * n] = lo;
+            out[2 * n + 1] = hi;
+            n++;
+        }
+    }
+    return n;
+}
 
 struct LoopbackComm : StripComm {
     int n;
@@ -1926,6 +1946,20 @@ struct LoopbackComm : StripComm {
                                        cudaMemcpyDeviceToDevice, runs[r]->ws.stream),
                        "loopback rows");
         }
+    }
+    void halo_rows(std::vector<sad_fit_run*>& runs, int b, int step) override {
+        const size_t row = static_cast<size_t>(runs[0]->ws.fd.gw) * runs[0]->ws.fd.k;
+        const std::vector<int>& strip = runs[0]->strip;
+        for (int r = 0; r < n; r++)
+            for (int q = 0; q < n; q++) {
+                if (q == r) continue;
+                int rg[4];
+                const int m = halo_ranges(strip, r, q, step, rg);
+                for (int j = 0; j < m; j++)
+                    ck(cudaMemcpyAsync(runs[r]->ws.ids[b].p + row * rg[2 * j], runs[q]->ws.ids[b].p + row * rg[2 * j],
+                                       4 * row * (rg[2 * j + 1] - rg[2 * j]), cudaMemcpyDeviceToDevice, runs[r]->ws.stream),
+                       "loopback halo");
+            }
     }
     void gather(std::vector<sad_fit_run*>& runs, const std::function<const void*(sad_fit_run*)>& self,
                 const std::function<void*(sad_fit_run*)>& all, size_t bytes) override {
@@ -1944,6 +1978,8 @@ struct NcclApi {
     ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*groupStart)() = nullptr;
     ncclResult_t (*groupEnd)() = nullptr;
     const char* (*errorString)(ncclResult_t) = nullptr;
@@ -1962,6 +1998,8 @@ struct NcclApi {
             a.commDestroy = reinterpret_cast<decltype(a.commDestroy)>(sym("ncclCommDestroy"));
             a.allGather = reinterpret_cast<decltype(a.allGather)>(sym("ncclAllGather"));
             a.broadcast = reinterpret_cast<decltype(a.broadcast)>(sym("ncclBroadcast"));
+            a.send = reinterpret_cast<decltype(a.send)>(sym("ncclSend"));
+            a.recv = reinterpret_cast<decltype(a.recv)>(sym("ncclRecv"));
             a.groupStart = reinterpret_cast<decltype(a.groupStart)>(sym("ncclGroupStart"));
             a.groupEnd = reinterpret_cast<decltype(a.groupEnd)>(sym("ncclGroupEnd"));
             a.errorString = reinterpret_cast<decltype(a.errorString)>(sym("ncclGetErrorString"));
@@ -1995,6 +2033,27 @@ struct NcclComm : StripComm {
             if (cnt)
                 api.check(api.broadcast(r->ws.ids[b].p + off, r->ws.ids[b].p + off, cnt, ncclUint32, q, comm, r->ws.stream),
                           "ncclBroadcast");
+        }
+        api.check(api.groupEnd(), "ncclGroupEnd");
+    }
+    void halo_rows(std::vector<sad_fit_run*>& runs, int b, int step) override {
+        sad_fit_run* r = runs[0];
+        const size_t row = static_cast<size_t>(r->ws.fd.gw) * r->ws.fd.k;
+        const int me = r->rank;
+        api.check(api.groupStart(), "ncclGroupStart");
+        for (int q = 0; q < n; q++) {
+            if (q == me) continue;
+            int rg[4];
+            int m = halo_ranges(r->strip, q, me, step, rg);  // rows q needs that I own: send
+            for (int j = 0; j < m; j++)
+                api.check(api.send(r->ws.ids[b].p + row * rg[2 * j], row * (rg[2 * j + 1] - rg[2 * j]), ncclUint32, q,
+                                   comm, r->ws.stream),
+                          "ncclSend");
+            m = halo_ranges(r->strip, me, q, step, rg);  // rows I need that q owns: receive
+            for (int j = 0; j < m; j++)
+                api.check(api.recv(r->ws.ids[b].p + row * rg[2 * j], row * (rg[2 * j + 1] - rg[2 * j]), ncclUint32, q,
+                                   comm, r->ws.stream),
+                          "ncclRecv");
         }
         api.check(api.groupEnd(), "ncclGroupEnd");
     }
@@ -2077,15 +2136,17 @@ static void fit_loop_strips(std::vector<sad_fit_run*>& runs, StripComm& T) {
     auto tgt_of = [&](sad_fit_run* r) {
         return fp64 ? static_cast<const void*>(r->ws.tgt_d.p) : static_cast<const void*>(r->ws.tgt_f.p);
     };
+    // Each pass reads rows [row0 - step, row1 + step) of the current buffer: those outside the strip are
+    // fetched from their owners right before the pass; the pass writes the strip of the other buffer.
     auto passes = [&](const std::vector<sad_pass_spec>& seq, uint32_t base) {
         for (size_t i = 0; i < seq.size(); i++) {
+            T.halo_rows(runs, r0->ws.cur, static_cast<int>(seq[i].step));
             for (sad_fit_run* r : runs) {
                 Workspace& ws = r->ws;
                 sadk::launch_propagate(fp64, ws.ids[ws.cur].p, ws.ids[1 - ws.cur].p, ws.pack.p, ws.act.p, ws.st.p, ws.fd,
                                        seq[i].step, seq[i].stencil, c.inject, c.seed, base + static_cast<uint32_t>(i),
                                        scale_n, ws.stream);
             }
-            T.gather_rows(runs, 1 - r0->ws.cur);
             for (sad_fit_run* r : runs) r->ws.cur = 1 - r->ws.cur;
         }
     };
@@ -2176,6 +2237,7 @@ static void fit_loop_strips(std::vector<sad_fit_run*>& runs, StripComm& T) {
     for (sad_fit_run* r : runs)
         sadk::launch_advance(r->ws.st.p, static_cast<int>(full_refresh_passes(r0->ws.fd.gw, r0->ws.fd.gh, c.final_passes).size()),
                              0, nullptr, nullptr, nullptr, 0, r->ws.otops.p, r->ws.stream);
+    T.gather_rows(runs, r0->ws.cur);  // every rank ends with the whole final field
     cudaEventRecord(e1, r0->ws.stream);
     for (sad_fit_run* r : runs) ck(cudaStreamSynchronize(r->ws.stream), "fit strips");
     float ms = 0;
