@@ -53,6 +53,8 @@ def parse():
                         "2-BPP fit on one GPU (each its own JSON line)")
     p.add_argument("--c3-iters", type=int, default=300)
     p.add_argument("--c5-iters", type=int, default=100)
+    p.add_argument("--c5-size", type=int, default=8192, help="config5 image side (smaller for smoke runs)")
+    p.add_argument("--c5-strips", action="store_true", help="config5: row-strip NCCL path even at N = 1")
     p.add_argument("--no-roofline-2048", action="store_true")
     return p.parse_args()
 
@@ -295,48 +297,89 @@ def run_config3(a):
 
 
 def run_config5(a):
-    """Config 5: one 8192x8192 image at 2 BPP (n0 = 1,677,722 sites) fitted on one GPU.  Two fits of
-    different length give the marginal cost per iteration (the densify/prune events of the default
-    schedule included, one every 20 iterations from t = 20); the whole short fit (device init, initial
-    full refresh, iterations, final refresh(Full, 16)) is reported too."""
+    """Config 5: one 8192x8192 image at 2 BPP (n0 = 1,677,722 sites).  N = 1: the resident single-GPU fit.
+    N > 1 (torchrun): the row-strip partition over NCCL (sad_fit_run_strips; bit-identical to the
+    single-GPU fit), time = max over ranks, strong scaling.  Two fits of different length give the
+    marginal cost per iteration (the densify/prune events of the default schedule included, one every
+    20 iterations from t = 20); the whole short fits are reported too."""
     import torch
     import paper_2604_21984_b200 as sad
     from paper_2604_21984_b200 import api
     from paper_2604_21984_b200.synth import synthetic_image
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     lib = api.load_library()
     ctx = C.c_void_p()
-    if lib.sad_ctx_create(C.c_int(0), C.c_void_p(stream.cuda_stream), C.byref(ctx)):
+    if lib.sad_ctx_create(C.c_int(local), C.c_void_p(stream.cuda_stream), C.byref(ctx)):
         raise RuntimeError(lib.sad_last_error().decode())
     G = api.Backend(lib, "sad_", "gpu", ctx=ctx)
-    W = H = 8192
+    W = H = a.c5_size
     img = synthetic_image(W, H, 5)
+    nid = None
+    if world > 1:
+        obj = [G.nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    strips = world > 1 or a.c5_strips
+    if strips and nid is None:
+        nid = G.nccl_unique_id()
+    comm = G.strip_comm(rank, world, nid) if strips else None
     res = {}
-    for iters in (max(a.c5_iters // 2, 20), a.c5_iters):
+    for iters in (5, max(a.c5_iters // 2, 20), a.c5_iters):  # the 5-iteration fit is the warm-up
         cfg = sad.TrainConfig(iters=iters, target_bpp=2.0, fp64=False)
-        run = C.c_void_p()
-        cc = cfg.to_c()
-        G._call("fit_create", C.c_int(W), C.c_int(H), C.byref(cc), C.byref(run))
-        G._call("fit_set_target", run, img.ctypes.data_as(C.POINTER(C.c_double)))
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        G._call("fit_run_init", run)
+        if not strips:
+            run = C.c_void_p()
+            cc = cfg.to_c()
+            G._call("fit_create", C.c_int(W), C.c_int(H), C.byref(cc), C.byref(run))
+            G._call("fit_set_target", run, img.ctypes.data_as(C.POINTER(C.c_double)))
+            G._call("fit_run_init", run)
+            info = sad_fit_info(G, run)
+            tot = C.c_double()
+            ph = (C.c_double * 8)()
+            G._call("fit_timing", run, C.byref(tot), ph)
+            loop_ms = tot.value
+            G.lib.sad_fit_destroy(run)
+        else:
+            out = G.fit_strips(sad.ImageBuffer(W, H, img), cfg, comm)
+            info = {"n_sites": out.sites.size(), "schedule_scale": out.schedule_scale}
+            loop_ms = out.timing["total_ms"]
         e1.record(stream)
         e1.synchronize()
-        info = sad_fit_info(G, run)
-        res[iters] = (e0.elapsed_time(e1), info)
-        G.lib.sad_fit_destroy(run)
+        # the fit loop's own device time (allocation / init / download excluded; both lengths share them)
+        ms = loop_ms
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        if iters != 5:
+            res[iters] = (ms, info)
     (i0, (t0, _)), (i1, (t1, info1)) = sorted(res.items())
     per_iter = (t1 - t0) / (i1 - i0)
-    out = {"metric": "fit iterations/s", "mode": "config5", "value": 1e3 / per_iter, "unit": "iters/s",
-           "ms_per_iter_marginal": per_iter, "fit_ms": {str(k): v[0] for k, v in res.items()},
-           "final_site_slots": info1["n_sites"], "schedule_scale": info1["schedule_scale"], "n_gpus": 1,
-           "config": {"workload": f"config5: 8192x8192 synthetic (seed 5), target 2.0 BPP (n0 1,677,722), fp32; "
-                                  f"marginal per-iteration time between a {i0}- and a {i1}-iteration fit "
-                                  f"(default event schedule)"},
-           "reference_cpu_s_per_warm_pass_8_threads": 9.32, "reference_cpu_initial_refresh_s": 393.7}
-    print(json.dumps(out), flush=True)
+    if rank == 0:
+        out = {"metric": "fit iterations/s", "mode": "config5", "value": 1e3 / per_iter, "unit": "iters/s",
+               "ms_per_iter_marginal": per_iter, "fit_ms": {str(k): v[0] for k, v in res.items()},
+               "final_site_slots": info1["n_sites"], "schedule_scale": info1["schedule_scale"], "n_gpus": world,
+               "scaling": "strong", "parallelism": f"row strips x{world} (NCCL)" if strips else "single GPU",
+               "config": {"workload": f"config5: {W}x{H} synthetic (seed 5), target 2.0 BPP, fp32; marginal "
+                                      f"per-iteration time between a {i0}- and a {i1}-iteration fit (default event "
+                                      f"schedule); N > 1: row-strip partition over NCCL, max over ranks"},
+               "reference_cpu_s_per_warm_pass_8_threads": 9.32, "reference_cpu_initial_refresh_s": 393.7}
+        print(json.dumps(out), flush=True)
+    if comm is not None:
+        G.lib.sad_strip_comm_destroy(comm)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
 
 
 def sad_fit_info(G, run):

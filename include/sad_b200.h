@@ -259,14 +259,17 @@ sad_status sad_decode_render(sad_ctx* ctx, const uint8_t* buf, size_t n, int k, 
  * One image split into row strips (multiples of 8 rows): each rank replicates sites and tables, computes
  * its strip of the propagation passes, backward and stats, and merges the exact per-rank partials in rank
  * order, so the result is bit-identical to the single-GPU fit.  One process per GPU: rank 0 calls
- * sad_nccl_unique_id and shares the 128 bytes (e.g. torch.distributed), then every rank creates its run
- * (sad_fit_create, sad_fit_set_target with the whole image) and calls sad_fit_run_strips (init NULL:
+ * sad_nccl_unique_id and shares the 128 bytes (e.g. torch.distributed), every rank creates one
+ * communicator (sad_strip_comm_create; NCCL ids are single-use), then per fit its run (sad_fit_create,
+ * sad_fit_set_target with the whole image) and calls sad_fit_run_strips (init NULL:
  * fit(), else fit_store() from `init`).  Results are read with sad_fit_info / sad_fit_download on any rank.
  * sad_fit_run_strips_loopback runs `world` virtual ranks (runs created on one context) on one device,
  * exchanging by device copies: the single-GPU check of the partition. */
+typedef struct sad_strip_comm sad_strip_comm; /* an NCCL communicator over the strip ranks (reusable) */
 sad_status sad_nccl_unique_id(uint8_t* out128);
-sad_status sad_fit_run_strips(sad_fit_run* run, int rank, int world, const uint8_t* nccl_id128,
-                              const sad_sites_view* init);
+sad_status sad_strip_comm_create(int rank, int world, const uint8_t* nccl_id128, sad_strip_comm** out);
+void sad_strip_comm_destroy(sad_strip_comm* comm);
+sad_status sad_fit_run_strips(sad_fit_run* run, sad_strip_comm* comm, const sad_sites_view* init);
 sad_status sad_fit_run_strips_loopback(sad_fit_run* const* runs, int world);
 
 /* ---------------------------------------------------------------- fit / fit_store in one call

@@ -440,8 +440,13 @@ class Backend:
     def _collect_run(self, run, w, h, cfg) -> FitResult:
         n, nh, sc = C.c_size_t(), C.c_int(), C.c_double()
         self._call("fit_info", run, C.byref(n), C.byref(nh), C.byref(sc))
-        return self._fit_collect(w, h, cfg, int(n.value), int(nh.value), float(sc.value),
-                                 lambda sv, fv, hist: self._call("fit_download", run, sv, fv, hist))
+        res = self._fit_collect(w, h, cfg, int(n.value), int(nh.value), float(sc.value),
+                                lambda sv, fv, hist: self._call("fit_download", run, sv, fv, hist))
+        tot = C.c_double()
+        ph = (C.c_double * 8)()
+        self._call("fit_timing", run, C.byref(tot), ph)
+        res.timing = {"total_ms": tot.value}  # device time of the fit loop (refreshes included)
+        return res
 
     def fit_strips_loopback(self, target: ImageBuffer, cfg: TrainConfig, world: int) -> List[FitResult]:
         """Row-strip fit (config 5 partition) with `world` virtual ranks on this device; returns every
@@ -462,8 +467,14 @@ class Backend:
             for r in runs:
                 self.lib.sad_fit_destroy(r)
 
-    def fit_strips(self, target: ImageBuffer, cfg: TrainConfig, rank: int, world: int, nccl_id: bytes,
-                   init: Optional[SiteStore] = None) -> FitResult:
+    def strip_comm(self, rank: int, world: int, nccl_id: bytes):
+        """NCCL communicator over the strip ranks (one per process; NCCL ids are single-use)."""
+        comm = C.c_void_p()
+        idb = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+        self._call("strip_comm_create", C.c_int(rank), C.c_int(world), idb, C.byref(comm))
+        return comm
+
+    def fit_strips(self, target: ImageBuffer, cfg: TrainConfig, comm, init: Optional[SiteStore] = None) -> FitResult:
         """This rank's part of a row-strip multi-GPU fit over NCCL (one process per GPU)."""
         c = cfg.to_c()
         w, h = target.width, target.height
@@ -471,11 +482,10 @@ class Backend:
         self._call("fit_create", C.c_int(w), C.c_int(h), C.byref(c), C.byref(run))
         try:
             self._call("fit_set_target", run, _ptr(target.data))
-            idb = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
             sv = None
             if init is not None:
                 sv, keep = init._view()
-            self._call("fit_run_strips", run, C.c_int(rank), C.c_int(world), idb, _ref(sv))
+            self._call("fit_run_strips", run, comm, _ref(sv))
             return self._collect_run(run, w, h, cfg)
         finally:
             self.lib.sad_fit_destroy(run)
@@ -622,7 +632,7 @@ class Backend:
 _NO_CTX = {"jump_step", "full_refresh_passes", "schedule_passes", "bpp_target_count", "simulate_schedule",
            "plan_schedule", "fit_set_target", "fit_set_target_device", "fit_run_init", "fit_run_store",
            "fit_info", "fit_download", "fit_render_device", "fit_timing", "fit_bench", "fit_set_profiling",
-           "fit_point_query", "fit_capacity", "fit_run_strips", "fit_run_strips_loopback", "nccl_unique_id", "encode", "decode", "decode_header", "bpp",
+           "fit_point_query", "fit_capacity", "fit_run_strips", "fit_run_strips_loopback", "nccl_unique_id", "strip_comm_create", "encode", "decode", "decode_header", "bpp",
            "last_error"}
 
 # ---------------------------------------------------------------------- product binding

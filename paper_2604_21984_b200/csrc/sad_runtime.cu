@@ -2270,17 +2270,39 @@ sad_status sad_nccl_unique_id(uint8_t* out) {
     });
 }
 
-sad_status sad_fit_run_strips(sad_fit_run* r, int rank, int world, const uint8_t* nccl_id, const sad_sites_view* init) {
+struct sad_strip_comm {
+    std::unique_ptr<NcclComm> comm;
+    int rank = 0, world = 1;
+};
+
+sad_status sad_strip_comm_create(int rank, int world, const uint8_t* nccl_id, sad_strip_comm** out) {
     return guard([&] {
         if (world < 1 || rank < 0 || rank >= world) fail(SAD_EINVAL, "strips: bad rank / world");
-        if (!nccl_id) fail(SAD_EINVAL, "strips: null NCCL id");
+        if (!nccl_id || !out) fail(SAD_EINVAL, "strips: null argument");
+        auto* c = new sad_strip_comm();
+        try {
+            c->comm.reset(new NcclComm(rank, world, nccl_id));
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        c->rank = rank;
+        c->world = world;
+        *out = c;
+    });
+}
+
+void sad_strip_comm_destroy(sad_strip_comm* c) { delete c; }
+
+sad_status sad_fit_run_strips(sad_fit_run* r, sad_strip_comm* comm, const sad_sites_view* init) {
+    return guard([&] {
+        if (!comm) fail(SAD_EINVAL, "strips: null communicator");
         if (init) upload_sites(r->ws, init);
         strips_prepare(r, !init);
-        r->rank = rank;
-        r->world = world;
-        NcclComm comm(rank, world, nccl_id);
+        r->rank = comm->rank;
+        r->world = comm->world;
         std::vector<sad_fit_run*> runs{r};
-        fit_loop_strips(runs, comm);
+        fit_loop_strips(runs, *comm->comm);
     });
 }
 

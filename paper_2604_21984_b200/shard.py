@@ -4,11 +4,10 @@
   images with no data-path collective (weak scaling), and the only communication is the timing /
   result reduction (`max_over_ranks`, `sum_over_ranks`) through torch.distributed (NCCL on B200s,
   gloo in the CPU tests).
-* Config 5 — one large image in row strips: `strip_bounds` / `halo_rows` give each rank's strip and
-  the neighbour rows a propagation pass at jump step `step` reads (Axial: rows y +- step; Box3: the
-  same rows, three columns).  The strip map is deterministic and partition-invariant: the injection
-  stream is keyed by the global (pass_index, cell), so a strip rank reproduces exactly the rows a
-  single-GPU pass would produce.
+* Config 5 — one large image in row strips (sad_fit_run_strips): `strip_bounds` / `halo_rows` give
+  each rank's strip and the rows it fetches before a propagation pass at jump `step`.  The strip map
+  is partition-invariant (the injection stream is keyed by the global (pass_index, cell)) and the
+  gradient / stats partials are merged exactly, so every rank reproduces the single-GPU fit.
 """
 from __future__ import annotations
 
@@ -30,38 +29,31 @@ def image_seeds(n_images_per_rank: int, world: int, rank: int, base_seed: int = 
 
 
 def strip_bounds(height: int, world: int, rank: int) -> Tuple[int, int]:
-    """Row strip [y0, y1) of `rank` for a `height`-row grid (balanced, contiguous)."""
+    """Row strip [y0, y1) of `rank` (the partition of sad_fit_run_strips, sad_runtime.cu strip_bounds):
+    balanced, contiguous, every boundary a multiple of the 8-row backward / stats tiles."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError("bad world/rank")
-    y0 = height * rank // world
-    y1 = height * (rank + 1) // world
-    return y0, y1
+    tiles = (height + 7) // 8
+
+    def b(q):
+        return min(height, 8 * (tiles * q // world))
+    return b(rank), b(rank + 1)
 
 
 def halo_rows(height: int, world: int, rank: int, step: int) -> List[Tuple[int, int, int]]:
-    """Rows outside this rank's strip that a pass at jump `step` reads, grouped by owner rank:
-    [(owner_rank, row0, row1), ...] with [row0, row1) inside the owner's strip.  Axial and Box3
-    stencils read the same rows (y - step, y + step) for y in the strip."""
+    """Rows outside this rank's strip that a pass at jump `step` reads (Axial and Box3 read rows y - step
+    and y + step): the bands [y0 - step, y0) and [y1, y1 + step), grouped by owner rank as
+    [(owner_rank, row0, row1), ...] -- what sad_fit_run_strips fetches before the pass."""
     y0, y1 = strip_bounds(height, world, rank)
-    need = set()
-    for y in range(y0, y1):
-        for ny in (y - step, y + step):
-            if 0 <= ny < height and not (y0 <= ny < y1):
-                need.add(ny)
     out = []
     for owner in range(world):
-        o0, o1 = strip_bounds(height, world, owner)
-        rows = sorted(r for r in need if o0 <= r < o1)
-        if not rows:
+        if owner == rank:
             continue
-        # contiguous runs
-        start = prev = rows[0]
-        for r in rows[1:]:
-            if r != prev + 1:
-                out.append((owner, start, prev + 1))
-                start = r
-            prev = r
-        out.append((owner, start, prev + 1))
+        o0, o1 = strip_bounds(height, world, owner)
+        for lo, hi in ((max(0, y0 - step), y0), (y1, min(height, y1 + step))):
+            a, b = max(lo, o0), min(hi, o1)
+            if b > a:
+                out.append((owner, a, b))
     return out
 
 

@@ -80,11 +80,15 @@ def test_strips_and_halos(height, world):
     bounds = [shard.strip_bounds(height, world, r) for r in range(world)]
     assert bounds[0][0] == 0 and bounds[-1][1] == height
     assert all(bounds[i][1] == bounds[i + 1][0] for i in range(world - 1))
+    assert all(b[0] % 8 == 0 for b in bounds)  # tile-aligned (8-row backward / stats tiles)
     for step in (1, 2, 16, 1024):
         for r in range(world):
             y0, y1 = bounds[r]
-            want = {ny for y in range(y0, y1) for ny in (y - step, y + step)
+            # every row a pass at `step` reads outside the strip is fetched (the fetched bands cover it)
+            need = {ny for y in range(y0, y1) for ny in (y - step, y + step)
                     if 0 <= ny < height and not (y0 <= ny < y1)}
+            want = {ny for ny in list(range(max(0, y0 - step), y0)) + list(range(y1, min(height, y1 + step)))}
+            assert need <= want
             got = set()
             for owner, a, b in shard.halo_rows(height, world, r, step):
                 o0, o1 = bounds[owner]

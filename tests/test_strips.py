@@ -36,5 +36,9 @@ def test_strips_nccl_world1():
     tgt = synth_target(48, 40, 3)
     cfg = sad.TrainConfig(iters=60, target_bpp=2.0, fp64=False, seed=4, densify_start=10, densify_every=10)
     ref = G.fit(tgt, cfg)
-    out = G.fit_strips(tgt, cfg, 0, 1, G.nccl_unique_id())
-    _same(out, ref)
+    comm = G.strip_comm(0, 1, G.nccl_unique_id())
+    try:
+        _same(G.fit_strips(tgt, cfg, comm), ref)
+        _same(G.fit_strips(tgt, cfg, comm), ref)  # the communicator is reusable across fits
+    finally:
+        G.lib.sad_strip_comm_destroy(comm)
