@@ -334,9 +334,14 @@ struct Workspace {
     } tb;
     DBuf<double> dens_ratio, dens_an;  // densify: split ratios and their host-computed anisotropy
     DBuf<uint32_t> dens_slots;
+    double* hpin_ratio = nullptr;  // pinned host mirrors of the above
+    double* hpin_an = nullptr;
+    int hpin_n = 0;
 
     ~Workspace() {
         if (hst) cudaFreeHost(hst);
+        if (hpin_ratio) cudaFreeHost(hpin_ratio);
+        if (hpin_an) cudaFreeHost(hpin_an);
     }
 
     sadk::SitesDev sites() { return sadk::SitesDev{params.p, active.p, frozen.p, cap}; }
@@ -745,22 +750,32 @@ void densify_device(Workspace& ws, double pct, const sad_train_config& c) {
     ws.dens_an.ensure(ws.cap);
     sadk::launch_densify_apply(ws.sites(), ws.st.p, ws.stats.p, ws.cap, ws.vals[1].p, ws.free_list.p, ws.tgt_d.p, pct,
                                hp, ws.m.p, ws.v.p, ws.dens_ratio.p, ws.dens_slots.p, ws.stream);
-    // split-axis anisotropy with the host's glibc log, as the reference (budget.cpp:198-199)
-    const DevState st = ws.get_state();
-    const int done = st.done;
+    // split-axis anisotropy with the host's glibc log, as the reference (budget.cpp:198-199): one
+    // synchronisation fetches the state and every candidate ratio into pinned memory; the results go
+    // back asynchronously from a second pinned buffer (reused only after the next event's sync)
+    if (ws.hpin_n < ws.cap) {  // (re)allocate once the stream no longer reads the old buffers
+        ck(cudaStreamSynchronize(ws.stream), "densify pinned");
+        if (ws.hpin_ratio) cudaFreeHost(ws.hpin_ratio);
+        if (ws.hpin_an) cudaFreeHost(ws.hpin_an);
+        ws.hpin_ratio = ws.hpin_an = nullptr;
+        ws.hpin_n = 0;
+        ck(cudaMallocHost(&ws.hpin_ratio, 8 * static_cast<size_t>(ws.cap)), "cudaMallocHost");
+        ck(cudaMallocHost(&ws.hpin_an, 8 * static_cast<size_t>(ws.cap)), "cudaMallocHost");
+        ws.hpin_n = ws.cap;
+    }
+    ck(cudaMemcpyAsync(ws.hst, ws.st.p, sizeof(DevState), cudaMemcpyDeviceToHost, ws.stream), "D2H state");
+    ck(cudaMemcpyAsync(ws.hpin_ratio, ws.dens_ratio.p, 8 * static_cast<size_t>(ws.cap), cudaMemcpyDeviceToHost,
+                       ws.stream),
+       "D2H ratio");
+    ck(cudaStreamSynchronize(ws.stream), "densify ratio");
+    const int done = ws.hst->done;
     if (done > 0) {
-        std::vector<double> ratio(static_cast<size_t>(done)), an(static_cast<size_t>(done));
-        ck(cudaMemcpyAsync(ratio.data(), ws.dens_ratio.p, 8 * static_cast<size_t>(done), cudaMemcpyDeviceToHost,
-                           ws.stream),
-           "D2H ratio");
-        ck(cudaStreamSynchronize(ws.stream), "densify ratio");
         for (int i = 0; i < done; i++)
-            an[i] = ratio[i] < 0 ? std::numeric_limits<double>::quiet_NaN()
-                                 : std::clamp(-0.5 * std::log(ratio[i]), c.aniso_min, c.aniso_max);
-        ck(cudaMemcpyAsync(ws.dens_an.p, an.data(), 8 * static_cast<size_t>(done), cudaMemcpyHostToDevice, ws.stream),
+            ws.hpin_an[i] = ws.hpin_ratio[i] < 0 ? std::numeric_limits<double>::quiet_NaN()
+                                                 : std::clamp(-0.5 * std::log(ws.hpin_ratio[i]), c.aniso_min, c.aniso_max);
+        ck(cudaMemcpyAsync(ws.dens_an.p, ws.hpin_an, 8 * static_cast<size_t>(done), cudaMemcpyHostToDevice, ws.stream),
            "H2D aniso");
         sadk::launch_densify_aniso(ws.params.p, ws.cap, done, ws.dens_slots.p, ws.dens_an.p, ws.stream);
-        ck(cudaStreamSynchronize(ws.stream), "densify aniso");  // `an` is host memory read by the copy above
     }
 }
 
