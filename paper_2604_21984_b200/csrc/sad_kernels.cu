@@ -2639,6 +2639,9 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
     const int cap = s.cap;
     // with `act` (plain iterations) the groups walk the ascending active list: inactive sites have no
     // records, no update and keep their tables, so skipping them is exact
+    // active-list mode: blocks whose 8 groups all lie past the active count have nothing to do (the grid
+    // is sized by the capacity because it is captured in a CUDA graph); block-uniform, before any barrier
+    if (act && static_cast<int>(blockIdx.x) * 8 >= st->n_active) return;
     const bool live = act ? grp < st->n_active : grp < st->n_sites;
     const int id = act ? (live ? static_cast<int>(act[grp]) : cap) : grp;
     const int k = lane16;

@@ -2486,6 +2486,15 @@ sad_status sad_fit_bench(sad_fit_run* r, int which, int reps, double* ms_per_lau
                 ws.plan_records();
                 break;
             case 5: stats_device(ws); break;
+            case 9:  // plain-iteration Adam over the active list on unchanged records (no reset, no claims)
+                sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.gred_adaptive(), ws.m.p, ws.v.p, hp, nullptr,
+                                  make_double2(1.0, 1.0), false, sn, ws.pack.p, ws.gtab.p, nullptr, s, nullptr,
+                                  nullptr, nullptr, ws.act.p);
+                break;
+            case 10:  // k_advance alone (loss partials of the last backward)
+                sadk::launch_advance(ws.st.p, 0, 0, nullptr, nullptr, ws.loss_part.p, sadk::backward_blocks(fp64, ws.fd),
+                                     nullptr, s);
+                break;
             case 7:  // one event refresh: seed + ceil(log2) Box3 floods + 4 Axial passes
                 ws.cur = 0;
                 sadk::launch_jfa_seed(ws.sites(), ws.st.p, ws.ids[0].p, ws.fd, sn, s);

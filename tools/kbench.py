@@ -15,7 +15,8 @@ from paper_2604_21984_b200 import api  # noqa: E402
 from paper_2604_21984_b200.synth import synthetic_image  # noqa: E402
 
 KERNELS = {"propagate_warm": 0, "fwd_bwd": 1, "render": 2, "propagate_flood": 3, "adam": 4, "stats": 5,
-           "memsets": 6, "refresh_full": 7, "box_step": 8}
+           "memsets": 6, "refresh_full": 7, "box_step": 8,
+           "adam_active": 9, "advance": 10}
 
 p = argparse.ArgumentParser()
 p.add_argument("--kernel", default="fwd_bwd", choices=list(KERNELS))
