@@ -31,6 +31,17 @@ def test_strips_loopback_equal_single_gpu(w, h, world):
         _same(o, ref)
 
 
+@pytest.mark.parametrize("fp64,k,world", [(True, 8, 2), (False, 5, 3), (False, 12, 2)])
+def test_strips_loopback_fp64_and_other_k(fp64, k, world):
+    G = sad.gpu_backend(0)
+    tgt = synth_target(56, 40, 9)
+    cfg = sad.TrainConfig(iters=80, target_bpp=2.0, fp64=fp64, k=k, seed=3, densify_start=10, densify_every=10,
+                          prune_start=20, prune_every=20)
+    ref = G.fit(tgt, cfg)
+    for o in G.fit_strips_loopback(tgt, cfg, world):
+        _same(o, ref)
+
+
 def test_strips_nccl_world1():
     G = sad.gpu_backend(0)
     tgt = synth_target(48, 40, 3)
