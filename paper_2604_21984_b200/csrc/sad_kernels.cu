@@ -515,6 +515,9 @@ __global__ void __launch_bounds__(256) k_propagate_k8(const uint32_t* __restrict
     out[1] = make_uint4(sel.id[4], sel.id[5], sel.id[6], sel.id[7]);
 }
 
+#ifndef SAD_QUEUE_BY
+#define SAD_QUEUE_BY 4  // block height of the queue kernels (32 x BY threads)
+#endif
 #ifndef SAD_PROP_MINB
 #define SAD_PROP_MINB 4
 #endif
@@ -674,12 +677,13 @@ __global__ void __launch_bounds__(256, SAD_PROP_MINB) k_prop8_stream(const uint3
 // filtered by id first and only the rest (plus the injected ids) go through a per-thread shared
 // queue that is scored convergently, with the next entry's table rows prefetched.
 template <bool BOX>
-__global__ void __launch_bounds__(256, SAD_PROP_MINB) k_prop8_queue(const uint32_t* __restrict__ prev, uint32_t* __restrict__ next,
+__global__ void __launch_bounds__(32 * SAD_QUEUE_BY, SAD_PROP_MINB * 8 / SAD_QUEUE_BY) k_prop8_queue(const uint32_t* __restrict__ prev, uint32_t* __restrict__ next,
                                                      const Q4<float>* __restrict__ pack,
                                                      const uint32_t* __restrict__ act, const DevState* __restrict__ st,
                                                      FieldDims f, int step, int inject, uint64_t seed,
                                                      uint32_t pass_offset, float s) {
-    __shared__ uint32_t q[kAxQ * 256];
+    constexpr int QB = 32 * SAD_QUEUE_BY;  // threads per block = per-thread queue stride
+    __shared__ uint32_t q[kAxQ * QB];
     const int tid = threadIdx.y * blockDim.x + threadIdx.x;
     const int gx = blockIdx.x * blockDim.x + threadIdx.x;
     const int gy = blockIdx.y * blockDim.y + threadIdx.y + f.row0;
@@ -717,7 +721,7 @@ __global__ void __launch_bounds__(256, SAD_PROP_MINB) k_prop8_queue(const uint32
 #pragma unroll
                 for (int i = 0; i < 8; i++) {
                     end = end || v[i] == kEmpty;
-                    if (!end && !L.contains(v[i])) q[nq++ * 256 + tid] = v[i];
+                    if (!end && !L.contains(v[i])) q[nq++ * QB + tid] = v[i];
                 }
             }
         }
@@ -725,14 +729,14 @@ __global__ void __launch_bounds__(256, SAD_PROP_MINB) k_prop8_queue(const uint32
             uint32_t rs = seeded_state(seed, st->pass_index + pass_offset,
                                        static_cast<uint32_t>(gy) * static_cast<uint32_t>(f.gw) + static_cast<uint32_t>(gx));
             for (int j = 0; j < inject; j++)
-                q[nq++ * 256 + tid] = __ldg(act + xs_next(rs) % static_cast<uint32_t>(n_act));
+                q[nq++ * QB + tid] = __ldg(act + xs_next(rs) % static_cast<uint32_t>(n_act));
         }
         if (nq > 0) {
             uint32_t c = q[tid];
             Q4<float> b = pack[2 * c + 1], a = pack[2 * c];
 #pragma unroll 1
             for (int j = 0; j < nq; j++) {
-                const uint32_t cn = j + 1 < nq ? q[(j + 1) * 256 + tid] : c;
+                const uint32_t cn = j + 1 < nq ? q[(j + 1) * QB + tid] : c;
                 const Q4<float> bn = pack[2 * cn + 1], an = pack[2 * cn];
                 if (b.w != 0.0f) {
                     const float l = score_logit(a, b, cx, cy, s);
@@ -768,6 +772,9 @@ static void propagate_t(const uint32_t* prev, uint32_t* next, const void* pack, 
     SAD_LAUNCHED();
 }
 
+#ifndef SAD_STREAM_BY
+#define SAD_STREAM_BY 4  // block height of the streaming Box3 kernel (32 x BY threads)
+#endif
 // largest Box3 step that uses the dedup-first queue kernel (SAD_BOX_QUEUE_STEP overrides, for A/B)
 static const int g_box_queue_max_step = getenv("SAD_BOX_QUEUE_STEP") ? atoi(getenv("SAD_BOX_QUEUE_STEP")) : 4;
 
@@ -781,14 +788,17 @@ void launch_propagate(bool fp64, const uint32_t* prev, uint32_t* next, const voi
         // Box3 floods at small steps see mostly ids already in the cell's list: dedup first (queue);
         // at larger steps most entries are new sites: score first (stream)
         if (box && (inject > 4 || step > g_box_queue_max_step))
-            k_prop8_stream<true><<<grid, block, 0, stream>>>(prev, next, (const Q4<float>*)pack, act, st, f, (int)step,
+            k_prop8_stream<true><<<dim3(grid.x, (rows_of(f, f.gh) + SAD_STREAM_BY - 1) / SAD_STREAM_BY),
+                                   dim3(32, SAD_STREAM_BY), 0, stream>>>(prev, next, (const Q4<float>*)pack, act, st, f, (int)step,
                                                              inject, seed, pass_offset, sf);
         else if (box)
-            k_prop8_queue<true><<<grid, block, 0, stream>>>(prev, next, (const Q4<float>*)pack, act, st, f, (int)step,
-                                                            inject, seed, pass_offset, sf);
+            k_prop8_queue<true><<<dim3(grid.x, (rows_of(f, f.gh) + SAD_QUEUE_BY - 1) / SAD_QUEUE_BY),
+                                  dim3(32, SAD_QUEUE_BY), 0, stream>>>(prev, next, (const Q4<float>*)pack, act, st, f,
+                                                                       (int)step, inject, seed, pass_offset, sf);
         else if (inject <= 4)
-            k_prop8_queue<false><<<grid, block, 0, stream>>>(prev, next, (const Q4<float>*)pack, act, st, f, (int)step,
-                                                             inject, seed, pass_offset, sf);
+            k_prop8_queue<false><<<dim3(grid.x, (rows_of(f, f.gh) + SAD_QUEUE_BY - 1) / SAD_QUEUE_BY),
+                                   dim3(32, SAD_QUEUE_BY), 0, stream>>>(prev, next, (const Q4<float>*)pack, act, st, f,
+                                                                        (int)step, inject, seed, pass_offset, sf);
         else
             k_prop8_stream<false><<<grid, block, 0, stream>>>(prev, next, (const Q4<float>*)pack, act, st, f,
                                                               (int)step, inject, seed, pass_offset, sf);
