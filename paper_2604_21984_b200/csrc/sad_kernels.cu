@@ -538,7 +538,10 @@ __device__ __forceinline__ uint64_t list_key(float l, uint32_t c) {
 struct KeyList8 {
     uint64_t k[8];
     __device__ __forceinline__ bool contains(uint32_t c) const {
-        const uint32_t nc = ~c;
+        // ~c through an opaque `not`: otherwise the compiler folds every compare into (k ^ c) == -1,
+        // two instructions each instead of one ISETP
+        uint32_t nc;
+        asm("not.b32 %0, %1;" : "=r"(nc) : "r"(c));
         bool d = false;
 #pragma unroll
         for (int i = 0; i < 8; i++) d |= (static_cast<uint32_t>(k[i]) == nc);
@@ -684,6 +687,8 @@ __global__ void __launch_bounds__(32 * SAD_QUEUE_BY, SAD_PROP_MINB * 8 / SAD_QUE
                                                      uint32_t pass_offset, float s) {
     constexpr int QB = 32 * SAD_QUEUE_BY;  // threads per block = per-thread queue stride
     __shared__ uint32_t q[kAxQ * QB];
+    // this thread's queue column as a shared-window address
+    const uint32_t qa = static_cast<uint32_t>(__cvta_generic_to_shared(q + (threadIdx.y * blockDim.x + threadIdx.x)));
     const int tid = threadIdx.y * blockDim.x + threadIdx.x;
     const int gx = blockIdx.x * blockDim.x + threadIdx.x;
     const int gy = blockIdx.y * blockDim.y + threadIdx.y + f.row0;
@@ -721,7 +726,13 @@ __global__ void __launch_bounds__(32 * SAD_QUEUE_BY, SAD_PROP_MINB * 8 / SAD_QUE
 #pragma unroll
                 for (int i = 0; i < 8; i++) {
                     end = end || v[i] == kEmpty;
-                    if (!end && !L.contains(v[i])) q[nq++ * QB + tid] = v[i];
+                    const bool push = !end && !L.contains(v[i]);
+                    // predicated st.shared at the precomputed queue address: no branch, no re-derivation
+                    // of the shared window per entry
+                    asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p st.shared.u32 [%0], %1; }"
+                                 :: "r"(qa + 4u * QB * static_cast<uint32_t>(nq)), "r"(v[i]), "r"(static_cast<uint32_t>(push))
+                                 : "memory");
+                    nq += push;
                 }
             }
         }
