@@ -1297,14 +1297,15 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM, NT>& sm, c
         const int off = (c - chunk_base[u]) * R::PT;
         const int n = static_cast<int>(sm.cnt[u]) - off;
         const int b = static_cast<int>(sm.start[u]) + off;
+        // branch-free: steps past the chunk end read the padding column E, which holds +0.0 in every
+        // channel; adding +0.0 to these accumulators is an exact no-op (a running double-double sum
+        // that starts at +0 is never -0)
 #pragma unroll
         for (int j = 0; j < R::PT; j++) {
-            if (j < n) {
-                const int e = sm.srt.order[b + j];
+            const int e = j < n ? static_cast<int>(sm.srt.order[b + j]) : R::E;
 #pragma unroll
-                for (int ch = 0; ch < R::CB; ch++)
-                    if (ch < nch) dd_add(acc[ch], static_cast<double>(sm.c[(ch0 + ch) * R::ES + e]));
-            }
+            for (int ch = 0; ch < R::CB; ch++)
+                if (ch < nch) dd_add(acc[ch], static_cast<double>(sm.c[(ch0 + ch) * R::ES + e]));
         }
     };
     DD* const carry_a = reinterpret_cast<DD*>(sm.c);
@@ -1390,6 +1391,7 @@ template <typename CT, int NCH, int TPX, int KM, int NT>
 __device__ __forceinline__ void tile_init(TileRed<CT, NCH, TPX, KM, NT>& sm) {
     using R = TileRed<CT, NCH, TPX, KM, NT>;
     for (int h = threadIdx.x; h < R::HT; h += NT) sm.hkey[h] = kEmpty;
+    if (threadIdx.x < NCH) sm.c[threadIdx.x * R::ES + R::E] = CT(0);  // padding column (step 4)
     if (threadIdx.x == 0) sm.n_local = 0;
 }
 
