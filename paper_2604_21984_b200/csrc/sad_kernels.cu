@@ -695,13 +695,32 @@ __global__ void __launch_bounds__(32 * SAD_QUEUE_BY, SAD_PROP_MINB * 8 / SAD_QUE
     if (gx >= f.gw || gy >= f.gh || gy >= f.row1) return;
     const float cx = static_cast<float>(gx * static_cast<double>(f.cell) + (f.cell - 1) * 0.5);
     const float cy = static_cast<float>(gy * static_cast<double>(f.cell) + (f.cell - 1) * 0.5);
+    // injected ids first: their act[] loads overlap the own-list scoring, they take queue slots
+    // [0, ni) (drained with the last group) and their table rows are prefetched into L1 long before
+    // the drain reaches them (random ids: the rows are rarely L1-resident otherwise)
+    const int n_act = st->n_active;
+    const int ni = (inject > 0 && n_act > 0) ? inject : 0;
+    uint32_t inj[4];
+    if (ni > 0) {
+        uint32_t rs = seeded_state(seed, st->pass_index + pass_offset,
+                                   static_cast<uint32_t>(gy) * static_cast<uint32_t>(f.gw) + static_cast<uint32_t>(gx));
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+            if (j < ni) inj[j] = __ldg(act + xs_next(rs) % static_cast<uint32_t>(n_act));
+    }
     KeyList8 L;
     bool ok = own_keys(prev, pack, f, gx, gy, cx, cy, s, L);
-    const int n_act = st->n_active;
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+        if (j < ni) {
+            q[j * QB + tid] = inj[j];
+            asm volatile("prefetch.global.L1 [%0];" :: "l"(pack + 2 * inj[j]));
+        }
     constexpr int NG = BOX ? 2 : 1;  // groups of four neighbour lists (Box3: axial, then diagonal)
 #pragma unroll 1
     for (int g = 0; g < NG; g++) {
-        int nq = 0;
+        int nq = ni;
+        const int j0 = g == NG - 1 ? 0 : ni;  // the injected slots are drained once, with the last group
 #pragma unroll 1
         for (int pr = 0; pr < 2; pr++) {
             uint4 u[4];
@@ -736,17 +755,11 @@ __global__ void __launch_bounds__(32 * SAD_QUEUE_BY, SAD_PROP_MINB * 8 / SAD_QUE
                 }
             }
         }
-        if (g == NG - 1 && inject > 0 && n_act > 0) {
-            uint32_t rs = seeded_state(seed, st->pass_index + pass_offset,
-                                       static_cast<uint32_t>(gy) * static_cast<uint32_t>(f.gw) + static_cast<uint32_t>(gx));
-            for (int j = 0; j < inject; j++)
-                q[nq++ * QB + tid] = __ldg(act + xs_next(rs) % static_cast<uint32_t>(n_act));
-        }
-        if (nq > 0) {
-            uint32_t c = q[tid];
+        if (nq > j0) {
+            uint32_t c = q[j0 * QB + tid];
             Q4<float> b = pack[2 * c + 1], a = pack[2 * c];
 #pragma unroll 1
-            for (int j = 0; j < nq; j++) {
+            for (int j = j0; j < nq; j++) {
                 const uint32_t cn = j + 1 < nq ? q[(j + 1) * QB + tid] : c;
                 const Q4<float> bn = pack[2 * cn + 1], an = pack[2 * cn];
                 if (b.w != 0.0f) {
