@@ -32,6 +32,43 @@ uint64_t launch_counter() { return g_launches.load(); }
 void add_launches(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 #define SAD_LAUNCHED() g_launches.fetch_add(1, std::memory_order_relaxed)
 
+// ---------------------------------------------------------------------- programmatic dependent launch
+// The per-iteration kernels (warm pass, fwd+bwd, Adam, bookkeeping) are launched with programmatic
+// stream serialisation, so the launch of each is prepared while its predecessor runs; every one waits
+// in griddepcontrol.wait before ANY global access (every RAW and WAR dependency on the predecessor is
+// respected).  Early triggers (launch_dependents at block start) let dependents occupy SMs during the
+// predecessor's last wave; measured on the config-2 fit that is neutral to +9 ms (the fwd+bwd -> Adam
+// edge), so by default no kernel triggers early and the gain is the launch latency (about 3 ms per
+// fit).  Without the attribute (or a programmatic predecessor) both instructions are no-ops.
+// SAD_NO_PDL=1 turns the attribute off (A/B).
+#ifndef SAD_PDL_TRIGGER
+#define SAD_PDL_TRIGGER 0  // bitmask of kernels that trigger early (1 prop, 2 bwd, 4 adam, 8 advance): measured no gain
+#endif
+template <int BIT>
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (SAD_PDL_TRIGGER & BIT) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+static const bool g_pdl = getenv("SAD_NO_PDL") == nullptr;
+template <typename... KP, typename... A>
+static void launch_pdl(void (*kern)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, A... args) {
+    if (!g_pdl) {
+        kern<<<grid, block, smem, stream>>>(args...);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KP>(args)...);
+}
+
 // ====================================================================== per-site tables
 // ScoreTable<T>::build (score_table.hpp:20-46), packed and unpacked, and GradTable<T>::build
 // (grad.cpp:79-111).  Coefficients are derived in double and rounded to T exactly as the reference.
@@ -685,6 +722,7 @@ __global__ void __launch_bounds__(32 * SAD_QUEUE_BY, SAD_PROP_MINB * 8 / SAD_QUE
                                                      const uint32_t* __restrict__ act, const DevState* __restrict__ st,
                                                      FieldDims f, int step, int inject, uint64_t seed,
                                                      uint32_t pass_offset, float s) {
+    pdl_enter<1>();
     constexpr int QB = 32 * SAD_QUEUE_BY;  // threads per block = per-thread queue stride
     __shared__ uint32_t q[kAxQ * QB];
     // this thread's queue column as a shared-window address
@@ -816,13 +854,13 @@ void launch_propagate(bool fp64, const uint32_t* prev, uint32_t* next, const voi
                                    dim3(32, SAD_STREAM_BY), 0, stream>>>(prev, next, (const Q4<float>*)pack, act, st, f, (int)step,
                                                              inject, seed, pass_offset, sf);
         else if (box)
-            k_prop8_queue<true><<<dim3(grid.x, (rows_of(f, f.gh) + SAD_QUEUE_BY - 1) / SAD_QUEUE_BY),
-                                  dim3(32, SAD_QUEUE_BY), 0, stream>>>(prev, next, (const Q4<float>*)pack, act, st, f,
-                                                                       (int)step, inject, seed, pass_offset, sf);
+            launch_pdl(k_prop8_queue<true>, dim3(grid.x, (rows_of(f, f.gh) + SAD_QUEUE_BY - 1) / SAD_QUEUE_BY),
+                       dim3(32, SAD_QUEUE_BY), 0, stream, prev, next, (const Q4<float>*)pack, act, st, f, (int)step,
+                       inject, seed, pass_offset, sf);
         else if (inject <= 4)
-            k_prop8_queue<false><<<dim3(grid.x, (rows_of(f, f.gh) + SAD_QUEUE_BY - 1) / SAD_QUEUE_BY),
-                                   dim3(32, SAD_QUEUE_BY), 0, stream>>>(prev, next, (const Q4<float>*)pack, act, st, f,
-                                                                        (int)step, inject, seed, pass_offset, sf);
+            launch_pdl(k_prop8_queue<false>, dim3(grid.x, (rows_of(f, f.gh) + SAD_QUEUE_BY - 1) / SAD_QUEUE_BY),
+                       dim3(32, SAD_QUEUE_BY), 0, stream, prev, next, (const Q4<float>*)pack, act, st, f, (int)step,
+                       inject, seed, pass_offset, sf);
         else
             k_prop8_stream<false><<<grid, block, 0, stream>>>(prev, next, (const Q4<float>*)pack, act, st, f,
                                                               (int)step, inject, seed, pass_offset, sf);
@@ -1664,6 +1702,7 @@ template <int KM, int MODE>
 __global__ void __launch_bounds__(256, SAD_BWD2_MINB) k_backward2(const uint32_t* __restrict__ ids, const Q4<float>* __restrict__ gtab,
                                                    const float* __restrict__ tgt, FieldDims f, float s, float inv_hw2,
                                                    RedTarget red, double2* __restrict__ loss_part, DevState* st) {
+    pdl_enter<2>();
     using T = float;
     constexpr int TW = 16, TH = 8, TPX = TW * TH, NT = 2 * TPX, H = KM / 2;
     constexpr int NCH = MODE == 1 ? 11 : 10;
@@ -1932,9 +1971,8 @@ static void backward_t(const uint32_t* ids, const void* gtab, const void* tgt, c
     if (sizeof(T) == 4 && !g_bwd1) {
         static_assert(BwdTile<float>::TW == 16 && BwdTile<float>::TH == 8, "k_backward2 tile");
         size_t smem = sizeof(TileRed<float, NCH, 128, KM, 256>);
-        k_backward2<KM, MODE><<<grid, 256, smem, stream>>>(ids, (const Q4<float>*)gtab, (const float*)tgt, f,
-                                                           static_cast<float>(scale), static_cast<float>(inv_hw2), red,
-                                                           loss_part, st);
+        launch_pdl(k_backward2<KM, MODE>, grid, dim3(256), smem, stream, ids, (const Q4<float>*)gtab,
+                   (const float*)tgt, f, static_cast<float>(scale), static_cast<float>(inv_hw2), red, loss_part, st);
     } else {
         size_t smem = sizeof(TileRed<T, NCH, TW * TH, KM>);
         auto kern = k_backward<T, KM, MODE>;
@@ -2668,6 +2706,7 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
                                               double scale, Q4<T>* pack, Q4<T>* gtab, int32_t* rcap_next,
                                               const double* __restrict__ totals, int32_t* roff_next,
                                               int32_t* pool_top, const uint32_t* __restrict__ act) {
+    pdl_enter<4>();
     __shared__ int32_t s_want[8], s_base;
     const int lane16 = threadIdx.x & 15;
     const int grp = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
@@ -2809,13 +2848,13 @@ void launch_adam(bool fp64, const SitesDev& s, DevState* st, const RedTarget& gr
     int grid = (s.cap + 7) / 8;  // 8 sites (16 lanes each) per 128-thread block
     if (grid < 1) grid = 1;
     if (fp64)
-        k_adam<double><<<grid, 128, 0, stream>>>(s, st, grads, m, v, hp, bc_table, bc_now, zero_grads ? 1 : 0, scale,
-                                                 (Q4<double>*)pack, (Q4<double>*)gtab, rcap_next, totals, roff_next,
-                                                 pool_top, act);
+        launch_pdl(k_adam<double>, dim3(grid), dim3(128), 0, stream, s, st, grads, m, v, hp, bc_table, bc_now,
+                   zero_grads ? 1 : 0, scale, (Q4<double>*)pack, (Q4<double>*)gtab, rcap_next, totals, roff_next, pool_top,
+                   act);
     else
-        k_adam<float><<<grid, 128, 0, stream>>>(s, st, grads, m, v, hp, bc_table, bc_now, zero_grads ? 1 : 0, scale,
-                                                (Q4<float>*)pack, (Q4<float>*)gtab, rcap_next, totals, roff_next,
-                                                pool_top, act);
+        launch_pdl(k_adam<float>, dim3(grid), dim3(128), 0, stream, s, st, grads, m, v, hp, bc_table, bc_now,
+                   zero_grads ? 1 : 0, scale, (Q4<float>*)pack, (Q4<float>*)gtab, rcap_next, totals, roff_next, pool_top,
+                   act);
     SAD_LAUNCHED();
 }
 
@@ -3147,6 +3186,7 @@ void launch_flag_active(const SitesDev& s, const DevState* st, uint8_t* flags, c
 __global__ void __launch_bounds__(1024) k_advance(DevState* st, int passes, int adam_steps, double2* loss_hist,
                                                   int32_t* active_hist, const double2* __restrict__ loss_part,
                                                   int n_part, int32_t* otop) {
+    pdl_enter<8>();
     if (otop && threadIdx.x == 0) {
         otop[0] = 0;  // gradient overflow pool
         otop[2] = 0;  // gradient record pool (claimed by the next k_adam)
@@ -3181,7 +3221,8 @@ __global__ void __launch_bounds__(1024) k_advance(DevState* st, int passes, int 
 
 void launch_advance(DevState* st, int passes, int adam_steps, double2* loss_hist, int32_t* active_hist,
                     const double2* loss_part, int n_part, int32_t* otop, cudaStream_t stream) {
-    k_advance<<<1, 1024, 0, stream>>>(st, passes, adam_steps, loss_hist, active_hist, loss_part, n_part, otop);
+    launch_pdl(k_advance, dim3(1), dim3(1024), 0, stream, st, passes, adam_steps, loss_hist, active_hist, loss_part,
+               n_part, otop);
     SAD_LAUNCHED();
 }
 
