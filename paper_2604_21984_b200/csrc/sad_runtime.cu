@@ -11,9 +11,11 @@
 #include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -64,6 +66,10 @@ sad_status guard(F&& f) {
 }
 
 // ------------------------------------------------------------------ device buffers
+// Bumped by every device allocation: cached CUDA graphs hold raw buffer addresses and are dropped
+// when it moves (sad_fit_run::plain).
+static std::atomic<uint64_t> g_alloc_epoch{0};
+
 template <typename T>
 struct DBuf {
     T* p = nullptr;
@@ -81,6 +87,7 @@ struct DBuf {
         n = 0;
         if (m == 0) m = 1;
         ck(cudaMalloc(&p, m * sizeof(T)), "cudaMalloc");
+        g_alloc_epoch.fetch_add(1, std::memory_order_relaxed);
         n = m;
     }
 };
@@ -910,11 +917,18 @@ struct sad_fit_run {
     bool bc_ready = false;
     int planned_n0 = -1;  // plan_schedule is a pure function of (n0, target, cfg): cached
     double planned_scale = 0;
-    // CUDA graphs of the plain iteration, per (field buffer parity, warm refresh this iteration)
-    cudaGraphExec_t plain[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    // CUDA graphs of runs of n plain iterations, keyed by (field buffer parity, warm refresh flag, n);
+    // value: the executable graph and the kernel launches it holds
+    std::map<int, std::pair<cudaGraphExec_t, uint64_t>> plain;
+    uint64_t graph_epoch = ~0ull;  // g_alloc_epoch when the cached graphs were captured
+    sad_train_config graph_cfg{};  // and the config whose scalars they hold
+    void drop_graphs() {
+        for (auto& g : plain)
+            if (g.second.first) cudaGraphExecDestroy(g.second.first);
+        plain.clear();
+    }
     bool profile = false;  // per-phase CUDA-event timing (disables graphs)
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
-    uint64_t plain_launches[2][2] = {{0, 0}, {0, 0}};
     // row-strip multi-GPU fit (config 5): this run's rank, the world size, every rank's first row
     // (world + 1 bounds), and the buffers of the exact cross-rank merges
     int rank = 0, world = 1;
@@ -923,11 +937,12 @@ struct sad_fit_run {
     DBuf<double> tot;
     DBuf<unsigned long long> valid_all;
     ~sad_fit_run() {
-        for (auto& a : plain)
-            for (auto& g : a)
-                if (g) cudaGraphExecDestroy(g);
+        drop_graphs();
     }
 };
+
+// plain iterations per graph launch (SAD_GRAPH_ITERS overrides; 1 = one graph per iteration)
+static const int g_graph_iters = getenv("SAD_GRAPH_ITERS") ? std::max(1, atoi(getenv("SAD_GRAPH_ITERS"))) : 8;
 
 extern "C" {
 
@@ -1816,30 +1831,46 @@ static void fit_loop(sad_fit_run* r) {
     };
     // SAD_STOP_AT=t (divergence hunting): stop after iteration t without the final refresh
     const int stop_at = getenv("SAD_STOP_AT") ? atoi(getenv("SAD_STOP_AT")) : 0;
+    auto refresh_at = [&](int t) { return (t - 1) % c.refresh_every == 0; };
+    auto event_d = [&](int t) { return budget && t >= c.densify_start && t <= c.densify_end && t % c.densify_every == 0; };
+    auto event_p = [&](int t) {
+        bool e = budget && t >= c.prune_start && t <= c.prune_end && t % c.prune_every == 0;
+        return e && !(!c.prune_during_densify && t <= c.densify_end);
+    };
     for (int t = 1; t <= c.iters; t++) {
         if (stop_at && t > stop_at) break;
-        const bool rf = (t - 1) % c.refresh_every == 0;
-        bool ev_d = budget && t >= c.densify_start && t <= c.densify_end && t % c.densify_every == 0;
-        bool ev_p = budget && t >= c.prune_start && t <= c.prune_end && t % c.prune_every == 0;
-        if (ev_p && !c.prune_during_densify && t <= c.densify_end) ev_p = false;
+        const bool rf = refresh_at(t);
+        bool ev_d = event_d(t);
+        bool ev_p = event_p(t);
         bool ev = ev_d || ev_p;
         if (!ev && use_graphs) {
+            // a run of n plain iterations with the same refresh flag, replayed as one graph
+            int n = 1;
+            const int last = stop_at ? std::min(stop_at, c.iters) : c.iters;
+            while (n < g_graph_iters && t + n <= last && refresh_at(t + n) == rf && !event_d(t + n) && !event_p(t + n)) n++;
+            if (r->graph_epoch != g_alloc_epoch.load() || std::memcmp(&r->graph_cfg, &c, sizeof c) != 0) {
+                r->drop_graphs();
+                r->graph_epoch = g_alloc_epoch.load();
+                r->graph_cfg = c;
+            }
             const int c0 = ws.cur;
-            cudaGraphExec_t& gx = r->plain[c0][rf ? 1 : 0];
-            if (!gx) {
+            const int key = c0 | (rf ? 2 : 0) | (n << 2);
+            auto& gx = r->plain[key];
+            if (!gx.first) {
                 cudaGraph_t g = nullptr;
                 uint64_t l0 = sadk::launch_counter();
                 ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
-                plain_iteration(rf);
+                for (int i = 0; i < n; i++) plain_iteration(rf);
                 ck(cudaStreamEndCapture(s, &g), "end capture");
-                ck(cudaGraphInstantiate(&gx, g, 0), "graph instantiate");
+                ck(cudaGraphInstantiate(&gx.first, g, 0), "graph instantiate");
                 cudaGraphDestroy(g);
-                r->plain_launches[c0][rf ? 1 : 0] = sadk::launch_counter() - l0;
+                gx.second = sadk::launch_counter() - l0;
                 ws.cur = c0;
             }
-            ck(cudaGraphLaunch(gx, s), "graph launch");
-            sadk::add_launches(r->plain_launches[c0][rf ? 1 : 0]);
-            if (rf && (warm.size() & 1)) ws.cur = 1 - c0;
+            ck(cudaGraphLaunch(gx.first, s), "graph launch");
+            sadk::add_launches(gx.second);
+            if (rf && (warm.size() & 1) && (n & 1)) ws.cur = 1 - c0;
+            t += n - 1;
             continue;
         }
         if (!ev) {
