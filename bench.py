@@ -542,6 +542,12 @@ def run_b200(a):
                 "traffic_source": traffic_src, "kernel": dom, "algorithmic_bytes_per_launch": bytes_per[dom],
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6650 GB/s",
                 "note": "768x512 working set is L2-resident; HBM fraction is judged at 2048^2 (see DESIGN.md)"}
+    if dom == "fwd_bwd" and os.path.exists(tf):
+        # what does bound it: SM issue / pipe utilisation from the same committed ncu capture
+        tj = json.load(open(tf))
+        if "issue_active_pct_of_peak" in tj:
+            roofline["compute"] = {k: tj[k] for k in ("sm_throughput_pct_of_peak", "issue_active_pct_of_peak",
+                                                      "fp64_pipe_active_pct_of_peak", "fma_pipe_active_pct_of_peak")}
 
     # end to end through the public API with host buffers
     tgt_host = sad.ImageBuffer(W, H, imgs[0])
