@@ -2721,24 +2721,35 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
     const int id = act ? (live ? static_cast<int>(act[grp]) : cap) : grp;
     const int k = lane16;
     unsigned long long skipped = 0;
+    const int kc = lane_channel(lane16);  // the parameter this lane updates (-1: none)
+    // the site's parameter, moments and flags do not depend on the gradient: their loads are issued
+    // before the record merge so their latency overlaps it
+    bool upd = false;
+    double p = 0.0, m0 = 0.0, v0 = 0.0;
+    double2 bc = bc_now;
+    if (live) {
+        upd = s.active[id] && !s.frozen[id];
+        if (kc >= 0) {
+            const size_t mi = static_cast<size_t>(kc) * cap + id;
+            p = s.p[mi];
+            m0 = m[mi];
+            v0 = v[mi];
+        }
+        if (bc_table) bc = bc_table[st->t + 1];
+    }
     // ---- gradient totals (all lanes of the group take part in the shuffles)
     DD g;
     const int claimed = merge_site(grads, id, live && !totals, lane16, gmask, cap, g);
-    const int kc = lane_channel(lane16);  // the parameter this lane updates (-1: none)
     if (live) {
-        const bool upd = s.active[id] && !s.frozen[id];
-        double p = 0.0;
-        if (kc >= 0) p = s.p[static_cast<size_t>(kc) * cap + id];
         if (upd && kc >= 0) {
             const int k = kc;
-            const double2 bc = bc_table ? bc_table[st->t + 1] : bc_now;
             double gv = totals ? totals[static_cast<size_t>(k) * cap + id] : g.hi + g.lo;
             if (!isfinite(gv)) {
                 skipped++;
             } else {
                 const size_t mi = static_cast<size_t>(k) * cap + id;
-                double mm = hp.beta1 * m[mi] + (1.0 - hp.beta1) * gv;
-                double vv = hp.beta2 * v[mi] + (1.0 - hp.beta2) * gv * gv;
+                double mm = hp.beta1 * m0 + (1.0 - hp.beta1) * gv;
+                double vv = hp.beta2 * v0 + (1.0 - hp.beta2) * gv * gv;
                 m[mi] = mm;
                 v[mi] = vv;
                 p -= hp.lr[k] * (mm / bc.x) / (__dsqrt_rn(vv / bc.y) + hp.eps);
