@@ -2724,11 +2724,12 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
     const int kc = lane_channel(lane16);  // the parameter this lane updates (-1: none)
     // the site's parameter, moments and flags do not depend on the gradient: their loads are issued
     // before the record merge so their latency overlaps it
-    bool upd = false;
+    bool upd = false, is_active = false;
     double p = 0.0, m0 = 0.0, v0 = 0.0;
     double2 bc = bc_now;
     if (live) {
-        upd = s.active[id] && !s.frozen[id];
+        is_active = s.active[id] != 0;
+        upd = is_active && !s.frozen[id];
         if (kc >= 0) {
             const size_t mi = static_cast<size_t>(kc) * cap + id;
             p = s.p[mi];
@@ -2785,7 +2786,7 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
         if (rcap_next && k == 0) {
             // next pass's record capacity: last count plus headroom (active sites only)
             const int cl = totals ? grads.cnt[id] : claimed;
-            int want = s.active[id] ? cl + (cl >> 2) + 2 : 0;
+            int want = is_active ? cl + (cl >> 2) + 2 : 0;
             want = want < 4096 ? want : 4096;
             rcap_next[id] = want;
             if (roff_next) s_want[threadIdx.x >> 4] = want;
@@ -2813,13 +2814,15 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
         if (k == 0 && id < cap) roff_next[id] = s_base + s_want[threadIdx.x >> 4];
     }
     if (skipped) atomicAdd(reinterpret_cast<unsigned long long*>(&st->skipped), skipped);
-    __syncwarp();
+    // the site's final parameters (each lane kc holds channel kc, updated or as loaded) to the table lanes
+    double q[10];
+#pragma unroll
+    for (int c = 0; c < 10; c++) q[c] = __shfl_sync(gmask, p, (threadIdx.x & 16) + channel_lane(c));
     if (live && lane16 < 5 && (pack || gtab)) {
         // same derivations as k_tables (score_table.hpp:20-46, grad.cpp:84-110), one output quad per lane
-        const double* pp = s.p;
-        const bool act = s.active[id] != 0;
-        const double x = pp[0 * cap + id], y = pp[1 * cap + id], lt = pp[2 * cap + id], r = pp[3 * cap + id];
-        const double ux = pp[7 * cap + id], uy = pp[8 * cap + id], an = pp[9 * cap + id];
+        const bool act = is_active;
+        const double x = q[0], y = q[1], lt = q[2], r = q[3];
+        const double ux = q[7], uy = q[8], an = q[9];
         if (lane16 == 0 && pack) {
             Q4<T> a{T(0), T(0), T(0), T(0)};
             if (act) a = {static_cast<T>(half_rt(x)), static_cast<T>(half_rt(y)), static_cast<T>(sad_dexp(half_rt(lt))),
@@ -2845,8 +2848,7 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
             gtab[3 * id + 1] = b;
         } else if (lane16 == 4 && gtab) {
             Q4<T> c{T(0), T(0), T(0), T(0)};
-            if (act) c = {static_cast<T>(pp[4 * cap + id]), static_cast<T>(pp[5 * cap + id]),
-                          static_cast<T>(pp[6 * cap + id]), T(1)};
+            if (act) c = {static_cast<T>(q[4]), static_cast<T>(q[5]), static_cast<T>(q[6]), T(1)};
             gtab[3 * id + 2] = c;
         }
     }
