@@ -121,3 +121,24 @@ def test_oneshot_fit_and_fit_store():
     with pytest.raises(sad.api.CapacityError):
         G._call("fit", tgt.data.ctypes.data_as(C.POINTER(C.c_double)), C.c_int(40), C.c_int(32), C.byref(cc),
                 C.byref(sv), None, None, None)
+
+
+def test_cached_run_graphs_follow_buffer_reallocation():
+    """A cached fit run replays CUDA graphs of plain iterations that hold raw buffer addresses: growing
+    the run's capacity (a larger initial store) must drop them, and fits before and after the growth
+    equal fresh one-shot fits."""
+    from tests.fixtures import synth_target
+    G = sad.gpu_backend(0)
+    tgt = synth_target(48, 40, 7)
+    cfg = sad.TrainConfig(iters=40, n_sites=60, fp64=False, seed=3)  # budget off: all iterations graph-replayed
+    a = G.fit(tgt, cfg)
+    big = G.fit(tgt, sad.TrainConfig(iters=5, n_sites=300, fp64=False, seed=4)).sites
+    c = G.fit_store(big, tgt, cfg)  # same cached run, capacity 60 -> 300
+    d = G.fit_oneshot(tgt, cfg, init=big)
+    assert [sad.history_line(r) for r in c.history] == [sad.history_line(r) for r in d.history]
+    for p in ("x", "y", "log_tau", "radius", "active"):
+        assert np.array_equal(getattr(c.sites, p), getattr(d.sites, p)), p
+    assert np.array_equal(c.field.ids, d.field.ids)
+    e = G.fit(tgt, cfg)  # the grown run again from init_sites
+    assert [sad.history_line(r) for r in e.history] == [sad.history_line(r) for r in a.history]
+    assert np.array_equal(e.field.ids, a.field.ids)
