@@ -19,7 +19,7 @@ KERNELS = {"propagate_warm": 0, "fwd_bwd": 1, "render": 2, "propagate_flood": 3,
            "adam_active": 9, "advance": 10}
 
 p = argparse.ArgumentParser()
-p.add_argument("--kernel", default="fwd_bwd", choices=list(KERNELS))
+p.add_argument("--kernel", default="fwd_bwd", help="one of %s, or a comma-separated list (one fit, several kernels)" % list(KERNELS))
 p.add_argument("--reps", type=int, default=20)
 p.add_argument("--width", type=int, default=768)
 p.add_argument("--height", type=int, default=512)
@@ -40,6 +40,7 @@ img = synthetic_image(a.width, a.height, 1)
 G._call("fit_set_target", run, img.ctypes.data_as(C.POINTER(C.c_double)))
 G._call("fit_run_init", run)
 out = C.c_double()
-G._call("fit_bench", run, C.c_int(KERNELS[a.kernel]), C.c_int(a.reps), C.byref(out))
-print(f"{a.kernel}: {out.value * 1e3:.2f} us/launch ({a.width}x{a.height})")
+for kn in a.kernel.split(","):
+    G._call("fit_bench", run, C.c_int(KERNELS[kn]), C.c_int(a.reps), C.byref(out))
+    print(f"{kn}: {out.value * 1e3:.2f} us/launch ({a.width}x{a.height})")
 G.lib.sad_fit_destroy(run)
