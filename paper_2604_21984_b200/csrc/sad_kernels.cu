@@ -948,23 +948,19 @@ __global__ void __launch_bounds__(256) k_render(const uint32_t* __restrict__ ids
     bool any = false, stop = false;
     T best = T(0);
     const T fx = static_cast<T>(px), fy = static_cast<T>(py);
+    // branch-free: slots past the first sentinel read site 0's rows and are masked out; a masked slot
+    // adds +0.0 to the running sums, an exact no-op (sums that start at +0 are never -0)
 #pragma unroll
     for (int i = 0; i < KM; i++) {
         stop = stop || cid[i] == kEmpty;
-        ok[i] = false;
-        lg[i] = T(0);
-        if (!stop) {
-            const Q4<T> a = rtab[3 * cid[i]], b = rtab[3 * cid[i] + 1];
-            if (b.w != T(0)) {
-                const T l = score_logit(a, b, fx, fy, s);
-                if (tfinite(l)) {
-                    ok[i] = true;
-                    lg[i] = l;
-                    if (!any || l > best) best = l;
-                    any = true;
-                }
-            }
-        }
+        const uint32_t id = stop ? 0u : cid[i];
+        const Q4<T> a = rtab[3 * id], b = rtab[3 * id + 1];
+        const T l = score_logit(a, b, fx, fy, s);
+        ok[i] = !stop && b.w != T(0) && tfinite(l);
+        lg[i] = ok[i] ? l : T(0);
+        best = (ok[i] && (!any || l > best)) ? l : best;
+        any = any || ok[i];
+        cid[i] = id;
     }
     if (!any) {
         atomicOr(&st->err, 1);
@@ -974,23 +970,20 @@ __global__ void __launch_bounds__(256) k_render(const uint32_t* __restrict__ ids
     T sum = T(0);
 #pragma unroll
     for (int i = 0; i < KM; i++) {
-        w[i] = T(0);
-        if (ok[i]) {
-            w[i] = texp(lg[i] - best);
-            sum += w[i];
-        }
+        const T e = texp(lg[i] - best);
+        w[i] = ok[i] ? e : T(0);
+        sum += w[i];
     }
     const T inv = trcp(sum);
     T r = T(0), g = T(0), b = T(0);
 #pragma unroll
-    for (int i = 0; i < KM; i++)
-        if (ok[i]) {
-            const T wi = w[i] * inv;
-            const Q4<T> c = rtab[3 * cid[i] + 2];
-            r += wi * c.x;
-            g += wi * c.y;
-            b += wi * c.z;
-        }
+    for (int i = 0; i < KM; i++) {
+        const T wi = w[i] * inv;
+        const Q4<T> c = rtab[3 * cid[i] + 2];
+        r += ok[i] ? wi * c.x : T(0);
+        g += ok[i] ? wi * c.y : T(0);
+        b += ok[i] ? wi * c.z : T(0);
+    }
     T* o = out + 3 * (static_cast<size_t>(py) * f.width + px);
     o[0] = r;
     o[1] = g;
