@@ -1069,24 +1069,29 @@ __global__ void __launch_bounds__(128) k_pixel_weights(const uint32_t* __restric
         const int px = xy[2 * q], py = xy[2 * q + 1];
         if (px >= 0 && py >= 0 && px < f.width && py < f.height) {
             const uint32_t* lst = ids + static_cast<size_t>(f.k) * cell_index(f, px, py);
+            // the whole list in one or two vector loads (random cells: one HBM round trip, not K), then
+            // a branch-free candidate loop whose table loads do not wait on the previous slot: slots past
+            // the first sentinel read site 0's rows and are masked
+            if (KM == 8 && f.k == 8) {
+                const uint4 u0 = __ldg(reinterpret_cast<const uint4*>(lst)), u1 = __ldg(reinterpret_cast<const uint4*>(lst) + 1);
+                const uint32_t v[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+#pragma unroll
+                for (int i = 0; i < KM; i++) cid[i] = v[i % 8];
+            } else {
+#pragma unroll
+                for (int i = 0; i < KM; i++) cid[i] = i < f.k ? __ldg(lst + i) : kEmpty;
+            }
             bool stop = false;
 #pragma unroll
             for (int i = 0; i < KM; i++) {
-                const uint32_t id = (!stop && i < f.k) ? __ldg(lst + i) : kEmpty;
-                stop = stop || id == kEmpty;
-                cid[i] = id;
-                if (!stop) {
-                    const Q4<double> a = rtab[3 * id], b = rtab[3 * id + 1];
-                    if (b.w != 0.0) {
-                        const double l = score_logit(a, b, static_cast<double>(px), static_cast<double>(py), s);
-                        if (isfinite(l)) {
-                            ok[i] = true;
-                            lg[i] = l;
-                            if (!any || l > best) best = l;
-                            any = true;
-                        }
-                    }
-                }
+                stop = stop || cid[i] == kEmpty;
+                const uint32_t id = stop ? 0u : cid[i];
+                const Q4<double> a = rtab[3 * id], b = rtab[3 * id + 1];
+                const double l = score_logit(a, b, static_cast<double>(px), static_cast<double>(py), s);
+                ok[i] = !stop && b.w != 0.0 && isfinite(l);
+                lg[i] = ok[i] ? l : 0.0;
+                best = (ok[i] && (!any || l > best)) ? l : best;
+                any = any || ok[i];
             }
         }
     }
@@ -1095,10 +1100,8 @@ __global__ void __launch_bounds__(128) k_pixel_weights(const uint32_t* __restric
 #pragma unroll
     for (int i = 0; i < KM; i++) {
         w[i] = 0;
-        if (ok[i]) {
-            w[i] = sad_dexp(lg[i] - best);
-            sum += w[i];
-        }
+        if (ok[i]) w[i] = sad_dexp(lg[i] - best);
+        sum += w[i];  // +0.0 for masked slots: exact
     }
     const double inv = 1.0 / sum;
     uint32_t* my_id = sid + threadIdx.x * RS;
@@ -1126,11 +1129,85 @@ __global__ void __launch_bounds__(128) k_pixel_weights(const uint32_t* __restric
     }
 }
 
+// K = 8 point queries with eight lanes per query (lane = list slot): every slot's table rows are in
+// flight at once instead of one slot after another, and the output rows are written straight from
+// registers, coalesced (four queries = 768 contiguous bytes per warp).  The order-dependent sums stay
+// sequential in slot order: lane 0 of the query adds the eight weights (+0.0 for masked slots, an
+// exact no-op) exactly as the one-thread kernel does; the maximum is order-independent.
+__global__ void __launch_bounds__(128) k_pixel_weights8(const uint32_t* __restrict__ ids,
+                                                        const Q4<double>* __restrict__ rtab, FieldDims f, double s,
+                                                        const int32_t* __restrict__ xy, int n_q,
+                                                        uint32_t* __restrict__ oid, double* __restrict__ ow,
+                                                        int32_t* __restrict__ on) {
+    const int lane = threadIdx.x & 31, slot = lane & 7, qbase = lane & 24;
+    const unsigned qmask = 0xffu << qbase;
+    const int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+    const bool valid_q = q < n_q;
+    int px = -1, py = -1;
+    if (valid_q) {
+        px = xy[2 * q];
+        py = xy[2 * q + 1];
+    }
+    const bool inside = valid_q && px >= 0 && py >= 0 && px < f.width && py < f.height;
+    uint32_t id = kEmpty;
+    if (inside) id = __ldg(ids + 8 * cell_index(f, px, py) + slot);
+    // the list is read up to its first sentinel: a slot is live if no earlier slot is empty
+    const unsigned empt = __ballot_sync(0xffffffffu, id == kEmpty) & qmask;
+    const unsigned before = (1u << lane) - 1u;  // lanes below this one
+    const bool stop = (empt & (before | (1u << lane)) & qmask) != 0u;
+    const uint32_t sid = stop ? 0u : id;
+    const Q4<double> a = rtab[3 * sid], b = rtab[3 * sid + 1];
+    const double l = score_logit(a, b, static_cast<double>(px), static_cast<double>(py), s);
+    const bool ok = inside && !stop && b.w != 0.0 && isfinite(l);
+    // maximum over the query's live slots (a value: independent of order)
+    double best = ok ? l : -INFINITY;
+#pragma unroll
+    for (int d = 4; d >= 1; d >>= 1) {
+        const double o = __shfl_xor_sync(0xffffffffu, best, d, 8);
+        best = o > best ? o : best;
+    }
+    const double w = ok ? sad_dexp(l - best) : 0.0;
+    // softmax denominator in slot order, as the one-thread loop
+    double sum = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) sum += __shfl_sync(0xffffffffu, w, qbase + i);
+    const double inv = 1.0 / sum;
+    const unsigned okm = __ballot_sync(0xffffffffu, ok) & qmask;
+    const int n = __popc(okm);
+    const int pos = __popc(okm & before);  // compacted output position of this slot
+    // rows of 16: live entries in list order at their compacted column, then kEmpty / 0 padding
+    if (valid_q) {
+        uint32_t* rid = oid + static_cast<size_t>(q) * 16;
+        double* rw = ow + static_cast<size_t>(q) * 16;
+        if (slot == 0) on[q] = n;
+        if (ok) {
+            rid[pos] = sid;
+            rw[pos] = w * inv;
+        }
+        // padding: 16 - n columns, two per lane at most (n <= 8 so 8 <= 16 - n <= 16)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int col = n + slot + 8 * h;
+            if (col < 16) {
+                rid[col] = kEmpty;
+                rw[col] = 0.0;
+            }
+        }
+    }
+}
+
+// SAD_PW1=1: one thread per point query (A/B)
+static const bool g_pw8 = getenv("SAD_PW1") == nullptr;
 void launch_pixel_weights(const uint32_t* ids, const void* rtab_d, const FieldDims& f, double scale, const int32_t* xy,
                           int n_q, uint32_t* out_ids, double* out_w, int32_t* out_n, cudaStream_t stream) {
     int grid = (n_q + 127) / 128;
     if (grid < 1) grid = 1;
-    if (f.k <= 8)
+    if (f.k == 8 && g_pw8) {
+        const long long thr = 8ll * n_q;
+        const int g8 = static_cast<int>((thr + 127) / 128);
+        k_pixel_weights8<<<g8 > 0 ? g8 : 1, 128, 0, stream>>>(ids, (const Q4<double>*)rtab_d, f, scale, xy, n_q,
+                                                               out_ids, out_w, out_n);
+    } else if (f.k <= 8)
         k_pixel_weights<8><<<grid, 128, 0, stream>>>(ids, (const Q4<double>*)rtab_d, f, scale, xy, n_q, out_ids, out_w,
                                                      out_n);
     else
