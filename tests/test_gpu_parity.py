@@ -236,6 +236,27 @@ def test_pixel_weights_batch(G, R, k):
     assert np.array_equal(wg.view(np.uint64), wr.view(np.uint64))
 
 
+def test_pixel_weights_short_lists(G, R):
+    """Point queries on lists that end in sentinels (6 sites, K=8) and hold an inactive site: the
+    eight-lanes-per-query kernel keeps the reference's break-at-sentinel / skip-inactive rules, every
+    pixel of the image, bit-identical; out-of-range queries are refused as in the reference."""
+    w, h = 33, 29
+    st = random_model(w, h, 6, 41)
+    st.deactivate(2)
+    f = _field(w, h, 8)
+    R.refresh(st, f, sad.RefreshMode.Full, 2, 4, 17, F32)
+    assert (f.ids.reshape(-1, 8) == 0xFFFFFFFF).any()
+    yy, xx = np.mgrid[0:h, 0:w]
+    pix = np.stack([xx.ravel(), yy.ravel()], 1)
+    ig, wg, ng = G.pixel_weights_batch(st, f, pix)
+    ir, wr, nr = R.pixel_weights_batch(st, f, pix)
+    assert np.array_equal(ng, nr) and np.array_equal(ig, ir)
+    assert np.array_equal(wg.view(np.uint64), wr.view(np.uint64))
+    for q in ([w, 0], [-1, 3], [0, h]):  # the reference's std::invalid_argument (render.cpp:95-96)
+        with pytest.raises(sad.api.InvalidArgument):
+            G.pixel_weights_batch(st, f, np.array([q]))
+
+
 def test_loss_identity_and_pixgrad(G, R):
     """test_grad.cpp:116-128: image_loss == backward loss; adjoint entry point parity."""
     st = random_model(64, 64, 60, 7)
