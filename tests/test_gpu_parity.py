@@ -252,6 +252,8 @@ def test_pixel_weights_short_lists(G, R):
     ir, wr, nr = R.pixel_weights_batch(st, f, pix)
     assert np.array_equal(ng, nr) and np.array_equal(ig, ir)
     assert np.array_equal(wg.view(np.uint64), wr.view(np.uint64))
+    # the branch-free render (masked slots add +0.0) on the same short lists
+    assert np.array_equal(G.render_image(st, f, F32).data, R.render_image(st, f, F32).data)
     for q in ([w, 0], [-1, 3], [0, h]):  # the reference's std::invalid_argument (render.cpp:95-96)
         with pytest.raises(sad.api.InvalidArgument):
             G.pixel_weights_batch(st, f, np.array([q]))
