@@ -1225,17 +1225,27 @@ void launch_pixel_weights(const uint32_t* ids, const void* rtab_d, const FieldDi
 //   2. site ids are hashed into a shared table and compacted to local bucket ids;
 //   3. entries are bucketed per site (counting sort) into `order`, bucket of each sorted position in
 //      `posloc`;
-//   4. every thread sums PT = KM consecutive sorted positions for all channels at once (10
-//      independent double-double chains — balanced work, high ILP); a bucket split across threads
-//      is finished by its first thread, which merges the carries of the following threads;
+//   4. buckets are cut into chunks of PT consecutive sorted positions; a thread sums one chunk for
+//      half of the channels (5 independent double-double chains); when there are at most NT/2
+//      chunks the two channel halves run at once on the two halves of the block;
 //   5. each (site, tile) total is one record, claimed with one atomicAdd per site (RedTarget).
+// Chunk length of step 4 and the one-pass split.  Measured on the config-2 fit (exp A/B, identical
+// results): chunks of 8 with two sequential channel halves 895 ms; chunks of 12 with the split 870 ms
+// (10 and 13 equal within noise, 16 876 ms; 12 without the split 885 ms).  Longer chunks give fewer
+// chunks (NC ~ entries / 12 + buckets / 2, usually <= 128), so both halves fit on the 256 threads at once.
+#ifndef SAD_TILE_PT
+#define SAD_TILE_PT 12  // 0: chunks of KM sorted positions
+#endif
+#ifndef SAD_TILE_SPLIT
+#define SAD_TILE_SPLIT 1  // 1: when NC <= NT/2, the two channel halves run at once on the two thread halves
+#endif
 template <typename CT, int NCH, int TPX, int KM, int NT = TPX>
 struct TileRed {  // TPX pixels, KM slots each, NT threads (TPX or 2 * TPX)
     static constexpr int E = TPX * KM;  // entries per tile
     static constexpr int UMAX = E / 4;  // distinct sites per tile kept in shared memory (rest: DD atomics)
     static constexpr int HT = E / 2;    // hash slots (load factor <= 1/2 up to UMAX sites)
     static constexpr int ES = E + 16 / static_cast<int>(sizeof(CT));  // row stride: 16-byte aligned rows
-    static constexpr int PT = KM;       // sorted positions per chunk in step 4
+    static constexpr int PT = SAD_TILE_PT > 0 ? SAD_TILE_PT : KM;  // sorted positions per chunk in step 4
     static constexpr int CA = NCH / 2, CB = NCH - CA;  // step 4 runs in two channel halves
     // step 4 writes the chunk partials of channels [0, CA) over rows [0, CA) and those of [CA, NCH)
     // over rows [CA, NCH): each half's rows are dead once its sums are read
@@ -1456,9 +1466,27 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM, NT>& sm, c
                 if (ch < nch) carry[(tid + NT) * nch + ch] = acc1[ch];
         }
     };
-    half(0, R::CA, carry_a);
-    PH(6);
-    half(R::CA, R::CB, carry_b);
+    if (SAD_TILE_SPLIT && NC <= NT / 2) {
+        // threads [0, NT/2) sum channel half A of chunk tid, threads [NT/2, NT) half B of chunk
+        // tid - NT/2: one pass, and each half's partials still overwrite only that half's rows
+        const bool hb = tid >= NT / 2;
+        const int c = hb ? tid - NT / 2 : tid;
+        const int ch0 = hb ? R::CA : 0, nch = hb ? R::CB : R::CA;
+        DD acc[R::CB];
+        if (c < NC) sum_chunk(c, ch0, nch, acc);
+        __syncthreads();
+        if (c < NC) {
+            DD* carry = hb ? carry_b : carry_a;
+#pragma unroll
+            for (int ch = 0; ch < R::CB; ch++)
+                if (ch < nch) carry[c * nch + ch] = acc[ch];
+        }
+        PH(6);
+    } else {
+        half(0, R::CA, carry_a);
+        PH(6);
+        half(R::CA, R::CB, carry_b);
+    }
     // record code per local site: bits 31-30 = 00 record index into part, 01 overflow record into opart,
     // 11 pool exhausted (exact DD CAS into over)
 #pragma unroll
