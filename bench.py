@@ -533,7 +533,7 @@ def run_b200(a):
     ach = kernels[dom]["GBps"]
     # DRAM traffic per launch of the dominant kernel from the committed ncu --set full capture
     traffic, traffic_src = None, None
-    tfs = [os.path.join(ROOT, "profiles", f) for f in ("r1e_ncu_fwd_bwd_traffic.json", "r1b_ncu_fwd_bwd_traffic.json")]
+    tfs = [os.path.join(ROOT, "profiles", f) for f in ("r1h_ncu_fwd_bwd_traffic.json", "r1e_ncu_fwd_bwd_traffic.json", "r1b_ncu_fwd_bwd_traffic.json")]
     tf = next((f for f in tfs if os.path.exists(f)), tfs[-1])
     if dom == "fwd_bwd" and os.path.exists(tf):
         tj = json.load(open(tf))

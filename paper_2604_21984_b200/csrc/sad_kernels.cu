@@ -1236,6 +1236,9 @@ void launch_pixel_weights(const uint32_t* ids, const void* rtab_d, const FieldDi
 #ifndef SAD_TILE_PT
 #define SAD_TILE_PT 12  // 0: chunks of KM sorted positions
 #endif
+#ifndef SAD_TILE_SCAN1
+#define SAD_TILE_SCAN1 1  // 1: the chunk scan runs inside the bucket scan (one warp-0 pass, one barrier less)
+#endif
 #ifndef SAD_TILE_SPLIT
 #define SAD_TILE_SPLIT 1  // 1: when NC <= NT/2, the two channel halves run at once on the two thread halves
 #endif
@@ -1360,23 +1363,39 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM, NT>& sm, c
         sm.local_of_entry[e] = loc;
     }
     __syncthreads();
-    // exclusive scan of cnt[0..U) by warp 0 (U <= E); n_valid = total
+    // exclusive scans by warp 0 (U <= E) of cnt[0..U) -> start, and (SAD_TILE_SCAN1) of the chunk
+    // counts ceil(cnt / PT) -> chunk_base (local_of_slot is dead after the counting above)
     __shared__ int n_valid;
+    __shared__ int n_chunks;
+    uint16_t* chunk_base = sm.local_of_slot;  // chunk index of each bucket's first chunk
     if (tid < 32) {
-        int carry = 0;
+        int carry = 0, ccarry = 0;
         for (int base = 0; base < U; base += 32) {
             int u = base + tid;
             int v = u < U ? static_cast<int>(sm.cnt[u]) : 0;
             int x = v;
+            int cv = SAD_TILE_SCAN1 ? (v + R::PT - 1) / R::PT : 0;
+            int cx = cv;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
                 int y = __shfl_up_sync(0xffffffffu, x, d);
                 if (tid >= d) x += y;
+                if (SAD_TILE_SCAN1) {
+                    int cy = __shfl_up_sync(0xffffffffu, cx, d);
+                    if (tid >= d) cx += cy;
+                }
             }
-            if (u < U) sm.start[u] = static_cast<uint32_t>(carry + x - v);
+            if (u < U) {
+                sm.start[u] = static_cast<uint32_t>(carry + x - v);
+                if (SAD_TILE_SCAN1) chunk_base[u] = static_cast<uint16_t>(ccarry + cx - cv);
+            }
             carry += __shfl_sync(0xffffffffu, x, 31);
+            if (SAD_TILE_SCAN1) ccarry += __shfl_sync(0xffffffffu, cx, 31);
         }
-        if (tid == 0) n_valid = carry;
+        if (tid == 0) {
+            n_valid = carry;
+            if (SAD_TILE_SCAN1) n_chunks = ccarry;
+        }
     }
     __syncthreads();  // key[] is dead from here: its storage becomes order/posloc
     PH(3);
@@ -1387,15 +1406,19 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM, NT>& sm, c
         sm.srt.order[pos] = static_cast<uint16_t>(e);
     }
     __syncthreads();
-    for (int u = tid; u < U; u += NT) sm.start[u] -= sm.cnt[u];  // cursor back to the bucket start
+    const int U2 = U;
+    uint16_t* chunk_bucket = sm.local_of_entry;  // dead after the scatter: bucket of each chunk
+    for (int u = tid; u < U; u += NT) {
+        sm.start[u] -= sm.cnt[u];  // cursor back to the bucket start
+        if (SAD_TILE_SCAN1) {
+            const int c0 = chunk_base[u], nc = static_cast<int>((sm.cnt[u] + R::PT - 1) / R::PT);
+            for (int c = c0; c < c0 + nc; c++) chunk_bucket[c] = static_cast<uint16_t>(u);
+        }
+    }
     PH(4);
     // 4. buckets split into chunks of PT sorted entries; thread t sums chunks t and t + NT for all
     //    channels (convergent fixed-trip loops, NCH independent double-double chains)
-    const int U2 = U;
-    uint16_t* chunk_base = sm.local_of_slot;  // dead after counting: chunk index of each bucket's first chunk
-    uint16_t* chunk_bucket = sm.local_of_entry;  // dead after the scatter: bucket of each chunk
-    __shared__ int n_chunks;
-    if (tid < 32) {
+    if (!SAD_TILE_SCAN1 && tid < 32) {
         int carry = 0;
         for (int base = 0; base < U2; base += 32) {
             int u = base + tid;
@@ -1411,10 +1434,12 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM, NT>& sm, c
         }
         if (tid == 0) n_chunks = carry;
     }
-    __syncthreads();
-    for (int u = tid; u < U2; u += NT) {
-        int c0 = chunk_base[u], nc = static_cast<int>((sm.cnt[u] + R::PT - 1) / R::PT);
-        for (int c = c0; c < c0 + nc; c++) chunk_bucket[c] = static_cast<uint16_t>(u);
+    if (!SAD_TILE_SCAN1) {
+        __syncthreads();
+        for (int u = tid; u < U2; u += NT) {
+            int c0 = chunk_base[u], nc = static_cast<int>((sm.cnt[u] + R::PT - 1) / R::PT);
+            for (int c = c0; c < c0 + nc; c++) chunk_bucket[c] = static_cast<uint16_t>(u);
+        }
     }
     __syncthreads();
     const int NC = n_chunks;
@@ -1793,6 +1818,12 @@ __global__ void __launch_bounds__(BwdTile<T>::TW * BwdTile<T>::TH)
 // partial (one shuffle each way), so every rounding equals the one-thread loop of k_backward.  The
 // shuffles run for every lane (pairs whose pixel is outside or empty compute unused values), and the
 // tile reduction then runs on all 256 threads.
+#ifndef SAD_BWD_HOIST_TGT
+#define SAD_BWD_HOIST_TGT 1  // measured: with SAD_BWD_EARLY_COL, config-2 fit 868.5 -> 865 ms
+#endif
+#ifndef SAD_BWD_EARLY_COL
+#define SAD_BWD_EARLY_COL 1
+#endif
 #ifndef SAD_BWD2_MINB
 #define SAD_BWD2_MINB 4
 #endif
@@ -1827,6 +1858,19 @@ __global__ void __launch_bounds__(256, SAD_BWD2_MINB) k_backward2(const uint32_t
     T best = T(0);
     unsigned long long nonfinite = 0;
     DD loss{0.0, 0.0};
+#if SAD_BWD_HOIST_TGT
+    // the pixel's target (or dL/dvalue) row: the only HBM stream of the kernel, issued before the list
+    T tq0 = T(0), tq1 = T(0), tq2 = T(0);
+    if (inside) {
+        const T* tq = tgt + 3 * (static_cast<size_t>(py) * f.width + px);
+        tq0 = tq[0];
+        tq1 = tq[1];
+        tq2 = tq[2];
+    }
+#endif
+#if SAD_BWD_EARLY_COL
+    Q4<T> col[H];
+#endif
     {
         uint32_t idv[H];
         const uint32_t* lst = ids + static_cast<size_t>(f.k) * cell_index(f, px, py);
@@ -1847,9 +1891,17 @@ __global__ void __launch_bounds__(256, SAD_BWD2_MINB) k_backward2(const uint32_t
             cid[j] = id;
             ok[j] = false;
             dxs[j] = dys[j] = ud[j] = vd[j] = nrm[j] = lg[j] = T(0);
+#if SAD_BWD_EARLY_COL
+            col[j] = Q4<T>{T(0), T(0), T(0), T(0)};
+#endif
             if (!stop) {
                 const Q4<T> a = gtab[3 * id], b = gtab[3 * id + 1];
+#if SAD_BWD_EARLY_COL
+                col[j] = gtab[3 * id + 2];
+                const T act = col[j].w;
+#else
                 const T act = gtab[3 * id + 2].w;
+#endif
                 T dx = fx - a.x, dy = fy - a.y;
                 T pa = b.z * dx + b.w * dy;
                 T pb = b.z * dy - b.w * dx;
@@ -1902,14 +1954,20 @@ __global__ void __launch_bounds__(256, SAD_BWD2_MINB) k_backward2(const uint32_t
     const T wsum = half == 0 ? from1 : wpart;
     const T invw = trcp(wsum);
     // blended colour, same hand-over
+#if !SAD_BWD_EARLY_COL
     Q4<T> col[H];
+#endif
     T c0 = T(0), c1 = T(0), c2 = T(0);
 #pragma unroll
     for (int j = 0; j < H; j++) {
+#if !SAD_BWD_EARLY_COL
         col[j] = Q4<T>{T(0), T(0), T(0), T(0)};
+#endif
         if (ok[j]) {
             w[j] *= invw;
+#if !SAD_BWD_EARLY_COL
             col[j] = gtab[3 * cid[j] + 2];
+#endif
         }
     }
     if (half == 0) {
@@ -1945,7 +2003,11 @@ __global__ void __launch_bounds__(256, SAD_BWD2_MINB) k_backward2(const uint32_t
     const T ch0 = c0, ch1 = c1, ch2 = c2;
     if (any_all) {
         T g0, g1, g2, t0 = T(0), t1 = T(0), t2 = T(0), pl = T(0);
+#if SAD_BWD_HOIST_TGT
+        const T tp[3] = {tq0, tq1, tq2};
+#else
         const T* tp = tgt + 3 * (static_cast<size_t>(py) * f.width + px);
+#endif
         if (MODE != 2) {
             t0 = tp[0];
             t1 = tp[1];
