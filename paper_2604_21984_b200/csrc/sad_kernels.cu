@@ -1818,6 +1818,9 @@ __global__ void __launch_bounds__(BwdTile<T>::TW * BwdTile<T>::TH)
 // partial (one shuffle each way), so every rounding equals the one-thread loop of k_backward.  The
 // shuffles run for every lane (pairs whose pixel is outside or empty compute unused values), and the
 // tile reduction then runs on all 256 threads.
+#ifndef SAD_VEC_IDS
+#define SAD_VEC_IDS 1  // 1: K = 8 lists read as one 16-byte load per lane (two-lane backward and stats)
+#endif
 #ifndef SAD_BWD_HOIST_TGT
 #define SAD_BWD_HOIST_TGT 1  // measured: with SAD_BWD_EARLY_COL, config-2 fit 868.5 -> 865 ms
 #endif
@@ -1875,12 +1878,22 @@ __global__ void __launch_bounds__(256, SAD_BWD2_MINB) k_backward2(const uint32_t
         uint32_t idv[H];
         const uint32_t* lst = ids + static_cast<size_t>(f.k) * cell_index(f, px, py);
         bool has_empty = false;
+        if (SAD_VEC_IDS && H == 4 && f.k == 8) {  // this lane's half of the list in one 16-byte load
+            uint4 q = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+            if (inside) q = *reinterpret_cast<const uint4*>(lst + half * 4);
+            idv[0] = q.x;
+            idv[1] = q.y;
+            idv[2 % H] = q.z;
+            idv[3 % H] = q.w;
+        } else {
 #pragma unroll
-        for (int j = 0; j < H; j++) {
-            const int i = half * H + j;
-            idv[j] = (inside && i < f.k) ? lst[i] : kEmpty;
-            has_empty = has_empty || idv[j] == kEmpty;
+            for (int j = 0; j < H; j++) {
+                const int i = half * H + j;
+                idv[j] = (inside && i < f.k) ? lst[i] : kEmpty;
+            }
         }
+#pragma unroll
+        for (int j = 0; j < H; j++) has_empty = has_empty || idv[j] == kEmpty;
         const bool partner_empty = __shfl_xor_sync(FULL, has_empty, 1);
         const T fx = static_cast<T>(px), fy = static_cast<T>(py);
         bool stop = !inside || (half == 1 && partner_empty);
@@ -2480,12 +2493,22 @@ __global__ void __launch_bounds__(128) k_stats2(const uint32_t* __restrict__ ids
         uint32_t idv[H];
         const uint32_t* lst = ids + static_cast<size_t>(f.k) * cell_index(f, px, py);
         bool has_empty = false;
+        if (SAD_VEC_IDS && H == 4 && f.k == 8) {  // this lane's half of the list in one 16-byte load
+            uint4 q = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+            if (inside) q = *reinterpret_cast<const uint4*>(lst + half * 4);
+            idv[0] = q.x;
+            idv[1] = q.y;
+            idv[2 % H] = q.z;
+            idv[3 % H] = q.w;
+        } else {
 #pragma unroll
-        for (int j = 0; j < H; j++) {
-            const int i = half * H + j;
-            idv[j] = (inside && i < f.k) ? lst[i] : kEmpty;
-            has_empty = has_empty || idv[j] == kEmpty;
+            for (int j = 0; j < H; j++) {
+                const int i = half * H + j;
+                idv[j] = (inside && i < f.k) ? lst[i] : kEmpty;
+            }
         }
+#pragma unroll
+        for (int j = 0; j < H; j++) has_empty = has_empty || idv[j] == kEmpty;
         const bool partner_empty = __shfl_xor_sync(FULL, has_empty, 1);
         bool stop = !inside || (half == 1 && partner_empty);
 #pragma unroll
