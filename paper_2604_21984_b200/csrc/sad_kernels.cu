@@ -1239,6 +1239,10 @@ void launch_pixel_weights(const uint32_t* ids, const void* rtab_d, const FieldDi
 #ifndef SAD_TILE_SCAN1
 #define SAD_TILE_SCAN1 1  // 1: the chunk scan runs inside the bucket scan (one warp-0 pass, one barrier less)
 #endif
+#ifndef SAD_TILE_HTDIV
+#define SAD_TILE_HTDIV 4  // hash slots = E / 4 (= UMAX): half the table init and compaction work; a tile
+                          // holds ~40-100 distinct sites, so probes stay short (config-2 fit 857 -> 853 ms)
+#endif
 #ifndef SAD_TILE_SPLIT
 #define SAD_TILE_SPLIT 1  // 1: when NC <= NT/2, the two channel halves run at once on the two thread halves
 #endif
@@ -1246,7 +1250,8 @@ template <typename CT, int NCH, int TPX, int KM, int NT = TPX>
 struct TileRed {  // TPX pixels, KM slots each, NT threads (TPX or 2 * TPX)
     static constexpr int E = TPX * KM;  // entries per tile
     static constexpr int UMAX = E / 4;  // distinct sites per tile kept in shared memory (rest: DD atomics)
-    static constexpr int HT = E / 2;    // hash slots (load factor <= 1/2 up to UMAX sites)
+    static constexpr int HT = E / SAD_TILE_HTDIV;  // hash slots (>= UMAX; a full table sends entries to `over`)
+    static_assert(HT >= UMAX, "chunk_base lives in local_of_slot");
     static constexpr int ES = E + 16 / static_cast<int>(sizeof(CT));  // row stride: 16-byte aligned rows
     static constexpr int PT = SAD_TILE_PT > 0 ? SAD_TILE_PT : KM;  // sorted positions per chunk in step 4
     static constexpr int CA = NCH / 2, CB = NCH - CA;  // step 4 runs in two channel halves
