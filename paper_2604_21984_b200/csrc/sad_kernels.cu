@@ -1625,7 +1625,10 @@ __device__ __forceinline__ unsigned long long block_sum_u64(unsigned long long v
 // MODE 0: MSE vs target, no removal (the fit's call, train.cpp:249); 1: with removal delta;
 // 2: caller-supplied dL/dvalue (backward_pixel_grad, grad.cpp:382-390).
 template <typename T> struct BwdTile;
-template <> struct BwdTile<float> { static constexpr int TW = 16, TH = 8; };
+#ifndef SAD_BWD2_TH
+#define SAD_BWD2_TH 8  // fp32 tile rows (16 x TH pixels, 32 * TH threads in k_backward2)
+#endif
+template <> struct BwdTile<float> { static constexpr int TW = 16, TH = SAD_BWD2_TH; };
 template <> struct BwdTile<double> { static constexpr int TW = 8, TH = 8; };
 
 template <typename T, int KM, int MODE>
@@ -1836,12 +1839,12 @@ __global__ void __launch_bounds__(BwdTile<T>::TW * BwdTile<T>::TH)
 #define SAD_BWD2_MINB 4
 #endif
 template <int KM, int MODE>
-__global__ void __launch_bounds__(256, SAD_BWD2_MINB) k_backward2(const uint32_t* __restrict__ ids, const Q4<float>* __restrict__ gtab,
+__global__ void __launch_bounds__(32 * SAD_BWD2_TH, SAD_BWD2_MINB * 8 / SAD_BWD2_TH) k_backward2(const uint32_t* __restrict__ ids, const Q4<float>* __restrict__ gtab,
                                                    const float* __restrict__ tgt, FieldDims f, float s, float inv_hw2,
                                                    RedTarget red, double2* __restrict__ loss_part, DevState* st) {
     pdl_enter<2>();
     using T = float;
-    constexpr int TW = 16, TH = 8, TPX = TW * TH, NT = 2 * TPX, H = KM / 2;
+    constexpr int TW = 16, TH = SAD_BWD2_TH, TPX = TW * TH, NT = 2 * TPX, H = KM / 2;
     constexpr int NCH = MODE == 1 ? 11 : 10;
     constexpr unsigned FULL = 0xffffffffu;
     using Red = TileRed<T, NCH, TPX, KM, NT>;
@@ -2133,7 +2136,7 @@ static void backward_attr() {
                          (int)sizeof(TileRed<T, NCH, TW * TH, KM>));
     if (sizeof(T) == 4)
         cudaFuncSetAttribute(k_backward2<KM, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(TileRed<float, NCH, 128, KM, 256>));
+                             (int)sizeof(TileRed<float, NCH, 16 * SAD_BWD2_TH, KM, 32 * SAD_BWD2_TH>));
 }
 
 // SAD_BWD1=1 selects the one-lane-per-pixel fp32 kernel (A/B and regression checks)
@@ -2147,9 +2150,9 @@ static void backward_t(const uint32_t* ids, const void* gtab, const void* tgt, c
     dim3 grid((f.width + TW - 1) / TW, (rows_of(f, f.height) + TH - 1) / TH);
     T inv_hw2 = static_cast<T>(2.0 / (static_cast<double>(f.width) * f.height));
     if (sizeof(T) == 4 && !g_bwd1) {
-        static_assert(BwdTile<float>::TW == 16 && BwdTile<float>::TH == 8, "k_backward2 tile");
-        size_t smem = sizeof(TileRed<float, NCH, 128, KM, 256>);
-        launch_pdl(k_backward2<KM, MODE>, grid, dim3(256), smem, stream, ids, (const Q4<float>*)gtab,
+        static_assert(BwdTile<float>::TW == 16 && BwdTile<float>::TH == SAD_BWD2_TH, "k_backward2 tile");
+        size_t smem = sizeof(TileRed<float, NCH, 16 * SAD_BWD2_TH, KM, 32 * SAD_BWD2_TH>);
+        launch_pdl(k_backward2<KM, MODE>, grid, dim3(32 * SAD_BWD2_TH), smem, stream, ids, (const Q4<float>*)gtab,
                    (const float*)tgt, f, static_cast<float>(scale), static_cast<float>(inv_hw2), red, loss_part, st);
     } else {
         size_t smem = sizeof(TileRed<T, NCH, TW * TH, KM>);
