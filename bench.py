@@ -242,7 +242,7 @@ def run_config3(a):
     ctx = C.c_void_p()
     if lib.sad_ctx_create(C.c_int(0), C.c_void_p(stream.cuda_stream), C.byref(ctx)):
         raise RuntimeError(lib.sad_last_error().decode())
-    G = api.Backend(lib, "sad_", "gpu", ctx=ctx)
+    G = api.Backend(lib, "sad_", ctx=ctx)
     W = H = 2048
     cfg = sad.TrainConfig(iters=a.c3_iters, n_sites=100000, fp64=False)
     run = C.c_void_p()
@@ -318,7 +318,7 @@ def run_config5(a):
     ctx = C.c_void_p()
     if lib.sad_ctx_create(C.c_int(local), C.c_void_p(stream.cuda_stream), C.byref(ctx)):
         raise RuntimeError(lib.sad_last_error().decode())
-    G = api.Backend(lib, "sad_", "gpu", ctx=ctx)
+    G = api.Backend(lib, "sad_", ctx=ctx)
     W = H = a.c5_size
     img = synthetic_image(W, H, 5)
     nid = None
@@ -413,7 +413,7 @@ def run_b200(a):
     rc = lib.sad_ctx_create(C.c_int(local), C.c_void_p(stream.cuda_stream), C.byref(ctx))
     if rc:
         raise RuntimeError(lib.sad_last_error().decode())
-    G = api.Backend(lib, "sad_", "gpu", ctx=ctx)
+    G = api.Backend(lib, "sad_", ctx=ctx)
     lib.sad_host_alloc.restype = C.c_void_p
     lib.sad_host_alloc.argtypes = [C.c_size_t]
 
@@ -437,7 +437,7 @@ def run_b200(a):
         cx = C.c_void_p()
         if lib.sad_ctx_create(C.c_int(local), C.c_void_p(st_i.cuda_stream), C.byref(cx)):
             raise RuntimeError(lib.sad_last_error().decode())
-        backends.append(api.Backend(lib, "sad_", "gpu", ctx=cx))
+        backends.append(api.Backend(lib, "sad_", ctx=cx))
     runs = []
     for cfg, B in zip(cfgs, backends):
         run = C.c_void_p()

@@ -207,10 +207,13 @@ sad_status sad_backward_image(sad_ctx* ctx, const sad_sites_view* sites, const s
 /* image_loss (grad.hpp:101-102, grad.cpp:374-380) */
 sad_status sad_image_loss(sad_ctx* ctx, const sad_sites_view* sites, const sad_field_view* field,
                           const double* target_rgb, int fp64, double* loss);
-/* backward_pixel_grad (grad.hpp:106-107, grad.cpp:382-390) */
+/* backward_pixel_grad (grad.hpp:106-107, grad.cpp:382-390).  dl_width x dl_height is the adjoint
+ * image's size; a size other than the field's -> EINVAL "backward: adjoint size mismatch"
+ * (grad.cpp:383-384), checked before any byte of dl_dvalue_rgb is read. */
 sad_status sad_backward_pixel_grad(sad_ctx* ctx, const sad_sites_view* sites,
                                    const sad_field_view* field, const double* dl_dvalue_rgb,
-                                   int fp64, double* grads, uint64_t* nonfinite);
+                                   int dl_width, int dl_height, int fp64, double* grads,
+                                   uint64_t* nonfinite);
 
 /* ---------------------------------------------------------------- train.hpp */
 /* adam_step (train.hpp:33-34, train.cpp:139-169) incl. clamp_project; updates sites and adam */

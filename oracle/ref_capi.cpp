@@ -412,11 +412,11 @@ int sadref_image_loss(const sad_sites_view* sv, const sad_field_view* fv, const 
 }
 
 int sadref_backward_pixel_grad(const sad_sites_view* sv, const sad_field_view* fv,
-                               const double* dl, int fp64, double* grads, uint64_t* nonfinite) {
+                               const double* dl, int dl_w, int dl_h, int fp64, double* grads, uint64_t* nonfinite) {
     return guard([&] {
         SiteStore st = to_store(sv);
         CandidateField f = to_field(fv);
-        ImageBuffer t = to_image(dl, f.width, f.height);
+        ImageBuffer t = to_image(dl, dl_w, dl_h);
         GradBuffer gb;
         backward_pixel_grad(st, f, t, gb, RunOpts{fp64 != 0, 1});
         grads_out(gb, st.size(), grads);
@@ -598,7 +598,7 @@ int sadref_decode(const uint8_t* buf, size_t n, sad_sites_view* sv, int* w, int*
     });
 }
 
-// ---- fit (library sad::fit when threads == 1, else the pre-warmed replica)
+// ---- fit: always the pre-warmed fit_impl replica above (tests/cpp/compat_check pins it to the library sad::fit)
 int sadref_fit(const double* tgt, int w, int h, const sad_train_config* c, const sad_sites_view* init,
                void** handle) {
     return guard([&] {

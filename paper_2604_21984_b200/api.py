@@ -78,30 +78,35 @@ def _ptr(a: np.ndarray, t=C.c_double):
 
 
 class Backend:
-    """One C-ABI implementation.  kind: 'gpu' (sad_, ctx-first), 'ref' (sadref_, threads args),
-    'c' (sado_)."""
+    """The C-ABI binding of include/sad_b200.h (`sad_` prefix, context-first calls).
 
-    def __init__(self, lib: C.CDLL, prefix: str, kind: str, ctx=None, threads: int = 1):
+    Test-only oracle bindings (oracle/bindings.py) subclass it and override the few hooks below
+    (`_pre`, `_thr`, `_fit`, `decode_render`) for the CPU libraries' argument conventions; the product
+    package itself knows nothing about them."""
+
+    def __init__(self, lib: C.CDLL, prefix: str = "sad_", ctx=None):
         self.lib = lib
         self.prefix = prefix
-        self.kind = kind
         self.ctx = ctx
-        self.threads = threads
         self.lib.__getattr__(prefix + "last_error").restype = C.c_char_p
 
     # ------------------------------------------------------------------ plumbing
     def _fn(self, name):
         return getattr(self.lib, self.prefix + name)
 
+    def _pre(self, name):
+        """Leading arguments of a call: the context handle, except for context-free entry points."""
+        return () if name in _NO_CTX else (self.ctx,)
+
     def _call(self, name, *args):
-        pre = (self.ctx,) if self.kind == "gpu" and name not in _NO_CTX else ()
-        rc = self._fn(name)(*pre, *args)
+        rc = self._fn(name)(*self._pre(name), *args)
         if rc != 0:
             msg = self._fn("last_error")().decode(errors="replace")
             raise _EXC.get(rc, SadError)(f"{self.prefix}{name}: {msg}")
 
     def _thr(self):
-        return (C.c_int(self.threads),) if self.kind == "ref" else ()
+        """Trailing worker-count arguments (none: RunOpts.threads is ignored on the device)."""
+        return ()
 
     # ------------------------------------------------------------------ device-resident objects
     def sites_alloc(self, capacity: int) -> "ResidentSites":
@@ -202,10 +207,7 @@ class Backend:
         out = ImageBuffer(field.width, field.height)
         sv, keep = sites._view()
         fv = field._view()
-        args = [_ref(sv), _ref(fv), C.c_int(int(opts.fp64))]
-        if self.kind == "ref":
-            args.append(C.c_int(self.threads))
-        self._call("render_image", *args, _ptr(out.data))
+        self._call("render_image", _ref(sv), _ref(fv), C.c_int(int(opts.fp64)), *self._thr(), _ptr(out.data))
         return out
 
     def pixel_weights_batch(self, sites, field, pixels):
@@ -242,10 +244,8 @@ class Backend:
         loss = C.c_double()
         sv, keep = sites._view()
         fv = field._view()
-        args = [_ref(sv), _ref(fv), _ptr(target.data), C.c_int(int(opts.fp64)), C.c_int(int(with_removal))]
-        if self.kind == "ref":
-            args.append(C.c_int(self.threads))
-        self._call("backward_image", *args, _ptr(g), C.byref(nf), C.byref(loss))
+        self._call("backward_image", _ref(sv), _ref(fv), _ptr(target.data), C.c_int(int(opts.fp64)),
+                   C.c_int(int(with_removal)), *self._thr(), _ptr(g), C.byref(nf), C.byref(loss))
         out.data = g[: sites.size() * 11].reshape(-1, 11).copy()
         out.nonfinite = int(nf.value)
         return float(loss.value)
@@ -266,8 +266,8 @@ class Backend:
         nf = C.c_uint64()
         sv, keep = sites._view()
         fv = field._view()
-        self._call("backward_pixel_grad", _ref(sv), _ref(fv), _ptr(dl.data), C.c_int(int(opts.fp64)),
-                   _ptr(g), C.byref(nf))
+        self._call("backward_pixel_grad", _ref(sv), _ref(fv), _ptr(dl.data), C.c_int(dl.width), C.c_int(dl.height),
+                   C.c_int(int(opts.fp64)), _ptr(g), C.byref(nf))
         out.data = g[: sites.size() * 11].reshape(-1, 11).copy()
         out.nonfinite = int(nf.value)
 
@@ -328,10 +328,8 @@ class Backend:
         valid = C.c_uint64()
         sv, keep = sites._view()
         fv = field._view()
-        args = [_ref(sv), _ref(fv), _ptr(target.data)]
-        if self.kind == "ref":
-            args.append(C.c_int(self.threads))
-        self._call("accumulate_stats", *args, _ptr(buf), C.byref(valid))
+        self._call("accumulate_stats", _ref(sv), _ref(fv), _ptr(target.data), *self._thr(), _ptr(buf),
+                   C.byref(valid))
         r.data = buf[: sites.size() * 8].reshape(-1, 8).copy()
         r.valid_pixels = int(valid.value)
         return r
@@ -413,12 +411,6 @@ class Backend:
                       fp64: bool = False):
         """Decode pipeline on the device: bytes -> sites -> refresh(Full, passes) -> render_image.
         Returns (ImageBuffer, SiteStore)."""
-        if self.kind != "gpu":
-            w, h, st = self.decode_sites(data)
-            f = CandidateField()
-            f.resize(w, h, k)
-            self.refresh(st, f, RefreshMode.Full, passes, inject, seed, RunOpts(fp64=fp64))
-            return self.render_image(st, f, RunOpts(fp64=fp64)), st
         buf = (C.c_uint8 * len(data)).from_buffer_copy(data)
         w, h, cnt = C.c_int(), C.c_int(), C.c_uint32()
         self._call("decode_header", buf, C.c_size_t(len(data)), C.byref(w), C.byref(h), C.byref(cnt))
@@ -549,70 +541,25 @@ class Backend:
     def _fit(self, target: ImageBuffer, cfg: TrainConfig, init: Optional[SiteStore]) -> FitResult:
         c = cfg.to_c()
         w, h = target.width, target.height
-        if self.kind == "gpu":
-            run = self._fit_run(w, h, c)
-            if True:
-                self._call("fit_set_target", run, _ptr(target.data))
-                if init is None:
-                    self._call("fit_run_init", run)
-                else:
-                    sv, keep = init._view()
-                    self._call("fit_run_store", run, _ref(sv))
-                n = C.c_size_t()
-                nh = C.c_int()
-                sc = C.c_double()
-                self._call("fit_info", run, C.byref(n), C.byref(nh), C.byref(sc))
-                res = self._fit_collect(w, h, cfg, int(n.value), int(nh.value), float(sc.value),
-                                        lambda sv, fv, hist: self._call("fit_download", run, sv, fv, hist))
-                tot = C.c_double()
-                ph = (C.c_double * 8)()
-                self._call("fit_timing", run, C.byref(tot), ph)
-                res.timing = {"total_ms": tot.value, "propagate_ms": ph[0], "fwd_bwd_ms": ph[1],
-                              "adam_ms": ph[2], "events_ms": ph[3]}
-                return res
-        if self.kind == "ref":
-            hd = _P()
-            if init is None:
-                self._call("fit", _ptr(target.data), C.c_int(w), C.c_int(h), C.byref(c), None, C.byref(hd))
-            else:
-                sv, keep = init._view()
-                self._call("fit", _ptr(target.data), C.c_int(w), C.c_int(h), C.byref(c), _ref(sv), C.byref(hd))
-            try:
-                n = C.c_size_t()
-                nh = C.c_int()
-                sc = C.c_double()
-                sec = C.c_double()
-                ph = (C.c_double * 8)()
-                self.lib.sadref_fit_info(hd, C.byref(n), C.byref(nh), C.byref(sc), C.byref(sec), ph)
-                res = self._fit_collect(w, h, cfg, int(n.value), int(nh.value), float(sc.value),
-                                        lambda sv, fv, hist: self._call("fit_download", hd, sv, fv, hist))
-                res.timing = {"total_ms": sec.value * 1e3, "propagate_ms": ph[0], "fwd_bwd_ms": ph[1],
-                              "adam_ms": ph[2], "events_ms": ph[3], "refresh_full_ms": ph[4], "init_ms": ph[5]}
-                return res
-            finally:
-                self.lib.sadref_fit_free(hd)
-        # plain-C restatement
-        cap = C.c_size_t()
-        self._call("fit_capacity", C.c_int(w), C.c_int(h), C.byref(c), C.c_size_t(init.size() if init else 0),
-                   C.byref(cap))
-        out = SiteStore(0)
-        sv, keep = out._view(capacity=int(cap.value))
-        f = CandidateField()
-        f.resize(w, h, cfg.k)
-        fv = f._view()
-        hist = (_abi.HistoryRowC * max(cfg.iters, 1))()
-        sc = C.c_double()
+        run = self._fit_run(w, h, c)
+        self._call("fit_set_target", run, _ptr(target.data))
         if init is None:
-            self._call("fit", _ptr(target.data), C.c_int(w), C.c_int(h), C.byref(c), None, _ref(sv), _ref(fv),
-                       hist, C.byref(sc))
+            self._call("fit_run_init", run)
         else:
-            iv, ikeep = init._view()
-            self._call("fit", _ptr(target.data), C.c_int(w), C.c_int(h), C.byref(c), C.byref(iv), _ref(sv),
-                       _ref(fv), hist, C.byref(sc))
-        out._absorb(sv, keep)
-        f._absorb(fv)
-        rows = [HistoryRow(r.iter, r.loss, r.psnr, r.active_sites, r.ms) for r in hist[: cfg.iters]]
-        return FitResult(out, f, rows, float(sc.value))
+            sv, keep = init._view()
+            self._call("fit_run_store", run, _ref(sv))
+        n = C.c_size_t()
+        nh = C.c_int()
+        sc = C.c_double()
+        self._call("fit_info", run, C.byref(n), C.byref(nh), C.byref(sc))
+        res = self._fit_collect(w, h, cfg, int(n.value), int(nh.value), float(sc.value),
+                                lambda sv, fv, hist: self._call("fit_download", run, sv, fv, hist))
+        tot = C.c_double()
+        ph = (C.c_double * 8)()
+        self._call("fit_timing", run, C.byref(tot), ph)
+        res.timing = {"total_ms": tot.value, "propagate_ms": ph[0], "fwd_bwd_ms": ph[1],
+                      "adam_ms": ph[2], "events_ms": ph[3]}
+        return res
 
     def _fit_collect(self, w, h, cfg, n, nh, sc, download) -> FitResult:
         st = SiteStore(0)
@@ -665,7 +612,7 @@ def gpu_backend(device: int = 0) -> Backend:
             rc = lib.sad_ctx_create(C.c_int(device), None, C.byref(ctx))
             if rc != 0:
                 raise CudaError("sad_ctx_create: " + lib.sad_last_error().decode(errors="replace"))
-            _gpu = Backend(lib, "sad_", "gpu", ctx=ctx)
+            _gpu = Backend(lib, "sad_", ctx=ctx)
         return _gpu
 
 

@@ -1252,6 +1252,7 @@ struct TileRed {  // TPX pixels, KM slots each, NT threads (TPX or 2 * TPX)
     static constexpr int UMAX = E / 4;  // distinct sites per tile kept in shared memory (rest: DD atomics)
     static constexpr int HT = E / SAD_TILE_HTDIV;  // hash slots (>= UMAX; a full table sends entries to `over`)
     static_assert(HT >= UMAX, "chunk_base lives in local_of_slot");
+    static_assert((HT & (HT - 1)) == 0, "the tile hash masks with HT - 1: HT must be a power of two");
     static constexpr int ES = E + 16 / static_cast<int>(sizeof(CT));  // row stride: 16-byte aligned rows
     static constexpr int PT = SAD_TILE_PT > 0 ? SAD_TILE_PT : KM;  // sorted positions per chunk in step 4
     static constexpr int CA = NCH / 2, CB = NCH - CA;  // step 4 runs in two channel halves
@@ -1740,13 +1741,16 @@ __global__ void __launch_bounds__(BwdTile<T>::TW * BwdTile<T>::TH)
             g1 = tp[1];
             g2 = tp[2];
         }
+        // A kept candidate whose softmax weight underflowed to exactly 0 contributes +-0 to every
+        // channel when the pixel's adjoint g (and, with removal, its loss pl) is finite: every term is
+        // a product with w or A = w * finite.  Dropping it then leaves every compensated sum and the
+        // non-finite count bit-identical, and shrinks the reduction.  With a non-finite g the
+        // reference's 0 * inf = NaN terms are scrubbed and counted, so such pixels keep the entry.
+        const bool wz_skip = c_finite(g0) && c_finite(g1) && c_finite(g2) && (MODE != 1 || c_finite(pl));
 #pragma unroll
         for (int i = 0; i < KM; i++) {
             const int e = i * TPX + tid;
-            // A kept candidate whose softmax weight underflowed to exactly 0 contributes +-0 to every
-            // channel (all terms are products with w or A = w * finite): dropping it leaves every
-            // compensated sum, and the non-finite count, bit-identical — and shrinks the reduction.
-            if (!ok[i] || w[i] == T(0)) {
+            if (!ok[i] || (w[i] == T(0) && wz_skip)) {
                 sm.key[e] = kEmpty;
                 continue;
             }
@@ -2051,10 +2055,11 @@ __global__ void __launch_bounds__(32 * SAD_BWD2_TH, SAD_BWD2_MINB * 8 / SAD_BWD2
             g1 = tp[1];
             g2 = tp[2];
         }
+        const bool wz_skip = c_finite(g0) && c_finite(g1) && c_finite(g2) && (MODE != 1 || c_finite(pl));
 #pragma unroll
         for (int j = 0; j < H; j++) {
             const int e = (half * H + j) * TPX + pix;
-            if (!ok[j] || w[j] == T(0)) {  // zero weight: +-0 in every channel (see k_backward)
+            if (!ok[j] || (w[j] == T(0) && wz_skip)) {  // zero weight: +-0 in every channel (see k_backward)
                 sm.key[e] = kEmpty;
                 continue;
             }
@@ -2121,6 +2126,13 @@ __global__ void __launch_bounds__(32 * SAD_BWD2_TH, SAD_BWD2_MINB * 8 / SAD_BWD2
     __syncthreads();
     unsigned long long nf = block_sum_u64<NT>(nonfinite, reinterpret_cast<unsigned long long*>(sm.warp_part));
     if (threadIdx.x == 0 && nf) atomicAdd(reinterpret_cast<unsigned long long*>(&st->nonfinite), nf);
+}
+
+static constexpr int gcd_c(int a, int b) { return b == 0 ? a : gcd_c(b, a % b); }
+static constexpr int lcm_c(int a, int b) { return a / gcd_c(a, b) * b; }
+int tile_row_quantum() {
+    constexpr int kStatsTH = 8;  // k_stats / k_stats2 tiles
+    return lcm_c(lcm_c(BwdTile<float>::TH, BwdTile<double>::TH), kStatsTH);
 }
 
 int backward_blocks(bool fp64, const FieldDims& f) {

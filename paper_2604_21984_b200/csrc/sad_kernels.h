@@ -113,6 +113,9 @@ void launch_pixel_weights(const uint32_t* ids, const void* rtab_d, const FieldDi
 // mode: 0 = MSE target, 1 = MSE target + removal delta, 2 = caller adjoint (pixgrad)
 // Per-block loss partials go to loss_part[block]; launch_loss_reduce / launch_advance reduce them.
 int backward_blocks(bool fp64, const FieldDims& f);
+// Row quantum of the per-tile kernels (least common multiple of the fp32/fp64 backward and the stats
+// tile heights): row strips that are multiples of it never split a tile.
+int tile_row_quantum();
 void launch_backward(bool fp64, int mode, const uint32_t* ids, const void* gtab, const void* tgt_or_pixgrad,
                      const FieldDims& f, double scale, const RedTarget& red, double2* loss_part, DevState* st,
                      cudaStream_t stream);

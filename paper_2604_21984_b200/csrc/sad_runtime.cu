@@ -1358,8 +1358,13 @@ sad_status sad_backward_image(sad_ctx* c, const sad_sites_view* s, const sad_fie
 }
 
 sad_status sad_backward_pixel_grad(sad_ctx* c, const sad_sites_view* s, const sad_field_view* f, const double* dl,
-                                   int fp64, double* grads, uint64_t* nonfinite) {
-    return guard([&] { backward_call(c, s, f, dl, fp64, 2, grads, nonfinite, nullptr); });
+                                   int dl_width, int dl_height, int fp64, double* grads, uint64_t* nonfinite) {
+    return guard([&] {
+        const sad_field_view* fv = field_arg(c, f);
+        if (!dl || dl_width != fv->width || dl_height != fv->height)  // grad.cpp:383-384
+            fail(SAD_EINVAL, "backward: adjoint size mismatch");
+        backward_call(c, s, f, dl, fp64, 2, grads, nonfinite, nullptr);
+    });
 }
 
 sad_status sad_image_loss(sad_ctx* c, const sad_sites_view* s_in, const sad_field_view* f_in, const double* tgt,
@@ -2110,15 +2115,28 @@ struct NcclComm : StripComm {
     }
 };
 
-// Row bounds of `world` strips over `rows` rows, each a multiple of the 8-row backward/stats tiles.
+// Row bounds of `world` strips over `rows` rows, each a multiple of the backward/stats tile heights
+// (sadk::tile_row_quantum), so no tile straddles two strips.
 static std::vector<int> strip_bounds(int rows, int world) {
-    const int tiles = (rows + 7) / 8;
+    const int qr = sadk::tile_row_quantum();
+    const int tiles = (rows + qr - 1) / qr;
     std::vector<int> b(static_cast<size_t>(world) + 1);
-    for (int q = 0; q <= world; q++) b[q] = std::min(rows, 8 * static_cast<int>(static_cast<long long>(tiles) * q / world));
+    for (int q = 0; q <= world; q++)
+        b[q] = std::min(rows, qr * static_cast<int>(static_cast<long long>(tiles) * q / world));
     return b;
 }
 
 static void fit_loop_strips(std::vector<sad_fit_run*>& runs, StripComm& T) {
+    // every exit (including an exception mid-fit) leaves the runs' field views on the whole image
+    struct RowRestore {
+        std::vector<sad_fit_run*>& rs;
+        ~RowRestore() {
+            for (sad_fit_run* r : rs) {
+                r->ws.fd.row0 = 0;
+                r->ws.fd.row1 = 1 << 30;
+            }
+        }
+    } restore_rows{runs};
     const int R = T.world();
     sad_fit_run* r0 = runs[0];
     const sad_train_config& c = r0->cfg;

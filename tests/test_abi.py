@@ -42,7 +42,7 @@ def test_struct_layouts():
 
 def test_host_entry_points_without_gpu():
     import paper_2604_21984_b200 as sad
-    B = api.Backend(api.load_library(), "sad_", "gpu", ctx=None)
+    B = api.Backend(api.load_library(), "sad_", ctx=None)
     assert B.jump_step(7, 2048) == 8
     assert [p.step for p in B.full_refresh_passes(768, 512, 4)] == [512, 256, 128, 64, 32, 16, 8, 4, 2, 1, 1, 1, 1, 1]
     assert B.bpp_target_count(2.0, 768, 512) == 6144

@@ -20,7 +20,7 @@ def _model():
 def _lib():
     """The product library's codec runs on the host; it loads without a GPU."""
     from paper_2604_21984_b200 import api
-    return api.Backend(api.load_library(), "sad_", "gpu", ctx=None)
+    return api.Backend(api.load_library(), "sad_", ctx=None)
 
 
 @pytest.mark.skipif(not have_ref(), reason="reference library not built")
