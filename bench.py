@@ -46,8 +46,8 @@ def parse():
     p.add_argument("--images-per-gpu", type=int, default=1)
     p.add_argument("--serial", action="store_true", help="fit a rank's images one after another")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--ref-iters", type=int, default=30, help="iterations per reference-arm sample")
-    p.add_argument("--cpu-iters", type=int, default=60, help="iterations of the cpu_baseline sample")
+    p.add_argument("--ref-iters", type=int, default=80, help="iterations per reference-arm sample")
+    p.add_argument("--cpu-iters", type=int, default=80, help="iterations of the cpu_baseline sample")
     p.add_argument("--mode", default="config2", choices=["config2", "config3", "config5"],
                    help="config3: 2048x2048 / 100k-site fit + 1e6 random point queries; config5: 8192x8192 "
                         "2-BPP fit on one GPU (each its own JSON line)")
@@ -137,21 +137,38 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------- reference arm
-def ref_sample(a, iters, threads, seed=1):
-    """One bounded sample of the config-2 fit on the reference library: iters/s over the loop."""
+def ref_sample(a, iters, threads, seed=1, fp64=False):
+    """One bounded sample of the config-2 fit on the reference library: the first `iters` iterations of
+    the real 4000-iteration schedule (cfg.iters unchanged, so validate()'s event windows and
+    plan_schedule are the full fit's; the loop stops after iteration `iters` via SAD_REF_STOP_AT,
+    oracle/ref_capi.cpp).  Returns iters/s over the loop (init and the initial refresh excluded)."""
     import paper_2604_21984_b200 as sad
     from oracle.bindings import ref_backend
     from paper_2604_21984_b200.synth import synthetic_image
     R = ref_backend(threads=threads)
     img = sad.ImageBuffer(a.width, a.height, synthetic_image(a.width, a.height, seed))
     cfg = train_config(a, seed)
-    cfg.iters = iters
+    cfg.fp64 = fp64
     cfg.threads = threads
-    t0 = time.perf_counter()
-    res = R.fit(img, cfg)
-    wall = time.perf_counter() - t0
+    old = os.environ.get("SAD_REF_STOP_AT")
+    os.environ["SAD_REF_STOP_AT"] = str(iters)
+    try:
+        t0 = time.perf_counter()
+        res = R.fit(img, cfg)
+        wall = time.perf_counter() - t0
+    finally:
+        if old is None:
+            os.environ.pop("SAD_REF_STOP_AT", None)
+        else:
+            os.environ["SAD_REF_STOP_AT"] = old
+    assert len(res.history) == iters
     loop_ms = sum(r.ms for r in res.history)
     return iters / (loop_ms / 1e3), loop_ms, wall, res
+
+
+# Full reference fits of this workload measured on the GPU box's host (16 threads; tools/config2_lockstep.py,
+# profiles/r1h_config2_lockstep.txt): 4000 iterations in 160.1 s = 25.0 iters/s including init and refreshes.
+REF_FULL_FIT = {"seconds": 160.1, "iters_per_s": 25.0, "threads": 16, "source": "profiles/r1h_config2_lockstep.txt"}
 
 
 def run_reference(a):
@@ -167,13 +184,15 @@ def run_reference(a):
         vals.append(v)
         mss.append(loop_ms)
     value = a.steps * a.ref_iters / (sum(mss) / 1e3)
-    sample = (f"first {a.ref_iters} iterations of the config-2 fit per step (loop time only; init and "
-              f"refreshes outside the loop excluded), reference library oracle/_ref, {threads} threads")
+    sample = (f"iterations 1-{a.ref_iters} of the real 4000-iteration config-2 schedule per step (events at "
+              f"t = 20, 40, ...; loop time only, init and initial refresh excluded), reference library "
+              f"oracle/_ref, {threads} threads")
     out = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": a.gpus,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": float(np.mean(mss)), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config_dict(a),
-        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": threads, "kind": "reference", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": threads, "kind": "reference", "sample": sample,
+                         "full_fit_measured": REF_FULL_FIT},
         "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -574,15 +593,33 @@ def run_b200(a):
         try:
             threads = os.cpu_count() or 1
             v, loop_ms, wall, _ = ref_sample(a, a.cpu_iters, threads)
+            v1, _, w1, _ = ref_sample(a, 20, 1)
+            v64, _, w64, _ = ref_sample(a, 40, threads, fp64=True)
             cpu = {"value": v, "unit": "iters/s", "cores": threads, "kind": "reference",
-                   "sample": f"first {a.cpu_iters} iterations of the same config-2 fit (loop time only), "
-                             f"reference library oracle/_ref, {threads} threads, {wall:.1f}s wall"}
+                   "sample": f"iterations 1-{a.cpu_iters} of the same 4000-iteration config-2 schedule (loop time "
+                             f"only), reference library oracle/_ref, {threads} threads, {wall:.1f}s wall",
+                   "rows": {"f32_1_thread": {"value": v1, "sample": "iterations 1-20, 1 thread"},
+                            "f64_all_threads": {"value": v64, "sample": f"iterations 1-40, fp64, {threads} threads"}},
+                   "full_fit_measured": REF_FULL_FIT}
         except Exception as e:  # oracle not built on this box
             cpu = {"value": None, "unit": "iters/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 
     rf2048 = None
     if rank == 0 and not a.no_roofline_2048:
         rf2048 = roofline_2048(G)
+    fp64_row = None
+    if rank == 0 and world == 1:
+        # the reference's default precision (TrainConfig.fp64 = true, types.hpp:162): all-double kernels
+        cfg64 = train_config(a, seeds[0])
+        cfg64.fp64 = True
+        tgt64 = sad.ImageBuffer(W, H, imgs[0])
+        G.fit(tgt64, cfg64)
+        t0 = time.perf_counter()
+        r64 = G.fit(tgt64, cfg64)
+        s64 = time.perf_counter() - t0
+        fp64_row = {"value": a.iters / (r64.timing["total_ms"] * 1e-3), "unit": "iters/s",
+                    "e2e": a.iters / s64, "encode_seconds_e2e": s64, "active_sites": r64.history[-1].active_sites,
+                    "workload": "the same config-2 fit with fp64=True (all-double kernels)"}
     paper = None
     if rank == 0 and world == 1 and not a.no_paper_config:
         # the paper's own GPU implementation encodes Kodak 768x512 with 50k sites, 4000
@@ -605,7 +642,7 @@ def run_b200(a):
             "e2e": {"value": e2e_val, "unit": "iters/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "encode_seconds": e2e_s / (a.steps * a.images_per_gpu)},
             "gpu_launches": launches, "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu,
-            "clocks": clk, "roofline_2048": rf2048, "paper_config": paper,
+            "clocks": clk, "roofline_2048": rf2048, "paper_config": paper, "fp64": fp64_row,
         }
         print(json.dumps(out), flush=True)
     for run in runs:

@@ -307,6 +307,10 @@ struct Workspace {
     DBuf<int32_t> gcnt, scnt;         // RedTarget.cnt
     DBuf<double2> loss_part;          // per-block loss partials
     int maxt = getenv("SAD_MAXT") ? atoi(getenv("SAD_MAXT")) : 16;  // record slots per site and pass
+    // Test knobs (read at context / run creation): force the overflow-record pool and the adaptive
+    // record pool down to a fixed size, so tests reach the exhausted-pool fallbacks (exact DD CAS).
+    int ocap_force = getenv("SAD_OCAP") ? std::max(1, atoi(getenv("SAD_OCAP"))) : 0;
+    long long apsize_force = getenv("SAD_APSIZE") ? std::max(1ll, atoll(getenv("SAD_APSIZE"))) : 0;
     DBuf<double> m, v;
     DBuf<uint32_t> act, free_list;
     DBuf<uint8_t> flags;
@@ -377,7 +381,7 @@ struct Workspace {
         return t;
     }
     void ensure_adaptive(size_t tiles) {
-        long long want = 16ll * cap + 64ll * static_cast<long long>(tiles);
+        long long want = apsize_force ? apsize_force : 16ll * cap + 64ll * static_cast<long long>(tiles);
         if (apsize < want || !apool.p) {
             apool.ensure(static_cast<size_t>(want) * 11);
             apsize = want;
@@ -391,7 +395,7 @@ struct Workspace {
     }
     // overflow pool sized from the number of reduction tiles (each tile adds at most its bucket count)
     void ensure_pool(size_t tiles) {
-        size_t want = std::max<size_t>(tiles * 16, 4096);
+        size_t want = ocap_force ? static_cast<size_t>(ocap_force) : std::max<size_t>(tiles * 16, 4096);
         if (static_cast<size_t>(ocap) >= want && otops.p) return;
         gnext.ensure(want);
         snext.ensure(want);

@@ -1,0 +1,92 @@
+"""Full-configuration fit parity on the GPU.
+
+* Config 1 (256x256, 4096 sites, 200 iterations, budget off), fp32 and fp64: the GPU fit against the
+  compiled reference run live on this box's host cores — every history line, the final sites and
+  the final map identical.
+* Config 2 (768x512 synthetic Kodak-shaped images, 2 BPP, 4000 iterations with 150 densify/prune
+  events), image seeds 1-8 in fp32 and seed 1 in fp64 (the reference's default precision), and
+  config 3 (2048x2048, 100k sites, 300 iterations): the GPU fit against goldens of complete
+  reference fits (tests/golden/fit_*.npz, written here by tests/golden/make_fit_golden.py from the
+  unmodified reference library; a reference fit takes minutes per image, the GPU's under a second).
+  Every history row (loss and PSNR as doubles, active count), the schedule scale, SHA-256 digests
+  of all final site arrays and of the final map, the pass index and the decode PSNR must be equal.
+"""
+import ast
+import glob
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+import paper_2604_21984_b200 as sad
+from oracle.bindings import c_backend, have_ref, ref_backend
+from paper_2604_21984_b200.synth import synthetic_image
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLDEN = sorted(glob.glob(os.path.join(HERE, "golden", "fit_*.npz")))
+SITE_ARRAYS = ("x", "y", "log_tau", "radius", "col_r", "col_g", "col_b", "dir_x", "dir_y", "aniso", "active",
+               "frozen")
+
+
+@pytest.fixture(scope="module")
+def G():
+    return sad.gpu_backend(0)
+
+
+def _digest(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _decode_psnr(G, res, img):
+    out = G.render_image(res.sites, res.field, sad.RunOpts(fp64=False)).data
+    mse = float(np.mean((out - img.data) ** 2))
+    return 99.0 if mse <= 0 else 10.0 * np.log10(1.0 / mse)
+
+
+@pytest.mark.parametrize("fp64", [False, True])
+def test_config1_full_fit_identical(G, fp64):
+    """Config 1: all 200 iterations bit-identical to the reference (live, all host threads)."""
+    R = ref_backend(threads=os.cpu_count() or 1) if have_ref() else c_backend()
+    tgt = sad.ImageBuffer(256, 256, synthetic_image(256, 256, 1))
+    cfg = sad.TrainConfig(iters=200, n_sites=4096, fp64=fp64, seed=1)
+    a = G.fit(tgt, cfg)
+    cfg.threads = os.cpu_count() or 1
+    b = R.fit(tgt, cfg)
+    assert [sad.history_line(r) for r in a.history] == [sad.history_line(r) for r in b.history]
+    for p in SITE_ARRAYS:
+        assert np.array_equal(getattr(a.sites, p), getattr(b.sites, p)), p
+    assert np.array_equal(a.field.ids, b.field.ids)
+    assert a.field.pass_index == b.field.pass_index
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p)[4:-4] for p in GOLDEN])
+def test_full_fit_matches_reference_golden(G, path):
+    d = np.load(path)
+    w, h, seed = int(d["width"]), int(d["height"]), int(d["image_seed"])
+    cfg = sad.TrainConfig(**ast.literal_eval(str(d["config"])))
+    img = sad.ImageBuffer(w, h, synthetic_image(w, h, seed))
+    res = G.fit(img, cfg)
+    loss = np.array([r.loss for r in res.history], np.float64)
+    psnr = np.array([r.psnr for r in res.history], np.float64)
+    active = np.array([r.active_sites for r in res.history], np.int64)
+    first = np.flatnonzero((loss.view(np.uint64) != d["loss"].view(np.uint64)) | (active != d["active"]))
+    assert loss.shape == d["loss"].shape
+    assert first.size == 0, f"history differs from iteration {first[0] + 1} on"
+    assert np.array_equal(psnr.view(np.uint64), d["psnr"].view(np.uint64))
+    assert res.schedule_scale == float(d["schedule_scale"])
+    assert res.sites.size() == int(d["n_sites"])
+    for p in SITE_ARRAYS:
+        assert _digest(getattr(res.sites, p)) == str(d["sha_" + p]), p
+    assert _digest(res.field.ids) == str(d["field_sha"])
+    assert res.field.pass_index == int(d["pass_index"])
+    assert _decode_psnr(G, res, img) == float(d["decode_psnr"])
+
+
+def test_golden_set_present():
+    """The committed goldens cover config 2 over >= 8 images, fp64, and config 3."""
+    names = {os.path.basename(p) for p in GOLDEN}
+    assert sum(n.startswith("fit_config2_s") for n in names) >= 8
+    assert "fit_config2_fp64_s1.npz" in names and "fit_config3_s1.npz" in names
