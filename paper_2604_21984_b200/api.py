@@ -168,6 +168,14 @@ class Backend:
         self._call("full_refresh_passes", C.c_int(gw), C.c_int(gh), C.c_int(extra_step1), buf, C.byref(n))
         return [PassSpec(buf[i].step, Stencil(buf[i].stencil)) for i in range(n.value)]
 
+    def schedule_passes(self, gw, gh, total) -> List[PassSpec]:
+        """schedule_passes (candidates.cpp:50-62): `total` passes of the jump schedule, Box3 floods at
+        halving steps then Axial step-1 passes."""
+        buf = (_abi.PassSpec * max(total, 1))()
+        n = C.c_int(len(buf))
+        self._call("schedule_passes", C.c_int(gw), C.c_int(gh), C.c_int(total), buf, C.byref(n))
+        return [PassSpec(buf[i].step, Stencil(buf[i].stencil)) for i in range(n.value)]
+
     def jfa_seed(self, sites: SiteStore, field: CandidateField):
         sv, keep = sites._view()
         fv = field._view()

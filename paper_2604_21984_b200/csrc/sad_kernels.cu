@@ -4,8 +4,7 @@
 // order; the library is built with --fmad=false (see sad_device.cuh).  None of these steps is a
 // dense contraction, so there are no tensor-core paths: the roofline is HBM / L2 bandwidth or the
 // FP32/FP64 pipes.
-#include "sad_device.cuh"
-#include "sad_kernels.h"
+#include "sad_kcommon.cuh"
 
 #ifndef SAD_EXPERIMENT
 #define SAD_EXPERIMENT 0
@@ -31,43 +30,6 @@ static std::atomic<uint64_t> g_launches{0};
 uint64_t launch_counter() { return g_launches.load(); }
 void add_launches(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 #define SAD_LAUNCHED() g_launches.fetch_add(1, std::memory_order_relaxed)
-
-// ---------------------------------------------------------------------- programmatic dependent launch
-// The per-iteration kernels (warm pass, fwd+bwd, Adam, bookkeeping) are launched with programmatic
-// stream serialisation, so the launch of each is prepared while its predecessor runs; every one waits
-// in griddepcontrol.wait before ANY global access (every RAW and WAR dependency on the predecessor is
-// respected).  Early triggers (launch_dependents at block start) let dependents occupy SMs during the
-// predecessor's last wave; measured on the config-2 fit that is neutral to +9 ms (the fwd+bwd -> Adam
-// edge), so by default no kernel triggers early and the gain is the launch latency (about 3 ms per
-// fit).  Without the attribute (or a programmatic predecessor) both instructions are no-ops.
-// SAD_NO_PDL=1 turns the attribute off (A/B).
-#ifndef SAD_PDL_TRIGGER
-#define SAD_PDL_TRIGGER 0  // bitmask of kernels that trigger early (1 prop, 2 bwd, 4 adam, 8 advance): measured no gain
-#endif
-template <int BIT>
-__device__ __forceinline__ void pdl_enter() {
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (SAD_PDL_TRIGGER & BIT) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-static const bool g_pdl = getenv("SAD_NO_PDL") == nullptr;
-template <typename... KP, typename... A>
-static void launch_pdl(void (*kern)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, A... args) {
-    if (!g_pdl) {
-        kern<<<grid, block, smem, stream>>>(args...);
-        return;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, kern, static_cast<KP>(args)...);
-}
 
 // ====================================================================== per-site tables
 // ScoreTable<T>::build (score_table.hpp:20-46), packed and unpacked, and GradTable<T>::build
@@ -145,19 +107,6 @@ void launch_tables(bool fp64, const SitesDev& s, const DevState* st, double scal
         k_tables<float><<<grid, 256, 0, stream>>>(s, st, scale, (Q4<float>*)pack, (Q4<float>*)gtab,
                                                   (Q4<float>*)rtab);
     SAD_LAUNCHED();
-}
-
-// Rows a kernel covers under the optional FieldDims row range (host and device).
-__host__ __device__ inline int rows_of(const FieldDims& f, int n) {
-    const int hi = f.row1 < n ? f.row1 : n;
-    return hi > f.row0 ? hi - f.row0 : 0;
-}
-
-// Candidate cell of pixel (px, py) (CandidateField::cell_x/cell_y, types.hpp:95-101); the fit's cell
-// size is 1, so the two integer divisions are skipped on that (launch-uniform) path.
-__device__ __forceinline__ size_t cell_index(const FieldDims& f, int px, int py) {
-    if (f.cell == 1) return static_cast<size_t>(py) * f.gw + px;
-    return static_cast<size_t>(py / f.cell) * f.gw + px / f.cell;
 }
 
 // ScoreTable<T>::logit (score_table.hpp:48-54), quadratic form, no contraction.
@@ -1281,16 +1230,6 @@ struct TileRed {  // TPX pixels, KM slots each, NT threads (TPX or 2 * TPX)
     DD warp_part[NT / 32];
 };
 
-template <typename CT>
-__device__ __forceinline__ bool c_finite(CT x);
-template <>
-__device__ __forceinline__ bool c_finite<float>(float x) {
-    return (__float_as_uint(x) & 0x7f800000u) != 0x7f800000u;
-}
-template <>
-__device__ __forceinline__ bool c_finite<double>(double x) {
-    return isfinite(x);
-}
 
 template <typename CT, int NCH, int TPX, int KM, int NT>
 __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM, NT>& sm, const RedTarget& red) {
