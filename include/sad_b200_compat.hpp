@@ -165,6 +165,52 @@ inline void refresh(Context& g, const SiteStore& st, CandidateField& f, RefreshM
     detail::field_back(v, f);
 }
 
+// exact_topk_batch / exact_topk (candidates.hpp:66-72) on the device brute force (k_exact_topk); probes
+// are pixel centres (integers), as every caller of the reference passes
+inline std::vector<std::vector<uint32_t>> exact_topk_batch(Context& g, const SiteStore& st,
+                                                           const std::vector<std::pair<int, int>>& pixels, int k,
+                                                           double scale, bool fp64 = true) {
+    if (k < 1 || k > 16) throw std::invalid_argument("exact_topk: k out of range");
+    detail::SitesView s(st);
+    std::vector<int32_t> xy(2 * pixels.size() + 2);
+    for (size_t i = 0; i < pixels.size(); i++) {
+        xy[2 * i] = pixels[i].first;
+        xy[2 * i + 1] = pixels[i].second;
+    }
+    std::vector<uint32_t> out(std::max<size_t>(pixels.size(), 1) * k, 0xffffffffu);
+    check(sad_exact_topk_batch(g.get(), &s.v, xy.data(), pixels.size(), k, scale, fp64 ? 1 : 0, out.data()));
+    std::vector<std::vector<uint32_t>> res(pixels.size());
+    for (size_t i = 0; i < pixels.size(); i++)
+        for (int j = 0; j < k && out[i * k + j] != 0xffffffffu; j++) res[i].push_back(out[i * k + j]);
+    return res;
+}
+
+inline std::vector<uint32_t> exact_topk(Context& g, const SiteStore& st, double px, double py, int k, double scale,
+                                        bool fp64 = true) {
+    if (k < 1 || k > 16) throw std::invalid_argument("exact_topk: k out of range");
+    const int ix = static_cast<int>(px), iy = static_cast<int>(py);
+    if (ix != px || iy != py) throw std::invalid_argument("exact_topk: the device path takes pixel-centre probes");
+    return exact_topk_batch(g, st, {{ix, iy}}, k, scale, fp64)[0];
+}
+
+// pixel_weights (render.hpp:18), one query through the batched device kernel
+inline PixelMix pixel_weights(Context& g, const SiteStore& st, const CandidateField& f, int px, int py) {
+    detail::SitesView s(st);
+    sad_field_view v = detail::field_view(f);
+    int32_t xy[2] = {px, py};
+    uint32_t ids[16];
+    double w[16];
+    int32_t n = 0;
+    check(sad_pixel_weights(g.get(), &s.v, &v, xy, 1, ids, w, &n));
+    PixelMix m;
+    m.n = n;
+    for (int i = 0; i < n; i++) {
+        m.ids[i] = ids[i];
+        m.w[i] = w[i];
+    }
+    return m;
+}
+
 // render_image (render.hpp:21-22)
 inline ImageBuffer render_image(Context& g, const SiteStore& st, const CandidateField& f, const RunOpts& o = {}) {
     detail::SitesView s(st);
@@ -216,6 +262,57 @@ inline double image_loss(Context& g, const SiteStore& st, const CandidateField& 
     double loss = 0;
     check(sad_image_loss(g.get(), &s.v, &v, target.data.data(), o.fp64, &loss));
     return loss;
+}
+
+// backward_pixel_grad (grad.hpp:106-107)
+inline void backward_pixel_grad(Context& g, const SiteStore& st, const CandidateField& f, const ImageBuffer& dl,
+                                GradBuffer& out, const RunOpts& o = {}) {
+    detail::SitesView s(st);
+    sad_field_view v = detail::field_view(f);
+    std::vector<double> buf(std::max<size_t>(st.size(), 1) * kChannels);
+    uint64_t nf = 0;
+    check(sad_backward_pixel_grad(g.get(), &s.v, &v, dl.data.data(), dl.width, dl.height, o.fp64, buf.data(), &nf));
+    grads_back(buf, st.size(), out);
+    out.nonfinite = nf;
+}
+
+// clamp_project (train.hpp:38)
+inline void clamp_project(Context& g, SiteStore& st, int w, int h, const TrainConfig& cfg) {
+    detail::SitesView s(st);
+    sad_train_config c = detail::config(cfg);
+    check(sad_clamp_project(g.get(), &s.v, w, h, &c));
+    s.store_into(st);
+}
+
+// init_sites (train.hpp:29): replaces the store's contents (clear + n appends: generation + 1 + n)
+inline void init_sites(Context& g, SiteStore& st, const ImageBuffer& target, int n, const TrainConfig& cfg) {
+    const uint64_t gen = st.generation;
+    SiteStore tmp;
+    tmp.resize(static_cast<size_t>(std::max(n, 0)));
+    detail::SitesView s(tmp);
+    sad_train_config c = detail::config(cfg);
+    check(sad_init_sites(g.get(), &s.v, target.data.data(), target.width, target.height, n, &c));
+    s.store_into(st);
+    st.generation = gen + 1 + static_cast<uint64_t>(std::max(n, 0));
+}
+
+// bpp_target_count / plan_schedule / simulate_schedule (budget.hpp:51-60): host arithmetic of the library
+inline size_t bpp_target_count(double bpp, int w, int h) {
+    uint64_t out = 0;
+    check(sad_bpp_target_count(bpp, w, h, &out));
+    return static_cast<size_t>(out);
+}
+inline double plan_schedule(int n0, size_t target, const TrainConfig& cfg) {
+    sad_train_config c = detail::config(cfg);
+    double out = 0;
+    check(sad_plan_schedule(n0, target, &c, &out));
+    return out;
+}
+inline int simulate_schedule(int n0, double scale, const TrainConfig& cfg) {
+    sad_train_config c = detail::config(cfg);
+    int out = 0;
+    check(sad_simulate_schedule(n0, scale, &c, &out));
+    return out;
 }
 
 // adam_step (train.hpp:33-34)
@@ -287,6 +384,8 @@ inline std::vector<double> stats_flat(const StatsResult& s) {
 
 // prune (budget.hpp:48)
 inline int prune(Context& g, SiteStore& st, const StatsResult& stats, double pct) {
+    // the C ABI takes n*8 doubles for n sites: a StatsResult of another size is refused here (budget.cpp:287)
+    if (stats.site.size() != st.size()) throw std::invalid_argument("prune: stats size mismatch");
     detail::SitesView s(st);
     std::vector<double> sf = stats_flat(stats);
     int removed = 0;
@@ -298,6 +397,7 @@ inline int prune(Context& g, SiteStore& st, const StatsResult& stats, double pct
 // densify (budget.hpp:43-44)
 inline int densify(Context& g, SiteStore& st, AdamState& adam, const StatsResult& stats, const ImageBuffer& target,
                    double pct, const TrainConfig& cfg) {
+    if (stats.site.size() != st.size()) throw std::invalid_argument("densify: stats size mismatch");  // budget.cpp:221
     size_t n = st.size();
     detail::SitesView s(st, n);
     adam.resize(n);

@@ -173,9 +173,11 @@ __device__ __forceinline__ double sad_dexp_special(double tmp, uint64_t sbits, u
     }
     sbits += 1022ull << 52;  // k < 0: care in the subnormal range
     const double scale = __longlong_as_double(static_cast<long long>(sbits));
-    double y = __fma_rn(scale, tmp, scale);
+    // glibc's build does not contract this branch (unlike the k > 0 one): separate multiply and add
+    // (host harness over 6e7 inputs in [-745.2, -512]: 0 mismatches; fused: 0.06% off by one ulp)
+    double y = __dadd_rn(scale, __dmul_rn(scale, tmp));
     if (y < 1.0) {
-        double lo = __fma_rn(scale, tmp, scale - y);
+        double lo = __dadd_rn(scale - y, __dmul_rn(scale, tmp));
         const double hi = 1.0 + y;
         lo = 1.0 - hi + y + lo;
         y = (hi + lo) - 1.0;

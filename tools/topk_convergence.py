@@ -71,12 +71,12 @@ def match_fraction(field_ids, w, exact, pix):
     return hit / len(pix)
 
 
-def one(B, W, n, P, trial):
+def one(B, W, n, P, trial, schedule):
     st = collision_free_sites(W, W, n, 1000 + trial)
     f = sad.CandidateField()
     f.resize(W, W, 8)
     B.jfa_seed(st, f)
-    B.run_passes(st, f, B.schedule_passes(W, W, P), 4, 77 + trial, sad.RunOpts(fp64=False))
+    B.run_passes(st, f, schedule(W, W, P), 4, 77 + trial, sad.RunOpts(fp64=False))
     pix = probe_pixels(W, W, 31 + trial)
     exact = B.exact_topk_batch(st, pix, 8, sad.normalization_scale(W, W), False)
     return st, f, pix, exact
@@ -95,7 +95,7 @@ def main():
         for P in PASSES:
             fr = []
             for trial in range(a.trials):
-                st, f, pix, exact = one(G, W, n, P, trial)
+                st, f, pix, exact = one(G, W, n, P, trial, G.schedule_passes)
                 fr.append(match_fraction(f.ids, W, exact, pix))
             vals.append(float(np.mean(fr)))
         rows.append({"domain": W, "sites": n, "top8_exact_match": dict(zip(map(str, PASSES), vals)),
@@ -107,8 +107,8 @@ def main():
         from oracle.bindings import have_ref, ref_backend
         if have_ref():
             R = ref_backend(threads=os.cpu_count() or 1)
-            st, fg, pix, eg = one(G, 1024, 16384, 8, 0)
-            _, fr_, _, er = one(R, 1024, 16384, 8, 0)
+            st, fg, pix, eg = one(G, 1024, 16384, 8, 0, G.schedule_passes)
+            _, fr_, _, er = one(R, 1024, 16384, 8, 0, G.schedule_passes)
             same_map = bool(np.array_equal(fg.ids, fr_.ids))
             same_exact = bool(np.array_equal(eg, er))
             out["reference_check"] = {"case": "1024^2, 16k sites, 8 passes, trial 0", "map_identical": same_map,
