@@ -259,21 +259,37 @@ sad_status sad_decode_render(sad_ctx* ctx, const uint8_t* buf, size_t n, int k, 
                              uint64_t seed, int fp64, double* out_rgb, sad_sites_view* out_sites);
 
 /* ---------------------------------------------------------------- row-strip multi-GPU fit (config 5)
- * One image split into row strips (multiples of 8 rows): each rank replicates sites and tables, computes
- * its strip of the propagation passes, backward and stats, and merges the exact per-rank partials in rank
- * order, so the result is bit-identical to the single-GPU fit.  One process per GPU: rank 0 calls
+ * One image split into row strips (multiples of the tile heights): each rank holds the sites and tables
+ * and computes its strip of the propagation passes, backward and stats.  Sites are owned by id slice
+ * (rank q: ids [q*slice, (q+1)*slice)): the partial totals of touched, non-owned sites travel to their
+ * owners, who merge them exactly and run Adam on their slice; the parameter slices are then all-gathered
+ * (events: stats totals too, and prune / densify run replicated).  Every merge is an exact double-double
+ * merge, so the result is bit-identical to the single-GPU fit.  One process per GPU: rank 0 calls
  * sad_nccl_unique_id and shares the 128 bytes (e.g. torch.distributed), every rank creates one
  * communicator (sad_strip_comm_create; NCCL ids are single-use), then per fit its run (sad_fit_create,
  * sad_fit_set_target with the whole image) and calls sad_fit_run_strips (init NULL:
  * fit(), else fit_store() from `init`).  Results are read with sad_fit_info / sad_fit_download on any rank.
  * sad_fit_run_strips_loopback runs `world` virtual ranks (runs created on one context) on one device,
- * exchanging by device copies: the single-GPU check of the partition. */
-typedef struct sad_strip_comm sad_strip_comm; /* an NCCL communicator over the strip ranks (reusable) */
+ * exchanging by device copies: the single-GPU check of the partition.
+ * sad_strip_comm_create_host builds a host-staged communicator: device data is copied to pinned host
+ * memory and moved by the caller's callbacks (return 0 on success) — e.g. a torch.distributed gloo group,
+ * which lets several processes share one GPU:
+ *   allgather(user, send, recv, bytes): recv[q*bytes, (q+1)*bytes) <- rank q's send;
+ *   exchange(user, n, peer, send, send_bytes, recv, recv_bytes): for each i, send send[i] to peer[i] and
+ *     receive recv[i] from it; transfers to one peer pair up in order, zero-byte entries are skipped.
+ * sad_fit_strip_exchange reports the gradient records this rank sent to owners during the last fit. */
+typedef struct sad_strip_comm sad_strip_comm; /* a communicator over the strip ranks (reusable) */
+typedef int (*sad_host_allgather_fn)(void* user, const void* send, void* recv, size_t bytes);
+typedef int (*sad_host_exchange_fn)(void* user, int n, const int* peer, const void* const* send,
+                                    const size_t* send_bytes, void* const* recv, const size_t* recv_bytes);
 sad_status sad_nccl_unique_id(uint8_t* out128);
 sad_status sad_strip_comm_create(int rank, int world, const uint8_t* nccl_id128, sad_strip_comm** out);
+sad_status sad_strip_comm_create_host(int rank, int world, sad_host_allgather_fn allgather,
+                                      sad_host_exchange_fn exchange, void* user, sad_strip_comm** out);
 void sad_strip_comm_destroy(sad_strip_comm* comm);
 sad_status sad_fit_run_strips(sad_fit_run* run, sad_strip_comm* comm, const sad_sites_view* init);
 sad_status sad_fit_run_strips_loopback(sad_fit_run* const* runs, int world);
+sad_status sad_fit_strip_exchange(sad_fit_run* run, long long* records_sent);
 
 /* ---------------------------------------------------------------- fit / fit_store in one call
  * fit (train.hpp:62-63, train.cpp:295-311) and fit_store (train.hpp:66-68): target upload, the whole

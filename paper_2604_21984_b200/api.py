@@ -462,7 +462,14 @@ class Backend:
                 self._call("fit_set_target", run, _ptr(target.data))
             arr = (C.c_void_p * world)(*[r.value for r in runs])
             self._call("fit_run_strips_loopback", arr, C.c_int(world))
-            return [self._collect_run(r, w, h, cfg) for r in runs]
+            out = []
+            for r in runs:
+                res = self._collect_run(r, w, h, cfg)
+                sent = C.c_longlong()
+                self._call("fit_strip_exchange", r, C.byref(sent))
+                res.timing["records_sent"] = sent.value
+                out.append(res)
+            return out
         finally:
             for r in runs:
                 self.lib.sad_fit_destroy(r)
@@ -485,10 +492,20 @@ class Backend:
             sv = None
             if init is not None:
                 sv, keep = init._view()
-            self._call("fit_run_strips", run, comm, _ref(sv))
-            return self._collect_run(run, w, h, cfg)
+            self._call("fit_run_strips", run, getattr(comm, "handle", comm), _ref(sv))
+            res = self._collect_run(run, w, h, cfg)
+            sent = C.c_longlong()
+            self._call("fit_strip_exchange", run, C.byref(sent))
+            res.timing["records_sent"] = sent.value
+            return res
         finally:
             self.lib.sad_fit_destroy(run)
+
+    def strip_comm_host(self, group=None) -> "HostStripComm":
+        """A host-staged strip communicator over a torch.distributed process group (e.g. gloo): the
+        library copies device data to pinned host memory and calls back into Python for each collective,
+        so several processes can share one GPU (tests) or GPUs without NCCL can take part."""
+        return HostStripComm(self, group)
 
     def nccl_unique_id(self) -> bytes:
         buf = (C.c_uint8 * 128)()
@@ -584,10 +601,78 @@ class Backend:
         return FitResult(st, f, rows, sc)
 
 
+_AG_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
+_EX_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_void_p), C.POINTER(C.c_size_t),
+                     C.POINTER(C.c_void_p), C.POINTER(C.c_size_t))
+
+
+class HostStripComm:
+    """sad_strip_comm_create_host over a torch.distributed group: all-gather and grouped point-to-point
+    transfers of host byte buffers (include/sad_b200.h).  Pass `.handle` to Backend.fit_strips."""
+
+    def __init__(self, backend: "Backend", group=None):
+        import torch
+        import torch.distributed as dist
+        self._B = backend
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        world = self.world
+
+        def _host(ptr, n):
+            return torch.frombuffer((C.c_uint8 * n).from_address(ptr), dtype=torch.uint8).clone()
+
+        def allgather(user, send, recv, nbytes):
+            try:
+                mine = _host(send, nbytes) if nbytes else torch.empty(0, dtype=torch.uint8)
+                outs = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
+                dist.all_gather(outs, mine, group=group)
+                for q, t in enumerate(outs):
+                    if nbytes:
+                        C.memmove(recv + q * nbytes, t.data_ptr(), nbytes)
+                return 0
+            except Exception:  # noqa: BLE001 - reported to the library as a failed collective
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        def exchange(user, n, peer, send, sbytes, recv, rbytes):
+            try:
+                reqs, outs = [], []
+                for i in range(n):
+                    if sbytes[i]:
+                        t = _host(send[i], sbytes[i])
+                        reqs.append((dist.isend(t, int(peer[i]), group=group), t))
+                    if rbytes[i]:
+                        t = torch.empty(rbytes[i], dtype=torch.uint8)
+                        reqs.append((dist.irecv(t, int(peer[i]), group=group), t))
+                        outs.append((recv[i], t))
+                for r, _ in reqs:
+                    r.wait()
+                for ptr, t in outs:
+                    C.memmove(ptr, t.data_ptr(), t.numel())
+                return 0
+            except Exception:  # noqa: BLE001
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        self._ag = _AG_FN(allgather)
+        self._ex = _EX_FN(exchange)
+        self.handle = C.c_void_p()
+        backend._call("strip_comm_create_host", C.c_int(self.rank), C.c_int(world), self._ag, self._ex, None,
+                      C.byref(self.handle))
+
+    def close(self):
+        if self.handle:
+            self._B.lib.sad_strip_comm_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+
 _NO_CTX = {"jump_step", "full_refresh_passes", "schedule_passes", "bpp_target_count", "simulate_schedule",
            "plan_schedule", "fit_set_target", "fit_set_target_device", "fit_run_init", "fit_run_store",
            "fit_info", "fit_download", "fit_render_device", "fit_timing", "fit_bench", "fit_set_profiling",
-           "fit_point_query", "fit_capacity", "fit_run_strips", "fit_run_strips_loopback", "nccl_unique_id", "strip_comm_create", "encode", "decode", "decode_header", "bpp",
+           "fit_point_query", "fit_capacity", "fit_run_strips", "fit_run_strips_loopback", "nccl_unique_id", "strip_comm_create",
+           "strip_comm_create_host", "fit_strip_exchange", "encode", "decode", "decode_header", "bpp",
            "last_error"}
 
 # ---------------------------------------------------------------------- product binding
@@ -606,6 +691,7 @@ def load_library(path: Optional[str] = None) -> C.CDLL:
     lib.sad_ctx_launch_count.restype = C.c_uint64
     lib.sad_ctx_launch_count.argtypes = [_P]
     lib.sad_fit_destroy.argtypes = [_P]
+    lib.sad_strip_comm_destroy.argtypes = [_P]
     lib.sad_ctx_destroy.argtypes = [_P]
     return lib
 

@@ -2841,13 +2841,155 @@ void launch_merge_partials(const double2* parts, int world, int cap, int nch, do
     SAD_LAUNCHED();
 }
 
+// ---------------------------------------------------------------------- owner-merged row-strip exchange
+// Site ownership by id slice: rank q owns ids [q * slice, (q + 1) * slice).  Each rank sends the partial
+// totals of the sites it touched (cnt > 0) that another rank owns, as (id, nch double-doubles) records
+// grouped by owner; the owner merges them exactly into its own partials (128-bit CAS: several sources may
+// add to one site).  The reduction state of every touched site is reset for the next pass here, and (for
+// gradients) the next pass's record capacities are planned from this rank's counts, as k_adam does.
+__global__ void k_owner_pack(const double2* __restrict__ part, int nch, RedTarget red, const DevState* __restrict__ st,
+                             const uint8_t* __restrict__ active, int slice, int me, int world, OwnRec* __restrict__ send,
+                             int send_cap, unsigned long long* __restrict__ counts, int32_t* __restrict__ rcap_next,
+                             int reset) {
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= st->n_sites) return;
+    const int cl = red.cnt[id];
+    if (rcap_next) {
+        int want = active[id] ? cl + (cl >> 2) + 2 : 0;
+        rcap_next[id] = want < 4096 ? want : 4096;
+    }
+    // touched: records claimed this pass (gradients), or (finalized stats, whose counts are already
+    // reset) any non-zero partial — an all-zero partial adds nothing to the owner's total
+    bool touched = cl > 0;
+    if (!rcap_next && !touched)
+        for (int c = 0; c < nch && !touched; c++) {
+            const double2 v = part[static_cast<size_t>(c) * red.cap + id];
+            touched = v.x != 0.0 || v.y != 0.0;
+        }
+    if (touched) {
+        const int q = id / slice;
+        if (q != me && q < world) {
+            const int pos = static_cast<int>(atomicAdd(counts + q, 1ull));
+            if (pos < send_cap) {
+                OwnRec& r = send[static_cast<size_t>(q) * send_cap + pos];
+                r.id = static_cast<uint32_t>(id);
+                for (int c = 0; c < nch; c++) r.v[c] = part[static_cast<size_t>(c) * red.cap + id];
+            }
+        }
+    }
+    if (reset) {
+        for (int c = 0; c < red.stride; c++) red.over[static_cast<size_t>(c) * red.cap + id] = make_double2(0.0, 0.0);
+        red.cnt[id] = 0;
+        red.head[id] = -1;
+    }
+}
+
+void launch_owner_pack(const double2* part, int nch, const RedTarget& red, const DevState* st, const uint8_t* active,
+                       int slice, int me, int world, OwnRec* send, int send_cap, unsigned long long* counts,
+                       int32_t* rcap_next, bool reset, cudaStream_t stream) {
+    const int grid = (red.cap + 255) / 256;
+    k_owner_pack<<<grid ? grid : 1, 256, 0, stream>>>(part, nch, red, st, active, slice, me, world, send, send_cap, counts,
+                                                      rcap_next, reset ? 1 : 0);
+    SAD_LAUNCHED();
+}
+
+__global__ void k_owner_merge(const OwnRec* __restrict__ recv, long long n, int nch, int cap, double2* __restrict__ part) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= n * nch) return;
+    const long long r = i / nch;
+    const int c = static_cast<int>(i - r * nch);
+    const OwnRec& rec = recv[r];
+    const double2 v = rec.v[c];
+    if (v.x != 0.0 || v.y != 0.0) dd_atomic_merge(part + static_cast<size_t>(c) * cap + rec.id, DD{v.x, v.y});
+}
+
+void launch_owner_merge(const OwnRec* recv, long long n, int nch, int cap, double2* part, cudaStream_t stream) {
+    if (n <= 0) return;
+    const long long items = n * nch;
+    k_owner_merge<<<static_cast<unsigned>((items + 255) / 256), 256, 0, stream>>>(recv, n, nch, cap, part);
+    SAD_LAUNCHED();
+}
+
+// Slice staging for the all-gathers: buf[c][i] = src[c][lo + i] (i < slice; zero past cap) and the inverse
+// over every rank's slice of the gathered buffer.
+template <typename T>
+__global__ void k_slice_pack(const T* __restrict__ src, int nch, int cap, int lo, int slice, T* __restrict__ buf) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= static_cast<long long>(nch) * slice) return;
+    const int c = static_cast<int>(i / slice), j = static_cast<int>(i - static_cast<long long>(c) * slice);
+    buf[i] = lo + j < cap ? src[static_cast<size_t>(c) * cap + lo + j] : T{};
+}
+
+template <typename T>
+__global__ void k_slice_unpack(const T* __restrict__ all, int nch, int cap, int slice, int world, T* __restrict__ dst) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    const long long per = static_cast<long long>(nch) * slice;
+    if (i >= per * world) return;
+    const int q = static_cast<int>(i / per);
+    const long long rem = i - q * per;
+    const int c = static_cast<int>(rem / slice), j = static_cast<int>(rem - static_cast<long long>(c) * slice);
+    const int id = q * slice + j;
+    if (id < cap) dst[static_cast<size_t>(c) * cap + id] = all[i];
+}
+
+template <typename T>
+void launch_slice_pack(const T* src, int nch, int cap, int lo, int slice, T* buf, cudaStream_t stream) {
+    const long long n = static_cast<long long>(nch) * slice;
+    k_slice_pack<T><<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(src, nch, cap, lo, slice, buf);
+    SAD_LAUNCHED();
+}
+template <typename T>
+void launch_slice_unpack(const T* all, int nch, int cap, int slice, int world, T* dst, cudaStream_t stream) {
+    const long long n = static_cast<long long>(nch) * slice * world;
+    k_slice_unpack<T><<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(all, nch, cap, slice, world, dst);
+    SAD_LAUNCHED();
+}
+template void launch_slice_pack<double>(const double*, int, int, int, int, double*, cudaStream_t);
+template void launch_slice_pack<double2>(const double2*, int, int, int, int, double2*, cudaStream_t);
+template void launch_slice_unpack<double>(const double*, int, int, int, int, double*, cudaStream_t);
+template void launch_slice_unpack<double2>(const double2*, int, int, int, int, double2*, cudaStream_t);
+
+// The owned range [a0, a1) of the ascending active list (ids in [lo, hi)) and the owned totals' values.
+__global__ void k_owned_range(const uint32_t* __restrict__ act, const DevState* __restrict__ st, int lo, int hi,
+                              int32_t* __restrict__ range) {
+    const int n = st->n_active;
+    auto lower = [&](int v) {
+        int a = 0, b = n;
+        while (a < b) {
+            const int mid = (a + b) >> 1;
+            if (static_cast<int>(act[mid]) < v) a = mid + 1;
+            else b = mid;
+        }
+        return a;
+    };
+    range[0] = lower(lo);
+    range[1] = lower(hi);
+}
+
+void launch_owned_range(const uint32_t* act, const DevState* st, int lo, int hi, int32_t* range, cudaStream_t stream) {
+    k_owned_range<<<1, 1, 0, stream>>>(act, st, lo, hi, range);
+    SAD_LAUNCHED();
+}
+
+__global__ void k_dd_values(const double2* __restrict__ dd, long long n, double* __restrict__ out) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i < n) out[i] = dd[i].x + dd[i].y;
+}
+
+void launch_dd_values(const double2* dd, long long n, double* out, cudaStream_t stream) {
+    if (n <= 0) return;
+    k_dd_values<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(dd, n, out);
+    SAD_LAUNCHED();
+}
+
 template <typename T>
 __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarget grads, double* __restrict__ m,
                                               double* __restrict__ v, AdamHyper hp,
                                               const double2* __restrict__ bc_table, double2 bc_now, int zero_grads,
                                               double scale, Q4<T>* pack, Q4<T>* gtab, int32_t* rcap_next,
                                               const double* __restrict__ totals, int32_t* roff_next,
-                                              int32_t* pool_top, const uint32_t* __restrict__ act) {
+                                              int32_t* pool_top, const uint32_t* __restrict__ act,
+                                              const int32_t* __restrict__ act_range) {
     pdl_enter<4>();
     __shared__ int32_t s_want[8], s_base;
     const int lane16 = threadIdx.x & 15;
@@ -2858,9 +3000,12 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
     // records, no update and keep their tables, so skipping them is exact
     // active-list mode: blocks whose 8 groups all lie past the active count have nothing to do (the grid
     // is sized by the capacity because it is captured in a CUDA graph); block-uniform, before any barrier
-    if (act && static_cast<int>(blockIdx.x) * 8 >= st->n_active) return;
-    const bool live = act ? grp < st->n_active : grp < st->n_sites;
-    const int id = act ? (live ? static_cast<int>(act[grp]) : cap) : grp;
+    // act_range (row-strip fits): only the owned slice act[a0, a1) of the active list
+    const int a0 = act_range ? act_range[0] : 0;
+    const int n_act = act_range ? act_range[1] - act_range[0] : (act ? st->n_active : 0);
+    if (act && static_cast<int>(blockIdx.x) * 8 >= n_act) return;
+    const bool live = act ? grp < n_act : grp < st->n_sites;
+    const int id = act ? (live ? static_cast<int>(act[a0 + grp]) : cap) : grp;
     const int k = lane16;
     unsigned long long skipped = 0;
     const int kc = lane_channel(lane16);  // the parameter this lane updates (-1: none)
@@ -2999,17 +3144,17 @@ __global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarge
 void launch_adam(bool fp64, const SitesDev& s, DevState* st, const RedTarget& grads, double* m, double* v,
                  const AdamHyper& hp, const double2* bc_table, double2 bc_now, bool zero_grads, double scale,
                  void* pack, void* gtab, int32_t* rcap_next, cudaStream_t stream, const double* totals,
-                 int32_t* roff_next, int32_t* pool_top, const uint32_t* act) {
+                 int32_t* roff_next, int32_t* pool_top, const uint32_t* act, const int32_t* act_range) {
     int grid = (s.cap + 7) / 8;  // 8 sites (16 lanes each) per 128-thread block
     if (grid < 1) grid = 1;
     if (fp64)
         launch_pdl(k_adam<double>, dim3(grid), dim3(128), 0, stream, s, st, grads, m, v, hp, bc_table, bc_now,
                    zero_grads ? 1 : 0, scale, (Q4<double>*)pack, (Q4<double>*)gtab, rcap_next, totals, roff_next, pool_top,
-                   act);
+                   act, act_range);
     else
         launch_pdl(k_adam<float>, dim3(grid), dim3(128), 0, stream, s, st, grads, m, v, hp, bc_table, bc_now,
                    zero_grads ? 1 : 0, scale, (Q4<float>*)pack, (Q4<float>*)gtab, rcap_next, totals, roff_next, pool_top,
-                   act);
+                   act, act_range);
     SAD_LAUNCHED();
 }
 

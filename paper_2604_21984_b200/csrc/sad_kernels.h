@@ -136,12 +136,28 @@ void launch_finalize(const RedTarget& red, int n_ch, const DevState* st, cudaStr
 void launch_adam(bool fp64, const SitesDev& s, DevState* st, const RedTarget& grads, double* m, double* v,
                  const AdamHyper& hp, const double2* bc_table, double2 bc_now, bool zero_grads, double scale,
                  void* pack, void* gtab, int32_t* rcap_next, cudaStream_t stream, const double* totals = nullptr,
-                 int32_t* roff_next = nullptr, int32_t* pool_top = nullptr, const uint32_t* act = nullptr);
+                 int32_t* roff_next = nullptr, int32_t* pool_top = nullptr, const uint32_t* act = nullptr,
+                 const int32_t* act_range = nullptr);
 void launch_math(const double* x, double* y, size_t n, int which, cudaStream_t stream);
 // row-strip fits (multi-GPU config 5)
 void launch_site_partials(const RedTarget& grads, const DevState* st, int cap, double2* out, cudaStream_t stream);
 void launch_merge_partials(const double2* parts, int world, int cap, int nch, double* values, double2* dd,
                            cudaStream_t stream);
+// owner-merged exchange of the row-strip fit: ids [q*slice, (q+1)*slice) belong to rank q
+struct OwnRec {
+    uint32_t id, pad[3];
+    double2 v[11];
+};
+void launch_owner_pack(const double2* part, int nch, const RedTarget& red, const DevState* st, const uint8_t* active,
+                       int slice, int me, int world, OwnRec* send, int send_cap, unsigned long long* counts,
+                       int32_t* rcap_next, bool reset, cudaStream_t stream);
+void launch_owner_merge(const OwnRec* recv, long long n, int nch, int cap, double2* part, cudaStream_t stream);
+template <typename T>
+void launch_slice_pack(const T* src, int nch, int cap, int lo, int slice, T* buf, cudaStream_t stream);
+template <typename T>
+void launch_slice_unpack(const T* all, int nch, int cap, int slice, int world, T* dst, cudaStream_t stream);
+void launch_owned_range(const uint32_t* act, const DevState* st, int lo, int hi, int32_t* range, cudaStream_t stream);
+void launch_dd_values(const double2* dd, long long n, double* out, cudaStream_t stream);
 // tau_diffusion pieces (train.cpp:171-213)
 void launch_site_totals(const RedTarget& grads, const DevState* st, int cap, double* tot, double* g0,
                         cudaStream_t stream);

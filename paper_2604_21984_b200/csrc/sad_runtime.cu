@@ -937,9 +937,17 @@ struct sad_fit_run {
     // (world + 1 bounds), and the buffers of the exact cross-rank merges
     int rank = 0, world = 1;
     std::vector<int> strip;
-    DBuf<double2> gpart_self, gpart_all, spart_all, loss_self, loss_all;
+    DBuf<double2> gpart_self, loss_self, loss_all;
     DBuf<double> tot;
     DBuf<unsigned long long> valid_all;
+    // owner-merged exchange: per-destination record counts (and the gathered R x R matrix), send /
+    // receive records, the owned range of the active list, parameter / stats slice staging
+    DBuf<unsigned long long> own_counts, own_matrix;
+    DBuf<sadk::OwnRec> own_send, own_recv;
+    DBuf<int32_t> own_range;
+    DBuf<double> slice_p, slice_all_p;
+    DBuf<double2> slice_s, slice_all_s;
+    long long xfer_records = 0;  // gradient records this rank sent to owners over the fit
     ~sad_fit_run() {
         drop_graphs();
     }
@@ -1946,18 +1954,39 @@ static void fit_loop(sad_fit_run* r) {
 }
 
 // ====================================================================== row-strip multi-GPU fit (config 5)
-// one large image split into row strips.  Every rank replicates the sites, tables, target
-// and the whole candidate field, but computes only its strip: propagation rows, backward and stats
-// tiles (FieldDims row range; strips are multiples of the 8-row tiles).  Exchanges per step:
-//   * before every propagation pass at jump s: the rows within s of the strip (owner -> reader);
-//     at the end, all strips (owner broadcasts), so every rank holds the whole final field;
-//   * after the backward: every rank's per-site double-double partial totals (10 channels) and its loss
-//     partial, merged in rank order by every rank (exact double-double: equals the single-GPU totals);
-//   * at events: the per-site stats partials (8 channels) and the valid-pixel counts, same merge.
-// Adam, prune, densify, seeding and the tables then run replicated and deterministically, so all ranks
-// hold the same state and the fit is bit-identical to the single-GPU fit.  The transport is NCCL (one
-// process per GPU; loaded with dlopen, no link-time dependency) or a loopback of R virtual ranks on one
-// device (the correctness test of the partition on a single GPU).
+// one large image split into row strips.  Every rank holds the sites, the tables, the target
+// and the whole candidate field, but computes only its strip: propagation rows, backward and stats tiles
+// (FieldDims row range; strips are multiples of the tile heights).  Sites are OWNED by id slice: rank q
+// owns ids [q*slice, (q+1)*slice), slice = ceil(cap / R); init_sites numbers sites in raster order, so
+// slices start out as row bands close to the strips.  Exchanges per iteration:
+//   * before every propagation pass at jump s: the rows within s of the strip (owner -> reader); at the
+//     end, all strips, so every rank holds the whole final field;
+//   * after the backward (owner merge): each rank's double-double partial totals of the sites it touched
+//     but does not own travel to their owners as (id, 10 double-doubles) records (counts first: one R x R
+//     all-gather and one host read, then grouped point-to-point), and the owner merges them exactly;
+//   * Adam runs on the owned slice only (moments live with the owner), then the updated parameters of
+//     every slice are all-gathered (10 doubles per site) and each rank rebuilds its tables;
+//   * at events: stats partials take the same owner merge, then the owned stats totals are all-gathered
+//     (8 double-doubles per site) so prune / densify (and the seeding) run replicated and deterministically.
+// Every sum is an exact double-double merge, so the strip fit is bit-identical to the single-GPU fit.
+// Transports: NCCL (one process per GPU; loaded with dlopen), a loopback of R virtual ranks on one device,
+// and a host-staged transport whose collectives are callbacks (the Python binding runs them over a
+// torch.distributed process group, e.g. gloo: two processes can share one GPU).
+struct XferPlan {  // one local rank's point-to-point exchange: peer i gets send[i], we get recv[i] from it
+    std::vector<int> peer;
+    std::vector<const void*> send;
+    std::vector<size_t> sbytes;
+    std::vector<void*> recv;
+    std::vector<size_t> rbytes;
+    void add(int q, const void* s, size_t sb, void* r, size_t rb) {
+        peer.push_back(q);
+        send.push_back(s);
+        sbytes.push_back(sb);
+        recv.push_back(r);
+        rbytes.push_back(rb);
+    }
+};
+
 struct StripComm {
     virtual ~StripComm() = default;
     virtual int world() const = 0;
@@ -1969,12 +1998,18 @@ struct StripComm {
     // slice q (bytes each) of every rank's `all` <- rank q's `self`
     virtual void gather(std::vector<sad_fit_run*>& runs, const std::function<const void*(sad_fit_run*)>& self,
                         const std::function<void*(sad_fit_run*)>& all, size_t bytes) = 0;
+    // grouped point-to-point transfers, plans[i] for runs[i] (device pointers; sizes agree pairwise)
+    virtual void exchange(std::vector<sad_fit_run*>& runs, std::vector<XferPlan>& plans) = 0;
 };
 
 // Rows rank `r` reads outside its strip at jump `step` that rank `q` owns: up to two [lo, hi) ranges.
+// A pass at jump s reads rows y - s, y, y + s for the strip's rows y: the bands [row0 - s, row1 - s) and
+// [row0 + s, row1 + s) outside the strip (for s >= the strip height, a strip-sized band, not s rows).
 static int halo_ranges(const std::vector<int>& strip, int r, int q, int step, int out[4]) {
     const int rows = strip.back();
-    const int need[2][2] = {{std::max(0, strip[r] - step), strip[r]}, {strip[r + 1], std::min(rows, strip[r + 1] + step)}};
+    const int r0 = strip[r], r1 = strip[r + 1];
+    const int need[2][2] = {{std::max(0, r0 - step), std::min(r0, r1 - step)},
+                            {std::max(r1, r0 + step), std::min(rows, r1 + step)}};
     int n = 0;
     for (const auto& nd : need) {
         const int lo = std::max(nd[0], strip[q]), hi = std::min(nd[1], strip[q + 1]);
@@ -1987,34 +2022,56 @@ static int halo_ranges(const std::vector<int>& strip, int r, int q, int step, in
     return n;
 }
 
+// The rows rank `r` must receive from rank `q` (and, symmetrically, send) for a halo at jump `step`.
+static void halo_plan(std::vector<sad_fit_run*>& runs, int b, int step, std::vector<XferPlan>& plans, int world) {
+    const size_t row = static_cast<size_t>(runs[0]->ws.fd.gw) * runs[0]->ws.fd.k;
+    plans.assign(runs.size(), XferPlan{});
+    for (size_t i = 0; i < runs.size(); i++) {
+        sad_fit_run* r = runs[i];
+        const int me = r->rank;
+        for (int q = 0; q < world; q++) {
+            if (q == me) continue;
+            int sr[4], rr[4];
+            const int ms = halo_ranges(r->strip, q, me, step, sr);  // rows q needs that I own
+            const int mr = halo_ranges(r->strip, me, q, step, rr);  // rows I need that q owns
+            for (int j = 0; j < std::max(ms, mr); j++) {
+                const uint32_t* sp = j < ms ? r->ws.ids[b].p + row * sr[2 * j] : nullptr;
+                uint32_t* rp = j < mr ? r->ws.ids[b].p + row * rr[2 * j] : nullptr;
+                plans[i].add(q, sp, j < ms ? 4 * row * (sr[2 * j + 1] - sr[2 * j]) : 0, rp,
+                             j < mr ? 4 * row * (rr[2 * j + 1] - rr[2 * j]) : 0);
+            }
+        }
+    }
+}
+
+// Every rank's strip to every other rank.
+static void rows_plan(std::vector<sad_fit_run*>& runs, int b, std::vector<XferPlan>& plans, int world) {
+    const size_t row = static_cast<size_t>(runs[0]->ws.fd.gw) * runs[0]->ws.fd.k;
+    plans.assign(runs.size(), XferPlan{});
+    for (size_t i = 0; i < runs.size(); i++) {
+        sad_fit_run* r = runs[i];
+        const int me = r->rank;
+        for (int q = 0; q < world; q++) {
+            if (q == me) continue;
+            plans[i].add(q, r->ws.ids[b].p + row * r->strip[me], 4 * row * (r->strip[me + 1] - r->strip[me]),
+                         r->ws.ids[b].p + row * r->strip[q], 4 * row * (r->strip[q + 1] - r->strip[q]));
+        }
+    }
+}
+
 struct LoopbackComm : StripComm {
     int n;
     explicit LoopbackComm(int world) : n(world) {}
     int world() const override { return n; }
     void gather_rows(std::vector<sad_fit_run*>& runs, int b) override {
-        const size_t row = static_cast<size_t>(runs[0]->ws.fd.gw) * runs[0]->ws.fd.k;
-        for (int q = 0; q < n; q++) {
-            const size_t off = row * runs[q]->strip[q], cnt = row * (runs[q]->strip[q + 1] - runs[q]->strip[q]);
-            for (int r = 0; r < n; r++)
-                if (r != q && cnt)
-                    ck(cudaMemcpyAsync(runs[r]->ws.ids[b].p + off, runs[q]->ws.ids[b].p + off, 4 * cnt,
-                                       cudaMemcpyDeviceToDevice, runs[r]->ws.stream),
-                       "loopback rows");
-        }
+        std::vector<XferPlan> plans;
+        rows_plan(runs, b, plans, n);
+        exchange(runs, plans);
     }
     void halo_rows(std::vector<sad_fit_run*>& runs, int b, int step) override {
-        const size_t row = static_cast<size_t>(runs[0]->ws.fd.gw) * runs[0]->ws.fd.k;
-        const std::vector<int>& strip = runs[0]->strip;
-        for (int r = 0; r < n; r++)
-            for (int q = 0; q < n; q++) {
-                if (q == r) continue;
-                int rg[4];
-                const int m = halo_ranges(strip, r, q, step, rg);
-                for (int j = 0; j < m; j++)
-                    ck(cudaMemcpyAsync(runs[r]->ws.ids[b].p + row * rg[2 * j], runs[q]->ws.ids[b].p + row * rg[2 * j],
-                                       4 * row * (rg[2 * j + 1] - rg[2 * j]), cudaMemcpyDeviceToDevice, runs[r]->ws.stream),
-                       "loopback halo");
-            }
+        std::vector<XferPlan> plans;
+        halo_plan(runs, b, step, plans, n);
+        exchange(runs, plans);
     }
     void gather(std::vector<sad_fit_run*>& runs, const std::function<const void*(sad_fit_run*)>& self,
                 const std::function<void*(sad_fit_run*)>& all, size_t bytes) override {
@@ -2023,6 +2080,26 @@ struct LoopbackComm : StripComm {
                 ck(cudaMemcpyAsync(static_cast<char*>(all(runs[r])) + bytes * q, self(runs[q]), bytes,
                                    cudaMemcpyDeviceToDevice, runs[r]->ws.stream),
                    "loopback gather");
+    }
+    void exchange(std::vector<sad_fit_run*>& runs, std::vector<XferPlan>& plans) override {
+        // every local rank holds both ends: the j-th non-empty send of r to q pairs with the j-th non-empty
+        // receive of q from r (the order NCCL and the host transport pair them in)
+        for (int r = 0; r < n; r++)
+            for (int q = 0; q < n; q++) {
+                if (q == r) continue;
+                std::vector<size_t> si, ri;
+                for (size_t i = 0; i < plans[r].peer.size(); i++)
+                    if (plans[r].peer[i] == q && plans[r].sbytes[i]) si.push_back(i);
+                for (size_t i = 0; i < plans[q].peer.size(); i++)
+                    if (plans[q].peer[i] == r && plans[q].rbytes[i]) ri.push_back(i);
+                if (si.size() != ri.size()) fail(SAD_ECUDA, "strips loopback: unmatched transfers");
+                for (size_t j = 0; j < si.size(); j++) {
+                    if (plans[r].sbytes[si[j]] != plans[q].rbytes[ri[j]]) fail(SAD_ECUDA, "strips loopback: size mismatch");
+                    ck(cudaMemcpyAsync(plans[q].recv[ri[j]], plans[r].send[si[j]], plans[r].sbytes[si[j]],
+                                       cudaMemcpyDeviceToDevice, runs[q]->ws.stream),
+                       "loopback exchange");
+                }
+            }
     }
 };
 
@@ -2092,30 +2169,104 @@ struct NcclComm : StripComm {
         api.check(api.groupEnd(), "ncclGroupEnd");
     }
     void halo_rows(std::vector<sad_fit_run*>& runs, int b, int step) override {
-        sad_fit_run* r = runs[0];
-        const size_t row = static_cast<size_t>(r->ws.fd.gw) * r->ws.fd.k;
-        const int me = r->rank;
-        api.check(api.groupStart(), "ncclGroupStart");
-        for (int q = 0; q < n; q++) {
-            if (q == me) continue;
-            int rg[4];
-            int m = halo_ranges(r->strip, q, me, step, rg);  // rows q needs that I own: send
-            for (int j = 0; j < m; j++)
-                api.check(api.send(r->ws.ids[b].p + row * rg[2 * j], row * (rg[2 * j + 1] - rg[2 * j]), ncclUint32, q,
-                                   comm, r->ws.stream),
-                          "ncclSend");
-            m = halo_ranges(r->strip, me, q, step, rg);  // rows I need that q owns: receive
-            for (int j = 0; j < m; j++)
-                api.check(api.recv(r->ws.ids[b].p + row * rg[2 * j], row * (rg[2 * j + 1] - rg[2 * j]), ncclUint32, q,
-                                   comm, r->ws.stream),
-                          "ncclRecv");
-        }
-        api.check(api.groupEnd(), "ncclGroupEnd");
+        std::vector<XferPlan> plans;
+        halo_plan(runs, b, step, plans, n);
+        exchange(runs, plans);
     }
     void gather(std::vector<sad_fit_run*>& runs, const std::function<const void*(sad_fit_run*)>& self,
                 const std::function<void*(sad_fit_run*)>& all, size_t bytes) override {
         sad_fit_run* r = runs[0];
         api.check(api.allGather(self(r), all(r), bytes, ncclChar, comm, r->ws.stream), "ncclAllGather");
+    }
+    void exchange(std::vector<sad_fit_run*>& runs, std::vector<XferPlan>& plans) override {
+        sad_fit_run* r = runs[0];
+        const XferPlan& pl = plans[0];
+        api.check(api.groupStart(), "ncclGroupStart");
+        for (size_t i = 0; i < pl.peer.size(); i++) {
+            if (pl.sbytes[i])
+                api.check(api.send(pl.send[i], pl.sbytes[i], ncclChar, pl.peer[i], comm, r->ws.stream), "ncclSend");
+            if (pl.rbytes[i])
+                api.check(api.recv(pl.recv[i], pl.rbytes[i], ncclChar, pl.peer[i], comm, r->ws.stream), "ncclRecv");
+        }
+        api.check(api.groupEnd(), "ncclGroupEnd");
+    }
+};
+
+// Host-staged transport: device data goes through pinned host buffers and the caller's collective
+// callbacks (sad_host_allgather_fn / sad_host_exchange_fn, include/sad_b200.h).
+struct HostComm : StripComm {
+    int n, me;
+    sad_host_allgather_fn ag;
+    sad_host_exchange_fn ex;
+    void* user;
+    std::vector<char*> pin;
+    std::vector<size_t> pin_n;
+    HostComm(int rank, int world, sad_host_allgather_fn a, sad_host_exchange_fn e, void* u)
+        : n(world), me(rank), ag(a), ex(e), user(u), pin(8, nullptr), pin_n(8, 0) {}
+    ~HostComm() override {
+        for (char* p : pin)
+            if (p) cudaFreeHost(p);
+    }
+    char* stage(int i, size_t bytes) {
+        if (pin_n[i] < bytes) {
+            if (pin[i]) cudaFreeHost(pin[i]);
+            pin[i] = nullptr;
+            ck(cudaMallocHost(&pin[i], std::max<size_t>(bytes, 1)), "cudaMallocHost");
+            pin_n[i] = bytes;
+        }
+        return pin[i];
+    }
+    int world() const override { return n; }
+    void gather_rows(std::vector<sad_fit_run*>& runs, int b) override {
+        std::vector<XferPlan> plans;
+        rows_plan(runs, b, plans, n);
+        exchange(runs, plans);
+    }
+    void halo_rows(std::vector<sad_fit_run*>& runs, int b, int step) override {
+        std::vector<XferPlan> plans;
+        halo_plan(runs, b, step, plans, n);
+        exchange(runs, plans);
+    }
+    void gather(std::vector<sad_fit_run*>& runs, const std::function<const void*(sad_fit_run*)>& self,
+                const std::function<void*(sad_fit_run*)>& all, size_t bytes) override {
+        sad_fit_run* r = runs[0];
+        char* hs = stage(0, bytes);
+        char* ha = stage(1, bytes * n);
+        ck(cudaMemcpyAsync(hs, self(r), bytes, cudaMemcpyDeviceToHost, r->ws.stream), "D2H gather");
+        ck(cudaStreamSynchronize(r->ws.stream), "host gather");
+        if (ag(user, hs, ha, bytes) != 0) fail(SAD_ECUDA, "strips: host all-gather callback failed");
+        ck(cudaMemcpyAsync(all(r), ha, bytes * n, cudaMemcpyHostToDevice, r->ws.stream), "H2D gather");
+        ck(cudaStreamSynchronize(r->ws.stream), "host gather");
+    }
+    void exchange(std::vector<sad_fit_run*>& runs, std::vector<XferPlan>& plans) override {
+        sad_fit_run* r = runs[0];
+        const XferPlan& pl = plans[0];
+        const size_t m = pl.peer.size();
+        size_t st = 0, rt = 0;
+        for (size_t i = 0; i < m; i++) {
+            st += pl.sbytes[i];
+            rt += pl.rbytes[i];
+        }
+        char* hs = stage(2, st);
+        char* hr = stage(3, rt);
+        std::vector<const void*> sp(m);
+        std::vector<void*> rp(m);
+        size_t so = 0, ro = 0;
+        for (size_t i = 0; i < m; i++) {
+            if (pl.sbytes[i])
+                ck(cudaMemcpyAsync(hs + so, pl.send[i], pl.sbytes[i], cudaMemcpyDeviceToHost, r->ws.stream), "D2H xfer");
+            sp[i] = hs + so;
+            rp[i] = hr + ro;
+            so += pl.sbytes[i];
+            ro += pl.rbytes[i];
+        }
+        ck(cudaStreamSynchronize(r->ws.stream), "host exchange");
+        if (m && ex(user, static_cast<int>(m), pl.peer.data(), sp.data(), pl.sbytes.data(), rp.data(), pl.rbytes.data()) != 0)
+            fail(SAD_ECUDA, "strips: host exchange callback failed");
+        for (size_t i = 0; i < m; i++)
+            if (pl.rbytes[i])
+                ck(cudaMemcpyAsync(pl.recv[i], rp[i], pl.rbytes[i], cudaMemcpyHostToDevice, r->ws.stream), "H2D xfer");
+        ck(cudaStreamSynchronize(r->ws.stream), "host exchange");
     }
 };
 
@@ -2128,6 +2279,54 @@ static std::vector<int> strip_bounds(int rows, int world) {
     for (int q = 0; q <= world; q++)
         b[q] = std::min(rows, qr * static_cast<int>(static_cast<long long>(tiles) * q / world));
     return b;
+}
+
+// Owner merge of one reduction (gradients: nch 10 from `part`; stats: 8): every rank sends the partials
+// of the touched sites it does not own to their owners, who merge them into `part` exactly.  Returns the
+// records each rank sent (for the exchange-volume report).
+static long long owner_merge(std::vector<sad_fit_run*>& runs, StripComm& T, int R, int slice, int nch,
+                             const std::function<double2*(sad_fit_run*)>& part,
+                             const std::function<sadk::RedTarget(sad_fit_run*)>& red, bool grads) {
+    const int send_cap = slice;
+    for (sad_fit_run* r : runs) {
+        Workspace& ws = r->ws;
+        ck(cudaMemsetAsync(r->own_counts.p, 0, sizeof(unsigned long long) * R, ws.stream), "memset counts");
+        sadk::launch_owner_pack(part(r), nch, red(r), ws.st.p, ws.active.p, slice, r->rank, R, r->own_send.p, send_cap,
+                                r->own_counts.p, grads ? ws.rcap.p : nullptr, grads, ws.stream);
+    }
+    T.gather(runs, [](sad_fit_run* r) { return static_cast<const void*>(r->own_counts.p); },
+             [](sad_fit_run* r) { return static_cast<void*>(r->own_matrix.p); }, sizeof(unsigned long long) * R);
+    long long sent = 0;
+    std::vector<XferPlan> plans(runs.size());
+    std::vector<std::vector<unsigned long long>> mats(runs.size(), std::vector<unsigned long long>(size_t(R) * R));
+    for (size_t i = 0; i < runs.size(); i++) {
+        ck(cudaMemcpyAsync(mats[i].data(), runs[i]->own_matrix.p, sizeof(unsigned long long) * R * R,
+                           cudaMemcpyDeviceToHost, runs[i]->ws.stream),
+           "D2H counts");
+        ck(cudaStreamSynchronize(runs[i]->ws.stream), "counts");
+    }
+    std::vector<long long> nrecv(runs.size(), 0);
+    for (size_t i = 0; i < runs.size(); i++) {
+        sad_fit_run* r = runs[i];
+        const int me = r->rank;
+        const auto& M = mats[i];  // M[src * R + dst]
+        long long roff = 0;
+        for (int q = 0; q < R; q++) {
+            if (q == me) continue;
+            const long long ns = std::min<long long>(M[static_cast<size_t>(me) * R + q], send_cap);
+            const long long nr = std::min<long long>(M[static_cast<size_t>(q) * R + me], send_cap);
+            plans[i].add(q, r->own_send.p + static_cast<size_t>(q) * send_cap, ns * sizeof(sadk::OwnRec),
+                         r->own_recv.p + roff, nr * sizeof(sadk::OwnRec));
+            roff += nr;
+            sent += ns;
+            if (grads) r->xfer_records += ns;
+        }
+        nrecv[i] = roff;
+    }
+    T.exchange(runs, plans);
+    for (size_t i = 0; i < runs.size(); i++)
+        sadk::launch_owner_merge(runs[i]->own_recv.p, nrecv[i], nch, runs[i]->ws.cap, part(runs[i]), runs[i]->ws.stream);
+    return sent;
 }
 
 static void fit_loop_strips(std::vector<sad_fit_run*>& runs, StripComm& T) {
@@ -2188,16 +2387,29 @@ static void fit_loop_strips(std::vector<sad_fit_run*>& runs, StripComm& T) {
         ws.plan_records();
         ck(cudaMemsetAsync(ws.gcnt.p, 0, sizeof(int32_t) * ws.cap, s), "memset gcnt");
         ck(cudaMemsetAsync(ws.ghead.p, 0xff, sizeof(int32_t) * ws.cap, s), "memset ghead");
-        const size_t cap = static_cast<size_t>(ws.cap);
-        r->gpart_self.ensure(10 * cap);
-        r->gpart_all.ensure(static_cast<size_t>(R) * 10 * cap);
-        r->spart_all.ensure(static_cast<size_t>(R) * 8 * cap);
-        r->loss_self.ensure(1);
-        r->loss_all.ensure(R);
-        r->tot.ensure(10 * cap);
-        r->valid_all.ensure(R);
     }
     const int cap = r0->ws.cap;
+    for (sad_fit_run* r : runs)
+        if (r->ws.cap != cap) fail(SAD_EINVAL, "strips: ranks disagree on the site capacity");
+    const int slice = (cap + R - 1) / R;
+    for (sad_fit_run* r : runs) {
+        const size_t sc = static_cast<size_t>(slice);
+        r->gpart_self.ensure(10 * static_cast<size_t>(cap));
+        r->loss_self.ensure(1);
+        r->loss_all.ensure(R);
+        r->tot.ensure(10 * static_cast<size_t>(cap));
+        r->valid_all.ensure(R);
+        r->own_counts.ensure(R);
+        r->own_matrix.ensure(static_cast<size_t>(R) * R);
+        r->own_send.ensure(static_cast<size_t>(R) * sc);
+        r->own_recv.ensure(static_cast<size_t>(R) * sc);
+        r->own_range.ensure(2);
+        r->slice_p.ensure(10 * sc);
+        r->slice_all_p.ensure(static_cast<size_t>(R) * 10 * sc);
+        r->slice_s.ensure(8 * sc);
+        r->slice_all_s.ensure(static_cast<size_t>(R) * 8 * sc);
+        r->xfer_records = 0;
+    }
     const sadk::AdamHyper hp = adam_hyper(c, w, h);
     const auto full4 = full_refresh_passes(r0->ws.fd.gw, r0->ws.fd.gh, 4);
     const std::vector<sad_pass_spec> warm(static_cast<size_t>(c.refresh_passes), sad_pass_spec{1, 0});
@@ -2224,6 +2436,15 @@ static void fit_loop_strips(std::vector<sad_fit_run*>& runs, StripComm& T) {
             sadk::launch_jfa_seed(r->ws.sites(), r->ws.st.p, r->ws.ids[0].p, r->ws.fd, scale_n, r->ws.stream);
         }
     };
+    // all-gather of the owned parameter slices (10 doubles per site)
+    auto gather_params = [&] {
+        for (sad_fit_run* r : runs)
+            sadk::launch_slice_pack<double>(r->ws.params.p, 10, cap, r->rank * slice, slice, r->slice_p.p, r->ws.stream);
+        T.gather(runs, [](sad_fit_run* r) { return static_cast<const void*>(r->slice_p.p); },
+                 [](sad_fit_run* r) { return static_cast<void*>(r->slice_all_p.p); }, sizeof(double) * 10 * slice);
+        for (sad_fit_run* r : runs)
+            sadk::launch_slice_unpack<double>(r->slice_all_p.p, 10, cap, slice, R, r->ws.params.p, r->ws.stream);
+    };
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -2246,7 +2467,7 @@ static void fit_loop_strips(std::vector<sad_fit_run*>& runs, StripComm& T) {
             passes(warm, 0);
             npass += static_cast<int>(warm.size());
         }
-        // backward on the strips, then the exact cross-rank merge of the site totals and the loss
+        // backward on the strips; each rank's partial totals of the sites it touched
         for (sad_fit_run* r : runs) {
             Workspace& ws = r->ws;
             sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt_of(r), ws.fd, scale_n, ws.gred_adaptive(),
@@ -2254,20 +2475,30 @@ static void fit_loop_strips(std::vector<sad_fit_run*>& runs, StripComm& T) {
             sadk::launch_loss_reduce(ws.loss_part.p, sadk::backward_blocks(fp64, ws.fd), r->loss_self.p, ws.stream);
             sadk::launch_site_partials(ws.gred_adaptive(), ws.st.p, cap, r->gpart_self.p, ws.stream);
         }
-        T.gather(runs, [](sad_fit_run* r) { return static_cast<const void*>(r->gpart_self.p); },
-                 [](sad_fit_run* r) { return static_cast<void*>(r->gpart_all.p); }, 10 * sizeof(double2) * cap);
         T.gather(runs, [](sad_fit_run* r) { return static_cast<const void*>(r->loss_self.p); },
                  [](sad_fit_run* r) { return static_cast<void*>(r->loss_all.p); }, sizeof(double2));
-        for (sad_fit_run* r : runs)
-            sadk::launch_merge_partials(r->gpart_all.p, R, cap, 10, r->tot.p, nullptr, r->ws.stream);
-        if (ev) {  // stats (budget.cpp:39-155) on the strips, merged the same way
+        // owner merge of the gradient partials; the owned totals' values feed Adam
+        owner_merge(
+            runs, T, R, slice, 10, [](sad_fit_run* r) { return r->gpart_self.p; },
+            [](sad_fit_run* r) { return r->ws.gred_adaptive(); }, true);
+        for (sad_fit_run* r : runs) {
+            sadk::launch_dd_values(r->gpart_self.p, 10ll * cap, r->tot.p, r->ws.stream);
+            r->ws.plan_records();  // next pass's record slices from the capacities owner_pack planned
+        }
+        if (ev) {  // stats (budget.cpp:39-155) on the strips: owner merge, then every rank gets all totals
             for (sad_fit_run* r : runs) stats_device(r->ws);
-            T.gather(runs, [](sad_fit_run* r) { return static_cast<const void*>(r->ws.stats.p); },
-                     [](sad_fit_run* r) { return static_cast<void*>(r->spart_all.p); }, 8 * sizeof(double2) * cap);
+            owner_merge(
+                runs, T, R, slice, 8, [](sad_fit_run* r) { return r->ws.stats.p; },
+                [](sad_fit_run* r) { return r->ws.sred(); }, false);
+            for (sad_fit_run* r : runs)
+                sadk::launch_slice_pack<double2>(r->ws.stats.p, 8, cap, r->rank * slice, slice, r->slice_s.p, r->ws.stream);
+            T.gather(runs, [](sad_fit_run* r) { return static_cast<const void*>(r->slice_s.p); },
+                     [](sad_fit_run* r) { return static_cast<void*>(r->slice_all_s.p); }, sizeof(double2) * 8 * slice);
+            for (sad_fit_run* r : runs)
+                sadk::launch_slice_unpack<double2>(r->slice_all_s.p, 8, cap, slice, R, r->ws.stats.p, r->ws.stream);
             T.gather(runs, [](sad_fit_run* r) { return static_cast<const void*>(&r->ws.st.p->valid); },
                      [](sad_fit_run* r) { return static_cast<void*>(r->valid_all.p); }, sizeof(unsigned long long));
             for (sad_fit_run* r : runs) {
-                sadk::launch_merge_partials(r->spart_all.p, R, cap, 8, nullptr, r->ws.stats.p, r->ws.stream);
                 std::vector<unsigned long long> va(R);
                 ck(cudaMemcpyAsync(va.data(), r->valid_all.p, 8 * R, cudaMemcpyDeviceToHost, r->ws.stream), "D2H valid");
                 ck(cudaStreamSynchronize(r->ws.stream), "valid");
@@ -2276,13 +2507,16 @@ static void fit_loop_strips(std::vector<sad_fit_run*>& runs, StripComm& T) {
                 r->ws.patch_state(offsetof(DevState, valid), vt);
             }
         }
+        // Adam on the owned slice of the active list, then every rank receives every slice
         for (sad_fit_run* r : runs) {
             Workspace& ws = r->ws;
+            sadk::launch_owned_range(ws.act.p, ws.st.p, r->rank * slice, std::min(cap, (r->rank + 1) * slice),
+                                     r->own_range.p, ws.stream);
             sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.gred_adaptive(), ws.m.p, ws.v.p, hp, r->bc_table.p,
-                              make_double2(0, 0), true, scale_n, ev ? nullptr : ws.pack.p, ev ? nullptr : ws.gtab.p,
-                              ws.rcap.p, ws.stream, r->tot.p, ws.roff.p, ws.otops.p + 2,
-                              (ev || g_adam_all) ? nullptr : ws.act.p);
+                              make_double2(0, 0), false, scale_n, nullptr, nullptr, nullptr, ws.stream, r->tot.p, nullptr,
+                              nullptr, ws.act.p, r->own_range.p);
         }
+        gather_params();
         if (ev) {
             for (sad_fit_run* r : runs) {
                 Workspace& ws = r->ws;
@@ -2294,6 +2528,8 @@ static void fit_loop_strips(std::vector<sad_fit_run*>& runs, StripComm& T) {
             reseed();
             passes(full4, static_cast<uint32_t>(npass));
             npass += static_cast<int>(full4.size());
+        } else {
+            for (sad_fit_run* r : runs) build_tables(r->ws, fp64, true, true, false);
         }
         for (sad_fit_run* r : runs)
             sadk::launch_advance(r->ws.st.p, npass, 1, r->loss_hist.p, r->active_hist.p, r->loss_all.p, R,
@@ -2339,7 +2575,7 @@ sad_status sad_nccl_unique_id(uint8_t* out) {
 }
 
 struct sad_strip_comm {
-    std::unique_ptr<NcclComm> comm;
+    std::unique_ptr<StripComm> comm;
     int rank = 0, world = 1;
 };
 
@@ -2360,7 +2596,27 @@ sad_status sad_strip_comm_create(int rank, int world, const uint8_t* nccl_id, sa
     });
 }
 
+sad_status sad_strip_comm_create_host(int rank, int world, sad_host_allgather_fn allgather,
+                                      sad_host_exchange_fn exchange, void* user, sad_strip_comm** out) {
+    return guard([&] {
+        if (world < 1 || rank < 0 || rank >= world) fail(SAD_EINVAL, "strips: bad rank / world");
+        if (!allgather || !exchange || !out) fail(SAD_EINVAL, "strips: null argument");
+        auto* c = new sad_strip_comm();
+        c->comm.reset(new HostComm(rank, world, allgather, exchange, user));
+        c->rank = rank;
+        c->world = world;
+        *out = c;
+    });
+}
+
 void sad_strip_comm_destroy(sad_strip_comm* c) { delete c; }
+
+sad_status sad_fit_strip_exchange(sad_fit_run* r, long long* records_sent) {
+    return guard([&] {
+        if (!records_sent) fail(SAD_EINVAL, "strips: null argument");
+        *records_sent = r->xfer_records;
+    });
+}
 
 sad_status sad_fit_run_strips(sad_fit_run* r, sad_strip_comm* comm, const sad_sites_view* init) {
     return guard([&] {

@@ -1,0 +1,142 @@
+"""The row-strip fit (config 5) with two OS processes, two CUDA contexts and the host-staged
+strip transport over a torch.distributed gloo group (sad_strip_comm_create_host): both ranks must end
+with exactly the single-GPU fit — every history line, every site array, the map.  This is the real
+multi-process code path (owner-merged gradient and stats exchange, sharded Adam, parameter all-gather,
+halo rows) that NCCL runs on several GPUs; gloo lets the two processes share the one GPU of the test box.
+
+The CPU test below runs the Python side of the host transport (the all-gather and point-to-point
+callbacks the library calls) in a world-2 gloo group without a GPU.
+"""
+import ctypes as C
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+import paper_2604_21984_b200 as sad
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+P = ("x", "y", "log_tau", "radius", "col_r", "col_g", "col_b", "dir_x", "dir_y", "aniso", "active")
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _cases():
+    return [
+        ("fp32", 80, 64, sad.TrainConfig(iters=100, target_bpp=2.0, fp64=False, seed=2, densify_start=10,
+                                         densify_every=10, prune_start=20, prune_every=20)),
+        ("fp64", 56, 48, sad.TrainConfig(iters=60, target_bpp=2.0, fp64=True, seed=3, densify_start=10,
+                                         densify_every=10, prune_start=20, prune_every=20)),
+    ]
+
+
+def _gpu_rank(rank, world, port, outdir):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from tests.fixtures import synth_target
+    G = sad.gpu_backend(0)
+    comm = G.strip_comm_host()
+    try:
+        for name, w, h, cfg in _cases():
+            res = G.fit_strips(synth_target(w, h, 7), cfg, comm)
+            np.savez(os.path.join(outdir, f"{name}_rank{rank}.npz"), ids=res.field.ids, pass_index=res.field.pass_index,
+                     lines=np.array([sad.history_line(r) for r in res.history]),
+                     sent=res.timing.get("records_sent", -1), **{p: getattr(res.sites, p) for p in P})
+    finally:
+        comm.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_strips_two_processes_host_transport(tmp_path):
+    world = 2
+    ctx = mp.get_context("spawn")
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_rank, args=(r, world, port, str(tmp_path))) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(600)
+        assert p.exitcode == 0
+    from tests.fixtures import synth_target
+    G = sad.gpu_backend(0)
+    for name, w, h, cfg in _cases():
+        ref = G.fit(synth_target(w, h, 7), cfg)
+        for r in range(world):
+            d = np.load(os.path.join(str(tmp_path), f"{name}_rank{r}.npz"))
+            assert list(d["lines"]) == [sad.history_line(x) for x in ref.history], (name, r)
+            for p in P:
+                assert np.array_equal(d[p], getattr(ref.sites, p)), (name, r, p)
+            assert np.array_equal(d["ids"], ref.field.ids), (name, r)
+            assert int(d["pass_index"]) == ref.field.pass_index
+            assert int(d["sent"]) >= 0
+
+
+def _cpu_rank(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2604_21984_b200 import api
+
+    class _NoLib:  # only the callbacks are exercised: no library call is made
+        pass
+
+    comm = api.HostStripComm.__new__(api.HostStripComm)
+    # build the callbacks exactly as HostStripComm does, without creating a library communicator
+    import types
+    fake = types.SimpleNamespace(_call=lambda *a: None, lib=_NoLib())
+    api.HostStripComm.__init__(comm, fake)
+    # all-gather of 12 bytes
+    mine = (C.c_uint8 * 12)(*[rank * 16 + i for i in range(12)])
+    allb = (C.c_uint8 * (12 * world))()
+    rc1 = comm._ag(None, C.addressof(mine), C.addressof(allb), 12)
+    # exchange with the other rank: two transfers (one empty), sizes differ per direction
+    peer = 1 - rank
+    s0 = (C.c_uint8 * (5 + rank))(*[100 + rank] * (5 + rank))
+    r0 = (C.c_uint8 * (5 + peer))()
+    peers = (C.c_int * 2)(peer, peer)
+    sp = (C.c_void_p * 2)(C.addressof(s0), None)
+    sb = (C.c_size_t * 2)(5 + rank, 0)
+    r1 = (C.c_uint8 * 3)()
+    s1 = (C.c_uint8 * 3)(7, 8, 9)
+    sp[1] = C.addressof(s1)
+    sb[1] = 3
+    rp = (C.c_void_p * 2)(C.addressof(r0), C.addressof(r1))
+    rb = (C.c_size_t * 2)(5 + peer, 3)
+    rc2 = comm._ex(None, 2, peers, sp, sb, rp, rb)
+    q.put((rank, rc1, rc2, bytes(allb), bytes(r0), bytes(r1)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_host_transport_callbacks_gloo_world2():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cpu_rank, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    expect_all = bytes([r * 16 + i for r in range(world) for i in range(12)])
+    for rank, rc1, rc2, allb, r0, r1 in res:
+        assert rc1 == 0 and rc2 == 0
+        assert allb == expect_all
+        peer = 1 - rank
+        assert r0 == bytes([100 + peer] * (5 + peer))
+        assert r1 == bytes([7, 8, 9])
