@@ -272,8 +272,14 @@ def roofline_2048(G, iters=200, n_sites=100000):
     peak, src = hbm_peak()
     for v in kt.values():
         v["frac_hbm"] = v["GBps"] / peak
-    return {"workload": f"2048x2048, {n_sites} sites, {iters}-iteration fit state", "fit_ms_per_iter": tot.value / iters,
-            "kernels": kt, "peak_gbs": peak, "peak_source": src}
+    out = {"workload": f"2048x2048, {n_sites} sites, {iters}-iteration fit state", "fit_ms_per_iter": tot.value / iters,
+           "kernels": kt, "peak_gbs": peak, "peak_source": src}
+    tf = os.path.join(ROOT, "profiles", "r2_ncu_fwd_bwd_traffic_2048.json")
+    if os.path.exists(tf):  # DRAM traffic of the fwd+bwd kernel at this size, from the committed ncu capture
+        tj = json.load(open(tf))
+        out["fwd_bwd_traffic"] = {"bytes_per_launch": tj["traffic_bytes"], "source": os.path.relpath(tf, ROOT),
+                                  "issue_active_pct_of_peak": tj.get("issue_active_pct_of_peak")}
+    return out
 
 
 def run_config3(a):
@@ -579,7 +585,8 @@ def run_b200(a):
     ach = kernels[dom]["GBps"]
     # DRAM traffic per launch of the dominant kernel from the committed ncu --set full capture
     traffic, traffic_src = None, None
-    tfs = [os.path.join(ROOT, "profiles", f) for f in ("r1h_ncu_fwd_bwd_traffic.json", "r1e_ncu_fwd_bwd_traffic.json", "r1b_ncu_fwd_bwd_traffic.json")]
+    tfs = [os.path.join(ROOT, "profiles", f) for f in ("r2_ncu_fwd_bwd_traffic.json", "r1h_ncu_fwd_bwd_traffic.json",
+                                                       "r1e_ncu_fwd_bwd_traffic.json")]
     tf = next((f for f in tfs if os.path.exists(f)), tfs[-1])
     if dom == "fwd_bwd" and os.path.exists(tf):
         tj = json.load(open(tf))
