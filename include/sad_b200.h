@@ -159,8 +159,8 @@ sad_status sad_field_alloc(sad_ctx* ctx, int width, int height, int k, int cell)
 sad_status sad_field_upload(sad_ctx* ctx, const sad_field_view* field);
 sad_status sad_field_download(sad_ctx* ctx, sad_field_view* field); /* ids: gw*gh*k or NULL (metadata only) */
 
-/* The device ports of glibc's exp (double; single != 0: expf) the kernels use, applied to n host
- * values -- exposed so their bit-identity with the host libm can be verified. */
+/* The device ports of glibc's math the kernels use, applied to n host values -- exposed so their
+ * bit-identity with the host libm can be verified.  single: 0 exp (double), 1 expf, 2 log (double). */
 sad_status sad_math_exp(sad_ctx* ctx, const double* x, double* y, size_t n, int single);
 
 /* ---------------------------------------------------------------- candidates.hpp */

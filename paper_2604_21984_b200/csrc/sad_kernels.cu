@@ -3228,7 +3228,8 @@ void launch_tau_mix(const uint64_t* uniq, const int* count, int max_items, int n
 __global__ void k_math(const double* __restrict__ x, double* __restrict__ y, size_t n, int which) {
     const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
     if (i >= n) return;
-    y[i] = which == 0 ? sad_dexp(x[i]) : static_cast<double>(sad_expf(static_cast<float>(x[i])));
+    y[i] = which == 0 ? sad_dexp(x[i])
+                      : which == 1 ? static_cast<double>(sad_expf(static_cast<float>(x[i]))) : sad_dlog(x[i]);
 }
 
 void launch_math(const double* x, double* y, size_t n, int which, cudaStream_t stream) {
@@ -3336,13 +3337,11 @@ __device__ __forceinline__ double luma_at(const double* img, int w, int h, int x
 // split_axis (budget.cpp:170-215) + the split of densify (budget.cpp:237-279).  Split i uses free
 // slot i while they last, then appends in order; parents are active so no two splits touch the same
 // slot, which makes the reference's sequential loop embarrassingly parallel.
-// The split-axis anisotropy -0.5*log(lam1/lam2) is not taken from the device libm: the kernel records
-// each split's ratio and child slots (ratio_out[i] < 0: no log needed) and the host applies glibc's log,
-// the one the reference uses (budget.cpp:198-199), through k_densify_aniso.
+// The split-axis anisotropy -0.5*log(lam1/lam2) uses sad_dlog, the device port of the host glibc's log
+// that the reference calls (budget.cpp:198-199): no host round trip per event.
 __global__ void k_densify_apply(SitesDev s, DevState* st, const double2* __restrict__ stats, int cap,
                                 const uint32_t* __restrict__ sorted, const uint32_t* __restrict__ free_list,
-                                const double* __restrict__ img, double pct, SplitHyper hp, double* m, double* v,
-                                double* __restrict__ ratio_out, uint32_t* __restrict__ slots_out) {
+                                const double* __restrict__ img, double pct, SplitHyper hp, double* m, double* v) {
     const int n_elig = st->n_elig, n_free = st->n_free, size0 = st->n_sites;
     int want = static_cast<int>(static_cast<double>(n_elig) * pct);
     if (pct <= 0 || want < 1) want = 0;
@@ -3382,8 +3381,9 @@ __global__ void k_densify_apply(SitesDev s, DevState* st, const double2* __restr
                 ax = vx / nn;
                 ay = vy / nn;
                 double ratio = l2 > 0 ? l1 / l2 : 1e18;
-                an = 0.0;  // set by the host from glibc's log(ratio)
-                ratio_out[i] = ratio;
+                // negative a elongates the influence region along the axis (budget.cpp:197-199); the device
+                // port of glibc's log is bit-identical to the host's
+                an = sclamp(-0.5 * sad_dlog(ratio), hp.aniso_min, hp.aniso_max);
                 fallback = false;
             }
         }
@@ -3406,7 +3406,6 @@ __global__ void k_densify_apply(SitesDev s, DevState* st, const double2* __restr
         }
         an = sclamp(0.8 * pan, hp.aniso_min, hp.aniso_max);
     }
-    if (fallback) ratio_out[i] = -1.0;
     double mag = sclamp(0.5 * __dsqrt_rn(smax(st8[0], 0.0)), 1.5, 48.0);
     double clt = smax(plt - 0.25, hp.log_tau_min);
     double cr = smax(pr * 0.85, hp.radius_min);
@@ -3417,7 +3416,6 @@ __global__ void k_densify_apply(SitesDev s, DevState* st, const double2* __restr
         int ix = static_cast<int>(llround(cx)), iy = static_cast<int>(llround(cy));
         const double* col = img + 3 * (static_cast<size_t>(iy) * hp.width + ix);
         uint32_t slot = side == 0 ? par : (i < n_free ? free_list[i] : static_cast<uint32_t>(size0 + (i - n_free)));
-        slots_out[2 * i + side] = slot < static_cast<uint32_t>(cap) ? slot : 0xffffffffu;
         if (slot >= static_cast<uint32_t>(cap)) {
             atomicOr(&st->err, 2);
             continue;
@@ -3449,25 +3447,11 @@ __global__ void k_densify_apply(SitesDev s, DevState* st, const double2* __restr
 
 void launch_densify_apply(const SitesDev& s, DevState* st, const double2* stats, int cap, const uint32_t* sorted,
                           const uint32_t* free_list, const double* tgt, double pct, const SplitHyper& hp, double* m,
-                          double* v, double* ratio_out, uint32_t* slots_out, cudaStream_t stream) {
-    k_densify_apply<<<(cap + 127) / 128, 128, 0, stream>>>(s, st, stats, cap, sorted, free_list, tgt, pct, hp, m, v,
-                                                           ratio_out, slots_out);
+                          double* v, cudaStream_t stream) {
+    k_densify_apply<<<(cap + 127) / 128, 128, 0, stream>>>(s, st, stats, cap, sorted, free_list, tgt, pct, hp, m, v);
     SAD_LAUNCHED();
 }
 
-__global__ void k_densify_aniso(double* __restrict__ p, int cap, int n, const uint32_t* __restrict__ slots,
-                                const double* __restrict__ an) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= 2 * n) return;
-    const uint32_t slot = slots[j];
-    if (slot != 0xffffffffu && an[j >> 1] == an[j >> 1]) p[9 * static_cast<size_t>(cap) + slot] = an[j >> 1];
-}
-
-void launch_densify_aniso(double* p, int cap, int n, const uint32_t* slots, const double* an, cudaStream_t stream) {
-    if (n <= 0) return;
-    k_densify_aniso<<<(2 * n + 127) / 128, 128, 0, stream>>>(p, cap, n, slots, an);
-    SAD_LAUNCHED();
-}
 
 __global__ void k_flag_active(SitesDev s, const DevState* st, uint8_t* flags) {
     const int id = blockIdx.x * blockDim.x + threadIdx.x;

@@ -177,8 +177,7 @@ void launch_densify_keys(const SitesDev& s, DevState* st, const double2* stats, 
                          unsigned long long* keys, uint32_t* vals, uint8_t* free_flags, cudaStream_t stream);
 void launch_densify_apply(const SitesDev& s, DevState* st, const double2* stats, int cap, const uint32_t* sorted,
                           const uint32_t* free_list, const double* tgt, double pct, const SplitHyper& hp, double* m,
-                          double* v, double* ratio_out, uint32_t* slots_out, cudaStream_t stream);
-void launch_densify_aniso(double* p, int cap, int n, const uint32_t* slots, const double* an, cudaStream_t stream);
+                          double* v, cudaStream_t stream);
 void launch_flag_active(const SitesDev& s, const DevState* st, uint8_t* flags, cudaStream_t stream);
 
 // ---------------------------------------------------------------- loop bookkeeping

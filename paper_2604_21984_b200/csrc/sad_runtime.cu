@@ -343,16 +343,9 @@ struct Workspace {
         DBuf<char> tmp;
         size_t tmp_bytes = 0;
     } tb;
-    DBuf<double> dens_ratio, dens_an;  // densify: split ratios and their host-computed anisotropy
-    DBuf<uint32_t> dens_slots;
-    double* hpin_ratio = nullptr;  // pinned host mirrors of the above
-    double* hpin_an = nullptr;
-    int hpin_n = 0;
 
     ~Workspace() {
         if (hst) cudaFreeHost(hst);
-        if (hpin_ratio) cudaFreeHost(hpin_ratio);
-        if (hpin_an) cudaFreeHost(hpin_an);
     }
 
     sadk::SitesDev sites() { return sadk::SitesDev{params.p, active.p, frozen.p, cap}; }
@@ -756,38 +749,8 @@ void densify_device(Workspace& ws, double pct, const sad_train_config& c) {
     }
     ws.sort_pairs(ws.cap);
     sadk::SplitHyper hp{c.log_tau_min, c.radius_min, c.aniso_min, c.aniso_max, ws.fd.width, ws.fd.height, c.max_sites};
-    ws.dens_ratio.ensure(ws.cap);
-    ws.dens_slots.ensure(2 * static_cast<size_t>(ws.cap));
-    ws.dens_an.ensure(ws.cap);
     sadk::launch_densify_apply(ws.sites(), ws.st.p, ws.stats.p, ws.cap, ws.vals[1].p, ws.free_list.p, ws.tgt_d.p, pct,
-                               hp, ws.m.p, ws.v.p, ws.dens_ratio.p, ws.dens_slots.p, ws.stream);
-    // split-axis anisotropy with the host's glibc log, as the reference (budget.cpp:198-199): one
-    // synchronisation fetches the state and every candidate ratio into pinned memory; the results go
-    // back asynchronously from a second pinned buffer (reused only after the next event's sync)
-    if (ws.hpin_n < ws.cap) {  // (re)allocate once the stream no longer reads the old buffers
-        ck(cudaStreamSynchronize(ws.stream), "densify pinned");
-        if (ws.hpin_ratio) cudaFreeHost(ws.hpin_ratio);
-        if (ws.hpin_an) cudaFreeHost(ws.hpin_an);
-        ws.hpin_ratio = ws.hpin_an = nullptr;
-        ws.hpin_n = 0;
-        ck(cudaMallocHost(&ws.hpin_ratio, 8 * static_cast<size_t>(ws.cap)), "cudaMallocHost");
-        ck(cudaMallocHost(&ws.hpin_an, 8 * static_cast<size_t>(ws.cap)), "cudaMallocHost");
-        ws.hpin_n = ws.cap;
-    }
-    ck(cudaMemcpyAsync(ws.hst, ws.st.p, sizeof(DevState), cudaMemcpyDeviceToHost, ws.stream), "D2H state");
-    ck(cudaMemcpyAsync(ws.hpin_ratio, ws.dens_ratio.p, 8 * static_cast<size_t>(ws.cap), cudaMemcpyDeviceToHost,
-                       ws.stream),
-       "D2H ratio");
-    ck(cudaStreamSynchronize(ws.stream), "densify ratio");
-    const int done = ws.hst->done;
-    if (done > 0) {
-        for (int i = 0; i < done; i++)
-            ws.hpin_an[i] = ws.hpin_ratio[i] < 0 ? std::numeric_limits<double>::quiet_NaN()
-                                                 : std::clamp(-0.5 * std::log(ws.hpin_ratio[i]), c.aniso_min, c.aniso_max);
-        ck(cudaMemcpyAsync(ws.dens_an.p, ws.hpin_an, 8 * static_cast<size_t>(done), cudaMemcpyHostToDevice, ws.stream),
-           "H2D aniso");
-        sadk::launch_densify_aniso(ws.params.p, ws.cap, done, ws.dens_slots.p, ws.dens_an.p, ws.stream);
-    }
+                               hp, ws.m.p, ws.v.p, ws.stream);
 }
 
 // Scratch for init_sites_device, allocated once per image size.
@@ -1117,7 +1080,7 @@ sad_status sad_math_exp(sad_ctx* c, const double* x, double* y, size_t n, int si
         dx.ensure(std::max<size_t>(n, 1));
         dy.ensure(std::max<size_t>(n, 1));
         ck(cudaMemcpyAsync(dx.p, x, 8 * n, cudaMemcpyHostToDevice, c->stream), "H2D");
-        sadk::launch_math(dx.p, dy.p, n, single ? 1 : 0, c->stream);
+        sadk::launch_math(dx.p, dy.p, n, single, c->stream);  // 0 exp, 1 expf, 2 log
         ck(cudaMemcpyAsync(y, dy.p, 8 * n, cudaMemcpyDeviceToHost, c->stream), "D2H");
         ck(cudaStreamSynchronize(c->stream), "math");
     });

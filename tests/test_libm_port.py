@@ -12,10 +12,11 @@ import paper_2604_21984_b200 as sad
 pytestmark = pytest.mark.gpu
 
 
-def _dev(G, x, single):
+def _dev(G, x, which):
+    """which: 0 exp, 1 expf, 2 log (the device ports of sad_device.cuh)."""
     y = np.empty_like(x)
     G._call("math_exp", x.ctypes.data_as(C.POINTER(C.c_double)), y.ctypes.data_as(C.POINTER(C.c_double)),
-            C.c_size_t(x.size), C.c_int(int(single)))
+            C.c_size_t(x.size), C.c_int(int(which)))
     return y
 
 
@@ -46,6 +47,26 @@ def test_double_exp_matches_glibc():
     ys = _dev(G, xs, False)
     rs = _glibc_exp(xs)
     assert np.array_equal(ys.view(np.uint64), rs.view(np.uint64))
+
+
+def test_double_log_matches_glibc():
+    """sad_dlog (densify's split anisotropy, budget.cpp:198-199) against this host's libm log: the
+    densify ratio range, the near-1 polynomial path, the whole normal range, subnormals and specials."""
+    import ctypes.util
+    G = sad.gpu_backend(0)
+    rng = np.random.default_rng(9)
+    x = np.ascontiguousarray(np.concatenate([
+        1.05 * np.exp(rng.random(1_000_000) * np.log(1e18 / 1.05)),
+        (1.0 - 2.0 ** -4) + rng.random(1_000_000) * (2.0 ** -4 + float.fromhex("0x1.09p-4")),
+        np.exp((rng.random(300_000) - 0.5) * 1400.0),
+        rng.random(1000) * 1e-310,
+        np.array([1.0, 2.0, 0.5, 1e18, 1.05, 1e300, np.inf, 0.0])]))
+    y = _dev(G, x, 2)
+    libm = C.CDLL(ctypes.util.find_library("m"))
+    libm.log.restype = C.c_double
+    libm.log.argtypes = [C.c_double]
+    ref = np.array([libm.log(float(v)) for v in x])
+    assert np.array_equal(y.view(np.uint64), ref.view(np.uint64))
 
 
 def test_float_expf_matches_glibc():
