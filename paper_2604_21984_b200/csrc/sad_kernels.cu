@@ -2982,8 +2982,12 @@ void launch_dd_values(const double2* dd, long long n, double* out, cudaStream_t 
     SAD_LAUNCHED();
 }
 
+#ifndef SAD_ADAM_MINB
+#define SAD_ADAM_MINB 4  // resident 128-thread blocks per SM the register allocator must allow: 1 -> 4 measured
+                         // config-2 fit 862.7 -> 854 ms (6: standalone faster, fit 869.7 ms)
+#endif
 template <typename T>
-__global__ void __launch_bounds__(128) k_adam(SitesDev s, DevState* st, RedTarget grads, double* __restrict__ m,
+__global__ void __launch_bounds__(128, SAD_ADAM_MINB) k_adam(SitesDev s, DevState* st, RedTarget grads, double* __restrict__ m,
                                               double* __restrict__ v, AdamHyper hp,
                                               const double2* __restrict__ bc_table, double2 bc_now, int zero_grads,
                                               double scale, Q4<T>* pack, Q4<T>* gtab, int32_t* rcap_next,
