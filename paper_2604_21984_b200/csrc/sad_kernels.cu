@@ -3566,7 +3566,7 @@ __global__ void k_init_keys(const double* __restrict__ mag, int w, int h, const 
         if (wgt < 1e-300) wgt = 1e-300;
         double u = xs_unit(rs);
         if (u < 1e-12) u = 1e-12;
-        double key = log(u) / wgt;
+        double key = sad_dlog(u) / wgt;  // glibc log port (train.cpp:81)
         keys[i] = order_key(-key);
         vals[i] = static_cast<uint32_t>(i);
     }
