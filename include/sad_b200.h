@@ -142,6 +142,9 @@ sad_status sad_ctx_create(int device, void* stream, sad_ctx** out);
 void sad_ctx_destroy(sad_ctx* ctx);
 sad_status sad_ctx_synchronize(sad_ctx* ctx);
 /* Number of kernel launches this context issued so far (evidence for the bench's gpu_launches). */
+/* Bound-check violations counted by the kernels of a checked build (libsad_b200_checked.so, built with
+ * -DSAD_CHECKED=1 by __graft_entry__.build_checked); -1 for the product build. */
+long long sad_debug_check_failures(void);
 uint64_t sad_ctx_launch_count(const sad_ctx* ctx);
 
 /* ---------------------------------------------------------------- device-resident objects

@@ -677,7 +677,8 @@ _NO_CTX = {"jump_step", "full_refresh_passes", "schedule_passes", "bpp_target_co
 
 # ---------------------------------------------------------------------- product binding
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsad_b200.so")
+# SAD_LIB selects another build of the same sources (tests: the bound-checked libsad_b200_checked.so)
+LIB_PATH = os.environ.get("SAD_LIB") or os.path.join(_HERE, "libsad_b200.so")
 _lock = threading.Lock()
 _gpu = None
 
@@ -690,6 +691,7 @@ def load_library(path: Optional[str] = None) -> C.CDLL:
     lib.sad_last_error.restype = C.c_char_p
     lib.sad_ctx_launch_count.restype = C.c_uint64
     lib.sad_ctx_launch_count.argtypes = [_P]
+    lib.sad_debug_check_failures.restype = C.c_longlong
     lib.sad_fit_destroy.argtypes = [_P]
     lib.sad_strip_comm_destroy.argtypes = [_P]
     lib.sad_ctx_destroy.argtypes = [_P]

@@ -8,6 +8,20 @@
 
 namespace sadk {
 
+// Checked build (-DSAD_CHECKED=1, __graft_entry__.build_checked -> libsad_b200_checked.so): index bounds
+// of shared-memory tables, record pools and site ids are tested in the kernels and violations counted in
+// a device counter (sad_debug_checks).  The stand-in for compute-sanitizer memcheck, which is unavailable
+// on the GPU pool used here.  Compiles to nothing in the product build.
+#ifndef SAD_CHECKED
+#define SAD_CHECKED 0
+#endif
+#if SAD_CHECKED
+static __device__ unsigned long long g_check_fail = 0;  // (kernels and reader live in sad_kernels.cu)
+#define SAD_CHECK(cond) do { if (!(cond)) atomicAdd(&::sadk::g_check_fail, 1ull); } while (0)
+#else
+#define SAD_CHECK(cond) do { } while (0)
+#endif
+
 // ---------------------------------------------------------------------- programmatic dependent launch
 // The per-iteration kernels (warm pass, fwd+bwd, Adam, bookkeeping) are launched with programmatic
 // stream serialisation, so the launch of each is prepared while its predecessor runs; every one waits

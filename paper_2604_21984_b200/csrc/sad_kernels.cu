@@ -27,6 +27,15 @@ extern "C" void sad_exp_phase(unsigned long long* out, int reset) {
 namespace sadk {
 
 static std::atomic<uint64_t> g_launches{0};
+long long debug_check_failures() {
+#if SAD_CHECKED
+    unsigned long long v = 0;
+    cudaMemcpyFromSymbol(&v, g_check_fail, sizeof v);
+    return static_cast<long long>(v);
+#else
+    return -1;  // not a checked build
+#endif
+}
 uint64_t launch_counter() { return g_launches.load(); }
 void add_launches(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 #define SAD_LAUNCHED() g_launches.fetch_add(1, std::memory_order_relaxed)
@@ -618,6 +627,7 @@ __global__ void __launch_bounds__(256, SAD_PROP_MINB) k_prop8_stream(const uint3
     KeyList8 L;
     bool ok = own_keys(prev, pack, f, gx, gy, cx, cy, s, L);
     auto feed = [&](uint32_t c) {
+        SAD_CHECK(c < static_cast<uint32_t>(st->n_sites));
         const Q4<float> b = pack[2 * c + 1], a = pack[2 * c];
         if (b.w == 0.0f) return;
         const float l = score_logit(a, b, cx, cy, s);
@@ -747,6 +757,7 @@ __global__ void __launch_bounds__(32 * SAD_QUEUE_BY, SAD_PROP_MINB * 8 / SAD_QUE
             Q4<float> b = pack[2 * c + 1], a = pack[2 * c];
 #pragma unroll 1
             for (int j = j0; j < nq; j++) {
+                SAD_CHECK(c < static_cast<uint32_t>(st->n_sites));
                 const uint32_t cn = j + 1 < nq ? q[(j + 1) * QB + tid] : c;
                 const Q4<float> bn = pack[2 * cn + 1], an = pack[2 * cn];
                 if (b.w != 0.0f) {
@@ -1244,6 +1255,7 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM, NT>& sm, c
     for (int e = tid; e < R::E; e += NT) {
         uint32_t key = sm.key[e];
         if (key == kEmpty) continue;
+        SAD_CHECK(key < static_cast<uint32_t>(red.cap));
         uint32_t h = (key * 2654435761u) & (R::HT - 1);
         uint16_t got = 0xffffu;  // stays 0xffff if the table is full: the entry goes to the atomic path
         for (int probe = 0; probe < R::HT; probe++) {
@@ -1348,6 +1360,7 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM, NT>& sm, c
         int loc = sm.local_of_entry[e];
         if (loc == 0xffff) continue;
         int pos = static_cast<int>(atomicAdd(&sm.start[loc], 1u));
+        SAD_CHECK(loc < R::UMAX && pos >= 0 && pos < R::E);
         sm.srt.order[pos] = static_cast<uint16_t>(e);
     }
     __syncthreads();
@@ -1403,6 +1416,7 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM, NT>& sm, c
         // that starts at +0 is never -0)
 #pragma unroll
         for (int j = 0; j < R::PT; j++) {
+            SAD_CHECK(j >= n || (b + j >= 0 && b + j < R::E));
             const int e = j < n ? static_cast<int>(sm.srt.order[b + j]) : R::E;
 #pragma unroll
             for (int ch = 0; ch < R::CB; ch++)
@@ -1493,8 +1507,11 @@ __device__ __forceinline__ void tile_reduce(TileRed<CT, NCH, TPX, KM, NT>& sm, c
         const uint32_t site = sm.site_of_local[u];
         const uint32_t code = sm.slot_of_local[u];
         if ((code >> 30) == 0u) {
+            SAD_CHECK(red.roff ? static_cast<long long>(code) < red.psize
+                               : static_cast<long long>(code) < static_cast<long long>(red.cap) * red.maxt);
             red.part[static_cast<size_t>(code) * red.stride + ch] = make_double2(t.hi, t.lo);
         } else if ((code >> 30) == 1u) {
+            SAD_CHECK(static_cast<int>(code & 0x3fffffffu) < red.ocap);
             red.opart[static_cast<size_t>(code & 0x3fffffffu) * red.stride + ch] = make_double2(t.hi, t.lo);
         } else {  // pool exhausted
 #if SAD_EXPERIMENT == 3
@@ -1859,6 +1876,7 @@ __global__ void __launch_bounds__(32 * SAD_BWD2_TH, SAD_BWD2_MINB * 8 / SAD_BWD2
             col[j] = Q4<T>{T(0), T(0), T(0), T(0)};
 #endif
             if (!stop) {
+                SAD_CHECK(id < static_cast<uint32_t>(st->n_sites));
                 const Q4<T> a = gtab[3 * id], b = gtab[3 * id + 1];
 #if SAD_BWD_EARLY_COL
                 col[j] = gtab[3 * id + 2];
@@ -2247,11 +2265,13 @@ __device__ __forceinline__ DD red_total(const RedTarget& red, int id, int ch, in
         rec = red.part + static_cast<size_t>(red.roff[id]) * red.stride + ch;
         if (n > red.rcap[id]) n = red.rcap[id];
     }
+    SAD_CHECK(!red.roff || n <= 0 || static_cast<long long>(red.roff[id]) + n <= red.psize);
     for (int s = 0; s < n; s++) {
         double2 r = rec[static_cast<size_t>(s) * red.stride];
         dd_merge(acc, DD{r.x, r.y});
     }
     for (int r = red.head[id]; r >= 0; r = red.onext[r]) {
+        SAD_CHECK(r < red.ocap);
         double2 o2 = red.opart[static_cast<size_t>(r) * red.stride + ch];
         dd_merge(acc, DD{o2.x, o2.y});
     }
@@ -2899,6 +2919,7 @@ __global__ void k_owner_merge(const OwnRec* __restrict__ recv, long long n, int 
     const long long r = i / nch;
     const int c = static_cast<int>(i - r * nch);
     const OwnRec& rec = recv[r];
+    SAD_CHECK(rec.id < static_cast<uint32_t>(cap));
     const double2 v = rec.v[c];
     if (v.x != 0.0 || v.y != 0.0) dd_atomic_merge(part + static_cast<size_t>(c) * cap + rec.id, DD{v.x, v.y});
 }

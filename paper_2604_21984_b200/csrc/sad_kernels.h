@@ -202,6 +202,8 @@ void launch_scatter_grads_out(const double2* grads, int cap, int n, double* out 
 
 // Number of kernel launches issued through these wrappers (process-wide; evidence counter).
 uint64_t launch_counter();
+// checked builds (-DSAD_CHECKED=1): kernel bound-check violations so far; -1 in the product build
+long long debug_check_failures();
 // Graph replays re-run captured launches without passing through the wrappers: account for them.
 void add_launches(uint64_t n);
 // Sets per-kernel attributes (opt-in shared memory); call once per device before launching.

@@ -979,6 +979,8 @@ sad_status sad_ctx_synchronize(sad_ctx* c) {
     return guard([&] { ck(cudaStreamSynchronize(c->stream), "sync"); });
 }
 
+long long sad_debug_check_failures(void) { return sadk::debug_check_failures(); }
+
 uint64_t sad_ctx_launch_count(const sad_ctx* c) { return sadk::launch_counter() - (c ? c->launches0 : 0); }
 
 // ====================================================================== candidates

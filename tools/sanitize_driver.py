@@ -1,7 +1,9 @@
-"""Small driver for compute-sanitizer (memcheck / racecheck / synccheck / initcheck): every kernel of
-libsad_b200.so once or twice at small sizes, each result checked against the CPU oracle so a run also
-proves the sanitised launches computed the right thing.
+"""Every kernel of the library once or twice at small sizes, each result checked against the CPU oracle.
+Run it under compute-sanitizer where that is available, and with the bound-checked build
+(SAD_LIB=paper_2604_21984_b200/libsad_b200_checked.so) everywhere: it then also reports the kernels'
+bound-check failures (tests/test_checked_build.py).
 
+    SAD_LIB=paper_2604_21984_b200/libsad_b200_checked.so python tools/sanitize_driver.py
     compute-sanitizer --tool racecheck python tools/sanitize_driver.py
 """
 import os
@@ -116,5 +118,6 @@ parts = G.fit_strips_loopback(img, cfg, 2)
 check("strips", all([sad.history_line(r) for r in p.history] == [sad.history_line(r) for r in single.history]
                     for p in parts))
 bad = [n for n, ok in checks if not ok]
-print(f"{len(checks)} checks, {len(bad)} mismatches {bad}")
-sys.exit(1 if bad else 0)
+fails = int(G.lib.sad_debug_check_failures())  # -1: product build (no bound checks compiled in)
+print(f"{len(checks)} checks, {len(bad)} mismatches {bad}; kernel bound-check failures: {fails}")
+sys.exit(1 if bad or fails > 0 else 0)
