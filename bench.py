@@ -57,6 +57,7 @@ def parse():
     p.add_argument("--c5-strips", action="store_true", help="config5: row-strip NCCL path even at N = 1")
     p.add_argument("--no-roofline-2048", action="store_true")
     p.add_argument("--no-paper-config", action="store_true", help="skip the paper-configuration encode timing")
+    p.add_argument("--no-configs", action="store_true", help="skip the config 1 / 3 / 5 measurements of the N=1 run")
     return p.parse_args()
 
 
@@ -282,12 +283,115 @@ def roofline_2048(G, iters=200, n_sites=100000):
     return out
 
 
-def run_config3(a):
-    """Config 3: 2048x2048 synthetic image, 100k sites, fit, then 1e6 random point queries."""
+def point_query_coords(W, H, nq=1_000_000):
+    """1e6 query coordinates from seeded_stream(5, 7, 9), one sequential xorshift32 stream."""
+    from paper_2604_21984_b200.synth import Rng
+    rng = Rng(5, 7, 9)
+    st = np.zeros(nq * 2, np.uint32)
+    x = int(rng.s)
+    for i in range(nq * 2):
+        x ^= (x << 13) & 0xFFFFFFFF
+        x ^= x >> 17
+        x ^= (x << 5) & 0xFFFFFFFF
+        st[i] = x
+    xy = np.empty((nq, 2), np.int32)
+    xy[:, 0] = st[0::2] % W
+    xy[:, 1] = st[1::2] % H
+    return xy
+
+
+def measure_config3(G, stream, iters=300, steps=1):
+    """Config 3: 2048x2048 synthetic image, 100k sites, `iters`-iteration fit, then 1e6 random point queries on
+    the fitted field (CUDA events on the library's stream)."""
     import torch
     import paper_2604_21984_b200 as sad
+    from paper_2604_21984_b200.synth import synthetic_image
+    W = H = 2048
+    cfg = sad.TrainConfig(iters=iters, n_sites=100000, fp64=False)
+    run = C.c_void_p()
+    cc = cfg.to_c()
+    G._call("fit_create", C.c_int(W), C.c_int(H), C.byref(cc), C.byref(run))
+    try:
+        img = synthetic_image(W, H, 3)
+        G._call("fit_set_target", run, img.ctypes.data_as(C.POINTER(C.c_double)))
+        G._call("fit_run_init", run)  # warm-up
+        ms = []
+        for _ in range(max(steps, 1)):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            G._call("fit_run_init", run)
+            e1.record(stream)
+            e1.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        nq = 1_000_000
+        dxy = torch.from_numpy(point_query_coords(W, H, nq)).cuda()
+        dids = torch.empty(nq * 16, dtype=torch.int32, device="cuda")
+        dw = torch.empty(nq * 16, dtype=torch.float64, device="cuda")
+        dn = torch.empty(nq, dtype=torch.int32, device="cuda")
+        args = (run, C.c_void_p(dxy.data_ptr()), C.c_size_t(nq), C.c_void_p(dids.data_ptr()),
+                C.c_void_p(dw.data_ptr()), C.c_void_p(dn.data_ptr()))
+        G._call("fit_point_query", *args)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(5):
+            G._call("fit_point_query", *args)
+        e1.record(stream)
+        e1.synchronize()
+        q_ms = e0.elapsed_time(e1) / 5
+    finally:
+        G.lib.sad_fit_destroy(run)
+    return {"point_queries_per_s": nq / (q_ms * 1e-3), "fit_ms": float(np.mean(ms)),
+            "fit_iters_per_s": iters / (np.mean(ms) * 1e-3),
+            "workload": f"config3: 2048x2048 synthetic, n_sites=100000, {iters}-iteration fit, then 1e6 random point "
+                        f"queries (seeded_stream(5,7,9)) on the fitted field"}
+
+
+def measure_config1(G):
+    """Config 1: 256x256, 4096 sites, 200 iterations, budget off, fp32 and fp64, through the API (warm)."""
+    import paper_2604_21984_b200 as sad
+    from paper_2604_21984_b200.synth import synthetic_image
+    img = sad.ImageBuffer(256, 256, synthetic_image(256, 256, 1))
+    out = {"workload": "config1: 256x256 synthetic, 4096 sites, 200 iterations, budget off"}
+    for fp64 in (False, True):
+        cfg = sad.TrainConfig(iters=200, n_sites=4096, fp64=fp64, seed=1)
+        G.fit(img, cfg)
+        t0 = time.perf_counter()
+        r = G.fit(img, cfg)
+        out["fp64" if fp64 else "fp32"] = {"fit_ms_e2e": (time.perf_counter() - t0) * 1e3,
+                                           "fit_ms_device": r.timing["total_ms"]}
+    return out
+
+
+def measure_config5(G, i0=20, i1=40, size=8192):
+    """Config 5 on one GPU: 8192x8192 at 2 BPP; marginal per-iteration device time between an i0- and an
+    i1-iteration fit (events of the default schedule included)."""
+    import paper_2604_21984_b200 as sad
+    from paper_2604_21984_b200.synth import synthetic_image
+    img = synthetic_image(size, size, 5)
+    res = {}
+    for iters in (5, i0, i1):
+        cfg = sad.TrainConfig(iters=iters, target_bpp=2.0, fp64=False)
+        run = C.c_void_p()
+        cc = cfg.to_c()
+        G._call("fit_create", C.c_int(size), C.c_int(size), C.byref(cc), C.byref(run))
+        try:
+            G._call("fit_set_target", run, img.ctypes.data_as(C.POINTER(C.c_double)))
+            G._call("fit_run_init", run)
+            tot, ph = C.c_double(), (C.c_double * 8)()
+            G._call("fit_timing", run, C.byref(tot), ph)
+            res[iters] = tot.value
+        finally:
+            G.lib.sad_fit_destroy(run)
+    per = (res[i1] - res[i0]) / (i1 - i0)
+    return {"ms_per_iter_marginal": per, "iters_per_s": 1e3 / per, "fit_ms": {str(k): v for k, v in res.items()},
+            "workload": f"config5: {size}x{size} synthetic (seed 5), 2 BPP, fp32, one GPU; marginal between a "
+                        f"{i0}- and a {i1}-iteration fit"}
+
+
+def run_config3(a):
+    """Config 3 as its own JSON line (bench.py --mode config3)."""
+    import torch
     from paper_2604_21984_b200 import api
-    from paper_2604_21984_b200.synth import Rng, synthetic_image
     stream = torch.cuda.Stream()  # explicit stream shared by the library and the timing events
     torch.cuda.set_stream(stream)
     lib = api.load_library()
@@ -295,56 +399,10 @@ def run_config3(a):
     if lib.sad_ctx_create(C.c_int(0), C.c_void_p(stream.cuda_stream), C.byref(ctx)):
         raise RuntimeError(lib.sad_last_error().decode())
     G = api.Backend(lib, "sad_", ctx=ctx)
-    W = H = 2048
-    cfg = sad.TrainConfig(iters=a.c3_iters, n_sites=100000, fp64=False)
-    run = C.c_void_p()
-    cc = cfg.to_c()
-    G._call("fit_create", C.c_int(W), C.c_int(H), C.byref(cc), C.byref(run))
-    img = synthetic_image(W, H, 3)
-    G._call("fit_set_target", run, img.ctypes.data_as(C.POINTER(C.c_double)))
-    G._call("fit_run_init", run)  # warm-up
-    ms = []
-    for _ in range(max(a.steps, 1)):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        G._call("fit_run_init", run)
-        e1.record(stream)
-        e1.synchronize()
-        ms.append(e0.elapsed_time(e1))
-    # 1e6 random point queries, coordinates from seeded_stream(5, 7, 9)
-    nq = 1_000_000
-    rng = Rng(5, 7, 9)
-    xy = np.empty((nq, 2), np.int32)
-    s = np.uint64(rng.s)
-    st = np.zeros(nq * 2, np.uint32)
-    x = int(rng.s)
-    for i in range(nq * 2):  # sequential xorshift32 stream
-        x ^= (x << 13) & 0xFFFFFFFF
-        x ^= x >> 17
-        x ^= (x << 5) & 0xFFFFFFFF
-        st[i] = x
-    xy[:, 0] = st[0::2] % W
-    xy[:, 1] = st[1::2] % H
-    dxy = torch.from_numpy(xy).cuda()
-    dids = torch.empty(nq * 16, dtype=torch.int32, device="cuda")
-    dw = torch.empty(nq * 16, dtype=torch.float64, device="cuda")
-    dn = torch.empty(nq, dtype=torch.int32, device="cuda")
-    args = (run, C.c_void_p(dxy.data_ptr()), C.c_size_t(nq), C.c_void_p(dids.data_ptr()),
-            C.c_void_p(dw.data_ptr()), C.c_void_p(dn.data_ptr()))
-    G._call("fit_point_query", *args)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(5):
-        G._call("fit_point_query", *args)
-    e1.record(stream)
-    e1.synchronize()
-    q_ms = e0.elapsed_time(e1) / 5
+    c3 = measure_config3(G, stream, a.c3_iters, a.steps)
     rf = roofline_2048(G, iters=a.c3_iters)
-    G.lib.sad_fit_destroy(run)
-    out = {"metric": METRIC, "mode": "config3", "value": nq / (q_ms * 1e-3), "unit": "point queries/s",
-           "fit_ms": float(np.mean(ms)), "fit_iters_per_s": a.c3_iters / (np.mean(ms) * 1e-3),
-           "config": {"workload": f"config3: 2048x2048 synthetic, n_sites=100000, {a.c3_iters}-iteration fit, "
-                                  f"then 1e6 random point queries (seeded_stream(5,7,9)) on the fitted field"},
+    out = {"metric": METRIC, "mode": "config3", "value": c3["point_queries_per_s"], "unit": "point queries/s",
+           "fit_ms": c3["fit_ms"], "fit_iters_per_s": c3["fit_iters_per_s"], "config": {"workload": c3["workload"]},
            "reference_pixel_weights_ms_per_query": 3.07, "roofline_2048": rf}
     print(json.dumps(out), flush=True)
 
@@ -642,6 +700,11 @@ def run_b200(a):
     rf2048 = None
     if rank == 0 and not a.no_roofline_2048:
         rf2048 = roofline_2048(G)
+    configs = None
+    if rank == 0 and world == 1 and not a.no_configs:
+        # the other single-GPU configurations of SURVEY §8d, measured in the same run (device time)
+        configs = {"config1": measure_config1(G), "config3": measure_config3(G, stream, 300, 1),
+                   "config5": measure_config5(G)}
     fp64_row = None
     if rank == 0 and world == 1:
         # the reference's default precision (TrainConfig.fp64 = true, types.hpp:162): all-double kernels
@@ -677,7 +740,7 @@ def run_b200(a):
             "e2e": {"value": e2e_val, "unit": "iters/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "encode_seconds": e2e_s / (a.steps * a.images_per_gpu)},
             "gpu_launches": launches, "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu,
-            "clocks": clk, "roofline_2048": rf2048, "paper_config": paper, "fp64": fp64_row,
+            "clocks": clk, "roofline_2048": rf2048, "paper_config": paper, "fp64": fp64_row, "configs": configs,
         }
         print(json.dumps(out), flush=True)
     for run in runs:
