@@ -12,6 +12,7 @@
 #define pixel_weights cpu_pixel_weights
 #define render_image cpu_render_image
 #define render_id_map cpu_render_id_map
+#define render_tau_map cpu_render_tau_map
 #define backward_image cpu_backward_image
 #define image_loss cpu_image_loss
 #define backward_pixel_grad cpu_backward_pixel_grad

@@ -5,10 +5,10 @@
 // in place of the reference's CPU definitions, so those tests run against libsad_b200.so.
 //
 // Replaced: jfa_seed, propagate_pass, run_passes, refresh, exact_topk(_batch) | pixel_weights,
-// render_image, render_id_map | backward_image, image_loss, backward_pixel_grad | init_sites, adam_step,
+// render_image, render_id_map, render_tau_map | backward_image, image_loss, backward_pixel_grad | init_sites, adam_step,
 // clamp_project, tau_diffusion, fit, fit_store | accumulate_stats, densify, prune, bpp_target_count,
 // plan_schedule, simulate_schedule.  Everything else (value types, codec, quality, GradBuffer,
-// TileReducer, for_each_contribution, the jump schedule helpers, render_tau_map, ...) is the reference's
+// TileReducer, for_each_contribution, the jump schedule helpers, boundary_map, ...) is the reference's
 // own code, built from its sources.
 #include "sad_b200_compat.hpp"
 
@@ -61,6 +61,14 @@ ImageBuffer render_image(const SiteStore& sites, const CandidateField& field, co
 
 std::vector<uint32_t> render_id_map(const SiteStore& sites, const CandidateField& field, const RunOpts&) {
     return b200::render_id_map(gpu(), sites, field);
+}
+
+// render_tau_map (render.cpp:157-163): the owner's log-temperature per pixel, owners from the device id map
+std::vector<double> render_tau_map(const SiteStore& sites, const CandidateField& field, const RunOpts& opts) {
+    std::vector<uint32_t> owners = render_id_map(sites, field, opts);
+    std::vector<double> out(owners.size());
+    for (size_t i = 0; i < owners.size(); i++) out[i] = sites.log_tau[owners[i]];
+    return out;
 }
 
 // ---------------------------------------------------------------- grad.hpp
