@@ -2872,7 +2872,11 @@ __global__ void k_owner_pack(const double2* __restrict__ part, int nch, RedTarge
                              int send_cap, unsigned long long* __restrict__ counts, int32_t* __restrict__ rcap_next,
                              int reset) {
     const int id = blockIdx.x * blockDim.x + threadIdx.x;
-    if (id >= st->n_sites) return;
+    if (id >= red.cap) return;
+    if (id >= st->n_sites) {  // unused slots claim no record space in the next pass's layout
+        if (rcap_next) rcap_next[id] = 0;
+        return;
+    }
     const int cl = red.cnt[id];
     if (rcap_next) {
         int want = active[id] ? cl + (cl >> 2) + 2 : 0;
