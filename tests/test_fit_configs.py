@@ -5,7 +5,8 @@
   the final map identical.
 * Config 2 (768x512 synthetic Kodak-shaped images, 2 BPP, 4000 iterations with 150 densify/prune
   events), image seeds 1-8 in fp32 and seed 1 in fp64 (the reference's default precision), and
-  config 3 (2048x2048, 100k sites, 300 iterations): the GPU fit against goldens of complete
+  config 3 (2048x2048, 100k sites, 300 iterations), and the config-5 shape (8192x8192, 2 BPP: 1.69M sites,
+  25 iterations incl. one densify event and its re-seeded refresh): the GPU fit against goldens of complete
   reference fits (tests/golden/fit_*.npz, written here by tests/golden/make_fit_golden.py from the
   unmodified reference library; a reference fit takes minutes per image, the GPU's under a second).
   Every history row (loss and PSNR as doubles, active count), the schedule scale, SHA-256 digests
@@ -116,3 +117,4 @@ def test_golden_set_present():
     names = {os.path.basename(p) for p in GOLDEN}
     assert sum(n.startswith("fit_config2_s") for n in names) >= 8
     assert "fit_config2_fp64_s1.npz" in names and "fit_config3_s1.npz" in names
+    assert "fit_config5_short_s5.npz" in names
