@@ -2262,8 +2262,10 @@ __device__ __forceinline__ DD red_total(const RedTarget& red, int id, int ch, in
     DD acc{o.x, o.y};
     const double2* rec = red.part + static_cast<size_t>(id) * red.maxt * red.stride + ch;
     if (red.roff) {
-        rec = red.part + static_cast<size_t>(red.roff[id]) * red.stride + ch;
+        const long long base = red.roff[id];
+        rec = red.part + static_cast<size_t>(base) * red.stride + ch;
         if (n > red.rcap[id]) n = red.rcap[id];
+        if (base + n > red.psize) n = static_cast<int>(red.psize - base > 0 ? red.psize - base : 0);
     }
     SAD_CHECK(!red.roff || n <= 0 || static_cast<long long>(red.roff[id]) + n <= red.psize);
     for (int s = 0; s < n; s++) {
@@ -2288,7 +2290,7 @@ __global__ void __launch_bounds__(128) k_finalize(RedTarget red, const DevState*
     const unsigned gmask = 0xffffu << (threadIdx.x & 16);
     const bool live = id < st->n_sites;
     int n = live ? red.cnt[id] : 0;
-    if (n > red.maxt) n = red.maxt;
+    if (!red.roff && n > red.maxt) n = red.maxt;  // (adaptive layout: red_total bounds n by rcap / the pool)
     if (live && lane16 < NCH) {
         const DD t = red_total(red, id, lane16, n);
         red.over[static_cast<size_t>(lane16) * red.cap + id] = make_double2(t.hi, t.lo);
@@ -3270,6 +3272,20 @@ void launch_math(const double* x, double* y, size_t n, int which, cudaStream_t s
 __global__ void k_fill_i32(int32_t* p, int n, int32_t v) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
+}
+
+// Stats record capacities from this pass's gradient record counts: a site's 8x8 stats tiles are halves of its
+// 16x8 backward tiles, so it claims at most twice as many stats records (+2 slack); unused slots claim none.
+__global__ void k_stats_plan(const int32_t* __restrict__ gcnt, const DevState* __restrict__ st, int cap,
+                             int32_t* __restrict__ rcap) {
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= cap) return;
+    rcap[id] = id < st->n_sites ? 2 * gcnt[id] + 2 : 0;
+}
+
+void launch_stats_plan(const int32_t* gcnt, const DevState* st, int cap, int32_t* rcap, cudaStream_t stream) {
+    k_stats_plan<<<(cap + 255) / 256, 256, 0, stream>>>(gcnt, st, cap, rcap);
+    SAD_LAUNCHED();
 }
 
 void launch_fill_i32(int32_t* p, int n, int32_t v, cudaStream_t stream) {

@@ -167,6 +167,7 @@ void launch_tau_mix(const uint64_t* uniq, const int* count, int max_items, int n
                     double* out, cudaStream_t stream);
 // Initial record plan: rcap = per_site for every slot (offsets follow from a scan).
 void launch_fill_i32(int32_t* p, int n, int32_t v, cudaStream_t stream);
+void launch_stats_plan(const int32_t* gcnt, const DevState* st, int cap, int32_t* rcap, cudaStream_t stream);
 void launch_clamp(const SitesDev& s, const DevState* st, const AdamHyper& hp, cudaStream_t stream);
 
 // ---------------------------------------------------------------- budget events

@@ -360,6 +360,19 @@ struct Workspace {
         return sadk::RedTarget{stats.p, spart.p, scnt.p, cap, maxt, 8, shead.p, snext.p, sopart.p, otops.p + 1, ocap,
                                nullptr, nullptr, 0};
     }
+    // Adaptive stats-record layout of the resident fit's events: capacities from the gradient record counts
+    // of the same pass (k_stats_plan), offsets by an exclusive scan; a pool of `spsize` 8-channel records
+    DBuf<double2> spool;
+    DBuf<int32_t> sroff, srcap;
+    long long spsize = 0;
+    sadk::RedTarget sred_adaptive() {
+        sadk::RedTarget t = sred();
+        t.roff = sroff.p;
+        t.rcap = srcap.p;
+        t.part = spool.p;
+        t.psize = spsize;
+        return t;
+    }
     // Adaptive gradient-record layout of the resident fit (see RedTarget): per-site capacity planned
     // from the previous pass, offsets by an exclusive scan, one pool.
     DBuf<double2> apool;
@@ -716,13 +729,30 @@ sadk::AdamHyper adam_hyper(const sad_train_config& c, int w, int h) {
     return hp;
 }
 
-void stats_device(Workspace& ws) {
+// accumulate_stats on the device.  from_grads: the gradient record counts of this pass are still live (the
+// resident fit's event iterations, between the backward and Adam), so the stats records get a planned
+// per-site layout instead of the fixed 16 slots + linked overflow records (long chains at 8x8 tiles).
+void stats_device(Workspace& ws, bool from_grads = false) {
     build_tables(ws, true, false, false, true);
     ws.zero_red(false);
     ws.zero_state_field(offsetof(DevState, valid), sizeof(uint64_t));
-    sadk::launch_stats(ws.ids[ws.cur].p, ws.rtab_d.p, ws.tgt_d.p, ws.fd, norm_scale(ws.fd.width, ws.fd.height),
-                       ws.sred(), ws.st.p, ws.stream);
-    sadk::launch_finalize(ws.sred(), 8, ws.st.p, ws.stream);
+    sadk::RedTarget red = ws.sred();
+    if (from_grads && ws.apsize > 0) {
+        const long long want = ws.apsize;  // >= the gradient records of a pass, typically 2-4x them
+        if (ws.spsize < want || !ws.spool.p) {
+            ws.spool.ensure(static_cast<size_t>(want) * 8);
+            ws.spsize = want;
+        }
+        ws.sroff.ensure(ws.cap);
+        ws.srcap.ensure(ws.cap);
+        sadk::launch_stats_plan(ws.gcnt.p, ws.st.p, ws.cap, ws.srcap.p, ws.stream);
+        size_t bytes = ws.cub_tmp.n;
+        ck(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, bytes, ws.srcap.p, ws.sroff.p, ws.cap, ws.stream), "DeviceScan");
+        red = ws.sred_adaptive();
+    }
+    sadk::launch_stats(ws.ids[ws.cur].p, ws.rtab_d.p, ws.tgt_d.p, ws.fd, norm_scale(ws.fd.width, ws.fd.height), red,
+                       ws.st.p, ws.stream);
+    sadk::launch_finalize(red, 8, ws.st.p, ws.stream);
 }
 
 void prune_device(Workspace& ws, double pct) {
@@ -1693,6 +1723,7 @@ static void finish_run(sad_fit_run* r, float ms, int n_rows) {
 
 // SAD_ADAM_ALL=1: plain-iteration Adam over every slot (A/B)
 static const bool g_adam_all = getenv("SAD_ADAM_ALL") != nullptr;
+static const bool g_stats_adaptive = getenv("SAD_STATS_FIXED") == nullptr;  // A/B: fixed stats record layout
 
 // fit_impl (train.cpp:221-291), resident in HBM.
 static void fit_loop(sad_fit_run* r) {
@@ -1869,7 +1900,7 @@ static void fit_loop(sad_fit_run* r) {
                                   ws.loss_part.p, ws.st.p, s);
             tau_step();
         });
-        mark(3, [&] { stats_device(ws); });
+        mark(3, [&] { stats_device(ws, g_stats_adaptive); });
         mark(2, [&] {
             sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.gred_adaptive(), ws.m.p, ws.v.p, hp, r->bc_table.p,
                               make_double2(0, 0), true, scale_n, nullptr, nullptr, ws.rcap.p, s, totals,
