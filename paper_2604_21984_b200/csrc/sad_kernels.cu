@@ -3009,6 +3009,61 @@ void launch_dd_values(const double2* dd, long long n, double* out, cudaStream_t 
     SAD_LAUNCHED();
 }
 
+// The loss of one backward call: the exact (double-double) sum of its per-block partials, always in
+// the order of a 1024-thread block (virtual thread j merges partials j, j + 1024, ...; a shuffle tree
+// per virtual warp, then one over the 32 warp sums) whatever the block size (1024 / V threads, each
+// warp playing V virtual warps with independent accumulators so their loads overlap), so k_advance
+// and k_adam's bookkeeping block produce the same bits.  Result in thread 0; parts: shared [32].
+template <int V>
+__device__ DD loss_total(const double2* __restrict__ part, int n, DD* parts) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = 32 / V;
+    DD acc[V];
+#pragma unroll
+    for (int v = 0; v < V; v++) acc[v] = DD{0.0, 0.0};
+    for (int base = lane; base < n; base += 1024) {
+#pragma unroll
+        for (int v = 0; v < V; v++) {
+            const int i = base + (warp + v * nw) * 32;
+            if (i < n) dd_merge(acc[v], DD{part[i].x, part[i].y});
+        }
+    }
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) {
+            DD o{__shfl_down_sync(0xffffffffu, acc[v].hi, d), __shfl_down_sync(0xffffffffu, acc[v].lo, d)};
+            dd_merge(acc[v], o);
+        }
+        if (lane == 0) parts[warp + v * nw] = acc[v];
+    }
+    __syncthreads();
+    DD t{0.0, 0.0};
+    if (threadIdx.x < 32) {
+        t = parts[threadIdx.x];
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) {
+            DD o{__shfl_down_sync(0xffffffffu, t.hi, d), __shfl_down_sync(0xffffffffu, t.lo, d)};
+            dd_merge(t, o);
+        }
+    }
+    return t;
+}
+
+// k_adam with AdvanceArgs: every Adam block reads t before it finishes; the last of the n to
+// finish advances t and resets the record pool top its blocks claimed from.
+__device__ __forceinline__ void adam_ticket(DevState* st, int32_t* otop, unsigned n) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (static_cast<unsigned>(atomicAdd(&st->ticket, 1)) == n - 1) {
+            __threadfence();
+            st->t += 1;
+            otop[2] = 0;
+            st->ticket = 0;
+        }
+    }
+}
+
 #ifndef SAD_ADAM_MINB
 #define SAD_ADAM_MINB 4  // resident 128-thread blocks per SM the register allocator must allow: 1 -> 4 measured
                          // config-2 fit 862.7 -> 854 ms (6: standalone faster, fit 869.7 ms)
@@ -3020,11 +3075,29 @@ __global__ void __launch_bounds__(128, SAD_ADAM_MINB) k_adam(SitesDev s, DevStat
                                               double scale, Q4<T>* pack, Q4<T>* gtab, int32_t* rcap_next,
                                               const double* __restrict__ totals, int32_t* roff_next,
                                               int32_t* pool_top, const uint32_t* __restrict__ act,
-                                              const int32_t* __restrict__ act_range) {
+                                              const int32_t* __restrict__ act_range, AdvanceArgs adv) {
     pdl_enter<4>();
     __shared__ int32_t s_want[8], s_base;
+    const bool book = adv.loss_hist != nullptr;
+    if (book && blockIdx.x == 0) {
+        // the bookkeeping block, dispatched first so its serial reduction overlaps the Adam blocks:
+        // k_advance's work except t and the record pool top, which the Adam blocks still read or claim
+        // from (adam_ticket does those)
+        __shared__ DD parts[32];
+        const DD loss = loss_total<8>(adv.loss_part, adv.n_part, parts);  // 128 threads
+        if (threadIdx.x == 0) {
+            const int it = st->iter;
+            adv.loss_hist[it] = make_double2(loss.hi, loss.lo);
+            if (adv.active_hist) adv.active_hist[it] = st->n_active;
+            st->iter = it + 1;
+            st->pass_index += static_cast<uint32_t>(adv.passes);
+            adv.otop[0] = 0;  // gradient overflow pool (read through the head/onext lists only)
+        }
+        return;
+    }
     const int lane16 = threadIdx.x & 15;
-    const int grp = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
+    const int bid = static_cast<int>(blockIdx.x) - (book ? 1 : 0);
+    const int grp = (bid * static_cast<int>(blockDim.x) + static_cast<int>(threadIdx.x)) >> 4;
     const unsigned gmask = 0xffffu << (threadIdx.x & 16);
     const int cap = s.cap;
     // with `act` (plain iterations) the groups walk the ascending active list: inactive sites have no
@@ -3034,7 +3107,12 @@ __global__ void __launch_bounds__(128, SAD_ADAM_MINB) k_adam(SitesDev s, DevStat
     // act_range (row-strip fits): only the owned slice act[a0, a1) of the active list
     const int a0 = act_range ? act_range[0] : 0;
     const int n_act = act_range ? act_range[1] - act_range[0] : (act ? st->n_active : 0);
-    if (act && static_cast<int>(blockIdx.x) * 8 >= n_act) return;
+    // blocks that read t and take the ticket: the ones with work (at least one)
+    const unsigned n_ticket = act ? static_cast<unsigned>(n_act > 0 ? (n_act + 7) / 8 : 1) : gridDim.x - 1;
+    if (act && bid * 8 >= n_act) {
+        if (book && bid == 0) adam_ticket(st, adv.otop, n_ticket);
+        return;
+    }
     const bool live = act ? grp < n_act : grp < st->n_sites;
     const int id = act ? (live ? static_cast<int>(act[a0 + grp]) : cap) : grp;
     const int k = lane16;
@@ -3170,22 +3248,25 @@ __global__ void __launch_bounds__(128, SAD_ADAM_MINB) k_adam(SitesDev s, DevStat
             gtab[3 * id + 2] = c;
         }
     }
+    if (book) adam_ticket(st, adv.otop, n_ticket);
 }
 
 void launch_adam(bool fp64, const SitesDev& s, DevState* st, const RedTarget& grads, double* m, double* v,
                  const AdamHyper& hp, const double2* bc_table, double2 bc_now, bool zero_grads, double scale,
                  void* pack, void* gtab, int32_t* rcap_next, cudaStream_t stream, const double* totals,
-                 int32_t* roff_next, int32_t* pool_top, const uint32_t* act, const int32_t* act_range) {
+                 int32_t* roff_next, int32_t* pool_top, const uint32_t* act, const int32_t* act_range,
+                 const AdvanceArgs& adv) {
     int grid = (s.cap + 7) / 8;  // 8 sites (16 lanes each) per 128-thread block
     if (grid < 1) grid = 1;
+    if (adv.loss_hist) grid += 1;  // + the bookkeeping block
     if (fp64)
         launch_pdl(k_adam<double>, dim3(grid), dim3(128), 0, stream, s, st, grads, m, v, hp, bc_table, bc_now,
                    zero_grads ? 1 : 0, scale, (Q4<double>*)pack, (Q4<double>*)gtab, rcap_next, totals, roff_next, pool_top,
-                   act, act_range);
+                   act, act_range, adv);
     else
         launch_pdl(k_adam<float>, dim3(grid), dim3(128), 0, stream, s, st, grads, m, v, hp, bc_table, bc_now,
                    zero_grads ? 1 : 0, scale, (Q4<float>*)pack, (Q4<float>*)gtab, rcap_next, totals, roff_next, pool_top,
-                   act, act_range);
+                   act, act_range, adv);
     SAD_LAUNCHED();
 }
 
@@ -3511,7 +3592,7 @@ void launch_flag_active(const SitesDev& s, const DevState* st, uint8_t* flags, c
 
 // ====================================================================== loop bookkeeping
 // End-of-iteration bookkeeping: loss = exact (double-double) sum of the per-tile partials, history
-// rows, pass index and Adam step.  1024 threads and two shuffle trees keep the serial part short.
+// rows, pass index and Adam step.
 __global__ void __launch_bounds__(1024) k_advance(DevState* st, int passes, int adam_steps, double2* loss_hist,
                                                   int32_t* active_hist, const double2* __restrict__ loss_part,
                                                   int n_part, int32_t* otop) {
@@ -3521,23 +3602,7 @@ __global__ void __launch_bounds__(1024) k_advance(DevState* st, int passes, int 
         otop[2] = 0;  // gradient record pool (claimed by the next k_adam)
     }
     __shared__ DD parts[32];
-    DD acc{0.0, 0.0};
-    if (loss_hist)
-        for (int i = threadIdx.x; i < n_part; i += blockDim.x) dd_merge(acc, DD{loss_part[i].x, loss_part[i].y});
-#pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) {
-        DD o{__shfl_down_sync(0xffffffffu, acc.hi, d), __shfl_down_sync(0xffffffffu, acc.lo, d)};
-        dd_merge(acc, o);
-    }
-    if ((threadIdx.x & 31) == 0) parts[threadIdx.x >> 5] = acc;
-    __syncthreads();
-    if (threadIdx.x >= 32) return;
-    acc = threadIdx.x < static_cast<int>(blockDim.x >> 5) ? parts[threadIdx.x] : DD{0.0, 0.0};
-#pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) {
-        DD o{__shfl_down_sync(0xffffffffu, acc.hi, d), __shfl_down_sync(0xffffffffu, acc.lo, d)};
-        dd_merge(acc, o);
-    }
+    const DD acc = loss_total<1>(loss_part, loss_hist ? n_part : 0, parts);
     if (threadIdx.x != 0) return;
     if (loss_hist) {
         loss_hist[st->iter] = make_double2(acc.hi, acc.lo);

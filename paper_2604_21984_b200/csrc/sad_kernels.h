@@ -31,6 +31,19 @@ struct DevState {
     uint64_t valid;       // StatsResult::valid_pixels
     uint64_t skipped;     // AdamState::skipped
     double2 loss;         // compensated loss sum of the current backward call
+    int32_t ticket;       // k_adam blocks finished (the last one advances t; reset by it)
+};
+
+// The end-of-iteration bookkeeping k_advance does, folded into a plain iteration's k_adam (one
+// extra block): history row, iter, pass_index and the overflow pool top; the last Adam block to
+// finish advances t and resets the record pool top.  loss_hist == nullptr: none.
+struct AdvanceArgs {
+    double2* loss_hist = nullptr;
+    int32_t* active_hist = nullptr;
+    const double2* loss_part = nullptr;
+    int n_part = 0;
+    int passes = 0;
+    int32_t* otop = nullptr;
 };
 
 struct SitesDev {
@@ -137,7 +150,7 @@ void launch_adam(bool fp64, const SitesDev& s, DevState* st, const RedTarget& gr
                  const AdamHyper& hp, const double2* bc_table, double2 bc_now, bool zero_grads, double scale,
                  void* pack, void* gtab, int32_t* rcap_next, cudaStream_t stream, const double* totals = nullptr,
                  int32_t* roff_next = nullptr, int32_t* pool_top = nullptr, const uint32_t* act = nullptr,
-                 const int32_t* act_range = nullptr);
+                 const int32_t* act_range = nullptr, const AdvanceArgs& adv = AdvanceArgs());
 void launch_math(const double* x, double* y, size_t n, int which, cudaStream_t stream);
 // row-strip fits (multi-GPU config 5)
 void launch_site_partials(const RedTarget& grads, const DevState* st, int cap, double2* out, cudaStream_t stream);

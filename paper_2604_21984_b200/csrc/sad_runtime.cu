@@ -1818,6 +1818,7 @@ static void fit_loop(sad_fit_run* r) {
     sadk::launch_advance(ws.st.p, static_cast<int>(full4.size()), 0, nullptr, nullptr, nullptr, 0, ws.otops.p, s);
 
     const bool use_graphs = getenv("SAD_NO_GRAPHS") == nullptr && !prof;
+    const bool fold_advance = getenv("SAD_NO_FOLD") == nullptr;
     // One plain iteration: warm pass(es) -> fused fwd+bwd -> Adam (+ tables for the next pass) ->
     // bookkeeping.  All per-iteration scalars live in DevState, so the sequence is replayable.
     auto plain_iteration = [&](bool rf) {
@@ -1831,16 +1832,28 @@ static void fit_loop(sad_fit_run* r) {
                                   ws.loss_part.p, ws.st.p, s);
             tau_step();
         });
+        // the iteration's bookkeeping rides in Adam's grid (AdvanceArgs) unless SAD_NO_FOLD is set
+        sadk::AdvanceArgs adv;
+        if (fold_advance) {
+            adv.loss_hist = r->loss_hist.p;
+            adv.active_hist = r->active_hist.p;
+            adv.loss_part = ws.loss_part.p;
+            adv.n_part = nbw;
+            adv.passes = np;
+            adv.otop = ws.otops.p;
+        }
         mark(2, [&] {
             // plain iterations: active sites only (event iterations below run every slot, which also
             // zeroes the record capacity of pruned slots before densify can reuse them)
             sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.gred_adaptive(), ws.m.p, ws.v.p, hp, r->bc_table.p,
                               make_double2(0, 0), true, scale_n, ws.pack.p, ws.gtab.p, ws.rcap.p, s, totals,
-                              ws.roff.p, ws.otops.p + 2, g_adam_all ? nullptr : ws.act.p);
+                              ws.roff.p, ws.otops.p + 2, g_adam_all ? nullptr : ws.act.p, nullptr, adv);
         });
-        mark(5, [&] {
-            sadk::launch_advance(ws.st.p, np, 1, r->loss_hist.p, r->active_hist.p, ws.loss_part.p, nbw, ws.otops.p, s);
-        });
+        if (!fold_advance)
+            mark(5, [&] {
+                sadk::launch_advance(ws.st.p, np, 1, r->loss_hist.p, r->active_hist.p, ws.loss_part.p, nbw,
+                                     ws.otops.p, s);
+            });
     };
     // SAD_STOP_AT=t (divergence hunting): stop after iteration t without the final refresh
     const int stop_at = getenv("SAD_STOP_AT") ? atoi(getenv("SAD_STOP_AT")) : 0;
