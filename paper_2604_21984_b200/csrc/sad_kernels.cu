@@ -2092,7 +2092,9 @@ int tile_row_quantum() {
     return lcm_c(lcm_c(BwdTile<float>::TH, BwdTile<double>::TH), kStatsTH);
 }
 
-int backward_blocks(bool fp64, const FieldDims& f) {
+int backward_ord_blocks(const FieldDims& f);
+int backward_blocks(bool fp64, const FieldDims& f, bool ordered) {
+    if (fp64 && ordered) return backward_ord_blocks(f);
     int tw = fp64 ? BwdTile<double>::TW : BwdTile<float>::TW, th = fp64 ? BwdTile<double>::TH : BwdTile<float>::TH;
     return ((f.width + tw - 1) / tw) * ((rows_of(f, f.height) + th - 1) / th);
 }
@@ -2132,15 +2134,28 @@ static void backward_t(const uint32_t* ids, const void* gtab, const void* tgt, c
     SAD_LAUNCHED();
 }
 
+template <int KM, int MODE>
+static void backward_ord_t(const uint32_t* ids, const void* gtab, const void* tgt, const FieldDims& f, double scale,
+                           const RedTarget& red, double2* loss_part, DevState* st, cudaStream_t stream);
+
 void launch_backward(bool fp64, int mode, const uint32_t* ids, const void* gtab, const void* tgt, const FieldDims& f,
                      double scale, const RedTarget& red, double2* loss_part, DevState* st, cudaStream_t stream) {
+#define SAD_BWD_ORD(KM)                                                                                 \
+    do {                                                                                               \
+        if (mode == 0) backward_ord_t<KM, 0>(ids, gtab, tgt, f, scale, red, loss_part, st, stream);     \
+        else if (mode == 1) backward_ord_t<KM, 1>(ids, gtab, tgt, f, scale, red, loss_part, st, stream); \
+        else backward_ord_t<KM, 2>(ids, gtab, tgt, f, scale, red, loss_part, st, stream);               \
+    } while (0)
 #define SAD_BWD(T, KM)                                                                                 \
     do {                                                                                               \
         if (mode == 0) backward_t<T, KM, 0>(ids, gtab, tgt, f, scale, red, loss_part, st, stream);      \
         else if (mode == 1) backward_t<T, KM, 1>(ids, gtab, tgt, f, scale, red, loss_part, st, stream); \
         else backward_t<T, KM, 2>(ids, gtab, tgt, f, scale, red, loss_part, st, stream);                \
     } while (0)
-    if (fp64) {
+    if (fp64 && red.tag) {  // the reference's summation order (k_backward_ord)
+        if (f.k <= 8) SAD_BWD_ORD(8);
+        else SAD_BWD_ORD(16);
+    } else if (fp64) {
         if (f.k <= 8) SAD_BWD(double, 8);
         else SAD_BWD(double, 16);
     } else {
@@ -2148,6 +2163,518 @@ void launch_backward(bool fp64, int mode, const uint32_t* ids, const void* gtab,
         else SAD_BWD(float, 16);
     }
 #undef SAD_BWD
+#undef SAD_BWD_ORD
+}
+
+bool fp64_ordered() {
+    static const bool on = getenv("SAD_FP64_DD") == nullptr;
+    return on;
+}
+
+// ====================================================================== fp64 backward in the reference's order
+// The reference's per-site sums are Accum cascades (accum.hpp:14-26: hi = fl(hi + x), lo += the
+// two-sum error), which are exact -- and so order-independent -- for float contributions but not for
+// doubles.  For fp64 the B200 path therefore replays the reference's order itself (backward_impl,
+// grad.cpp:242-289, at RunOpts::threads = 1, the library default, types.hpp:163-172):
+//   * 16x16 tiles in raster order; inside a tile the TileReducer (grad.cpp:37-64) with its 256-slot
+//     table, tile_hash and 8 linear probes (grad.hpp:67-90): a site that finds a slot accumulates a
+//     per-tile Accum over the tile's contributions in pixel-major order (pixels row-major, list slots
+//     in order) and is flushed into the buffer as add(hi), add(lo); a site that finds none overflows
+//     and each of its contributions is added to the buffer directly, in pixel order;
+//   * the output buffer then receives the worker buffer as add(hi), add(lo) (GradBuffer::merge), and
+//     grad() is hi + lo.
+// k_backward_ord emits one tagged record per (site, tile) Accum and one per overflowed contribution
+// (tag = tile << 9 | [0x100 | pixel] for raw contributions); ord_total replays a site's records in tag
+// order through the same Accum.  All arithmetic is the reference's (--fmad=false): contributions are
+// recomputed in the replay from the forward pass's weights and per-pixel state, with the same
+// expressions as k_backward, so every contribution has the same bits in both places.
+constexpr int kRefTile = 16;    // grad.cpp:81 kTile
+constexpr int kRefTable = 256;  // grad.hpp:67 TileReducer::kTableSize
+constexpr int kRefProbes = 8;   // grad.hpp:68 kMaxProbes
+constexpr uint32_t kTagRaw = 0x100u;
+__device__ __forceinline__ uint32_t ref_tile_hash(uint32_t site) { return (site * 2654435761u) >> 24; }
+
+// Accum::add (accum.hpp:14-21)
+__device__ __forceinline__ void ref_add(DD& a, double x) {
+    const double sum = __dadd_rn(a.hi, x);
+    const double bb = __dsub_rn(sum, a.hi);
+    const double err = __dadd_rn(__dsub_rn(a.hi, __dsub_rn(sum, bb)), __dsub_rn(x, bb));
+    a.hi = sum;
+    a.lo = __dadd_rn(a.lo, err);
+}
+
+template <int KM, int NPX>
+struct OrdTile {
+    uint32_t key[kRefTile * kRefTile * KM];  // kept candidate of entry e = pixel * KM + slot, else kEmpty
+    double w[kRefTile * kRefTile * KM];      // its normalised softmax weight
+    double pix[NPX][kRefTile * kRefTile];    // per pixel: g0 g1 g2 ch0 ch1 ch2 [t0 t1 t2 pl]
+    uint32_t tkey[kRefTable];                // the TileReducer table: site per slot (kEmpty: free)
+    uint32_t mask[kRefTable][kRefTile * kRefTile / 32];  // per slot: the tile pixels holding its site
+    DD warp_part[8];
+};
+
+// The eleven contribution components of one kept candidate (grad.cpp:193-238): the expressions of
+// k_backward in the same order.  Returns the number of non-finite components (scrubbed to zero).
+template <int NCH>
+__device__ __forceinline__ int ord_contrib(double fx, double fy, double wi, const Q4<double>& a, const Q4<double>& b,
+                                           const Q4<double>& c, double s, const double* pix, int pstride,
+                                           double (&v)[NCH]) {
+    constexpr double kTiny = 1e-18;
+    const double dx = fx - a.x, dy = fy - a.y;
+    const double pa = b.z * dx + b.w * dy;
+    const double pb = b.z * dy - b.w * dx;
+    double q = b.x * pa * pa + b.y * pb * pb;
+    if (q < 0.0) q = 0.0;
+    const double m = __dsqrt_rn(q);
+    const double l = -a.z * (m * s - a.w * s);
+    const double g0 = pix[0], g1 = pix[pstride], g2 = pix[2 * pstride];
+    const double ch0 = pix[3 * pstride], ch1 = pix[4 * pstride], ch2 = pix[5 * pstride];
+    const double dc0 = c.x - ch0, dc1 = c.y - ch1, dc2 = c.z - ch2;
+    const double A = wi * (g0 * dc0 + g1 * dc1 + g2 * dc2);
+    const double ts = a.z * s;
+    v[4] = wi * g0;
+    v[5] = wi * g1;
+    v[6] = wi * g2;
+    v[2] = A * l;
+    v[3] = A * ts;
+    if (m > kTiny) {
+        const double inv_n = __drcp_rn(m);
+        const double eau = b.x * pa;
+        const double iav = b.y * pb;
+        const double coef = A * ts * inv_n;
+        v[0] = coef * (eau * b.z - iav * b.w);
+        v[1] = coef * (eau * b.w + iav * b.z);
+        v[7] = -coef * (eau * dx + iav * dy);
+        v[8] = -coef * (eau * dy - iav * dx);
+        v[9] = -A * ts * 0.5 * inv_n * (eau * pa - iav * pb);
+    } else {
+        v[0] = v[1] = v[7] = v[8] = v[9] = 0.0;
+    }
+    if constexpr (NCH == 11) {
+        const double t0 = pix[6 * pstride], t1 = pix[7 * pstride], t2 = pix[8 * pstride], pl = pix[9 * pstride];
+        if (wi >= 1.0 - 1e-6) {
+            v[10] = 1e6;
+        } else {
+            const double inv_rest = __drcp_rn(1.0 - wi);
+            const double r0 = (ch0 - wi * c.x) * inv_rest - t0;
+            const double r1 = (ch1 - wi * c.y) * inv_rest - t1;
+            const double r2 = (ch2 - wi * c.z) * inv_rest - t2;
+            v[10] = r0 * r0 + r1 * r1 + r2 * r2 - pl;
+        }
+    }
+    int bad = 0;
+#pragma unroll
+    for (int t = 0; t < NCH; t++)
+        if (!c_finite(v[t])) {
+            v[t] = 0.0;
+            bad++;
+        }
+    return bad;
+}
+
+// One tagged record for `site`: its next slice slot, else the overflow pool; a full pool (the caller
+// sized it too small) falls back to a double-double CAS into `over` and flags st->err bit 3.
+template <int NCH>
+__device__ __forceinline__ void ord_store(const RedTarget& red, uint32_t site, uint32_t tag, const double (&hi)[NCH],
+                                          const double (&lo)[NCH], DevState* st) {
+    const int slot = atomicAdd(red.cnt + site, 1);
+    double2* dst = nullptr;
+    if (red.roff) {
+        const long long rec = static_cast<long long>(red.roff[site]) + slot;
+        if (slot < red.rcap[site] && rec < red.psize) {
+            dst = red.part + static_cast<size_t>(rec) * red.stride;
+            red.tag[rec] = tag;
+        }
+    } else if (slot < red.maxt) {
+        const size_t rec = static_cast<size_t>(site) * red.maxt + slot;
+        dst = red.part + rec * red.stride;
+        red.tag[rec] = tag;
+    }
+    if (!dst) {
+        const int ro = atomicAdd(red.otop, 1);
+        if (ro < red.ocap) {
+            dst = red.opart + static_cast<size_t>(ro) * red.stride;
+            red.otag[ro] = tag;
+            __threadfence();
+            red.onext[ro] = atomicExch(red.head + site, ro);
+        }
+    }
+    if (dst) {
+#pragma unroll
+        for (int ch = 0; ch < NCH; ch++) dst[ch] = make_double2(hi[ch], lo[ch]);
+    } else {
+        atomicOr(&st->err, 8);
+#pragma unroll
+        for (int ch = 0; ch < NCH; ch++)
+            dd_atomic_merge(red.over + static_cast<size_t>(ch) * red.cap + site, DD{hi[ch], lo[ch]});
+    }
+}
+
+template <int KM, int MODE>
+__global__ void __launch_bounds__(256) k_backward_ord(const uint32_t* __restrict__ ids, const Q4<double>* __restrict__ gtab,
+                                                      const double* __restrict__ tgt, FieldDims f, double s,
+                                                      double inv_hw2, RedTarget red, double2* __restrict__ loss_part,
+                                                      DevState* st) {
+    constexpr int NCH = MODE == 1 ? 11 : 10, NPX = MODE == 1 ? 10 : 6, NP = kRefTile * kRefTile;
+    using Sm = OrdTile<KM, NPX>;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    Sm& sm = *reinterpret_cast<Sm*>(smraw);
+    const int tid = threadIdx.x;
+    const int px = blockIdx.x * kRefTile + (tid % kRefTile);
+    const int py = blockIdx.y * kRefTile + (tid / kRefTile) + f.row0;
+    const bool inside = px < f.width && py < f.height && py < f.row1;
+    const uint32_t tile = blockIdx.y * gridDim.x + blockIdx.x;  // raster order of the reference's tiles
+    sm.tkey[tid] = kEmpty;
+#pragma unroll
+    for (int j = 0; j < NP / 32; j++) sm.mask[tid][j] = 0u;
+    const double fx = static_cast<double>(px), fy = static_cast<double>(py);
+
+    // ---- forward of this thread's pixel (k_backward's first half, same expressions)
+    unsigned long long nonfinite = 0;
+    DD loss{0.0, 0.0};
+    {
+        uint32_t cid[KM];
+        double lg[KM], w[KM];
+        bool ok[KM];
+        bool any = false;
+        double best = 0.0;
+        const uint32_t* lst = ids + static_cast<size_t>(f.k) * cell_index(f, px, py);
+        bool stop = !inside;
+#pragma unroll
+        for (int i = 0; i < KM; i++) {
+            uint32_t id = kEmpty;
+            if (!stop && i < f.k) id = lst[i];
+            stop = stop || id == kEmpty;
+            cid[i] = id;
+            ok[i] = false;
+            lg[i] = 0.0;
+            w[i] = 0.0;
+            if (!stop) {
+                const Q4<double> a = gtab[3 * id], b = gtab[3 * id + 1];
+                const double act = gtab[3 * id + 2].w;
+                const double dx = fx - a.x, dy = fy - a.y;
+                const double pa = b.z * dx + b.w * dy;
+                const double pb = b.z * dy - b.w * dx;
+                double q = b.x * pa * pa + b.y * pb * pb;
+                if (q < 0.0) q = 0.0;
+                const double m = __dsqrt_rn(q);
+                const double l = -a.z * (m * s - a.w * s);
+                ok[i] = act != 0.0 && c_finite(l);
+                lg[i] = l;
+                if (ok[i] && (!any || l > best)) best = l;
+                any = any || ok[i];
+            }
+        }
+        if (inside && !any) atomicOr(&st->err, 1);
+        double ch0 = 0.0, ch1 = 0.0, ch2 = 0.0, g0 = 0.0, g1 = 0.0, g2 = 0.0, t0 = 0.0, t1 = 0.0, t2 = 0.0, pl = 0.0;
+        if (any) {
+            double wsum = 0.0;
+#pragma unroll
+            for (int i = 0; i < KM; i++) {
+                w[i] = 0.0;
+                if (ok[i]) {
+                    w[i] = sad_dexp(lg[i] - best);
+                    wsum += w[i];
+                }
+            }
+            const double invw = __drcp_rn(wsum);
+#pragma unroll
+            for (int i = 0; i < KM; i++)
+                if (ok[i]) {
+                    w[i] *= invw;
+                    const Q4<double> c = gtab[3 * cid[i] + 2];
+                    ch0 += w[i] * c.x;
+                    ch1 += w[i] * c.y;
+                    ch2 += w[i] * c.z;
+                }
+            const double* tp = tgt + 3 * (static_cast<size_t>(py) * f.width + px);
+            if (MODE != 2) {
+                t0 = tp[0];
+                t1 = tp[1];
+                t2 = tp[2];
+                const double e0 = ch0 - t0, e1 = ch1 - t1, e2 = ch2 - t2;
+                pl = e0 * e0 + e1 * e1 + e2 * e2;
+                double plv = pl;
+                if (!c_finite(pl)) {
+                    nonfinite++;
+                    plv = 0;
+                }
+                dd_add(loss, plv);
+                g0 = inv_hw2 * e0;
+                g1 = inv_hw2 * e1;
+                g2 = inv_hw2 * e2;
+            } else {
+                g0 = tp[0];
+                g1 = tp[1];
+                g2 = tp[2];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < KM; i++) {
+            sm.key[tid * KM + i] = any && ok[i] ? cid[i] : kEmpty;
+            sm.w[tid * KM + i] = w[i];
+        }
+        sm.pix[0][tid] = g0;
+        sm.pix[1][tid] = g1;
+        sm.pix[2][tid] = g2;
+        sm.pix[3][tid] = ch0;
+        sm.pix[4][tid] = ch1;
+        sm.pix[5][tid] = ch2;
+        if constexpr (NPX == 10) {
+            sm.pix[6][tid] = t0;
+            sm.pix[7][tid] = t1;
+            sm.pix[8][tid] = t2;
+            sm.pix[9][tid] = pl;
+        }
+    }
+    __syncthreads();
+
+    // ---- warp 0 replays the TileReducer's inserts in entry order (grad.cpp:40-57): only a site's
+    // first appearance can change the table, so each batch of 32 entries first drops the ones whose
+    // site already holds one of its probe slots, then inserts the rest one by one in entry order
+    if (tid < 32) {
+        for (int base = 0; base < NP * KM; base += 32) {
+            const uint32_t k = sm.key[base + tid];
+            bool need = false;
+            if (k != kEmpty) {
+                const uint32_t h = ref_tile_hash(k);
+                bool found = false;
+#pragma unroll
+                for (int q = 0; q < kRefProbes; q++) found |= sm.tkey[(h + q) & (kRefTable - 1)] == k;
+                need = !found;
+            }
+            unsigned todo = __ballot_sync(0xffffffffu, need);
+            while (todo) {
+                const int l = __ffs(todo) - 1;
+                todo &= todo - 1;
+                const uint32_t kk = __shfl_sync(0xffffffffu, k, l);
+                const uint32_t slot = (ref_tile_hash(kk) + (tid & (kRefProbes - 1))) & (kRefTable - 1);
+                const uint32_t t = sm.tkey[slot];
+                // the probe stops at the first free slot or at the site itself; none: overflow
+                const unsigned hit = __ballot_sync(0xffffffffu, tid < kRefProbes && (t == kEmpty || t == kk));
+                if (hit && tid == __ffs(hit) - 1 && t == kEmpty) sm.tkey[slot] = kk;
+                __syncwarp();
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- each entry: its table slot (pixel bit in the slot's mask) or, overflowed, a raw record now
+    const double* pix = &sm.pix[0][tid];
+#pragma unroll 1
+    for (int i = 0; i < KM; i++) {
+        const uint32_t k = sm.key[tid * KM + i];
+        if (k == kEmpty) continue;
+        const uint32_t h = ref_tile_hash(k);
+        int u = -1;
+#pragma unroll
+        for (int q = kRefProbes - 1; q >= 0; q--)
+            if (sm.tkey[(h + q) & (kRefTable - 1)] == k) u = static_cast<int>((h + q) & (kRefTable - 1));
+        if (u >= 0) {
+            atomicOr(&sm.mask[u][tid >> 5], 1u << (tid & 31));
+        } else {
+            double v[NCH], z[NCH];
+            nonfinite += ord_contrib<NCH>(fx, fy, sm.w[tid * KM + i], gtab[3 * k], gtab[3 * k + 1], gtab[3 * k + 2], s,
+                                          pix, NP, v);
+#pragma unroll
+            for (int ch = 0; ch < NCH; ch++) z[ch] = 0.0;
+            ord_store<NCH>(red, k, (tile << 9) | kTagRaw | static_cast<uint32_t>(tid), v, z, st);
+        }
+    }
+    __syncthreads();
+
+    // ---- thread u: the per-tile Accum of the site in table slot u, over its pixels in order
+    {
+        const uint32_t site = sm.tkey[tid];
+        if (site != kEmpty) {
+            const Q4<double> a = gtab[3 * site], b = gtab[3 * site + 1], c = gtab[3 * site + 2];
+            DD acc[NCH];
+#pragma unroll
+            for (int ch = 0; ch < NCH; ch++) acc[ch] = DD{0.0, 0.0};
+#pragma unroll 1
+            for (int j = 0; j < NP / 32; j++) {
+                unsigned mbits = sm.mask[tid][j];
+                while (mbits) {
+                    const int p = j * 32 + __ffs(mbits) - 1;
+                    mbits &= mbits - 1;
+                    int e = p * KM;
+#pragma unroll 1
+                    while (sm.key[e] != site) e++;
+                    const double ffx = static_cast<double>(blockIdx.x * kRefTile + (p % kRefTile));
+                    const double ffy = static_cast<double>(blockIdx.y * kRefTile + (p / kRefTile) + f.row0);
+                    double v[NCH];
+                    nonfinite += ord_contrib<NCH>(ffx, ffy, sm.w[e], a, b, c, s, &sm.pix[0][p], NP, v);
+#pragma unroll
+                    for (int ch = 0; ch < NCH; ch++) ref_add(acc[ch], v[ch]);
+                }
+            }
+            double hi[NCH], lo[NCH];
+#pragma unroll
+            for (int ch = 0; ch < NCH; ch++) {
+                hi[ch] = acc[ch].hi;
+                lo[ch] = acc[ch].lo;
+            }
+            ord_store<NCH>(red, site, tile << 9, hi, lo, st);
+        }
+    }
+    __syncthreads();
+    if (MODE != 2) block_dd_store<NP>(loss, sm.warp_part, loss_part + blockIdx.y * gridDim.x + blockIdx.x);
+    __syncthreads();
+    unsigned long long nf = block_sum_u64<NP>(nonfinite, reinterpret_cast<unsigned long long*>(sm.warp_part));
+    if (threadIdx.x == 0 && nf) atomicAdd(reinterpret_cast<unsigned long long*>(&st->nonfinite), nf);
+}
+
+int backward_ord_blocks(const FieldDims& f) {
+    return ((f.width + kRefTile - 1) / kRefTile) * ((rows_of(f, f.height) + kRefTile - 1) / kRefTile);
+}
+
+template <int KM, int MODE>
+static void backward_ord_t(const uint32_t* ids, const void* gtab, const void* tgt, const FieldDims& f, double scale,
+                           const RedTarget& red, double2* loss_part, DevState* st, cudaStream_t stream) {
+    constexpr int NPX = MODE == 1 ? 10 : 6;
+    const size_t smem = sizeof(OrdTile<KM, NPX>);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_backward_ord<KM, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    dim3 grid((f.width + kRefTile - 1) / kRefTile, (rows_of(f, f.height) + kRefTile - 1) / kRefTile);
+    const double inv_hw2 = 2.0 / (static_cast<double>(f.width) * f.height);
+    k_backward_ord<KM, MODE><<<grid, kRefTile * kRefTile, smem, stream>>>(
+        ids, (const Q4<double>*)gtab, (const double*)tgt, f, scale, inv_hw2, red, loss_part, st);
+    SAD_LAUNCHED();
+}
+
+// ---- replay of one site's records in tag order (grad.cpp:59-64 flushes, :285-288 merge): one warp
+// per site; up to kOrdFast records are ranked in shared memory, more take a selection walk over the
+// tags in global memory.  Lane ch < NCH replays channel ch; returns the output Accum of the channel.
+constexpr int kOrdFast = 128;
+struct OrdRef {
+    uint32_t tag;
+    int32_t rec;  // >= 0: part record, < 0: opart record ~rec
+};
+
+template <int NCH>
+__device__ DD ord_total(const RedTarget& red, int id, int n_slice, long long base, OrdRef* buf, int* sorted) {
+    const int lane = threadIdx.x & 31;
+    // gather: the slice, then the overflow list (walked by lane 0)
+    int n = n_slice;
+    for (int j = lane; j < n_slice && j < kOrdFast; j += 32)
+        buf[j] = OrdRef{red.tag[base + j], static_cast<int32_t>(base + j)};
+    if (lane == 0) {
+        for (int r = red.head[id]; r >= 0; r = red.onext[r]) {
+            if (n < kOrdFast) buf[n] = OrdRef{red.otag[r], ~r};
+            n++;
+        }
+    }
+    n = __shfl_sync(0xffffffffu, n, 0);
+    __syncwarp();
+    DD buf_acc{0.0, 0.0};
+    auto replay = [&](int32_t rec, uint32_t tag) {
+        if (lane >= NCH) return;
+        const double2 v = rec >= 0 ? red.part[static_cast<size_t>(rec) * red.stride + lane]
+                                   : red.opart[static_cast<size_t>(~rec) * red.stride + lane];
+        ref_add(buf_acc, v.x);
+        if (!(tag & kTagRaw)) ref_add(buf_acc, v.y);
+    };
+    if (n <= kOrdFast) {
+        for (int j = lane; j < n; j += 32) {
+            const uint32_t t = buf[j].tag;
+            int rank = 0;
+            for (int q = 0; q < n; q++) rank += buf[q].tag < t;
+            sorted[rank] = j;
+        }
+        __syncwarp();
+        for (int r = 0; r < n; r++) {
+            const OrdRef o = buf[sorted[r]];
+            replay(o.rec, o.tag);
+        }
+    } else {
+        // selection walk: the next larger tag each step (tags of one site are distinct)
+        long long last = -1;
+        for (int step = 0; step < n; step++) {
+            unsigned best = 0xffffffffu;
+            int32_t brec = 0;
+            for (int j = lane; j < n_slice; j += 32) {
+                const uint32_t t = red.tag[base + j];
+                if (static_cast<long long>(t) > last && t <= best) {
+                    best = t;
+                    brec = static_cast<int32_t>(base + j);
+                }
+            }
+            if (lane == 0)
+                for (int r = red.head[id]; r >= 0; r = red.onext[r]) {
+                    const uint32_t t = red.otag[r];
+                    if (static_cast<long long>(t) > last && t <= best) {
+                        best = t;
+                        brec = ~r;
+                    }
+                }
+            const unsigned m = __reduce_min_sync(0xffffffffu, best);
+            const int src = __ffs(__ballot_sync(0xffffffffu, best == m)) - 1;
+            const int32_t rec = __shfl_sync(0xffffffffu, brec, src);
+            replay(rec, m);
+            last = m;
+        }
+    }
+    // GradBuffer::merge into the zeroed output (grad.cpp:285-288): add(hi), add(lo); a full record
+    // pool's CAS totals (st->err bit 3) come last
+    DD out{0.0, 0.0};
+    ref_add(out, buf_acc.hi);
+    ref_add(out, buf_acc.lo);
+    if (lane < NCH) {
+        const double2 o = red.over[static_cast<size_t>(lane) * red.cap + id];
+        if (o.x != 0.0 || o.y != 0.0) dd_merge(out, DD{o.x, o.y});
+    }
+    return out;
+}
+
+// per-site slice bounds of either record layout
+__device__ __forceinline__ int ord_slice(const RedTarget& red, int id, long long& base) {
+    int n = red.cnt[id];
+    if (red.roff) {
+        base = red.roff[id];
+        if (n > red.rcap[id]) n = red.rcap[id];
+        if (base + n > red.psize) n = static_cast<int>(red.psize - base > 0 ? red.psize - base : 0);
+    } else {
+        base = static_cast<long long>(id) * red.maxt;
+        if (n > red.maxt) n = red.maxt;
+    }
+    return n;
+}
+
+// Ordered totals of every live site: values (hi + lo, GradBuffer::grad) into tot[ch][cap] and, with
+// `dd`, the output Accums into red.over (the per-call GradBuffer); with `reset` the counters too.
+template <int NCH>
+__global__ void __launch_bounds__(128) k_ordered_totals(RedTarget red, const DevState* __restrict__ st,
+                                                        double* __restrict__ tot, double* __restrict__ g0, int reset) {
+    __shared__ OrdRef buf[4][kOrdFast];
+    __shared__ int sorted[4][kOrdFast];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int id = blockIdx.x * 4 + warp;
+    if (id >= st->n_sites) return;
+    long long base = 0;
+    const int n_slice = ord_slice(red, id, base);
+    const DD t = ord_total<NCH>(red, id, n_slice, base, buf[warp], sorted[warp]);
+    if (lane < NCH) {
+        if (tot) tot[static_cast<size_t>(lane) * red.cap + id] = t.hi + t.lo;
+        if (g0 && lane == 2) g0[id] = t.hi + t.lo;
+        if (!tot) red.over[static_cast<size_t>(lane) * red.cap + id] = make_double2(t.hi, t.lo);
+    }
+    __syncwarp();
+    if (reset && lane == 0) {
+        red.cnt[id] = 0;
+        red.head[id] = -1;
+    }
+}
+
+void launch_ordered_totals(const RedTarget& red, int n_ch, const DevState* st, double* tot, double* g0, bool reset,
+                           cudaStream_t stream) {
+    int grid = (red.cap + 3) / 4;
+    if (grid < 1) grid = 1;
+    if (n_ch == 11) k_ordered_totals<11><<<grid, 128, 0, stream>>>(red, st, tot, g0, reset ? 1 : 0);
+    else k_ordered_totals<10><<<grid, 128, 0, stream>>>(red, st, tot, g0, reset ? 1 : 0);
+    SAD_LAUNCHED();
 }
 
 // ====================================================================== image_loss (grad.cpp:291-360)

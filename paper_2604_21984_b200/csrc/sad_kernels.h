@@ -76,6 +76,10 @@ struct RedTarget {
     const int32_t* roff;
     int32_t* rcap;
     long long psize;
+    // fp64 backward in the reference's summation order (k_backward_ord): one order tag per record
+    // (tag[rec] for part, otag[r] for opart); nullptr: the double-double path
+    uint32_t* tag = nullptr;
+    uint32_t* otag = nullptr;
 };
 
 struct FieldDims {
@@ -125,7 +129,14 @@ void launch_pixel_weights(const uint32_t* ids, const void* rtab_d, const FieldDi
 // ---------------------------------------------------------------- backward / loss / stats
 // mode: 0 = MSE target, 1 = MSE target + removal delta, 2 = caller adjoint (pixgrad)
 // Per-block loss partials go to loss_part[block]; launch_loss_reduce / launch_advance reduce them.
-int backward_blocks(bool fp64, const FieldDims& f);
+int backward_blocks(bool fp64, const FieldDims& f, bool ordered = false);
+// fp64 in the reference's summation order (default; SAD_FP64_DD=1 selects the double-double path):
+// the runtime then passes RedTargets with order tags, launch_backward runs k_backward_ord, and the
+// totals come from launch_ordered_totals (GradBuffer Accums into red.over with tot == nullptr, else
+// values into tot[ch][cap], g0 = channel 2) instead of k_finalize / the Adam merge.
+bool fp64_ordered();
+void launch_ordered_totals(const RedTarget& red, int n_ch, const DevState* st, double* tot, double* g0, bool reset,
+                           cudaStream_t stream);
 // Row quantum of the per-tile kernels (least common multiple of the fp32/fp64 backward and the stats
 // tile heights): row strips that are multiples of it never split a tile.
 int tile_row_quantum();

@@ -386,6 +386,26 @@ struct Workspace {
         t.psize = apsize;
         return t;
     }
+    // order tags of the fp64 reference-order reduction (sadk::fp64_ordered): per record of gpart
+    // (cap * maxt), of the adaptive pool and of the overflow pool; per-site values for Adam
+    DBuf<uint32_t> gtag, atag, otag;
+    DBuf<double> otot;
+    sadk::RedTarget gred_ord() {
+        sadk::RedTarget t = gred();
+        gtag.ensure(static_cast<size_t>(cap) * maxt);
+        otag.ensure(static_cast<size_t>(ocap));
+        t.tag = gtag.p;
+        t.otag = otag.p;
+        return t;
+    }
+    sadk::RedTarget gred_adaptive_ord() {
+        sadk::RedTarget t = gred_adaptive();
+        atag.ensure(static_cast<size_t>(apsize));
+        otag.ensure(static_cast<size_t>(ocap));
+        t.tag = atag.p;
+        t.otag = otag.p;
+        return t;
+    }
     void ensure_adaptive(size_t tiles) {
         long long want = apsize_force ? apsize_force : 16ll * cap + 64ll * static_cast<long long>(tiles);
         if (apsize < want || !apool.p) {
@@ -1339,18 +1359,28 @@ static void backward_call(sad_ctx* c, const sad_sites_view* s_in, const sad_fiel
     ws.zero_red(true);
     ws.zero_state_field(offsetof(DevState, nonfinite), sizeof(uint64_t));
     ws.zero_state_field(offsetof(DevState, loss), sizeof(double2));
+    const bool ordered = fp64 && sadk::fp64_ordered();
+    const sadk::RedTarget red = ordered ? ws.gred_ord() : ws.gred();
     sadk::launch_backward(fp64 != 0, mode, ws.ids[ws.cur].p, ws.gtab.p,
                           fp64 ? static_cast<const void*>(ws.tgt_d.p) : static_cast<const void*>(ws.tgt_f.p), ws.fd,
-                          norm_scale(f->width, f->height), ws.gred(), ws.loss_part.p, ws.st.p, ws.stream);
-    sadk::launch_finalize(ws.gred(), mode == 1 ? 11 : 10, ws.st.p, ws.stream);  // channel 10 only with removal
+                          norm_scale(f->width, f->height), red, ws.loss_part.p, ws.st.p, ws.stream);
+    // channel 10 only with removal
+    if (ordered) sadk::launch_ordered_totals(red, mode == 1 ? 11 : 10, ws.st.p, nullptr, nullptr, true, ws.stream);
+    else sadk::launch_finalize(red, mode == 1 ? 11 : 10, ws.st.p, ws.stream);
     if (mode != 2)
-        sadk::launch_loss_reduce(ws.loss_part.p, sadk::backward_blocks(fp64 != 0, ws.fd), &ws.st.p->loss, ws.stream);
+        sadk::launch_loss_reduce(ws.loss_part.p, sadk::backward_blocks(fp64 != 0, ws.fd, ordered), &ws.st.p->loss,
+                                 ws.stream);
     DBuf<double> out;
     size_t n = s->size;
     out.ensure(std::max<size_t>(n, 1) * 11);
     if (n) sadk::launch_scatter_grads_out(ws.grads.p, ws.cap, static_cast<int>(n), out.p, ws.stream);
     if (n) ck(cudaMemcpyAsync(grads, out.p, n * 11 * 8, cudaMemcpyDeviceToHost, ws.stream), "D2H grads");
     DevState st = ws.get_state();
+    if (st.err & 8) {
+        ws.zero_state_field(offsetof(DevState, err), sizeof(int32_t));
+        std::fprintf(stderr, "sad: fp64 ordered reduction: record pools full, some sums merged as double-doubles "
+                             "(raise SAD_OCAP)\n");
+    }
     if (st.err & 1) {
         ws.zero_state_field(offsetof(DevState, err), sizeof(int32_t));
         fail(SAD_EEMPTY, "backward: empty candidate list at a pixel");
@@ -1717,6 +1747,9 @@ static void finish_run(sad_fit_run* r, float ms, int n_rows) {
     r->done = true;
     if (fs.err & 1) fail(SAD_EEMPTY, "backward: empty candidate list at a pixel");
     if (fs.err & 2) fail(SAD_ENOMEM, "fit: site capacity exhausted");
+    if (fs.err & 8)
+        std::fprintf(stderr, "sad: fp64 ordered reduction: record pools full, some sums merged as double-doubles "
+                             "(raise SAD_OCAP)\n");
     for (int t = 0; t < n_rows; t++)
         if (!std::isfinite(r->hist[t].loss)) fail(SAD_ENUMERIC, "fit: non-finite loss");
 }
@@ -1767,10 +1800,19 @@ static void fit_loop(sad_fit_run* r) {
     const bool tau = c.tau_diffusion_lambda > 0;
     if (tau && c.iters >= 1 && c.tau_diffusion_lambda > 1) fail(SAD_EINVAL, "tau_diffusion: lambda out of [0,1]");
     if (tau) ensure_tau(ws);
-    const double* totals = tau ? ws.tb.tot.p : nullptr;
+    // fp64: per-site sums in the reference's order (sadk::fp64_ordered): tagged records, then the ordered
+    // totals (values) for Adam; tau_diffusion then works on those values as on the double-double ones
+    const bool ordered = fp64 && sadk::fp64_ordered();
+    if (ordered) ws.otot.ensure(10 * static_cast<size_t>(ws.cap));
+    auto gred = [&] { return ordered ? ws.gred_adaptive_ord() : ws.gred_adaptive(); };
+    if (ordered) (void)gred();  // the tag arrays exist before any graph capture
+    const double* totals = tau ? ws.tb.tot.p : ordered ? ws.otot.p : nullptr;
     auto tau_step = [&] {
+        if (ordered)
+            sadk::launch_ordered_totals(gred(), 10, ws.st.p, const_cast<double*>(totals), tau ? ws.tb.g0.p : nullptr,
+                                        false, s);
         if (!tau) return;
-        sadk::launch_site_totals(ws.gred_adaptive(), ws.st.p, ws.cap, ws.tb.tot.p, ws.tb.g0.p, s);
+        if (!ordered) sadk::launch_site_totals(gred(), ws.st.p, ws.cap, ws.tb.tot.p, ws.tb.g0.p, s);
         tau_device(ws, c.tau_diffusion_lambda, ws.tb.tot.p + 2 * static_cast<size_t>(ws.cap), ws.tb.g0.p);
     };
     sadk::launch_fill_i32(ws.rcap.p, ws.cap, 16, s);
@@ -1814,7 +1856,7 @@ static void fit_loop(sad_fit_run* r) {
     ws.cur = 0;
     sadk::launch_jfa_seed(ws.sites(), ws.st.p, ws.ids[0].p, ws.fd, scale_n, s);
     passes_device(ws, full4, c.inject, c.seed, fp64, 0);
-    const int nbw = sadk::backward_blocks(fp64, ws.fd);
+    const int nbw = sadk::backward_blocks(fp64, ws.fd, ordered);
     sadk::launch_advance(ws.st.p, static_cast<int>(full4.size()), 0, nullptr, nullptr, nullptr, 0, ws.otops.p, s);
 
     const bool use_graphs = getenv("SAD_NO_GRAPHS") == nullptr && !prof;
@@ -1828,7 +1870,7 @@ static void fit_loop(sad_fit_run* r) {
             np = static_cast<int>(warm.size());
         }
         mark(1, [&] {
-            sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt, ws.fd, scale_n, ws.gred_adaptive(),
+            sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt, ws.fd, scale_n, gred(),
                                   ws.loss_part.p, ws.st.p, s);
             tau_step();
         });
@@ -1845,7 +1887,7 @@ static void fit_loop(sad_fit_run* r) {
         mark(2, [&] {
             // plain iterations: active sites only (event iterations below run every slot, which also
             // zeroes the record capacity of pruned slots before densify can reuse them)
-            sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.gred_adaptive(), ws.m.p, ws.v.p, hp, r->bc_table.p,
+            sadk::launch_adam(fp64, ws.sites(), ws.st.p, gred(), ws.m.p, ws.v.p, hp, r->bc_table.p,
                               make_double2(0, 0), true, scale_n, ws.pack.p, ws.gtab.p, ws.rcap.p, s, totals,
                               ws.roff.p, ws.otops.p + 2, g_adam_all ? nullptr : ws.act.p, nullptr, adv);
         });
@@ -1909,13 +1951,13 @@ static void fit_loop(sad_fit_run* r) {
             npass += static_cast<int>(warm.size());
         }
         mark(1, [&] {
-            sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt, ws.fd, scale_n, ws.gred_adaptive(),
+            sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt, ws.fd, scale_n, gred(),
                                   ws.loss_part.p, ws.st.p, s);
             tau_step();
         });
         mark(3, [&] { stats_device(ws, g_stats_adaptive); });
         mark(2, [&] {
-            sadk::launch_adam(fp64, ws.sites(), ws.st.p, ws.gred_adaptive(), ws.m.p, ws.v.p, hp, r->bc_table.p,
+            sadk::launch_adam(fp64, ws.sites(), ws.st.p, gred(), ws.m.p, ws.v.p, hp, r->bc_table.p,
                               make_double2(0, 0), true, scale_n, nullptr, nullptr, ws.rcap.p, s, totals,
                               ws.roff.p, ws.otops.p + 2);
         });
