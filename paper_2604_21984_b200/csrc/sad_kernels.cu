@@ -4,6 +4,9 @@
 // order; the library is built with --fmad=false (see sad_device.cuh).  None of these steps is a
 // dense contraction, so there are no tensor-core paths: the roofline is HBM / L2 bandwidth or the
 // FP32/FP64 pipes.
+#if SAD_ORD_DEBUG
+#include <cstdio>
+#endif
 #include "sad_kcommon.cuh"
 
 #ifndef SAD_EXPERIMENT
@@ -2203,15 +2206,50 @@ __device__ __forceinline__ void ref_add(DD& a, double x) {
     a.lo = __dadd_rn(a.lo, err);
 }
 
-template <int KM, int NPX>
+// Shared state of one reference tile.  The contributions are computed and replayed in 4 bands of 4
+// rows (64 pixels), so only a band's contributions are resident; the per-(site, channel) Accums
+// stay in registers across the bands.
+constexpr int kOrdBandPx = 64;
+template <int KM, int NPX, int NCH>
 struct OrdTile {
-    uint32_t key[kRefTile * kRefTile * KM];  // kept candidate of entry e = pixel * KM + slot, else kEmpty
-    double w[kRefTile * kRefTile * KM];      // its normalised softmax weight
-    double pix[NPX][kRefTile * kRefTile];    // per pixel: g0 g1 g2 ch0 ch1 ch2 [t0 t1 t2 pl]
-    uint32_t tkey[kRefTable];                // the TileReducer table: site per slot (kEmpty: free)
-    uint32_t mask[kRefTable][kRefTile * kRefTile / 32];  // per slot: the tile pixels holding its site
+    static constexpr int NP = kRefTile * kRefTile, BE = kOrdBandPx * KM, CS = BE + 1;  // CS: padded row
+    uint32_t key[NP * KM];  // kept candidate of entry e = pixel * KM + slot, else kEmpty
+    double w[NP * KM];      // its normalised softmax weight
+    double pix[NPX][NP];    // per pixel: g0 g1 g2 ch0 ch1 ch2 [t0 t1 t2 pl]
+    double c[NCH * CS];     // the band's contributions, channel-major
+    uint32_t bm[kRefTable][2];         // per table slot: the band pixels holding its site (64 bits)
+    long long rec[kRefTable];          // record claimed per occupied slot (ord_claim code)
+    uint32_t tkey[kRefTable];          // the TileReducer table: site per slot (kEmpty: free)
+    uint16_t occ[kRefTable];           // occupied slots, compacted
+    uint16_t bstart[kRefTable];        // band bucket start per slot
+    uint16_t list[BE];                 // band entries bucketed by slot, in pixel order
+    uint16_t eslot[BE];                // slot of each band entry (0xffff: none / overflowed)
+    int wsum[8];
     DD warp_part[8];
 };
+
+// exclusive scan of one int per thread over a 256-thread block
+__device__ __forceinline__ int block_excl_scan256(int v, int* wsum, int& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    int off = 0, tot = 0;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+        const int t = wsum[q];
+        off += q < warp ? t : 0;
+        tot += t;
+    }
+    __syncthreads();
+    total = tot;
+    return off + x - v;
+}
 
 // The eleven contribution components of one kept candidate (grad.cpp:193-238): the expressions of
 // k_backward in the same order.  Returns the number of non-finite components (scrubbed to zero).
@@ -2310,13 +2348,48 @@ __device__ __forceinline__ void ord_store(const RedTarget& red, uint32_t site, u
     }
 }
 
+// A site's per-tile record in two steps: one thread claims it (code >= 0: part record, <= -2: opart
+// record -2 - code, -1: pools full) and writes the tag; each channel's owner then stores its Accum.
+__device__ __forceinline__ long long ord_claim(const RedTarget& red, uint32_t site, uint32_t tag) {
+    const int slot = atomicAdd(red.cnt + site, 1);
+    if (red.roff) {
+        const long long rec = static_cast<long long>(red.roff[site]) + slot;
+        if (slot < red.rcap[site] && rec < red.psize) {
+            red.tag[rec] = tag;
+            return rec;
+        }
+    } else if (slot < red.maxt) {
+        const long long rec = static_cast<long long>(site) * red.maxt + slot;
+        red.tag[rec] = tag;
+        return rec;
+    }
+    const int ro = atomicAdd(red.otop, 1);
+    if (ro >= red.ocap) return -1;
+    red.otag[ro] = tag;
+    red.onext[ro] = atomicExch(red.head + site, ro);
+    return -2 - static_cast<long long>(ro);
+}
+
+__device__ __forceinline__ void ord_put(const RedTarget& red, long long code, uint32_t site, int ch, const DD& a,
+                                        DevState* st) {
+    if (code >= 0) {
+        red.part[static_cast<size_t>(code) * red.stride + ch] = make_double2(a.hi, a.lo);
+    } else if (code <= -2) {
+        red.opart[static_cast<size_t>(-2 - code) * red.stride + ch] = make_double2(a.hi, a.lo);
+    } else {
+        atomicOr(&st->err, 8);
+        dd_atomic_merge(red.over + static_cast<size_t>(ch) * red.cap + site, a);
+    }
+}
+
 template <int KM, int MODE>
 __global__ void __launch_bounds__(256) k_backward_ord(const uint32_t* __restrict__ ids, const Q4<double>* __restrict__ gtab,
                                                       const double* __restrict__ tgt, FieldDims f, double s,
                                                       double inv_hw2, RedTarget red, double2* __restrict__ loss_part,
                                                       DevState* st) {
     constexpr int NCH = MODE == 1 ? 11 : 10, NPX = MODE == 1 ? 10 : 6, NP = kRefTile * kRefTile;
-    using Sm = OrdTile<KM, NPX>;
+    using Sm = OrdTile<KM, NPX, NCH>;
+    constexpr int BE = Sm::BE, CS = Sm::CS;
     extern __shared__ __align__(16) unsigned char smraw[];
     Sm& sm = *reinterpret_cast<Sm*>(smraw);
     const int tid = threadIdx.x;
@@ -2325,8 +2398,6 @@ __global__ void __launch_bounds__(256) k_backward_ord(const uint32_t* __restrict
     const bool inside = px < f.width && py < f.height && py < f.row1;
     const uint32_t tile = blockIdx.y * gridDim.x + blockIdx.x;  // raster order of the reference's tiles
     sm.tkey[tid] = kEmpty;
-#pragma unroll
-    for (int j = 0; j < NP / 32; j++) sm.mask[tid][j] = 0u;
     const double fx = static_cast<double>(px), fy = static_cast<double>(py);
 
     // ---- forward of this thread's pixel (k_backward's first half, same expressions)
@@ -2459,62 +2530,93 @@ __global__ void __launch_bounds__(256) k_backward_ord(const uint32_t* __restrict
     }
     __syncthreads();
 
-    // ---- each entry: its table slot (pixel bit in the slot's mask) or, overflowed, a raw record now
-    const double* pix = &sm.pix[0][tid];
-#pragma unroll 1
-    for (int i = 0; i < KM; i++) {
-        const uint32_t k = sm.key[tid * KM + i];
-        if (k == kEmpty) continue;
-        const uint32_t h = ref_tile_hash(k);
-        int u = -1;
-#pragma unroll
-        for (int q = kRefProbes - 1; q >= 0; q--)
-            if (sm.tkey[(h + q) & (kRefTable - 1)] == k) u = static_cast<int>((h + q) & (kRefTable - 1));
-        if (u >= 0) {
-            atomicOr(&sm.mask[u][tid >> 5], 1u << (tid & 31));
-        } else {
-            double v[NCH], z[NCH];
-            nonfinite += ord_contrib<NCH>(fx, fy, sm.w[tid * KM + i], gtab[3 * k], gtab[3 * k + 1], gtab[3 * k + 2], s,
-                                          pix, NP, v);
-#pragma unroll
-            for (int ch = 0; ch < NCH; ch++) z[ch] = 0.0;
-            ord_store<NCH>(red, k, (tile << 9) | kTagRaw | static_cast<uint32_t>(tid), v, z, st);
-        }
-    }
-    __syncthreads();
-
-    // ---- thread u: the per-tile Accum of the site in table slot u, over its pixels in order
+    // ---- the occupied table slots, compacted; thread t owns the (slot, channel) items t + 256 j
+    int n_occ;
     {
-        const uint32_t site = sm.tkey[tid];
-        if (site != kEmpty) {
-            const Q4<double> a = gtab[3 * site], b = gtab[3 * site + 1], c = gtab[3 * site + 2];
-            DD acc[NCH];
+        const bool o = sm.tkey[tid] != kEmpty;
+        const int pos = block_excl_scan256(o ? 1 : 0, sm.wsum, n_occ);
+        if (o) sm.occ[pos] = static_cast<uint16_t>(tid);
+    }
+    const int n_items = n_occ * NCH;
+    DD acc[NCH];
 #pragma unroll
-            for (int ch = 0; ch < NCH; ch++) acc[ch] = DD{0.0, 0.0};
+    for (int j = 0; j < NCH; j++) acc[j] = DD{0.0, 0.0};
 #pragma unroll 1
-            for (int j = 0; j < NP / 32; j++) {
-                unsigned mbits = sm.mask[tid][j];
-                while (mbits) {
-                    const int p = j * 32 + __ffs(mbits) - 1;
-                    mbits &= mbits - 1;
-                    int e = p * KM;
+    for (int band = 0; band < NP / kOrdBandPx; band++) {
+        sm.bm[tid][0] = sm.bm[tid][1] = 0u;
+        __syncthreads();
+        // contributions of the band's entries (pixel-major); an overflowed site's go out as raw records
 #pragma unroll 1
-                    while (sm.key[e] != site) e++;
-                    const double ffx = static_cast<double>(blockIdx.x * kRefTile + (p % kRefTile));
-                    const double ffy = static_cast<double>(blockIdx.y * kRefTile + (p / kRefTile) + f.row0);
-                    double v[NCH];
-                    nonfinite += ord_contrib<NCH>(ffx, ffy, sm.w[e], a, b, c, s, &sm.pix[0][p], NP, v);
+        for (int le = tid; le < BE; le += NP) {
+            const int lp = le / KM, p = band * kOrdBandPx + lp, e = p * KM + (le - lp * KM);
+            const uint32_t k = sm.key[e];
+            uint16_t us = 0xffffu;
+            if (k != kEmpty) {
+                const uint32_t h = ref_tile_hash(k);
+                int u = -1;
 #pragma unroll
-                    for (int ch = 0; ch < NCH; ch++) ref_add(acc[ch], v[ch]);
+                for (int q = kRefProbes - 1; q >= 0; q--)
+                    if (sm.tkey[(h + q) & (kRefTable - 1)] == k) u = static_cast<int>((h + q) & (kRefTable - 1));
+                double v[NCH];
+                const double ffx = static_cast<double>(blockIdx.x * kRefTile + (p % kRefTile));
+                const double ffy = static_cast<double>(blockIdx.y * kRefTile + (p / kRefTile) + f.row0);
+                nonfinite += ord_contrib<NCH>(ffx, ffy, sm.w[e], gtab[3 * k], gtab[3 * k + 1], gtab[3 * k + 2], s,
+                                              &sm.pix[0][p], NP, v);
+                if (u >= 0) {
+#pragma unroll
+                    for (int ch = 0; ch < NCH; ch++) sm.c[ch * CS + le] = v[ch];
+                    atomicOr(&sm.bm[u][lp >> 5], 1u << (lp & 31));
+                    us = static_cast<uint16_t>(u);
+                } else {
+                    double z[NCH];
+#pragma unroll
+                    for (int ch = 0; ch < NCH; ch++) z[ch] = 0.0;
+                    ord_store<NCH>(red, k, (tile << 9) | kTagRaw | static_cast<uint32_t>(p), v, z, st);
                 }
             }
-            double hi[NCH], lo[NCH];
+            sm.eslot[le] = us;
+        }
+        __syncthreads();
+        // bucket the band's entries by slot, in pixel order (a site occurs once per pixel)
+        {
+            int tot;
+            sm.bstart[tid] = static_cast<uint16_t>(
+                block_excl_scan256(__popc(sm.bm[tid][0]) + __popc(sm.bm[tid][1]), sm.wsum, tot));
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (int le = tid; le < BE; le += NP) {
+            const int us = sm.eslot[le];
+            if (us == 0xffff) continue;
+            const int lp = le / KM;
+            const unsigned long long bits = sm.bm[us][0] | (static_cast<unsigned long long>(sm.bm[us][1]) << 32);
+            sm.list[sm.bstart[us] + __popcll(bits & ((1ull << lp) - 1ull))] = static_cast<uint16_t>(le);
+        }
+        __syncthreads();
+        // replay: each item continues its (site, channel) Accum over the band's bucket
 #pragma unroll
-            for (int ch = 0; ch < NCH; ch++) {
-                hi[ch] = acc[ch].hi;
-                lo[ch] = acc[ch].lo;
+        for (int j = 0; j < NCH; j++) {
+            const int item = tid + NP * j;
+            if (item < n_items) {
+                const int ui = item / NCH, ch = item - ui * NCH;
+                const int u = sm.occ[ui];
+                const int b0 = sm.bstart[u], n = __popc(sm.bm[u][0]) + __popc(sm.bm[u][1]);
+                const double* crow = sm.c + ch * CS;
+#pragma unroll 4
+                for (int q = 0; q < n; q++) ref_add(acc[j], crow[sm.list[b0 + q]]);
             }
-            ord_store<NCH>(red, site, tile << 9, hi, lo, st);
+        }
+        __syncthreads();
+    }
+    // ---- one record per occupied slot: the per-tile Accums, flushed as end_tile does
+    for (int ui = tid; ui < n_occ; ui += NP) sm.rec[ui] = ord_claim(red, sm.tkey[sm.occ[ui]], tile << 9);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NCH; j++) {
+        const int item = tid + NP * j;
+        if (item < n_items) {
+            const int ui = item / NCH, ch = item - ui * NCH;
+            ord_put(red, sm.rec[ui], sm.tkey[sm.occ[ui]], ch, acc[j], st);
         }
     }
     __syncthreads();
@@ -2531,8 +2633,8 @@ int backward_ord_blocks(const FieldDims& f) {
 template <int KM, int MODE>
 static void backward_ord_t(const uint32_t* ids, const void* gtab, const void* tgt, const FieldDims& f, double scale,
                            const RedTarget& red, double2* loss_part, DevState* st, cudaStream_t stream) {
-    constexpr int NPX = MODE == 1 ? 10 : 6;
-    const size_t smem = sizeof(OrdTile<KM, NPX>);
+    constexpr int NPX = MODE == 1 ? 10 : 6, NCH = MODE == 1 ? 11 : 10;
+    const size_t smem = sizeof(OrdTile<KM, NPX, NCH>);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_backward_ord<KM, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -2549,6 +2651,9 @@ static void backward_ord_t(const uint32_t* ids, const void* gtab, const void* tg
 // per site; up to kOrdFast records are ranked in shared memory, more take a selection walk over the
 // tags in global memory.  Lane ch < NCH replays channel ch; returns the output Accum of the channel.
 constexpr int kOrdFast = 128;
+#if SAD_ORD_DEBUG
+__device__ int g_ord_dbg;
+#endif
 struct OrdRef {
     uint32_t tag;
     int32_t rec;  // >= 0: part record, < 0: opart record ~rec
@@ -2655,6 +2760,17 @@ __global__ void __launch_bounds__(128) k_ordered_totals(RedTarget red, const Dev
     if (id >= st->n_sites) return;
     long long base = 0;
     const int n_slice = ord_slice(red, id, base);
+#if SAD_ORD_DEBUG
+    if (lane == 0) {
+        int nl = 0, nraw = 0;
+        for (int r = red.head[id]; r >= 0; r = red.onext[r]) nl++;
+        for (int j = 0; j < n_slice; j++) nraw += (red.tag[base + j] & kTagRaw) != 0;
+        const int cnt = red.cnt[id];
+        if (n_slice + nl > 64 && atomicAdd(&g_ord_dbg, 1) < 40)
+            printf("ord site %d cnt %d slice %d (rcap %d) list %d raw-in-slice %d\n", id, cnt, n_slice,
+                   red.roff ? red.rcap[id] : red.maxt, nl, nraw);
+    }
+#endif
     const DD t = ord_total<NCH>(red, id, n_slice, base, buf[warp], sorted[warp]);
     if (lane < NCH) {
         if (tot) tot[static_cast<size_t>(lane) * red.cap + id] = t.hi + t.lo;
@@ -3701,6 +3817,8 @@ __global__ void __launch_bounds__(128, SAD_ADAM_MINB) k_adam(SitesDev s, DevStat
             else p = (kc == 7 ? nx : ny) / norm;
         }
         if (upd && kc >= 0) s.p[static_cast<size_t>(kc) * cap + id] = p;
+        // this pass's record count (with precomputed totals, merge_site did not read it): before the reset
+        const int cl = totals ? grads.cnt[id] : claimed;
         if (zero_grads) {
             if (k < 11) grads.over[static_cast<size_t>(k) * cap + id] = make_double2(0.0, 0.0);
             if (k == 0) grads.cnt[id] = 0;
@@ -3708,7 +3826,6 @@ __global__ void __launch_bounds__(128, SAD_ADAM_MINB) k_adam(SitesDev s, DevStat
         }
         if (rcap_next && k == 0) {
             // next pass's record capacity: last count plus headroom (active sites only)
-            const int cl = totals ? grads.cnt[id] : claimed;
             int want = is_active ? cl + (cl >> 2) + 2 : 0;
             want = want < 4096 ? want : 4096;
             rcap_next[id] = want;

@@ -10,7 +10,7 @@ from paper_2604_21984_b200.types import _PARAMS
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 4000
 W, H = int(os.environ.get("W", 768)), int(os.environ.get("H", 512))
 G = sad.gpu_backend(0)
-cfg = sad.TrainConfig(iters=iters, target_bpp=2.0, fp64=False)
+cfg = sad.TrainConfig(iters=iters, target_bpp=2.0, fp64=os.environ.get("FP64") == "1")
 img = synthetic_image(W, H, 1)
 r = G.fit(sad.ImageBuffer(W, H, img), cfg)
 h = hashlib.sha256()
