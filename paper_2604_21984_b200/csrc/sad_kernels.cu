@@ -2169,10 +2169,7 @@ void launch_backward(bool fp64, int mode, const uint32_t* ids, const void* gtab,
 #undef SAD_BWD_ORD
 }
 
-bool fp64_ordered() {
-    static const bool on = getenv("SAD_FP64_DD") == nullptr;
-    return on;
-}
+bool fp64_ordered() { return getenv("SAD_FP64_DD") == nullptr; }  // read per fit / per call
 
 // ====================================================================== fp64 backward in the reference's order
 // The reference's per-site sums are Accum cascades (accum.hpp:14-26: hi = fl(hi + x), lo += the
@@ -2690,9 +2687,29 @@ __device__ DD ord_total(const RedTarget& red, int id, int n_slice, long long bas
             sorted[rank] = j;
         }
         __syncwarp();
-        for (int r = 0; r < n; r++) {
-            const OrdRef o = buf[sorted[r]];
-            replay(o.rec, o.tag);
+        // eight records' values in flight per lane, then their cascade steps in order
+        if (lane < NCH) {
+            for (int r0 = 0; r0 < n; r0 += 8) {
+                double2 v[8];
+                bool raw[8];
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    v[q] = make_double2(0.0, 0.0);
+                    raw[q] = true;
+                    if (r0 + q < n) {
+                        const OrdRef o = buf[sorted[r0 + q]];
+                        v[q] = o.rec >= 0 ? red.part[static_cast<size_t>(o.rec) * red.stride + lane]
+                                          : red.opart[static_cast<size_t>(~o.rec) * red.stride + lane];
+                        raw[q] = (o.tag & kTagRaw) != 0;
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 8; q++)
+                    if (r0 + q < n) {
+                        ref_add(buf_acc, v[q].x);
+                        if (!raw[q]) ref_add(buf_acc, v[q].y);
+                    }
+            }
         }
     } else {
         // selection walk: the next larger tag each step (tags of one site are distinct)

@@ -2,6 +2,8 @@
 of the propagation, backward and stats and merges the exact per-rank partials, so each rank ends with
 exactly the single-GPU fit.  Checked here with virtual ranks on one device (loopback exchange) and with
 the real NCCL transport at world size 1."""
+import os
+
 import numpy as np
 import pytest
 
@@ -37,9 +39,21 @@ def test_strips_loopback_fp64_and_other_k(fp64, k, world):
     tgt = synth_target(56, 40, 9)
     cfg = sad.TrainConfig(iters=80, target_bpp=2.0, fp64=fp64, k=k, seed=3, densify_start=10, densify_every=10,
                           prune_start=20, prune_every=20)
-    ref = G.fit(tgt, cfg)
+    ref = single_gpu_fit(G, tgt, cfg)
     for o in G.fit_strips_loopback(tgt, cfg, world):
         _same(o, ref)
+
+
+def single_gpu_fit(G, tgt, cfg):
+    """The single-GPU fit a strip fit must equal.  In fp64 that is the double-double reduction
+    (SAD_FP64_DD): strips merge per-site double-double partials, the reference-order replay is single-GPU."""
+    if not cfg.fp64:
+        return G.fit(tgt, cfg)
+    os.environ["SAD_FP64_DD"] = "1"
+    try:
+        return G.fit(tgt, cfg)
+    finally:
+        del os.environ["SAD_FP64_DD"]
 
 
 def test_strips_nccl_world1():

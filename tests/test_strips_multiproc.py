@@ -16,6 +16,7 @@ import pytest
 import torch.multiprocessing as mp
 
 import paper_2604_21984_b200 as sad
+from tests.test_strips import single_gpu_fit
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 P = ("x", "y", "log_tau", "radius", "col_r", "col_g", "col_b", "dir_x", "dir_y", "aniso", "active")
@@ -72,7 +73,7 @@ def test_strips_two_processes_host_transport(tmp_path):
     from tests.fixtures import synth_target
     G = sad.gpu_backend(0)
     for name, w, h, cfg in _cases():
-        ref = G.fit(synth_target(w, h, 7), cfg)
+        ref = single_gpu_fit(G, synth_target(w, h, 7), cfg)
         for r in range(world):
             d = np.load(os.path.join(str(tmp_path), f"{name}_rank{r}.npz"))
             assert list(d["lines"]) == [sad.history_line(x) for x in ref.history], (name, r)

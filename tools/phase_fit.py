@@ -11,7 +11,7 @@ import paper_2604_21984_b200 as sad  # noqa: E402
 from paper_2604_21984_b200.synth import synthetic_image  # noqa: E402
 
 W, H = int(os.environ.get("W", 768)), int(os.environ.get("H", 512))
-cfg = sad.TrainConfig(iters=int(os.environ.get("ITERS", 4000)), target_bpp=2.0, fp64=False)
+cfg = sad.TrainConfig(iters=int(os.environ.get("ITERS", 4000)), target_bpp=2.0, fp64=os.environ.get("FP64") == "1")
 G = sad.gpu_backend(0)
 run = C.c_void_p()
 cc = cfg.to_c()
