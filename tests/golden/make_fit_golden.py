@@ -35,6 +35,9 @@ def cases():
     for seed in range(1, 9):  # config 2: 768x512 Kodak-shaped, 2 BPP, 4000 iterations, events
         out[f"config2_s{seed}"] = (768, 512, seed, dict(iters=4000, target_bpp=2.0, fp64=False, seed=1))
     out["config2_fp64_s1"] = (768, 512, 1, dict(iters=4000, target_bpp=2.0, fp64=True, seed=1))
+    # fp64 with the reference's default RunOpts::threads = 1 (types.hpp:163): the summation order the GPU's
+    # fp64 path replays, on a second image
+    out["config2_fp64_t1_s2"] = (768, 512, 2, dict(iters=4000, target_bpp=2.0, fp64=True, seed=1, threads=1))
     out["config3_s1"] = (2048, 2048, 1, dict(iters=300, n_sites=100000, fp64=False, seed=1))
     # config 5 shape (8192^2, 2 BPP): 25 iterations, i.e. the initial refresh, one densify event (t = 20) with
     # its full re-seeded refresh, and the final refresh(Full, 16) (about 25 minutes on 8 host cores)
@@ -76,16 +79,18 @@ def main(names):
             continue
         img = sad.ImageBuffer(w, h, synthetic_image(w, h, seed))
         cfg = sad.TrainConfig(**kw)
-        cfg.threads = threads
+        nt = kw.get("threads", threads)
+        cfg.threads = nt
+        Rk = R if nt == threads else ref_backend(threads=nt)
         t0 = time.perf_counter()
-        res = R.fit(img, cfg)
+        res = Rk.fit(img, cfg)
         sec = time.perf_counter() - t0
         rec = fit_record(res, img, lambda st, f: R.render_image(st, f, sad.RunOpts(fp64=False)).data)
         rec.update(width=np.int64(w), height=np.int64(h), image_seed=np.int64(seed), ref_seconds=np.float64(sec),
-                   ref_threads=np.int64(threads), config=repr(kw))
+                   ref_threads=np.int64(nt), config=repr({k: v for k, v in kw.items() if k != "threads"}))
         np.savez_compressed(path, **rec)
         print(f"{name}: {len(res.history)} rows, active {res.history[-1].active_sites}, decode PSNR "
-              f"{float(rec['decode_psnr']):.6f} dB, reference {sec:.1f} s on {threads} threads", flush=True)
+              f"{float(rec['decode_psnr']):.6f} dB, reference {sec:.1f} s on {nt} threads", flush=True)
 
 
 if __name__ == "__main__":
