@@ -2206,7 +2206,13 @@ __device__ __forceinline__ void ref_add(DD& a, double x) {
 // Shared state of one reference tile.  The contributions are computed and replayed in 4 bands of 4
 // rows (64 pixels), so only a band's contributions are resident; the per-(site, channel) Accums
 // stay in registers across the bands.
-constexpr int kOrdBandPx = 64;
+#ifndef SAD_ORD_BAND
+#define SAD_ORD_BAND 64  // pixels per band (a multiple of 32, at most 64)
+#endif
+#ifndef SAD_ORD_MINB
+#define SAD_ORD_MINB 1
+#endif
+constexpr int kOrdBandPx = SAD_ORD_BAND;
 template <int KM, int NPX, int NCH>
 struct OrdTile {
     static constexpr int NP = kRefTile * kRefTile, BE = kOrdBandPx * KM, CS = BE + 1;  // CS: padded row
@@ -2380,7 +2386,7 @@ __device__ __forceinline__ void ord_put(const RedTarget& red, long long code, ui
 }
 
 template <int KM, int MODE>
-__global__ void __launch_bounds__(256) k_backward_ord(const uint32_t* __restrict__ ids, const Q4<double>* __restrict__ gtab,
+__global__ void __launch_bounds__(256, SAD_ORD_MINB) k_backward_ord(const uint32_t* __restrict__ ids, const Q4<double>* __restrict__ gtab,
                                                       const double* __restrict__ tgt, FieldDims f, double s,
                                                       double inv_hw2, RedTarget red, double2* __restrict__ loss_part,
                                                       DevState* st) {
