@@ -2,10 +2,13 @@
 record-pool fallbacks, of non-finite adjoints, and of the two entry points with no other test
 (`exact_topk_batch`, candidates.cpp:198-248; `clamp_project`, train.cpp:113-137).
 
-The device groups each tile's per-(site, channel) contributions in a shared-memory hash of
-UMAX = entries/4 local sites (sad_kernels.cu TileRed); beyond that, and when the per-site record
-slots or the overflow-record pool run out, sums merge exactly into per-site double-double totals
-with 128-bit CAS.  Every path is exact, so every result must equal the reference's bit for bit.
+fp32 (and stats): the device groups each tile's per-(site, channel) contributions in a shared-memory
+hash of UMAX = entries/4 local sites (sad_kernels.cu TileRed); beyond that, and when the per-site record
+slots or the overflow-record pool run out, sums merge exactly into per-site double-double totals with
+128-bit CAS.  fp64 gradients replay the reference's TileReducer itself (k_backward_ord: 16x16 tiles,
+256 slots, 8 probes; an overflowed site's contributions become raw records), so the 320-site and
+hash-collision cases below drive the reference's own overflow path on the device.  Every result must
+equal the reference's bit for bit.
 """
 import ctypes as C
 import os
@@ -160,6 +163,23 @@ def test_record_pool_exhaustion_fit(R):
     try:
         tgt = synth_target(64, 48, 3)
         cfg = sad.TrainConfig(iters=80, target_bpp=3.0, fp64=False, seed=2)
+        a = B.fit(tgt, cfg)
+        b = R.fit(tgt, cfg)
+        assert [sad.history_line(r) for r in a.history] == [sad.history_line(r) for r in b.history]
+        assert np.array_equal(a.sites.x, b.sites.x) and np.array_equal(a.field.ids, b.field.ids)
+        B.close()
+    finally:
+        B.lib.sad_ctx_destroy(B.ctx)
+
+
+def test_fp64_ordered_fit_overflow_lists(R):
+    """fp64 fit with the adaptive record pool capped at 64 records (SAD_APSIZE) and a large overflow pool:
+    nearly every tagged (site, tile) record travels through the per-site overflow lists, whose order the
+    ordered merge restores from the tags; the fit must equal the reference's."""
+    B = _fresh_backend({"SAD_APSIZE": "64", "SAD_OCAP": "200000"})
+    try:
+        tgt = synth_target(64, 48, 5)
+        cfg = sad.TrainConfig(iters=60, target_bpp=3.0, fp64=True, seed=4)
         a = B.fit(tgt, cfg)
         b = R.fit(tgt, cfg)
         assert [sad.history_line(r) for r in a.history] == [sad.history_line(r) for r in b.history]
