@@ -217,6 +217,29 @@ def test_tiles_ragged_and_other_k(G, R, w, h, k, cell):
     assert np.array_equal(sg.data, sr.data)
 
 
+@pytest.mark.parametrize("w,h,k,cell", [(37, 29, 1, 1), (50, 34, 8, 1), (40, 30, 16, 2), (23, 17, 5, 3)])
+def test_fp64_ordered_ragged_and_other_k(G, R, w, h, k, cell):
+    """The fp64 reference-order backward (16x16 reference tiles, TileReducer replay) on ragged image
+    sizes, short lists, K = 16 and coarse cells: loss, every gradient channel (with and without the
+    removal delta, and the adjoint entry point) and the non-finite count bit-identical."""
+    st = random_model(w, h, 45, 31 + k)
+    st.deactivate(3)
+    tgt = random_target(w, h, 9 + k)
+    f = _field(w, h, k, cell)
+    R.refresh(st, f, sad.RefreshMode.Full, 3, 4, 11, F64)
+    for removal in (False, True):
+        gg, gr = sad.GradBuffer(), sad.GradBuffer()
+        assert G.backward_image(st, f, tgt, gg, F64, removal) == R.backward_image(st, f, tgt, gr, F64, removal)
+        assert np.array_equal(gg.data, gr.data)
+        assert gg.nonfinite == gr.nonfinite
+    dl = random_target(w, h, 4)
+    dl.data -= 0.5
+    gg, gr = sad.GradBuffer(), sad.GradBuffer()
+    G.backward_pixel_grad(st, f, dl, gg, F64)
+    R.backward_pixel_grad(st, f, dl, gr, F64)
+    assert np.array_equal(gg.data[:, :10], gr.data[:, :10])
+
+
 @pytest.mark.parametrize("k", [5, 8, 12])
 def test_pixel_weights_batch(G, R, k):
     """pixel_weights (render.cpp:92-104) batched: per query the kept ids in list order and their double
