@@ -2399,7 +2399,8 @@ __global__ void __launch_bounds__(256, SAD_ORD_MINB) k_backward_ord(const uint32
     const int px = blockIdx.x * kRefTile + (tid % kRefTile);
     const int py = blockIdx.y * kRefTile + (tid / kRefTile) + f.row0;
     const bool inside = px < f.width && py < f.height && py < f.row1;
-    const uint32_t tile = blockIdx.y * gridDim.x + blockIdx.x;  // raster order of the reference's tiles
+    // raster order of the reference's tiles over the whole image (a strip starts at a tile row: row0 % 16 == 0)
+    const uint32_t tile = (blockIdx.y + static_cast<uint32_t>(f.row0) / kRefTile) * gridDim.x + blockIdx.x;
     sm.tkey[tid] = kEmpty;
     const double fx = static_cast<double>(px), fy = static_cast<double>(py);
 
@@ -3600,6 +3601,103 @@ void launch_owner_merge(const OwnRec* recv, long long n, int nch, int cap, doubl
     if (n <= 0) return;
     const long long items = n * nch;
     k_owner_merge<<<static_cast<unsigned>((items + 255) / 256), 256, 0, stream>>>(recv, n, nch, cap, part);
+    SAD_LAUNCHED();
+}
+
+// ---------------------------------------------------------------------- ordered (fp64) strip exchange
+// The records of one site on this rank: its slice [0, n_slice) and its overflow list.
+template <typename F>
+__device__ __forceinline__ void for_site_records(const RedTarget& red, int id, F&& fn) {
+    long long base = 0;
+    const int n_slice = ord_slice(red, id, base);
+    for (int j = 0; j < n_slice; j++)
+        fn(red.part + static_cast<size_t>(base + j) * red.stride, red.tag[base + j]);
+    for (int r = red.head[id]; r >= 0; r = red.onext[r]) fn(red.opart + static_cast<size_t>(r) * red.stride, red.otag[r]);
+}
+
+__global__ void k_owner_count_ord(RedTarget red, const DevState* __restrict__ st, int slice, int me, int world,
+                                  unsigned long long* __restrict__ counts) {
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= st->n_sites || red.cnt[id] <= 0) return;
+    const int q = id / slice;
+    if (q == me || q >= world) return;
+    unsigned long long n = 0;
+    for_site_records(red, id, [&](const double2*, uint32_t) { n++; });
+    atomicAdd(counts + q, n);
+}
+
+__global__ void k_owner_pack_ord(RedTarget red, const DevState* __restrict__ st, int slice, int me, int world,
+                                 OwnRec* __restrict__ send, long long send_cap, unsigned long long* __restrict__ cursors) {
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= st->n_sites || red.cnt[id] <= 0) return;
+    const int q = id / slice;
+    if (q == me || q >= world) return;
+    unsigned long long n = 0;
+    for_site_records(red, id, [&](const double2*, uint32_t) { n++; });
+    long long pos = static_cast<long long>(atomicAdd(cursors + q, n));
+    for_site_records(red, id, [&](const double2* v, uint32_t tag) {
+        SAD_CHECK(pos < send_cap);
+        OwnRec& r = send[static_cast<size_t>(q) * send_cap + pos++];
+        r.id = static_cast<uint32_t>(id);
+        r.pad[0] = tag;
+        for (int c = 0; c < 10; c++) r.v[c] = v[c];
+    });
+}
+
+__global__ void k_owner_merge_ord(const OwnRec* __restrict__ recv, long long n, RedTarget red, DevState* st) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const OwnRec& rec = recv[i];
+    SAD_CHECK(rec.id < static_cast<uint32_t>(red.cap));
+    const int ro = atomicAdd(red.otop, 1);
+    if (ro < red.ocap) {
+        for (int c = 0; c < 10; c++) red.opart[static_cast<size_t>(ro) * red.stride + c] = rec.v[c];
+        red.otag[ro] = rec.pad[0];
+        red.onext[ro] = atomicExch(red.head + rec.id, ro);
+    } else {
+        atomicOr(&st->err, 8);
+        for (int c = 0; c < 10; c++)
+            dd_atomic_merge(red.over + static_cast<size_t>(c) * red.cap + rec.id, DD{rec.v[c].x, rec.v[c].y});
+    }
+}
+
+__global__ void k_ord_finish(RedTarget red, const DevState* __restrict__ st, const uint8_t* __restrict__ active,
+                             int32_t* __restrict__ rcap_next) {
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= red.cap) return;
+    if (id >= st->n_sites) {
+        rcap_next[id] = 0;
+        return;
+    }
+    const int cl = red.cnt[id];
+    const int want = active[id] ? cl + (cl >> 2) + 2 : 0;
+    rcap_next[id] = want < 4096 ? want : 4096;
+    for (int c = 0; c < red.stride; c++) red.over[static_cast<size_t>(c) * red.cap + id] = make_double2(0.0, 0.0);
+    red.cnt[id] = 0;
+    red.head[id] = -1;
+}
+
+void launch_owner_count_ord(const RedTarget& red, const DevState* st, int slice, int me, int world,
+                            unsigned long long* counts, cudaStream_t stream) {
+    const int grid = (red.cap + 255) / 256;
+    k_owner_count_ord<<<grid ? grid : 1, 256, 0, stream>>>(red, st, slice, me, world, counts);
+    SAD_LAUNCHED();
+}
+void launch_owner_pack_ord(const RedTarget& red, const DevState* st, int slice, int me, int world, OwnRec* send,
+                           long long send_cap, unsigned long long* cursors, cudaStream_t stream) {
+    const int grid = (red.cap + 255) / 256;
+    k_owner_pack_ord<<<grid ? grid : 1, 256, 0, stream>>>(red, st, slice, me, world, send, send_cap, cursors);
+    SAD_LAUNCHED();
+}
+void launch_owner_merge_ord(const OwnRec* recv, long long n, const RedTarget& red, DevState* st, cudaStream_t stream) {
+    if (n <= 0) return;
+    k_owner_merge_ord<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(recv, n, red, st);
+    SAD_LAUNCHED();
+}
+void launch_ord_finish(const RedTarget& red, const DevState* st, const uint8_t* active, int32_t* rcap_next,
+                       cudaStream_t stream) {
+    const int grid = (red.cap + 255) / 256;
+    k_ord_finish<<<grid ? grid : 1, 256, 0, stream>>>(red, st, active, rcap_next);
     SAD_LAUNCHED();
 }
 

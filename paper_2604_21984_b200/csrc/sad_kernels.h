@@ -176,6 +176,17 @@ void launch_owner_pack(const double2* part, int nch, const RedTarget& red, const
                        int slice, int me, int world, OwnRec* send, int send_cap, unsigned long long* counts,
                        int32_t* rcap_next, bool reset, cudaStream_t stream);
 void launch_owner_merge(const OwnRec* recv, long long n, int nch, int cap, double2* part, cudaStream_t stream);
+// fp64 reference-order strips: the tagged records themselves travel to the owners (OwnRec.pad[0] = tag).
+// count: records per destination rank; pack: writes them at per-destination cursors (send + q * send_cap);
+// merge: the owner links each received record into the site's overflow list; finish: next pass's record
+// capacities from this rank's own counts, then the per-site reduction state is reset.
+void launch_owner_count_ord(const RedTarget& red, const DevState* st, int slice, int me, int world,
+                            unsigned long long* counts, cudaStream_t stream);
+void launch_owner_pack_ord(const RedTarget& red, const DevState* st, int slice, int me, int world, OwnRec* send,
+                           long long send_cap, unsigned long long* cursors, cudaStream_t stream);
+void launch_owner_merge_ord(const OwnRec* recv, long long n, const RedTarget& red, DevState* st, cudaStream_t stream);
+void launch_ord_finish(const RedTarget& red, const DevState* st, const uint8_t* active, int32_t* rcap_next,
+                       cudaStream_t stream);
 template <typename T>
 void launch_slice_pack(const T* src, int nch, int cap, int lo, int slice, T* buf, cudaStream_t stream);
 template <typename T>

@@ -957,6 +957,7 @@ struct sad_fit_run {
     // receive records, the owned range of the active list, parameter / stats slice staging
     DBuf<unsigned long long> own_counts, own_matrix;
     DBuf<sadk::OwnRec> own_send, own_recv;
+    DBuf<sadk::OwnRec> ord_send, ord_recv;  // fp64 reference-order strips: tagged records
     DBuf<int32_t> own_range;
     DBuf<double> slice_p, slice_all_p;
     DBuf<double2> slice_s, slice_all_s;
@@ -2323,8 +2324,9 @@ struct HostComm : StripComm {
 
 // Row bounds of `world` strips over `rows` rows, each a multiple of the backward/stats tile heights
 // (sadk::tile_row_quantum), so no tile straddles two strips.
-static std::vector<int> strip_bounds(int rows, int world) {
-    const int qr = sadk::tile_row_quantum();
+static std::vector<int> strip_bounds(int rows, int world, bool ordered) {
+    // the fp64 reference-order backward works on the reference's 16-row tiles
+    const int qr = ordered ? std::max(16, sadk::tile_row_quantum()) : sadk::tile_row_quantum();
     const int tiles = (rows + qr - 1) / qr;
     std::vector<int> b(static_cast<size_t>(world) + 1);
     for (int q = 0; q <= world; q++)
@@ -2380,6 +2382,62 @@ static long long owner_merge(std::vector<sad_fit_run*>& runs, StripComm& T, int 
     return sent;
 }
 
+// fp64 reference-order strips: every rank sends the tagged records of the sites it touched but does not own to
+// their owners (counts first), who link them into the sites' overflow lists; the ordered merge then replays
+// each owned site's records from all strips in the reference's tile order.  Returns the records sent.
+static long long owner_merge_ord(std::vector<sad_fit_run*>& runs, StripComm& T, int R, int slice) {
+    for (sad_fit_run* r : runs) {
+        Workspace& ws = r->ws;
+        ck(cudaMemsetAsync(r->own_counts.p, 0, sizeof(unsigned long long) * R, ws.stream), "memset counts");
+        sadk::launch_owner_count_ord(ws.gred_adaptive_ord(), ws.st.p, slice, r->rank, R, r->own_counts.p, ws.stream);
+    }
+    T.gather(runs, [](sad_fit_run* r) { return static_cast<const void*>(r->own_counts.p); },
+             [](sad_fit_run* r) { return static_cast<void*>(r->own_matrix.p); }, sizeof(unsigned long long) * R);
+    std::vector<std::vector<unsigned long long>> mats(runs.size(), std::vector<unsigned long long>(size_t(R) * R));
+    for (size_t i = 0; i < runs.size(); i++) {
+        ck(cudaMemcpyAsync(mats[i].data(), runs[i]->own_matrix.p, sizeof(unsigned long long) * R * R,
+                           cudaMemcpyDeviceToHost, runs[i]->ws.stream),
+           "D2H counts");
+        ck(cudaStreamSynchronize(runs[i]->ws.stream), "counts");
+    }
+    long long sent = 0;
+    std::vector<XferPlan> plans(runs.size());
+    std::vector<long long> nrecv(runs.size(), 0);
+    for (size_t i = 0; i < runs.size(); i++) {
+        sad_fit_run* r = runs[i];
+        Workspace& ws = r->ws;
+        const int me = r->rank;
+        const auto& M = mats[i];  // M[src * R + dst]
+        long long send_cap = 1, recv_n = 0;
+        for (int q = 0; q < R; q++) {
+            send_cap = std::max<long long>(send_cap, static_cast<long long>(M[static_cast<size_t>(me) * R + q]));
+            if (q != me) recv_n += static_cast<long long>(M[static_cast<size_t>(q) * R + me]);
+        }
+        r->ord_send.ensure(static_cast<size_t>(R) * send_cap);
+        r->ord_recv.ensure(static_cast<size_t>(std::max<long long>(recv_n, 1)));
+        ck(cudaMemsetAsync(r->own_counts.p, 0, sizeof(unsigned long long) * R, ws.stream), "memset cursors");
+        sadk::launch_owner_pack_ord(ws.gred_adaptive_ord(), ws.st.p, slice, me, R, r->ord_send.p, send_cap,
+                                    r->own_counts.p, ws.stream);
+        long long roff = 0;
+        for (int q = 0; q < R; q++) {
+            if (q == me) continue;
+            const long long ns = static_cast<long long>(M[static_cast<size_t>(me) * R + q]);
+            const long long nr = static_cast<long long>(M[static_cast<size_t>(q) * R + me]);
+            plans[i].add(q, r->ord_send.p + static_cast<size_t>(q) * send_cap, ns * sizeof(sadk::OwnRec),
+                         r->ord_recv.p + roff, nr * sizeof(sadk::OwnRec));
+            roff += nr;
+            sent += ns;
+            r->xfer_records += ns;
+        }
+        nrecv[i] = roff;
+    }
+    T.exchange(runs, plans);
+    for (size_t i = 0; i < runs.size(); i++)
+        sadk::launch_owner_merge_ord(runs[i]->ord_recv.p, nrecv[i], runs[i]->ws.gred_adaptive_ord(), runs[i]->ws.st.p,
+                                     runs[i]->ws.stream);
+    return sent;
+}
+
 static void fit_loop_strips(std::vector<sad_fit_run*>& runs, StripComm& T) {
     // every exit (including an exception mid-fit) leaves the runs' field views on the whole image
     struct RowRestore {
@@ -2396,6 +2454,7 @@ static void fit_loop_strips(std::vector<sad_fit_run*>& runs, StripComm& T) {
     const sad_train_config& c = r0->cfg;
     const int w = r0->w, h = r0->h;
     const bool fp64 = c.fp64 != 0;
+    const bool ordered = fp64 && sadk::fp64_ordered();  // fp64: the reference's summation order (§3)
     const bool budget = c.target_bpp > 0;
     const double scale_n = norm_scale(w, h);
     if (c.tau_diffusion_lambda > 0) fail(SAD_EINVAL, "strips: tau_diffusion is not supported");
@@ -2430,10 +2489,11 @@ static void fit_loop_strips(std::vector<sad_fit_run*>& runs, StripComm& T) {
         init.n_sites = st0.n_sites;
         init.n_active = sta.n_active;
         ws.set_state(init);
-        r->strip = strip_bounds(h, R);
+        r->strip = strip_bounds(h, R, ordered);
         ws.fd.row0 = r->strip[r->rank];
         ws.fd.row1 = r->strip[r->rank + 1];
         ws.ensure_adaptive(static_cast<size_t>(sadk::backward_blocks(fp64, ws.fd)));
+        if (ordered) (void)ws.gred_adaptive_ord();  // tag arrays
         sadk::launch_fill_i32(ws.rcap.p, ws.cap, 16, s);
         ws.plan_records();
         ck(cudaMemsetAsync(ws.gcnt.p, 0, sizeof(int32_t) * ws.cap, s), "memset gcnt");
@@ -2521,20 +2581,33 @@ static void fit_loop_strips(std::vector<sad_fit_run*>& runs, StripComm& T) {
         // backward on the strips; each rank's partial totals of the sites it touched
         for (sad_fit_run* r : runs) {
             Workspace& ws = r->ws;
-            sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt_of(r), ws.fd, scale_n, ws.gred_adaptive(),
-                                  ws.loss_part.p, ws.st.p, ws.stream);
-            sadk::launch_loss_reduce(ws.loss_part.p, sadk::backward_blocks(fp64, ws.fd), r->loss_self.p, ws.stream);
-            sadk::launch_site_partials(ws.gred_adaptive(), ws.st.p, cap, r->gpart_self.p, ws.stream);
+            sadk::launch_backward(fp64, 0, ws.ids[ws.cur].p, ws.gtab.p, tgt_of(r), ws.fd, scale_n,
+                                  ordered ? ws.gred_adaptive_ord() : ws.gred_adaptive(), ws.loss_part.p, ws.st.p,
+                                  ws.stream);
+            sadk::launch_loss_reduce(ws.loss_part.p, sadk::backward_blocks(fp64, ws.fd, ordered), r->loss_self.p,
+                                     ws.stream);
+            if (!ordered) sadk::launch_site_partials(ws.gred_adaptive(), ws.st.p, cap, r->gpart_self.p, ws.stream);
         }
         T.gather(runs, [](sad_fit_run* r) { return static_cast<const void*>(r->loss_self.p); },
                  [](sad_fit_run* r) { return static_cast<void*>(r->loss_all.p); }, sizeof(double2));
         // owner merge of the gradient partials; the owned totals' values feed Adam
-        owner_merge(
-            runs, T, R, slice, 10, [](sad_fit_run* r) { return r->gpart_self.p; },
-            [](sad_fit_run* r) { return r->ws.gred_adaptive(); }, true);
-        for (sad_fit_run* r : runs) {
-            sadk::launch_dd_values(r->gpart_self.p, 10ll * cap, r->tot.p, r->ws.stream);
-            r->ws.plan_records();  // next pass's record slices from the capacities owner_pack planned
+        if (ordered) {
+            owner_merge_ord(runs, T, R, slice);
+            for (sad_fit_run* r : runs) {
+                Workspace& ws = r->ws;
+                const sadk::RedTarget red = ws.gred_adaptive_ord();
+                sadk::launch_ordered_totals(red, 10, ws.st.p, r->tot.p, nullptr, false, ws.stream);
+                sadk::launch_ord_finish(red, ws.st.p, ws.active.p, ws.rcap.p, ws.stream);
+                ws.plan_records();
+            }
+        } else {
+            owner_merge(
+                runs, T, R, slice, 10, [](sad_fit_run* r) { return r->gpart_self.p; },
+                [](sad_fit_run* r) { return r->ws.gred_adaptive(); }, true);
+            for (sad_fit_run* r : runs) {
+                sadk::launch_dd_values(r->gpart_self.p, 10ll * cap, r->tot.p, r->ws.stream);
+                r->ws.plan_records();  // next pass's record slices from the capacities owner_pack planned
+            }
         }
         if (ev) {  // stats (budget.cpp:39-155) on the strips: owner merge, then every rank gets all totals
             for (sad_fit_run* r : runs) stats_device(r->ws);

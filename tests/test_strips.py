@@ -45,15 +45,9 @@ def test_strips_loopback_fp64_and_other_k(fp64, k, world):
 
 
 def single_gpu_fit(G, tgt, cfg):
-    """The single-GPU fit a strip fit must equal.  In fp64 that is the double-double reduction
-    (SAD_FP64_DD): strips merge per-site double-double partials, the reference-order replay is single-GPU."""
-    if not cfg.fp64:
-        return G.fit(tgt, cfg)
-    os.environ["SAD_FP64_DD"] = "1"
-    try:
-        return G.fit(tgt, cfg)
-    finally:
-        del os.environ["SAD_FP64_DD"]
+    """The single-GPU fit a strip fit must equal — in fp64 too: the strips ship the tagged per-tile records
+    of the reference-order reduction to the sites' owners, who replay them in the reference's order."""
+    return G.fit(tgt, cfg)
 
 
 def test_strips_nccl_world1():
