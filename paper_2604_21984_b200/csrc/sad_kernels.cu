@@ -2210,7 +2210,7 @@ __device__ __forceinline__ void ref_add(DD& a, double x) {
 #define SAD_ORD_BAND 64  // pixels per band (a multiple of 32, at most 64)
 #endif
 #ifndef SAD_ORD_MINB
-#define SAD_ORD_MINB 1
+#define SAD_ORD_MINB 2  // two 256-thread blocks per SM (<= 128 registers; the shared footprint allows two)
 #endif
 constexpr int kOrdBandPx = SAD_ORD_BAND;
 template <int KM, int NPX, int NCH>
@@ -2385,6 +2385,22 @@ __device__ __forceinline__ void ord_put(const RedTarget& red, long long code, ui
     }
 }
 
+#if SAD_ORD_DEBUG
+__device__ unsigned long long g_ord_clk[8];
+__device__ unsigned long long g_ord_launch;
+#define ORD_T(i)                                                  \
+    do {                                                          \
+        if (threadIdx.x == 0) {                                   \
+            const long long _n = clock64();                       \
+            atomicAdd(&g_ord_clk[i], (unsigned long long)(_n - _t)); \
+            _t = _n;                                              \
+        }                                                         \
+    } while (0)
+#else
+#define ORD_T(i) \
+    do {         \
+    } while (0)
+#endif
 template <int KM, int MODE>
 __global__ void __launch_bounds__(256, SAD_ORD_MINB) k_backward_ord(const uint32_t* __restrict__ ids, const Q4<double>* __restrict__ gtab,
                                                       const double* __restrict__ tgt, FieldDims f, double s,
@@ -2396,6 +2412,9 @@ __global__ void __launch_bounds__(256, SAD_ORD_MINB) k_backward_ord(const uint32
     extern __shared__ __align__(16) unsigned char smraw[];
     Sm& sm = *reinterpret_cast<Sm*>(smraw);
     const int tid = threadIdx.x;
+#if SAD_ORD_DEBUG
+    long long _t = clock64();
+#endif
     const int px = blockIdx.x * kRefTile + (tid % kRefTile);
     const int py = blockIdx.y * kRefTile + (tid / kRefTile) + f.row0;
     const bool inside = px < f.width && py < f.height && py < f.row1;
@@ -2503,36 +2522,105 @@ __global__ void __launch_bounds__(256, SAD_ORD_MINB) k_backward_ord(const uint32
         }
     }
     __syncthreads();
+    ORD_T(0);
 
-    // ---- warp 0 replays the TileReducer's inserts in entry order (grad.cpp:40-57): only a site's
-    // first appearance can change the table, so each batch of 32 entries first drops the ones whose
-    // site already holds one of its probe slots, then inserts the rest one by one in entry order
-    if (tid < 32) {
-        for (int base = 0; base < NP * KM; base += 32) {
-            const uint32_t k = sm.key[base + tid];
-            bool need = false;
-            if (k != kEmpty) {
-                const uint32_t h = ref_tile_hash(k);
-                bool found = false;
-#pragma unroll
-                for (int q = 0; q < kRefProbes; q++) found |= sm.tkey[(h + q) & (kRefTable - 1)] == k;
-                need = !found;
+    // ---- the TileReducer's table (grad.cpp:40-57, grad.hpp:67-90).  Only a site's first appearance in
+    // entry order can change it (later ones find the site, or overflow again: the table only fills), so:
+    // (1) first appearances, in parallel: a tile-local hash (in the band buffer, unused until the bands)
+    //     keeps each distinct site's smallest entry index;
+    // (2) those sites compacted in entry order (block scan over the threads' pixel-major entries);
+    // (3) warp 0 inserts them 32 at a time speculatively: each lane takes the first free slot of its 8
+    //     probes in the current table; a lane whose probe run [home, slot] holds an earlier lane's slot
+    //     would have probed differently, so the batch commits up to the first such lane and resumes there.
+    {
+        constexpr int HS = NP * KM;  // local hash slots (>= distinct sites)
+        uint32_t* hk = reinterpret_cast<uint32_t*>(sm.c);
+        int* hf = reinterpret_cast<int*>(hk + HS);
+        uint16_t* he = reinterpret_cast<uint16_t*>(hf + HS);
+        uint32_t* fa = reinterpret_cast<uint32_t*>(he + HS);
+        for (int j = tid; j < HS; j += NP) {
+            hk[j] = kEmpty;
+            hf[j] = 0x7fffffff;
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (int i = 0; i < KM; i++) {
+            const int e = tid * KM + i;
+            const uint32_t k = sm.key[e];
+            // lanes holding the same site in list slot i: the lowest (smallest entry) inserts for all
+            const unsigned grp = __match_any_sync(0xffffffffu, k);
+            const int leader = __ffs(grp) - 1;
+            uint32_t h = 0;
+            if (k != kEmpty && (tid & 31) == leader) {
+                h = (k * 2654435761u) & (HS - 1);
+                for (;;) {
+                    const uint32_t old = atomicCAS(&hk[h], kEmpty, k);
+                    if (old == kEmpty || old == k) break;
+                    h = (h + 1) & (HS - 1);
+                }
+                atomicMin(&hf[h], e);
             }
-            unsigned todo = __ballot_sync(0xffffffffu, need);
-            while (todo) {
-                const int l = __ffs(todo) - 1;
-                todo &= todo - 1;
-                const uint32_t kk = __shfl_sync(0xffffffffu, k, l);
-                const uint32_t slot = (ref_tile_hash(kk) + (tid & (kRefProbes - 1))) & (kRefTable - 1);
-                const uint32_t t = sm.tkey[slot];
-                // the probe stops at the first free slot or at the site itself; none: overflow
-                const unsigned hit = __ballot_sync(0xffffffffu, tid < kRefProbes && (t == kEmpty || t == kk));
-                if (hit && tid == __ffs(hit) - 1 && t == kEmpty) sm.tkey[slot] = kk;
+            h = __shfl_sync(0xffffffffu, h, leader);
+            if (k != kEmpty) he[e] = static_cast<uint16_t>(h);
+        }
+        __syncthreads();
+        int nfirst = 0;
+#pragma unroll 1
+        for (int i = 0; i < KM; i++) {
+            const int e = tid * KM + i;
+            nfirst += sm.key[e] != kEmpty && hf[he[e]] == e;
+        }
+        int n_fa;
+        int pos = block_excl_scan256(nfirst, sm.wsum, n_fa);
+#pragma unroll 1
+        for (int i = 0; i < KM; i++) {
+            const int e = tid * KM + i;
+            if (sm.key[e] != kEmpty && hf[he[e]] == e) fa[pos++] = sm.key[e];
+        }
+        __syncthreads();
+        int* claim = reinterpret_cast<int*>(fa + HS);  // [kRefTable], 32 = unclaimed
+        static_assert(HS * 14 + kRefTable * 4 <= NCH * CS * 8, "claim array exceeds the band buffer");
+        for (int j = tid; j < kRefTable; j += NP) claim[j] = 32;
+        __syncthreads();
+        if (tid < 32) {
+            const int lane = tid;
+            for (int base = 0; base < n_fa;) {
+                const int m = n_fa - base < 32 ? n_fa - base : 32;
+                const uint32_t k = lane < m ? fa[base + lane] : kEmpty;
+                const uint32_t h = ref_tile_hash(k);
+                int slot = -1;  // first free probe slot, -1: all eight taken (overflow)
+                if (lane < m) {
+                    uint32_t t[kRefProbes];
+#pragma unroll
+                    for (int q = 0; q < kRefProbes; q++) t[q] = sm.tkey[(h + q) & (kRefTable - 1)];
+#pragma unroll
+                    for (int q = kRefProbes - 1; q >= 0; q--)
+                        if (t[q] == kEmpty) slot = q;
+                }
+                // claim[pos]: the lowest lane whose chosen slot is pos (the batch's speculative inserts)
+                const uint32_t mine = (h + static_cast<uint32_t>(slot)) & (kRefTable - 1);
+                if (slot >= 0) atomicMin(&claim[mine], lane);
                 __syncwarp();
+                bool valid = true;
+                if (slot > 0) {  // an earlier lane's slot inside my probe run [home, home + slot]
+#pragma unroll
+                    for (int q = 0; q < kRefProbes; q++)
+                        if (q <= slot && claim[(h + q) & (kRefTable - 1)] < lane) valid = false;
+                } else if (slot == 0) {
+                    valid = claim[mine] == lane;
+                }
+                __syncwarp();
+                if (slot >= 0) claim[mine] = 32;
+                const unsigned bad = __ballot_sync(0xffffffffu, lane < m && !valid);
+                const int commit = bad ? __ffs(bad) - 1 : m;  // lane 0 is always valid: commit >= 1
+                if (lane < commit && slot >= 0) sm.tkey[(h + static_cast<uint32_t>(slot)) & (kRefTable - 1)] = k;
+                __syncwarp();
+                base += commit;
             }
         }
     }
     __syncthreads();
+    ORD_T(1);
 
     // ---- the occupied table slots, compacted; thread t owns the (slot, channel) items t + 256 j
     int n_occ;
@@ -2549,6 +2637,7 @@ __global__ void __launch_bounds__(256, SAD_ORD_MINB) k_backward_ord(const uint32
     for (int band = 0; band < NP / kOrdBandPx; band++) {
         sm.bm[tid][0] = sm.bm[tid][1] = 0u;
         __syncthreads();
+        ORD_T(2);
         // contributions of the band's entries (pixel-major); an overflowed site's go out as raw records
 #pragma unroll 1
         for (int le = tid; le < BE; le += NP) {
@@ -2581,6 +2670,7 @@ __global__ void __launch_bounds__(256, SAD_ORD_MINB) k_backward_ord(const uint32
             sm.eslot[le] = us;
         }
         __syncthreads();
+        ORD_T(3);
         // bucket the band's entries by slot, in pixel order (a site occurs once per pixel)
         {
             int tot;
@@ -2588,6 +2678,7 @@ __global__ void __launch_bounds__(256, SAD_ORD_MINB) k_backward_ord(const uint32
                 block_excl_scan256(__popc(sm.bm[tid][0]) + __popc(sm.bm[tid][1]), sm.wsum, tot));
         }
         __syncthreads();
+        ORD_T(4);
 #pragma unroll 1
         for (int le = tid; le < BE; le += NP) {
             const int us = sm.eslot[le];
@@ -2597,6 +2688,7 @@ __global__ void __launch_bounds__(256, SAD_ORD_MINB) k_backward_ord(const uint32
             sm.list[sm.bstart[us] + __popcll(bits & ((1ull << lp) - 1ull))] = static_cast<uint16_t>(le);
         }
         __syncthreads();
+        ORD_T(5);
         // replay: each item continues its (site, channel) Accum over the band's bucket
 #pragma unroll
         for (int j = 0; j < NCH; j++) {
@@ -2611,10 +2703,12 @@ __global__ void __launch_bounds__(256, SAD_ORD_MINB) k_backward_ord(const uint32
             }
         }
         __syncthreads();
+        ORD_T(6);
     }
     // ---- one record per occupied slot: the per-tile Accums, flushed as end_tile does
     for (int ui = tid; ui < n_occ; ui += NP) sm.rec[ui] = ord_claim(red, sm.tkey[sm.occ[ui]], tile << 9);
     __syncthreads();
+    ORD_T(7);
 #pragma unroll
     for (int j = 0; j < NCH; j++) {
         const int item = tid + NP * j;
@@ -2624,6 +2718,7 @@ __global__ void __launch_bounds__(256, SAD_ORD_MINB) k_backward_ord(const uint32
         }
     }
     __syncthreads();
+    ORD_T(7);
     if (MODE != 2) block_dd_store<NP>(loss, sm.warp_part, loss_part + blockIdx.y * gridDim.x + blockIdx.x);
     __syncthreads();
     unsigned long long nf = block_sum_u64<NP>(nonfinite, reinterpret_cast<unsigned long long*>(sm.warp_part));
@@ -2785,7 +2880,14 @@ __global__ void __launch_bounds__(128) k_ordered_totals(RedTarget red, const Dev
     long long base = 0;
     const int n_slice = ord_slice(red, id, base);
 #if SAD_ORD_DEBUG
-    if (lane == 0) {
+    if (id == 0 && lane == 0) {
+        const unsigned long long L = atomicAdd(&g_ord_launch, 1ull);
+        if (L % 1000 == 999)
+            printf("ord clk/tile A %llu B %llu D1 %llu scan %llu scat %llu D2 %llu rec %llu end %llu\n",
+                   g_ord_clk[0] / (L + 1), g_ord_clk[1] / (L + 1), g_ord_clk[2] / (L + 1), g_ord_clk[3] / (L + 1),
+                   g_ord_clk[4] / (L + 1), g_ord_clk[5] / (L + 1), g_ord_clk[6] / (L + 1), g_ord_clk[7] / (L + 1));
+    }
+    if (lane == 0 && false) {
         int nl = 0, nraw = 0;
         for (int r = red.head[id]; r >= 0; r = red.onext[r]) nl++;
         for (int j = 0; j < n_slice; j++) nraw += (red.tag[base + j] & kTagRaw) != 0;
