@@ -3931,8 +3931,9 @@ __device__ __forceinline__ void adam_ticket(DevState* st, int32_t* otop, unsigne
 }
 
 #ifndef SAD_ADAM_MINB
-#define SAD_ADAM_MINB 4  // resident 128-thread blocks per SM the register allocator must allow: 1 -> 4 measured
-                         // config-2 fit 862.7 -> 854 ms (6: standalone faster, fit 869.7 ms)
+#define SAD_ADAM_MINB 5  // resident 128-thread blocks per SM the register allocator must allow: config-2 fit
+                         // 1: 862.7, 4: 854 (r1), 4 -> 5: 851 -> 846.5 ms (96 regs; the ~5k active sites' blocks
+                         // fit one wave), 6: 866 ms (spills)
 #endif
 template <typename T>
 __global__ void __launch_bounds__(128, SAD_ADAM_MINB) k_adam(SitesDev s, DevState* st, RedTarget grads, double* __restrict__ m,
