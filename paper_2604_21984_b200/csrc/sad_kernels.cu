@@ -2313,44 +2313,6 @@ __device__ __forceinline__ int ord_contrib(double fx, double fy, double wi, cons
     return bad;
 }
 
-// One tagged record for `site`: its next slice slot, else the overflow pool; a full pool (the caller
-// sized it too small) falls back to a double-double CAS into `over` and flags st->err bit 3.
-template <int NCH>
-__device__ __forceinline__ void ord_store(const RedTarget& red, uint32_t site, uint32_t tag, const double (&hi)[NCH],
-                                          const double (&lo)[NCH], DevState* st) {
-    const int slot = atomicAdd(red.cnt + site, 1);
-    double2* dst = nullptr;
-    if (red.roff) {
-        const long long rec = static_cast<long long>(red.roff[site]) + slot;
-        if (slot < red.rcap[site] && rec < red.psize) {
-            dst = red.part + static_cast<size_t>(rec) * red.stride;
-            red.tag[rec] = tag;
-        }
-    } else if (slot < red.maxt) {
-        const size_t rec = static_cast<size_t>(site) * red.maxt + slot;
-        dst = red.part + rec * red.stride;
-        red.tag[rec] = tag;
-    }
-    if (!dst) {
-        const int ro = atomicAdd(red.otop, 1);
-        if (ro < red.ocap) {
-            dst = red.opart + static_cast<size_t>(ro) * red.stride;
-            red.otag[ro] = tag;
-            __threadfence();
-            red.onext[ro] = atomicExch(red.head + site, ro);
-        }
-    }
-    if (dst) {
-#pragma unroll
-        for (int ch = 0; ch < NCH; ch++) dst[ch] = make_double2(hi[ch], lo[ch]);
-    } else {
-        atomicOr(&st->err, 8);
-#pragma unroll
-        for (int ch = 0; ch < NCH; ch++)
-            dd_atomic_merge(red.over + static_cast<size_t>(ch) * red.cap + site, DD{hi[ch], lo[ch]});
-    }
-}
-
 // A site's per-tile record in two steps: one thread claims it (code >= 0: part record, <= -2: opart
 // record -2 - code, -1: pools full) and writes the tag; each channel's owner then stores its Accum.
 __device__ __forceinline__ long long ord_claim(const RedTarget& red, uint32_t site, uint32_t tag) {
@@ -2383,6 +2345,15 @@ __device__ __forceinline__ void ord_put(const RedTarget& red, long long code, ui
         atomicOr(&st->err, 8);
         dd_atomic_merge(red.over + static_cast<size_t>(ch) * red.cap + site, a);
     }
+}
+
+// One tagged record for `site` written by one thread (raw contributions of an overflowed site).
+template <int NCH>
+__device__ __forceinline__ void ord_store(const RedTarget& red, uint32_t site, uint32_t tag, const double (&hi)[NCH],
+                                          const double (&lo)[NCH], DevState* st) {
+    const long long code = ord_claim(red, site, tag);
+#pragma unroll
+    for (int ch = 0; ch < NCH; ch++) ord_put(red, code, site, ch, DD{hi[ch], lo[ch]}, st);
 }
 
 #if SAD_ORD_DEBUG
@@ -2880,21 +2851,21 @@ __global__ void __launch_bounds__(128) k_ordered_totals(RedTarget red, const Dev
     long long base = 0;
     const int n_slice = ord_slice(red, id, base);
 #if SAD_ORD_DEBUG
+    // diagnostics build: k_backward_ord's per-phase clocks (cycles summed over tiles, per launch) every
+    // 1000 launches, and sites with long record lists
     if (id == 0 && lane == 0) {
         const unsigned long long L = atomicAdd(&g_ord_launch, 1ull);
         if (L % 1000 == 999)
-            printf("ord clk/tile A %llu B %llu D1 %llu scan %llu scat %llu D2 %llu rec %llu end %llu\n",
+            printf("ord clk A %llu B %llu bandstart %llu D1 %llu scan %llu scatter %llu D2 %llu records %llu\n",
                    g_ord_clk[0] / (L + 1), g_ord_clk[1] / (L + 1), g_ord_clk[2] / (L + 1), g_ord_clk[3] / (L + 1),
                    g_ord_clk[4] / (L + 1), g_ord_clk[5] / (L + 1), g_ord_clk[6] / (L + 1), g_ord_clk[7] / (L + 1));
     }
-    if (lane == 0 && false) {
-        int nl = 0, nraw = 0;
+    if (lane == 0) {
+        int nl = 0;
         for (int r = red.head[id]; r >= 0; r = red.onext[r]) nl++;
-        for (int j = 0; j < n_slice; j++) nraw += (red.tag[base + j] & kTagRaw) != 0;
-        const int cnt = red.cnt[id];
         if (n_slice + nl > 64 && atomicAdd(&g_ord_dbg, 1) < 40)
-            printf("ord site %d cnt %d slice %d (rcap %d) list %d raw-in-slice %d\n", id, cnt, n_slice,
-                   red.roff ? red.rcap[id] : red.maxt, nl, nraw);
+            printf("ord site %d cnt %d slice %d (cap %d) list %d\n", id, red.cnt[id], n_slice,
+                   red.roff ? red.rcap[id] : red.maxt, nl);
     }
 #endif
     const DD t = ord_total<NCH>(red, id, n_slice, base, buf[warp], sorted[warp]);

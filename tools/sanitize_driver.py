@@ -117,6 +117,11 @@ single = G.fit(img, cfg)
 parts = G.fit_strips_loopback(img, cfg, 2)
 check("strips", all([sad.history_line(r) for r in p.history] == [sad.history_line(r) for r in single.history]
                     for p in parts))
+cfg64 = sad.TrainConfig(iters=25, target_bpp=3.0, fp64=True, seed=3, densify_start=10, densify_every=10)
+single64 = G.fit(img, cfg64)
+parts64 = G.fit_strips_loopback(img, cfg64, 2)  # fp64: tagged records shipped to the owners (ordered strips)
+check("strips fp64", all([sad.history_line(r) for r in p.history] == [sad.history_line(r) for r in single64.history]
+                         for p in parts64))
 bad = [n for n, ok in checks if not ok]
 fails = int(G.lib.sad_debug_check_failures())  # -1: product build (no bound checks compiled in)
 print(f"{len(checks)} checks, {len(bad)} mismatches {bad}; kernel bound-check failures: {fails}")
