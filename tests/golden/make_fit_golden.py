@@ -39,6 +39,7 @@ def cases():
     # fp64 path replays, on a second image
     out["config2_fp64_t1_s2"] = (768, 512, 2, dict(iters=4000, target_bpp=2.0, fp64=True, seed=1, threads=1))
     out["config3_s1"] = (2048, 2048, 1, dict(iters=300, n_sites=100000, fp64=False, seed=1))
+    out["config3_fp64_s1"] = (2048, 2048, 1, dict(iters=300, n_sites=100000, fp64=True, seed=1))
     # config 5 shape (8192^2, 2 BPP): 25 iterations, i.e. the initial refresh, one densify event (t = 20) with
     # its full re-seeded refresh, and the final refresh(Full, 16) (about 25 minutes on 8 host cores)
     out["config5_short_s5"] = (8192, 8192, 5, dict(iters=25, target_bpp=2.0, fp64=False, seed=1))

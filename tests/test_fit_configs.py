@@ -6,7 +6,7 @@
 * Config 2 (768x512 synthetic Kodak-shaped images, 2 BPP, 4000 iterations with 150 densify/prune
   events), image seeds 1-8 in fp32 and seeds 1 (reference on 8 threads) and 2 (on its default single
   thread) in fp64 (the reference's default precision), and
-  config 3 (2048x2048, 100k sites, 300 iterations), and the config-5 shape (8192x8192, 2 BPP: 1.69M sites,
+  config 3 (2048x2048, 100k sites, 300 iterations) in fp32 and fp64, and the config-5 shape (8192x8192, 2 BPP: 1.69M sites,
   25 iterations incl. one densify event and its re-seeded refresh): the GPU fit against goldens of complete
   reference fits (tests/golden/fit_*.npz, written here by tests/golden/make_fit_golden.py from the
   unmodified reference library; a reference fit takes minutes per image, the GPU's under a second).
