@@ -1344,6 +1344,14 @@ sad_status sad_tau_diffusion(sad_ctx* c, const sad_sites_view* s_in, const sad_f
     });
 }
 
+// fp64 per-site gradient sums in the reference's summation order (sadk::fp64_ordered).  The
+// record tags hold the reference tile's raster index in 23 bits: beyond 2^23 tiles (an image over ~46k^2
+// pixels) the double-double reduction is used.
+static bool use_ordered(bool fp64, const sadk::FieldDims& fd) {
+    const long long tiles = ((fd.width + 15ll) / 16) * ((fd.height + 15ll) / 16);
+    return fp64 && sadk::fp64_ordered() && tiles < (1ll << 23);
+}
+
 // ====================================================================== grad
 static void backward_call(sad_ctx* c, const sad_sites_view* s_in, const sad_field_view* f_in, const double* img,
                           int fp64, int mode, double* grads, uint64_t* nonfinite, double* loss) {
@@ -1360,7 +1368,7 @@ static void backward_call(sad_ctx* c, const sad_sites_view* s_in, const sad_fiel
     ws.zero_red(true);
     ws.zero_state_field(offsetof(DevState, nonfinite), sizeof(uint64_t));
     ws.zero_state_field(offsetof(DevState, loss), sizeof(double2));
-    const bool ordered = fp64 && sadk::fp64_ordered();
+    const bool ordered = use_ordered(fp64 != 0, ws.fd);
     const sadk::RedTarget red = ordered ? ws.gred_ord() : ws.gred();
     sadk::launch_backward(fp64 != 0, mode, ws.ids[ws.cur].p, ws.gtab.p,
                           fp64 ? static_cast<const void*>(ws.tgt_d.p) : static_cast<const void*>(ws.tgt_f.p), ws.fd,
@@ -1803,7 +1811,7 @@ static void fit_loop(sad_fit_run* r) {
     if (tau) ensure_tau(ws);
     // fp64: per-site sums in the reference's order (sadk::fp64_ordered): tagged records, then the ordered
     // totals (values) for Adam; tau_diffusion then works on those values as on the double-double ones
-    const bool ordered = fp64 && sadk::fp64_ordered();
+    const bool ordered = use_ordered(fp64, ws.fd);
     if (ordered) ws.otot.ensure(10 * static_cast<size_t>(ws.cap));
     auto gred = [&] { return ordered ? ws.gred_adaptive_ord() : ws.gred_adaptive(); };
     if (ordered) (void)gred();  // the tag arrays exist before any graph capture
@@ -2454,7 +2462,7 @@ static void fit_loop_strips(std::vector<sad_fit_run*>& runs, StripComm& T) {
     const sad_train_config& c = r0->cfg;
     const int w = r0->w, h = r0->h;
     const bool fp64 = c.fp64 != 0;
-    const bool ordered = fp64 && sadk::fp64_ordered();  // fp64: the reference's summation order (§3)
+    const bool ordered = use_ordered(fp64, r0->ws.fd);  // fp64: the reference's summation order (§3)
     const bool budget = c.target_bpp > 0;
     const double scale_n = norm_scale(w, h);
     if (c.tau_diffusion_lambda > 0) fail(SAD_EINVAL, "strips: tau_diffusion is not supported");
