@@ -38,6 +38,7 @@ def cases():
     # fp64 with the reference's default RunOpts::threads = 1 (types.hpp:163): the summation order the GPU's
     # fp64 path replays, on a second image
     out["config2_fp64_t1_s2"] = (768, 512, 2, dict(iters=4000, target_bpp=2.0, fp64=True, seed=1, threads=1))
+    out["config2_fp64_s3"] = (768, 512, 3, dict(iters=4000, target_bpp=2.0, fp64=True, seed=1))
     out["config3_s1"] = (2048, 2048, 1, dict(iters=300, n_sites=100000, fp64=False, seed=1))
     out["config3_fp64_s1"] = (2048, 2048, 1, dict(iters=300, n_sites=100000, fp64=True, seed=1))
     # config 5 shape (8192^2, 2 BPP): 25 iterations, i.e. the initial refresh, one densify event (t = 20) with

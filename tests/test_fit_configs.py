@@ -4,7 +4,7 @@
   compiled reference run live on this box's host cores — every history line, the final sites and
   the final map identical.
 * Config 2 (768x512 synthetic Kodak-shaped images, 2 BPP, 4000 iterations with 150 densify/prune
-  events), image seeds 1-8 in fp32 and seeds 1 (reference on 8 threads) and 2 (on its default single
+  events), image seeds 1-8 in fp32 and seeds 1, 3 (reference on 8 threads) and 2 (on its default single
   thread) in fp64 (the reference's default precision), and
   config 3 (2048x2048, 100k sites, 300 iterations) in fp32 and fp64, and the config-5 shape (8192x8192, 2 BPP: 1.69M sites,
   25 iterations incl. one densify event and its re-seeded refresh): the GPU fit against goldens of complete
